@@ -1,0 +1,310 @@
+/*
+ * prx.h -- C ABI of the B200-native photon-path verification and reuse engine.
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2111.06906 as implemented by
+ * the reference `pathreuse` C++ library (/root/reference/proj).  The reference exposes
+ * no plugin/FFI layer; its public surface is the C++ `pathreuse::Engine`
+ * and the pybind11 module `_pathreuse`.  Every entry point below replaces one of those
+ * calls; the reference interface it replaces is cited beside it (paths relative to
+ * /root/reference/proj).  Plain pointers and sizes only -- no C++ or torch types.
+ *
+ * Error behaviour mirrors the reference's exception types (SURVEY.md s8b "Errors"):
+ * every fallible call returns a prx_status; the message of the last failure on the
+ * calling thread is available from prx_last_error().  Language bindings map
+ *   PRX_E_INVALID_ARGUMENT -> std::invalid_argument / ValueError
+ *   PRX_E_OUT_OF_RANGE     -> std::out_of_range     / IndexError
+ *   PRX_E_LOGIC            -> std::logic_error      / RuntimeError
+ *   PRX_E_SCENE            -> pathreuse::SceneError / RuntimeError
+ *   PRX_E_CUDA, PRX_E_RUNTIME -> std::runtime_error / RuntimeError
+ */
+#ifndef PRX_H_
+#define PRX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRX_ABI_VERSION 1
+#define PRX_MAX_LIGHTS 16
+
+typedef enum prx_status {
+    PRX_OK = 0,
+    PRX_E_INVALID_ARGUMENT = 1,
+    PRX_E_OUT_OF_RANGE = 2,
+    PRX_E_LOGIC = 3,
+    PRX_E_SCENE = 4,
+    PRX_E_RUNTIME = 5,
+    PRX_E_CUDA = 6
+} prx_status;
+
+/* ---- scene description (POD mirror of pathreuse::Scene, scene.hpp:16-60) ---------- */
+
+typedef struct prx_vec3 { float x, y, z; } prx_vec3;
+typedef struct prx_quat { float x, y, z, w; } prx_quat;            /* transform.hpp:10 */
+typedef struct prx_triangle { prx_vec3 a, b, c; } prx_triangle;    /* geometry.hpp:61  */
+
+typedef struct prx_keyframe {                                      /* scene.hpp:24, light.hpp:15 */
+    int32_t frame;
+    prx_quat rotation;
+    prx_vec3 translation;
+    float scale;
+} prx_keyframe;
+
+enum { PRX_MATERIAL_DIFFUSE = 0, PRX_MATERIAL_GLOSSY = 1 };        /* scene.hpp:16 */
+
+typedef struct prx_material {                                      /* scene.hpp:18-22 */
+    int32_t kind;
+    prx_vec3 albedo;
+    float glossy_exponent;
+} prx_material;
+
+typedef struct prx_object_desc {                                   /* scene.hpp:29-37 */
+    const char* name;
+    const prx_triangle* mesh;       /* object-local space */
+    uint32_t n_triangles;
+    prx_material material;
+    const prx_keyframe* keyframes;  /* may be NULL/0: identity at frame 0 */
+    uint32_t n_keyframes;
+} prx_object_desc;
+
+enum {                                                             /* light.hpp:13 */
+    PRX_LIGHT_POINT = 0,
+    PRX_LIGHT_SPOT = 1,
+    PRX_LIGHT_DISC_AREA = 2,
+    PRX_LIGHT_RECT_AREA = 3
+};
+
+typedef struct prx_light_desc {                                    /* light.hpp:24-37 */
+    int32_t kind;
+    prx_vec3 flux;
+    float cone_angle_deg;
+    float radius;
+    float half_x, half_y;
+    const prx_keyframe* keyframes;
+    uint32_t n_keyframes;
+} prx_light_desc;
+
+typedef struct prx_camera {                                        /* scene.hpp:39-45 */
+    prx_vec3 position;
+    prx_vec3 look_at;
+    float fov_deg;
+    uint32_t width, height;
+} prx_camera;
+
+typedef struct prx_scene_desc {                                    /* scene.hpp:47-60 */
+    const prx_object_desc* objects;
+    uint32_t n_objects;
+    const prx_light_desc* lights;
+    uint32_t n_lights;
+    prx_camera camera;
+    int32_t frames;
+} prx_scene_desc;
+
+typedef struct prx_scene prx_scene;     /* finalized scene: validated, static BVH built */
+typedef struct prx_engine prx_engine;   /* per-GPU engine over a path range           */
+
+/* ---- engine configuration / statistics ------------------------------------------ */
+
+enum { PRX_MODE_BASELINE = 0, PRX_MODE_NAIVE = 1, PRX_MODE_ERROR = 2 }; /* engine.hpp:14 */
+
+typedef struct prx_config {                                        /* engine.hpp:43-53 */
+    int32_t mode;
+    uint32_t n_paths;
+    uint32_t max_bounces;       /* 1..16 */
+    uint32_t dm_dims[4];
+    float threshold;
+    uint64_t seed;
+    float gather_radius;
+    uint32_t workers;           /* accepted for API parity; the GPU ignores it */
+    int32_t record_flags;
+    /* B200 extensions (0 = defaults) */
+    int32_t device;             /* CUDA device ordinal                              */
+    uint32_t shard_begin;       /* path range owned by this engine; [0,0) = all     */
+    uint32_t shard_end;
+    int32_t exact_trig;         /* 1 (default): host-libm cosf/sinf table for bounces */
+} prx_config;
+
+typedef struct prx_frame_stats {                                   /* engine.hpp:19-30 */
+    int32_t frame;
+    int32_t mode;
+    uint64_t rays_traced;
+    uint64_t rays_reused;
+    uint64_t paths_replaced;
+    uint64_t paths_pruned;
+    uint64_t paths_filled;
+    uint64_t visibility_rays;
+    double t_update, t_occlusion, t_dm, t_prune, t_fill, t_trace, t_gather;
+    /* B200 extensions: device time (ms, CUDA events) of the named north_star stages */
+    double ms_frame_update, ms_verify, ms_retrace, ms_splat;
+    uint64_t live_segments_before;  /* segments verified this frame (paths live at entry) */
+    uint64_t paths_retraced;        /* paths with retrace_start != 0xFF after verify    */
+} prx_frame_stats;
+
+typedef struct prx_engine_info {
+    uint32_t n_paths;           /* total paths of the (unsharded) problem */
+    uint32_t max_bounces;
+    uint32_t n_lights;
+    uint32_t shard_begin, shard_end;
+    float eps_world;            /* engine.cpp:74 */
+    float diagonal;
+    int32_t frames_run;
+    uint32_t n_pruned;          /* length of the last frame's pruned list */
+    uint32_t light_path_begin[PRX_MAX_LIGHTS];
+    uint32_t light_path_end[PRX_MAX_LIGHTS];
+    uint32_t dm_ndims[PRX_MAX_LIGHTS];
+    uint32_t dm_dims[PRX_MAX_LIGHTS][4];
+    uint32_t dm_cells[PRX_MAX_LIGHTS];
+    float flux_per_path[PRX_MAX_LIGHTS][3];
+    uint64_t device_bytes;      /* device memory held by the engine */
+} prx_engine_info;
+
+/* State fields for prx_engine_download / prx_engine_upload.  Vertex fields are
+ * bounce-major [max_bounces][n_paths] (photon_store.cpp:32-36); path fields are
+ * [n_paths] (shard-local when sharded).                                          */
+typedef enum prx_field {
+    PRX_FIELD_PHOTONS = 0,     /* 32-byte pathreuse::Photon records (photon_store.hpp:13) */
+    PRX_FIELD_AUX = 1,         /* 24-byte PathVertexAux records (photon_store.hpp:75)     */
+    PRX_FIELD_POS_OBJ = 2,     /* float4 {position, object id bits}                       */
+    PRX_FIELD_ENERGY = 3,      /* float4 {energy rgb, radius}                             */
+    PRX_FIELD_IN_DIR = 4,      /* float4 {incoming dir, 0}                                */
+    PRX_FIELD_OUT_DIR = 5,     /* float4 {outgoing dir, 0}                                */
+    PRX_FIELD_ORIGIN = 6,      /* float4 per path                                         */
+    PRX_FIELD_EMISSION_DIR = 7,/* float4 per path                                         */
+    PRX_FIELD_CANONICAL = 8,   /* float4 per path (canonical coords c[0..3])              */
+    PRX_FIELD_CELL = 9,        /* u32 per path                                            */
+    PRX_FIELD_EPOCH = 10,      /* u32 per path                                            */
+    PRX_FIELD_PATH_INFO = 11,  /* u32 per path (photon_store.hpp:23-40)                   */
+    PRX_FIELD_META = 12,       /* u8x4 per path {photon_count, escaped, status, filled}   */
+    PRX_FIELD_RETRACE_START = 13, /* u8 per path (0xFF = no retrace)                      */
+    PRX_FIELD_SEGMENT_FLAGS = 14, /* u32 per path (record_flags)                          */
+    PRX_FIELD_DM_TARGET = 15,  /* u32 [cells] of light `index`                            */
+    PRX_FIELD_DM_CURRENT = 16, /* u32 [cells] of light `index`                            */
+    PRX_FIELD_PRUNED = 17      /* u32 [n_pruned], ascending path ids                      */
+} prx_field;
+
+/* ---- pure functions (pybind module.cpp:47-82) ------------------------------------ */
+
+/* light.hpp:132-135 */
+double prx_prune_probability(uint32_t dm_current, uint32_t dm_target);
+/* engine.hpp:34-41 */
+int prx_energies_close(const float e_old[3], const float e_new[3], float threshold);
+/* photon_store.cpp:9-20 (PRX_E_OUT_OF_RANGE on a field overflow) */
+prx_status prx_encode_path_info(uint32_t cell, uint32_t seg_count, uint32_t retrace_start,
+                                int replace, int reuse_light, uint32_t* word_out);
+/* photon_store.cpp:22-30 */
+void prx_decode_path_info(uint32_t word, uint32_t* cell, uint32_t* seg_count,
+                          uint32_t* retrace_start, int* replace, int* reuse_light);
+/* photon_store.cpp:38-54; out[7] = {path_info, origin_positions, distribution_maps,
+ * pruned_array, photon_map, subtotal_reuse, total} in MiB */
+void prx_memory_footprint(uint64_t n_paths, uint32_t max_bounces, const uint32_t* dm_dims,
+                          uint32_t n_dims, int area_light, double out[7]);
+
+/* ---- scenes ----------------------------------------------------------------------- */
+
+/* finalize_scene (scene.cpp:63-113): validates, assigns dense ids, builds the static BVH. */
+prx_status prx_scene_create(const prx_scene_desc* desc, prx_scene** out);
+/* make_builtin_scene (scene.cpp:603-611); names as in builtin_scenes() (module.cpp:57-61). */
+prx_status prx_scene_builtin(const char* name, prx_scene** out);
+/* Procedural BASELINE configurations: "C1".."C5" plus parameters
+ * (0 = default): C5 uses n_dynamic objects; tri_scale scales static tessellation.   */
+prx_status prx_scene_synthetic(const char* name, uint32_t n_dynamic, float tri_scale,
+                               prx_scene** out);
+/* Borrowed view of the finalized scene's description (valid until destroy). */
+prx_status prx_scene_describe(const prx_scene* scene, prx_scene_desc* out);
+/* Static BVH permutation (Bvh::permutation, bvh.hpp:36) -- parity harness. */
+prx_status prx_scene_bvh_permutation(const prx_scene* scene, uint32_t* out, size_t capacity,
+                                     size_t* count);
+/* counts: {static triangles, dynamic triangles, bvh nodes, objects} */
+prx_status prx_scene_counts(const prx_scene* scene, uint64_t counts[4]);
+float prx_scene_diagonal(const prx_scene* scene);
+void prx_scene_destroy(prx_scene* scene);
+
+/* ---- engine (engine.hpp:69-179) --------------------------------------------------- */
+
+/* Engine::Engine(Scene, EngineConfig) -- engine.cpp:63-117 */
+prx_status prx_engine_create(const prx_scene* scene, const prx_config* cfg, prx_engine** out);
+void prx_engine_destroy(prx_engine* engine);
+prx_status prx_engine_get_info(const prx_engine* engine, prx_engine_info* out);
+
+/* Engine::run_frame() -- engine.cpp:201-242.  Equivalent to frame_update, verify_paths,
+ * retrace_invalid in order; synchronous, fills stats on return. */
+prx_status prx_run_frame(prx_engine* engine, prx_frame_stats* stats);
+
+/* north_star stage split of run_frame (SURVEY.md s8b "New named entry points"):
+ *   frame_update   = state_at + run_frame prelude (scene.cpp:115-134, engine.cpp:202-226)
+ *   verify_paths   = stage_update_origins + stage_occlusions + stage_compute_dm
+ *   retrace_invalid= stage_prune + stage_fill + stage_trace
+ * Stats accumulate into the struct passed to each call (zero it before frame_update). */
+prx_status prx_frame_update(prx_engine* engine, prx_frame_stats* stats);
+prx_status prx_verify_paths(prx_engine* engine, prx_frame_stats* stats);
+prx_status prx_retrace_invalid(prx_engine* engine, prx_frame_stats* stats);
+
+/* Sub-stages of the above for multi-GPU orchestration and stage-level parity tests.
+ * stage ids: */
+typedef enum prx_stage {
+    PRX_STAGE_UPDATE_ORIGINS = 0,   /* engine.cpp:244-304 */
+    PRX_STAGE_OCCLUSIONS = 1,       /* engine.cpp:306-337 */
+    PRX_STAGE_COMPUTE_DM = 2,       /* engine.cpp:405-441 (local histogram only)      */
+    PRX_STAGE_PRUNE = 3,            /* engine.cpp:473-497 (single shard)              */
+    PRX_STAGE_FILL = 4,             /* engine.cpp:499-546 (single shard)              */
+    PRX_STAGE_TRACE = 5,            /* engine.cpp:548-598 (+ refresh_path_info)       */
+    PRX_STAGE_RELEASE_ALL = 6       /* baseline prelude engine.cpp:228-232            */
+} prx_stage;
+prx_status prx_run_stage(prx_engine* engine, int stage, prx_frame_stats* stats);
+
+/* Sharded prune/fill exchange points.  All buffers are DEVICE pointers
+ * on the engine's device, ordered on the engine stream.
+ *  - after COMPUTE_DM: the caller all-reduces DM_C of each light (prx_engine_dm_current
+ *    gives its device address) across shards;
+ *  - prx_prune_count: marks paths, writes per-cell unmarked counts for light `li` into
+ *    `unmarked_out[cells]`;
+ *  - caller all-gathers those; passes (sum over shards < this, total over shards);
+ *  - prx_prune_apply: trims survivors, updates DM_C, builds the pruned list;
+ *  - prx_fill_count: writes the number of dead slots of light `li` into *dead_out (host);
+ *  - prx_fill_apply: with the global exclusive prefix of dead slots and the global
+ *    total, assigns deficit units to this shard's slots and samples them.          */
+prx_status prx_engine_dm_current(prx_engine* engine, uint32_t light, void** dev_ptr,
+                                 uint32_t* cells);
+prx_status prx_prune_count(prx_engine* engine, uint32_t light, uint32_t* unmarked_out_dev);
+prx_status prx_prune_apply(prx_engine* engine, uint32_t light, const uint32_t* prefix_dev,
+                           const uint32_t* total_dev, prx_frame_stats* stats);
+prx_status prx_fill_count(prx_engine* engine, uint32_t light, uint32_t* dead_out);
+prx_status prx_fill_apply(prx_engine* engine, uint32_t light, uint64_t dead_prefix,
+                          uint64_t dead_total, prx_frame_stats* stats);
+/* Stream the engine orders its work on (cudaStream_t as void*); NULL = engine-owned. */
+prx_status prx_engine_set_stream(prx_engine* engine, void* cuda_stream);
+prx_status prx_engine_synchronize(prx_engine* engine);
+
+/* gather_image (gather.cpp:35-75) as a GPU splat over the engine's live photons.
+ * rgb_out: host float[3*w*h] (may be NULL) -- top-left origin, RGB rows;
+ * rgb_dev: optional device float[3*w*h] written on the engine stream.
+ * mode: 0 = tiled shared-memory atomic splat, 1 = ordered gather (bit-exact vs the
+ * reference's 27-cell insertion order). */
+prx_status prx_splat(prx_engine* engine, const prx_camera* camera, float radius, int mode,
+                     float* rgb_out, float* rgb_dev, prx_frame_stats* stats);
+
+/* Lazy host mirrors for the introspection accessors (engine.hpp:76-122) and the
+ * state-injection parity harness.  `index` selects the light for DM fields.
+ * bytes must equal the field size (prx_field_bytes). */
+size_t prx_field_bytes(const prx_engine* engine, int field, uint32_t index);
+prx_status prx_engine_download(prx_engine* engine, int field, uint32_t index, void* dst,
+                               size_t bytes);
+prx_status prx_engine_upload(prx_engine* engine, int field, uint32_t index, const void* src,
+                             size_t bytes);
+/* Sets frames_run and the previous light poses as if frame (frames_run-1) had run --
+ * used after uploading a full state captured from another implementation. */
+prx_status prx_engine_set_frame_counter(prx_engine* engine, int32_t frames_run);
+
+/* Number of kernel launches issued by this engine since creation (bench evidence). */
+uint64_t prx_engine_launch_count(const prx_engine* engine);
+
+const char* prx_last_error(void);
+int prx_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRX_H_ */

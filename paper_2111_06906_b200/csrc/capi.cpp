@@ -1,0 +1,288 @@
+// capi.cpp -- the extern "C" boundary declared in include/prx.h.
+//
+// Every entry point catches the C++ exception its reference counterpart would throw and
+// returns the matching prx_status (SURVEY.md s8b "Errors"); prx_last_error() returns the
+// message on the calling thread.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "engine.h"
+#include "host_scene.h"
+#include "prx.h"
+
+struct prx_scene {
+    std::shared_ptr<prx::Scene> scene;
+};
+
+struct prx_engine {
+    std::unique_ptr<prx::Engine> engine;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+prx_status fail(const std::exception& e) {
+    g_error = e.what();
+    if (dynamic_cast<const prx::SceneError*>(&e)) return PRX_E_SCENE;
+    if (dynamic_cast<const prx::CudaError*>(&e)) return PRX_E_CUDA;
+    if (dynamic_cast<const std::invalid_argument*>(&e)) return PRX_E_INVALID_ARGUMENT;
+    if (dynamic_cast<const std::out_of_range*>(&e)) return PRX_E_OUT_OF_RANGE;
+    if (dynamic_cast<const std::logic_error*>(&e)) return PRX_E_LOGIC;
+    return PRX_E_RUNTIME;
+}
+
+template <typename F>
+prx_status guarded(F&& f) {
+    try {
+        f();
+        return PRX_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    } catch (...) {
+        g_error = "unknown error";
+        return PRX_E_RUNTIME;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) throw std::invalid_argument(std::string(what) + " is NULL");
+}
+
+prx::Engine& eng(prx_engine* e) {
+    need(e, "engine");
+    return *e->engine;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* prx_last_error(void) { return g_error.c_str(); }
+int prx_abi_version(void) { return PRX_ABI_VERSION; }
+
+double prx_prune_probability(uint32_t dm_current, uint32_t dm_target) {
+    return prx::prune_probability(dm_current, dm_target);
+}
+
+int prx_energies_close(const float e_old[3], const float e_new[3], float threshold) {
+    return prx::energies_close(prx::V3{e_old[0], e_old[1], e_old[2]}, prx::V3{e_new[0], e_new[1], e_new[2]},
+                               threshold)
+               ? 1
+               : 0;
+}
+
+// photon_store.cpp:9-20
+prx_status prx_encode_path_info(uint32_t cell, uint32_t seg_count, uint32_t retrace_start, int replace,
+                                int reuse_light, uint32_t* word_out) {
+    return guarded([&] {
+        need(word_out, "word_out");
+        if (cell >= (1u << 22)) throw std::out_of_range("path info: cell id needs 22 bits");
+        if (seg_count < 1 || seg_count > 16) throw std::out_of_range("path info: segment count must be in 1..16");
+        if (retrace_start > 15) throw std::out_of_range("path info: retrace start must be in 0..15");
+        *word_out = prx::pack_path_info(cell, seg_count, retrace_start, replace != 0, reuse_light != 0);
+    });
+}
+
+void prx_decode_path_info(uint32_t word, uint32_t* cell, uint32_t* seg_count, uint32_t* retrace_start,
+                          int* replace, int* reuse_light) {
+    if (cell) *cell = word & ((1u << 22) - 1);
+    if (seg_count) *seg_count = ((word >> 22) & 0xF) + 1;
+    if (retrace_start) *retrace_start = (word >> 26) & 0xF;
+    if (replace) *replace = (word >> 30) & 1;
+    if (reuse_light) *reuse_light = (word >> 31) & 1;
+}
+
+// photon_store.cpp:38-54 (Table 1 of the paper)
+void prx_memory_footprint(uint64_t n_paths, uint32_t max_bounces, const uint32_t* dm_dims, uint32_t n_dims,
+                          int area_light, double out[7]) {
+    constexpr double kMiB = 1024.0 * 1024.0;
+    uint64_t cells = 1;
+    for (uint32_t i = 0; i < n_dims; ++i) cells *= dm_dims[i];
+    const double n = static_cast<double>(n_paths);
+    out[0] = 4.0 * n / kMiB;
+    out[1] = area_light ? 12.0 * n / kMiB : 0.0;
+    out[2] = 2.0 * 4.0 * static_cast<double>(cells) / kMiB;
+    out[3] = 4.0 * n / kMiB;
+    out[4] = 32.0 * n * max_bounces / kMiB;
+    out[5] = out[0] + out[1] + out[2] + out[3];
+    out[6] = out[5] + out[4];
+}
+
+prx_status prx_scene_create(const prx_scene_desc* desc, prx_scene** out) {
+    return guarded([&] {
+        need(desc, "desc");
+        need(out, "out");
+        auto s = std::make_unique<prx_scene>();
+        s->scene = std::make_shared<prx::Scene>(prx::scene_from_desc(*desc));
+        *out = s.release();
+    });
+}
+
+prx_status prx_scene_builtin(const char* name, prx_scene** out) {
+    return guarded([&] {
+        need(name, "name");
+        need(out, "out");
+        auto s = std::make_unique<prx_scene>();
+        s->scene = std::make_shared<prx::Scene>(prx::make_builtin_scene(name));
+        *out = s.release();
+    });
+}
+
+prx_status prx_scene_synthetic(const char* name, uint32_t n_dynamic, float tri_scale, prx_scene** out) {
+    return guarded([&] {
+        need(name, "name");
+        need(out, "out");
+        auto s = std::make_unique<prx_scene>();
+        s->scene = std::make_shared<prx::Scene>(prx::make_synthetic_scene(name, n_dynamic, tri_scale));
+        *out = s.release();
+    });
+}
+
+prx_status prx_scene_describe(const prx_scene* scene, prx_scene_desc* out) {
+    return guarded([&] {
+        need(scene, "scene");
+        need(out, "out");
+        const prx::Scene& s = *scene->scene;
+        out->objects = s.desc_objects.data();
+        out->n_objects = static_cast<uint32_t>(s.desc_objects.size());
+        out->lights = s.desc_lights.data();
+        out->n_lights = static_cast<uint32_t>(s.desc_lights.size());
+        out->camera.position = {s.camera.position.x, s.camera.position.y, s.camera.position.z};
+        out->camera.look_at = {s.camera.look_at.x, s.camera.look_at.y, s.camera.look_at.z};
+        out->camera.fov_deg = s.camera.fov_deg;
+        out->camera.width = s.camera.width;
+        out->camera.height = s.camera.height;
+        out->frames = s.frames;
+    });
+}
+
+prx_status prx_scene_bvh_permutation(const prx_scene* scene, uint32_t* out, size_t capacity, size_t* count) {
+    return guarded([&] {
+        need(scene, "scene");
+        need(count, "count");
+        const auto& perm = scene->scene->bvh_perm;
+        *count = perm.size();
+        if (out) std::memcpy(out, perm.data(), std::min(capacity, perm.size()) * 4);
+    });
+}
+
+prx_status prx_scene_counts(const prx_scene* scene, uint64_t counts[4]) {
+    return guarded([&] {
+        need(scene, "scene");
+        const prx::Scene& s = *scene->scene;
+        uint64_t dyn = 0;
+        for (const auto& o : s.objects)
+            if (o.dynamic) dyn += o.mesh.size();
+        counts[0] = s.static_tris.size();
+        counts[1] = dyn;
+        counts[2] = s.bvh_nodes.size();
+        counts[3] = s.objects.size();
+    });
+}
+
+float prx_scene_diagonal(const prx_scene* scene) { return scene ? scene->scene->diagonal() : 0.0f; }
+
+void prx_scene_destroy(prx_scene* scene) { delete scene; }
+
+prx_status prx_engine_create(const prx_scene* scene, const prx_config* cfg, prx_engine** out) {
+    return guarded([&] {
+        need(scene, "scene");
+        need(cfg, "cfg");
+        need(out, "out");
+        auto e = std::make_unique<prx_engine>();
+        e->engine = std::make_unique<prx::Engine>(scene->scene, *cfg);
+        *out = e.release();
+    });
+}
+
+void prx_engine_destroy(prx_engine* engine) { delete engine; }
+
+prx_status prx_engine_get_info(const prx_engine* engine, prx_engine_info* out) {
+    return guarded([&] {
+        need(engine, "engine");
+        need(out, "out");
+        engine->engine->info(out);
+    });
+}
+
+prx_status prx_run_frame(prx_engine* engine, prx_frame_stats* stats) {
+    return guarded([&] { eng(engine).run_frame(stats); });
+}
+prx_status prx_frame_update(prx_engine* engine, prx_frame_stats* stats) {
+    return guarded([&] { eng(engine).frame_update(stats); });
+}
+prx_status prx_verify_paths(prx_engine* engine, prx_frame_stats* stats) {
+    return guarded([&] { eng(engine).verify_paths(stats); });
+}
+prx_status prx_retrace_invalid(prx_engine* engine, prx_frame_stats* stats) {
+    return guarded([&] { eng(engine).retrace_invalid(stats); });
+}
+prx_status prx_run_stage(prx_engine* engine, int stage, prx_frame_stats* stats) {
+    return guarded([&] { eng(engine).run_stage(stage, stats); });
+}
+
+prx_status prx_engine_dm_current(prx_engine* engine, uint32_t light, void** dev_ptr, uint32_t* cells) {
+    return guarded([&] { eng(engine).dm_current_ptr(light, dev_ptr, cells); });
+}
+prx_status prx_prune_count(prx_engine* engine, uint32_t light, uint32_t* unmarked_out_dev) {
+    return guarded([&] { eng(engine).prune_count(light, unmarked_out_dev); });
+}
+prx_status prx_prune_apply(prx_engine* engine, uint32_t light, const uint32_t* prefix_dev,
+                           const uint32_t* total_dev, prx_frame_stats* stats) {
+    return guarded([&] { eng(engine).prune_apply(light, prefix_dev, total_dev, stats); });
+}
+prx_status prx_fill_count(prx_engine* engine, uint32_t light, uint32_t* dead_out) {
+    return guarded([&] { eng(engine).fill_count(light, dead_out); });
+}
+prx_status prx_fill_apply(prx_engine* engine, uint32_t light, uint64_t dead_prefix, uint64_t dead_total,
+                          prx_frame_stats* stats) {
+    return guarded([&] { eng(engine).fill_apply(light, dead_prefix, dead_total, stats); });
+}
+prx_status prx_engine_set_stream(prx_engine* engine, void* cuda_stream) {
+    return guarded([&] { eng(engine).set_stream(static_cast<cudaStream_t>(cuda_stream)); });
+}
+prx_status prx_engine_synchronize(prx_engine* engine) {
+    return guarded([&] { eng(engine).synchronize(); });
+}
+
+prx_status prx_splat(prx_engine* engine, const prx_camera* camera, float radius, int mode, float* rgb_out,
+                     float* rgb_dev, prx_frame_stats* stats) {
+    return guarded([&] { eng(engine).splat(camera, radius, mode, rgb_out, rgb_dev, stats); });
+}
+
+size_t prx_field_bytes(const prx_engine* engine, int field, uint32_t index) {
+    try {
+        if (!engine) return 0;
+        return engine->engine->field_bytes(field, index);
+    } catch (const std::exception& e) {
+        fail(e);
+        return 0;
+    }
+}
+
+prx_status prx_engine_download(prx_engine* engine, int field, uint32_t index, void* dst, size_t bytes) {
+    return guarded([&] {
+        if (bytes) need(dst, "dst");
+        eng(engine).download(field, index, dst, bytes);
+    });
+}
+
+prx_status prx_engine_upload(prx_engine* engine, int field, uint32_t index, const void* src, size_t bytes) {
+    return guarded([&] {
+        if (bytes) need(src, "src");
+        eng(engine).upload(field, index, src, bytes);
+    });
+}
+
+prx_status prx_engine_set_frame_counter(prx_engine* engine, int32_t frames_run) {
+    return guarded([&] { eng(engine).set_frame_counter(frames_run); });
+}
+
+uint64_t prx_engine_launch_count(const prx_engine* engine) {
+    return engine ? engine->engine->launches() : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,592 @@
+// device_scene.cuh -- device-side scene, traversal and light math of the B200 engine.
+//
+// Everything here is __device__ code compiled with --fmad=false and IEEE div/sqrt, in the
+// reference's operation order, so that the per-path results are bit-identical to the CPU
+// reference.  Tie rules of intersect_scene (scene.cpp:136-168):
+//   * static BVH first, visited in the reference tree's left-first DFS order with the
+//     double-precision node test against the shrinking t_max (bvh.cpp:79-106);
+//   * then every dynamic object in index order, gated by the double ray/box test of its
+//     current bounds with the already-shrunk t_max (scene.cpp:153-155);
+//   * inside a dynamic mesh the lexicographic minimum (t, triangle index) wins -- exactly
+//     what brute_force_intersect's strict `<` yields (bvh.cpp:108-117).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <float.h>
+#include <stdint.h>
+
+#include "dev_types.h"
+
+namespace prx {
+
+// --------------------------------------------------------------------------- rays
+struct Hit {
+    float t;
+    uint32_t obj;
+    V3 pos;
+    V3 normal;
+};
+
+__device__ __forceinline__ V3 ld3(const float4 v) { return V3{v.x, v.y, v.z}; }
+
+// Filtered exact ray/box test: a float slab test with a certified error margin decides
+// the clear cases; anything inside the margin falls back to the reference's double test
+// (ray_box_exact), so the boolean is always the reference's.
+struct RayPre {
+    V3 o, d;
+    float inv[3];
+    bool safe;  // all |d| components either 0 or large enough for the float filter
+};
+
+__device__ __forceinline__ RayPre make_ray(V3 o, V3 d) {
+    RayPre r;
+    r.o = o;
+    r.d = d;
+    r.safe = true;
+    for (int a = 0; a < 3; ++a) {
+        const float da = comp(d, a);
+        r.inv[a] = da != 0.0f ? 1.0f / da : 0.0f;
+        if (da != 0.0f && fabsf(da) < 1e-18f) r.safe = false;
+    }
+    return r;
+}
+
+__device__ __forceinline__ bool ray_box(const RayPre& r, float t_min, float t_max, const Box& b) {
+    if (!r.safe) return ray_box_exact(r.o, r.d, t_min, t_max, b);
+    // Float slab: each quotient q = (bound - o) / d is approximated by f = fl(fl(bound - o)
+    // * fl(1/d)), |f - q| <= 3 * 2^-24 * |f| (+ denormal slack).  The max/min over such
+    // values inherit the bound, so |t0_f - t0| + |t1_f - t1| <= 1.8e-7 (|t0_f| + |t1_f|).
+    float t0 = t_min, t1 = t_max;
+    for (int a = 0; a < 3; ++a) {
+        const float da = comp(r.d, a);
+        const float oa = comp(r.o, a);
+        const float lo = comp(b.lo, a), hi = comp(b.hi, a);
+        if (da == 0.0f) {
+            if (oa < lo || oa > hi) return false;
+            continue;
+        }
+        float tn = (lo - oa) * r.inv[a];
+        float tf = (hi - oa) * r.inv[a];
+        if (tn > tf) {
+            const float s = tn;
+            tn = tf;
+            tf = s;
+        }
+        t0 = fmax_std(t0, tn);
+        t1 = fmin_std(t1, tf);
+    }
+    // reference: miss iff t0 > t1 (double); decide only outside the certified band
+    const float slack = 4.0e-7f * (fabsf(t0) + fabsf(t1)) + 1e-30f;
+    if (t0 - t1 > slack) return false;
+    if (t1 - t0 > slack) return true;
+    return ray_box_exact(r.o, r.d, t_min, t_max, b);
+}
+
+// Static BVH closest hit (bvh.cpp:79-106) -- identical visit order, identical culling.
+__device__ __forceinline__ bool static_closest(const SceneDev& S, const RayPre& r, float t_min,
+                                               float& t_max, uint32_t& best) {
+    if (S.n_nodes == 0) return false;
+    uint32_t stack[64];
+    int sp = 0;
+    stack[sp++] = 0;
+    bool found = false;
+    while (sp > 0) {
+        const uint32_t ni = stack[--sp];
+        const float4 A = __ldg(&S.nodes[2 * ni]);
+        const float4 B = __ldg(&S.nodes[2 * ni + 1]);
+        const Box box{{A.x, A.y, A.z}, {B.x, B.y, B.z}};
+        if (!ray_box(r, t_min, t_max, box)) continue;
+        const uint32_t a = __float_as_uint(A.w), b = __float_as_uint(B.w);
+        if (a & kLeafBit) {
+            const uint32_t first = a & ~kLeafBit;
+            for (uint32_t i = first; i < first + b; ++i) {
+                const float4 ta = __ldg(&S.stris[3 * i]);
+                const float4 t1 = __ldg(&S.stris[3 * i + 1]);
+                const float4 t2 = __ldg(&S.stris[3 * i + 2]);
+                float t;
+                if (intersect_tri(r.o, r.d, t_min, t_max, ld3(ta), ld3(t1), ld3(t2), t)) {
+                    found = true;
+                    best = i;
+                    t_max = t;
+                }
+            }
+        } else {
+            stack[sp++] = b;  // right child
+            stack[sp++] = a;  // left child (popped first)
+        }
+    }
+    return found;
+}
+
+__device__ __forceinline__ bool static_any(const SceneDev& S, const RayPre& r, float t_min,
+                                           float t_max) {
+    if (S.n_nodes == 0) return false;
+    uint32_t stack[64];
+    int sp = 0;
+    stack[sp++] = 0;
+    while (sp > 0) {
+        const uint32_t ni = stack[--sp];
+        const float4 A = __ldg(&S.nodes[2 * ni]);
+        const float4 B = __ldg(&S.nodes[2 * ni + 1]);
+        const Box box{{A.x, A.y, A.z}, {B.x, B.y, B.z}};
+        if (!ray_box(r, t_min, t_max, box)) continue;
+        const uint32_t a = __float_as_uint(A.w), b = __float_as_uint(B.w);
+        if (a & kLeafBit) {
+            const uint32_t first = a & ~kLeafBit;
+            for (uint32_t i = first; i < first + b; ++i) {
+                const float4 ta = __ldg(&S.stris[3 * i]);
+                const float4 t1 = __ldg(&S.stris[3 * i + 1]);
+                const float4 t2 = __ldg(&S.stris[3 * i + 2]);
+                float t;
+                if (intersect_tri(r.o, r.d, t_min, t_max, ld3(ta), ld3(t1), ld3(t2), t)) return true;
+            }
+        } else {
+            stack[sp++] = b;
+            stack[sp++] = a;
+        }
+    }
+    return false;
+}
+
+// Conservative float slab for LBVH culling (no exactness needed: the result of the
+// object query is the lexicographic min (t, index), independent of visit order, so a
+// node may only be skipped when it provably holds no accepted triangle).
+__device__ __forceinline__ bool ray_box_conservative(const RayPre& r, float t_min, float t_max,
+                                                     float4 lo, float4 hi) {
+    float t0 = t_min, t1 = t_max;
+    for (int a = 0; a < 3; ++a) {
+        const float da = comp(r.d, a);
+        const float oa = comp(r.o, a);
+        const float l = a == 0 ? lo.x : (a == 1 ? lo.y : lo.z);
+        const float h = a == 0 ? hi.x : (a == 1 ? hi.y : hi.z);
+        if (da == 0.0f) {
+            if (oa < l || oa > h) return false;
+            continue;
+        }
+        if (!r.safe) continue;  // no culling on an axis the float filter cannot bound
+        float tn = (l - oa) * r.inv[a];
+        float tf = (h - oa) * r.inv[a];
+        if (tn > tf) {
+            const float s = tn;
+            tn = tf;
+            tf = s;
+        }
+        t0 = fmax_std(t0, tn);
+        t1 = fmin_std(t1, tf);
+    }
+    return t0 - t1 <= 2.0e-6f * (fabsf(t0) + fabsf(t1)) + 1e-30f;
+}
+
+
+// Closest hit inside one dynamic object: the (t, index)-lexicographic minimum over its
+// triangles with t in (t_min, t_max) -- brute_force_intersect's result (bvh.cpp:108-117).
+__device__ __forceinline__ bool dyn_closest(const SceneDev& S, const DynObj& D, const RayPre& r,
+                                            float t_min, float& t_max, uint32_t& best_tri) {
+    bool found = false;
+    const float4* T = S.dtris + 3ull * D.tri_begin;
+    if (D.node_begin == kLbvhBrute) {
+        for (uint32_t i = 0; i < D.tri_count; ++i) {
+            float t;
+            if (intersect_tri(r.o, r.d, t_min, t_max, ld3(__ldg(&T[3 * i])), ld3(__ldg(&T[3 * i + 1])),
+                              ld3(__ldg(&T[3 * i + 2])), t)) {
+                found = true;
+                best_tri = i;
+                t_max = t;
+            }
+        }
+        return found;
+    }
+    // LBVH: nodes[node_begin + k], k < tri_count - 1 internal; children with kLeafBit are
+    // leaves (index into the sorted leaf list).  Node = {lmin,l} {lmax,-} {rmin,r} {rmax,-}.
+    const float4* N = S.dnodes + 4ull * D.node_begin;
+    const uint32_t* L = S.dleaf + D.tri_begin;
+    const float t_in = t_max;  // acceptance window is (t_min, t_in); ties -> lower index
+    float best_t = t_in;
+    uint32_t bi = 0xFFFFFFFFu;
+    uint32_t stack[64];
+    int sp = 0;
+    if (D.tri_count == 1) {
+        stack[sp++] = kLeafBit | 0;
+    } else {
+        stack[sp++] = 0;
+    }
+    while (sp > 0) {
+        const uint32_t c = stack[--sp];
+        if (c & kLeafBit) {
+            const uint32_t i = L[c & ~kLeafBit];
+            float t;
+            // accept t < t_in; replace if t < best_t or (t == best_t and lower index)
+            if (intersect_tri(r.o, r.d, t_min, t_in, ld3(__ldg(&T[3 * i])), ld3(__ldg(&T[3 * i + 1])),
+                              ld3(__ldg(&T[3 * i + 2])), t)) {
+                if (t < best_t || (t == best_t && i < bi)) {
+                    best_t = t;
+                    bi = i;
+                }
+            }
+            continue;
+        }
+        const float4 lmin = __ldg(&N[4 * c]), lmax = __ldg(&N[4 * c + 1]);
+        const float4 rmin = __ldg(&N[4 * c + 2]), rmax = __ldg(&N[4 * c + 3]);
+        const bool hl = ray_box_conservative(r, t_min, best_t, lmin, lmax);
+        const bool hr = ray_box_conservative(r, t_min, best_t, rmin, rmax);
+        if (hr) stack[sp++] = __float_as_uint(rmin.w);
+        if (hl) stack[sp++] = __float_as_uint(lmin.w);
+    }
+    if (bi != 0xFFFFFFFFu) {
+        best_tri = bi;
+        t_max = best_t;
+        return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool dyn_any(const SceneDev& S, const DynObj& D, const RayPre& r,
+                                        float t_min, float t_max) {
+    const float4* T = S.dtris + 3ull * D.tri_begin;
+    if (D.node_begin == kLbvhBrute) {
+        for (uint32_t i = 0; i < D.tri_count; ++i) {
+            float t;
+            if (intersect_tri(r.o, r.d, t_min, t_max, ld3(__ldg(&T[3 * i])), ld3(__ldg(&T[3 * i + 1])),
+                              ld3(__ldg(&T[3 * i + 2])), t))
+                return true;
+        }
+        return false;
+    }
+    const float4* N = S.dnodes + 4ull * D.node_begin;
+    const uint32_t* L = S.dleaf + D.tri_begin;
+    uint32_t stack[64];
+    int sp = 0;
+    stack[sp++] = D.tri_count == 1 ? (kLeafBit | 0) : 0;
+    while (sp > 0) {
+        const uint32_t c = stack[--sp];
+        if (c & kLeafBit) {
+            const uint32_t i = L[c & ~kLeafBit];
+            float t;
+            if (intersect_tri(r.o, r.d, t_min, t_max, ld3(__ldg(&T[3 * i])), ld3(__ldg(&T[3 * i + 1])),
+                              ld3(__ldg(&T[3 * i + 2])), t))
+                return true;
+            continue;
+        }
+        const float4 lmin = __ldg(&N[4 * c]), lmax = __ldg(&N[4 * c + 1]);
+        const float4 rmin = __ldg(&N[4 * c + 2]), rmax = __ldg(&N[4 * c + 3]);
+        if (ray_box_conservative(r, t_min, t_max, rmin, rmax)) stack[sp++] = __float_as_uint(rmin.w);
+        if (ray_box_conservative(r, t_min, t_max, lmin, lmax)) stack[sp++] = __float_as_uint(lmin.w);
+    }
+    return false;
+}
+
+// intersect_scene (scene.cpp:136-168)
+__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min,
+                                                Hit& h) {
+    const RayPre r = make_ray(o, d);
+    float t_max = FLT_MAX;
+    uint32_t sbest = 0;
+    bool found = static_closest(S, r, t_min, t_max, sbest);
+    int kind = found ? 0 : -1;  // 0 static, 1 dynamic
+    uint32_t dj = 0, dtri = 0;
+    const FrameParams* fp = S.fp;
+    const uint32_t n_dyn = fp->n_dyn;
+    for (uint32_t j = 0; j < n_dyn; ++j) {
+        const DynObj D = fp->dyn[j];
+        if (!ray_box_exact(o, d, t_min, t_max, D.cur)) continue;
+        uint32_t bt;
+        if (dyn_closest(S, D, r, t_min, t_max, bt)) {
+            kind = 1;
+            dj = j;
+            dtri = bt;
+        }
+    }
+    if (kind < 0) return false;
+    V3 e1, e2;
+    if (kind == 0) {
+        const float4 q1 = __ldg(&S.stris[3 * sbest + 1]);
+        const float4 q2 = __ldg(&S.stris[3 * sbest + 2]);
+        e1 = ld3(q1);
+        e2 = ld3(q2);
+        h.obj = __float_as_uint(q1.w);
+    } else {
+        const DynObj& D = fp->dyn[dj];
+        const float4* T = S.dtris + 3ull * (D.tri_begin + dtri);
+        e1 = ld3(__ldg(&T[1]));
+        e2 = ld3(__ldg(&T[2]));
+        h.obj = D.obj;
+    }
+    h.t = t_max;
+    h.pos = add(o, mul(d, t_max));
+    V3 n = normalized(cross(e1, e2));  // Triangle::geometric_normal (geometry.hpp:64)
+    if (dot(n, d) > 0.0f) n = neg(n);
+    h.normal = n;
+    return true;
+}
+
+// occluded (scene.cpp:170-177)
+__device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_min, float t_max) {
+    const RayPre r = make_ray(o, d);
+    if (static_any(S, r, t_min, t_max)) return true;
+    const FrameParams* fp = S.fp;
+    for (uint32_t j = 0; j < fp->n_dyn; ++j) {
+        const DynObj D = fp->dyn[j];
+        if (!ray_box_exact(o, d, t_min, t_max, D.cur)) continue;
+        if (dyn_any(S, D, r, t_min, t_max)) return true;
+    }
+    return false;
+}
+
+// --------------------------------------------------------------------------- bounces
+// cosine_sample (engine.cpp:25-32); cos/sin(phi) come from the host-libm table when
+// available (phi = fl(2pi_f) * k * 2^-24 is a function of the 24-bit draw k).
+__device__ __forceinline__ V3 cosine_sample(const SceneDev& S, V3 normal, float u1, uint32_t k2) {
+    const float u2 = (float)k2 * 5.9604644775390625e-8f;
+    const float r = sqrtf(u1);
+    float cphi, sphi;
+    if (S.trig) {
+        const float2 cs = __ldg(&S.trig[k2]);
+        cphi = cs.x;
+        sphi = cs.y;
+    } else {
+        const float phi = 2.0f * 3.14159265358979323846f * u2;
+        cphi = cosf(phi);
+        sphi = sinf(phi);
+    }
+    const float z = sqrtf(fmax_std(0.0f, 1.0f - u1));
+    V3 t, b;
+    orthonormal_basis(normal, t, b);
+    return normalized(add(add(mul(t, r * cphi), mul(b, r * sphi)), mul(normal, z)));
+}
+
+// phong_lobe_sample (engine.cpp:34-42) -- glossy only (device powf: tolerance class C)
+__device__ __forceinline__ V3 phong_sample(const SceneDev& S, V3 mirror, float exponent, float u1,
+                                           uint32_t k2) {
+    const float u2 = (float)k2 * 5.9604644775390625e-8f;
+    const float cos_theta = powf(u1, 1.0f / (exponent + 1.0f));
+    const float sin_theta = sqrtf(fmax_std(0.0f, 1.0f - cos_theta * cos_theta));
+    float cphi, sphi;
+    if (S.trig) {
+        const float2 cs = __ldg(&S.trig[k2]);
+        cphi = cs.x;
+        sphi = cs.y;
+    } else {
+        const float phi = 2.0f * 3.14159265358979323846f * u2;
+        cphi = cosf(phi);
+        sphi = sinf(phi);
+    }
+    V3 t, b;
+    orthonormal_basis(mirror, t, b);
+    return normalized(add(add(mul(t, sin_theta * cphi), mul(b, sin_theta * sphi)), mul(mirror, cos_theta)));
+}
+
+// Engine::sample_bounce (engine.cpp:159-170)
+__device__ __forceinline__ V3 sample_bounce(const SceneDev& S, uint32_t obj, V3 normal, V3 incoming,
+                                            uint32_t path, uint32_t epoch, uint32_t bounce_key) {
+    const float u1 = rng_uniform_m(S.seed_mix, path, epoch, bounce_key, kBounceDir, 0);
+    const uint32_t k2 = rng_u24_m(S.seed_mix, path, epoch, bounce_key, kBounceDir, 1);
+    const uint32_t flags = __ldg(&S.oflags[obj]);
+    if (!(flags & 2u)) return cosine_sample(S, normal, u1, k2);
+    const float4 m = __ldg(&S.mat[obj]);
+    const V3 mirror = normalized(sub(incoming, mul(normal, 2.0f * dot(incoming, normal))));
+    V3 out = phong_sample(S, mirror, m.w, u1, k2);
+    if (dot(out, normal) <= 0.0f) out = mirror;
+    return out;
+}
+
+// --------------------------------------------------------------------------- lights
+__device__ __forceinline__ double wrap_unit(double v) {  // light.cpp:49-53
+    v -= floor(v);
+    if (v >= 1.0) v = 0.0;
+    return v;
+}
+
+__device__ __forceinline__ double dclamp(double v, double lo, double hi) {
+    return (v < lo) ? lo : ((hi < v) ? hi : v);
+}
+
+// dir_from_angles (light.cpp:40-47)
+__device__ __forceinline__ V3 dir_from_angles(const LightDev& L, double cos_theta, double phi) {
+    const double sin_theta = sqrt(dmax_std(0.0, 1.0 - cos_theta * cos_theta));
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    const double cx = cp * sin_theta;
+    const double cy = sp * sin_theta;
+    return normalized(add(add(mul(L.tangent, (float)cx), mul(L.bitangent, (float)cy)),
+                          mul(L.normal, (float)cos_theta)));
+}
+
+// warp_canonical (light.cpp:70-117): canonical coords -> (origin, dir)
+__device__ __forceinline__ void warp_canonical(const LightDev& L, const float c[4], V3& origin,
+                                               V3& dir) {
+    switch (L.kind) {
+        case PRX_LIGHT_POINT: {
+            const double cos_theta = 1.0 - 2.0 * (double)c[0];
+            origin = L.position;
+            dir = dir_from_angles(L, cos_theta, kTwoPiD * (double)c[1]);
+            break;
+        }
+        case PRX_LIGHT_SPOT: {
+            const double cos_theta = 1.0 - (double)c[0] * (1.0 - L.cos_half);
+            origin = L.position;
+            dir = dir_from_angles(L, cos_theta, kTwoPiD * (double)c[1]);
+            break;
+        }
+        case PRX_LIGHT_DISC_AREA: {
+            const double r_max = (double)L.radius * (double)L.scale;
+            const double r = r_max * sqrt((double)c[0]);
+            const double phi_s = kTwoPiD * (double)c[1];
+            double sp, cp;
+            sincos(phi_s, &sp, &cp);
+            origin = add(add(L.position, mul(L.tangent, (float)(r * cp))), mul(L.bitangent, (float)(r * sp)));
+            const double cos_theta = sqrt(dmax_std(0.0, 1.0 - (double)c[2]));
+            dir = dir_from_angles(L, cos_theta, kTwoPiD * (double)c[3]);
+            break;
+        }
+        default: {  // rect
+            const float hx = L.half_x * L.scale;
+            const float hy = L.half_y * L.scale;
+            origin = add(add(L.position, mul(L.tangent, (2.0f * c[0] - 1.0f) * hx)),
+                         mul(L.bitangent, (2.0f * c[1] - 1.0f) * hy));
+            const double cos_theta = sqrt(dmax_std(0.0, 1.0 - (double)c[2]));
+            dir = dir_from_angles(L, cos_theta, kTwoPiD * (double)c[3]);
+            break;
+        }
+    }
+}
+
+// canonical_of (light.cpp:119-175); returns false when the configuration does not
+// parametrise (off-surface / outside the emission domain).
+__device__ __forceinline__ bool canonical_of(const LightDev& L, V3 origin, V3 dir, float c[4]) {
+    c[0] = c[1] = c[2] = c[3] = 0.0f;
+    const double dn = dot(dir, L.normal);
+    const double dt = dot(dir, L.tangent);
+    const double db = dot(dir, L.bitangent);
+    const double phi = wrap_unit(atan2(db, dt) / kTwoPiD);
+    const double kTol = 1e-4;
+    switch (L.kind) {
+        case PRX_LIGHT_POINT:
+            c[0] = (float)dclamp((1.0 - dn) / 2.0, 0.0, 1.0);
+            c[1] = (float)phi;
+            return true;
+        case PRX_LIGHT_SPOT: {
+            const double q = (1.0 - dn) / (1.0 - L.cos_half);
+            if (q < 0.0 || q > 1.0) return false;
+            c[0] = (float)dmin_std(q, 1.0);
+            c[1] = (float)phi;
+            return true;
+        }
+        default: {
+            const V3 rel = sub(origin, L.position);
+            const double lz = dot(rel, L.normal);
+            const double lx = dot(rel, L.tangent);
+            const double ly = dot(rel, L.bitangent);
+            if (L.kind == PRX_LIGHT_DISC_AREA) {
+                const double r_max = (double)L.radius * (double)L.scale;
+                if (fabs(lz) > kTol * r_max) return false;
+                const double q = (lx * lx + ly * ly) / (r_max * r_max);
+                if (q > 1.0 + kTol) return false;
+                c[0] = (float)dmin_std(q, 1.0);
+                c[1] = (float)wrap_unit(atan2(ly, lx) / kTwoPiD);
+            } else {
+                const double hx = (double)L.half_x * (double)L.scale;
+                const double hy = (double)L.half_y * (double)L.scale;
+                if (fabs(lz) > kTol * dmax_std(hx, hy)) return false;
+                const double u = (lx / hx + 1.0) / 2.0;
+                const double v = (ly / hy + 1.0) / 2.0;
+                if (u < -kTol || u > 1.0 + kTol || v < -kTol || v > 1.0 + kTol) return false;
+                c[0] = (float)dclamp(u, 0.0, 1.0);
+                c[1] = (float)dclamp(v, 0.0, 1.0);
+            }
+            if (dn <= 0.0) return false;
+            c[2] = (float)dclamp(1.0 - dn * dn, 0.0, 1.0);
+            c[3] = (float)phi;
+            return true;
+        }
+    }
+}
+
+// cell_of_canonical (light.cpp:177-186)
+__device__ __forceinline__ uint32_t cell_of(const LightDev& L, const float c[4]) {
+    uint32_t cell = 0;
+    for (uint32_t a = 0; a < L.ndims; ++a) {
+        const uint32_t dim = L.dims[a];
+        uint32_t idx = (uint32_t)(c[a] * (float)dim);
+        if (idx >= dim) idx = dim - 1;
+        cell = cell * dim + idx;
+    }
+    return cell;
+}
+
+// sample_in_cell (light.cpp:211-228) with key {path, epoch, 0, Emission, lane 0}
+__device__ __forceinline__ void sample_in_cell(const LightDev& L, uint32_t cell, uint64_t seed_mix,
+                                               uint32_t path, uint32_t epoch, float c[4], V3& origin,
+                                               V3& dir) {
+    float lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+    uint32_t rest = cell;
+    for (int a = (int)L.ndims - 1; a >= 0; --a) {
+        const uint32_t dim = L.dims[a];
+        const uint32_t idx = rest % dim;
+        rest /= dim;
+        lo[a] = (float)idx / (float)dim;
+        hi[a] = (float)(idx + 1) / (float)dim;
+    }
+    c[0] = c[1] = c[2] = c[3] = 0.0f;
+    for (uint32_t a = 0; a < L.ndims; ++a) {
+        const double u = rng_uniform_d_m(seed_mix, path, epoch, 0, kEmission, a);
+        const double width = (double)hi[a] - (double)lo[a];
+        const double m0 = 2e-5 / width;
+        const double margin = (m0 < 0.4) ? m0 : 0.4;
+        const double t = margin + u * (1.0 - 2.0 * margin);
+        c[a] = (float)((double)lo[a] + t * width);
+    }
+    warp_canonical(L, c, origin, dir);
+}
+
+__device__ __forceinline__ uint32_t light_of(const FrameParams* fp, uint32_t p) {
+    uint32_t li = 0;
+    for (uint32_t k = 1; k < fp->n_lights; ++k)
+        if (p >= fp->lights[k].begin) li = k;
+    return li;
+}
+
+}  // namespace prx
+
+namespace prx {
+
+// segment_intersects_aabb (geometry.hpp:107-134), filtered: a float slab test with a
+// certified margin decides clear cases; borderline cases run the reference's double test.
+__device__ __forceinline__ bool segment_box(V3 a, V3 b, const Box& box) {
+    bool swap;
+    if (b.x != a.x) swap = b.x < a.x;
+    else if (b.y != a.y) swap = b.y < a.y;
+    else swap = b.z < a.z;
+    if (swap) {
+        const V3 t = a;
+        a = b;
+        b = t;
+    }
+    float t0 = 0.0f, t1 = 1.0f;
+    for (int axis = 0; axis < 3; ++axis) {
+        const float o = comp(a, axis), e = comp(b, axis);
+        const float lo = comp(box.lo, axis), hi = comp(box.hi, axis);
+        if (o == e) {  // d == 0 in double as well
+            if (o < lo || o > hi) return false;
+            continue;
+        }
+        const float d = e - o;
+        if (fabsf(d) < 1e-30f) return segment_box_exact(a, b, box);
+        const float inv = 1.0f / d;
+        float tn = (lo - o) * inv;
+        float tf = (hi - o) * inv;
+        if (tn > tf) {
+            const float s = tn;
+            tn = tf;
+            tf = s;
+        }
+        t0 = fmax_std(t0, tn);
+        t1 = fmin_std(t1, tf);
+    }
+    // each quotient carries <= 4 roundings (2.4e-7 relative) vs the double reference
+    const float slack = 6.0e-7f * (fabsf(t0) + fabsf(t1)) + 1e-30f;
+    if (t0 - t1 > slack) return false;
+    if (t1 - t0 > slack) return true;
+    return segment_box_exact(a, b, box);
+}
+
+}  // namespace prx

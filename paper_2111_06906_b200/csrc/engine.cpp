@@ -1,0 +1,980 @@
+// engine.cpp -- host orchestration of the B200 path-reuse engine (see engine.h).
+//
+// Compiled by the host compiler without -march/fast-math: the keyframe, light-pose and
+// box arithmetic done here matches the reference's host arithmetic bit for bit.
+#include "engine.h"
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numbers>
+#include <thread>
+
+#include "prims.h"
+
+namespace prx {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                        cudaGetErrorString(e) + ") at " + what);
+}
+
+void DevBuf::alloc(size_t bytes) {
+    reset();
+    if (bytes == 0) return;
+    PRX_CUDA(cudaMalloc(&p_, bytes));
+    n_ = bytes;
+}
+
+void DevBuf::reset() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+}
+
+namespace {
+
+enum { kCntTrim = 0, kCntPruned = 1, kCntRetrace = 2, kCntDead = 3, kCntNeed = 4, kCntN = 8 };
+enum {
+    kEvFrame0 = 0,
+    kEvVerify0 = 1,
+    kEvOccl0 = 2,
+    kEvDm0 = 3,
+    kEvPrune0 = 4,
+    kEvFill0 = 5,
+    kEvTrace0 = 6,
+    kEvEnd = 7,
+    kEvSplat0 = 8,
+    kEvSplat1 = 9
+};
+
+float4 f4(V3 v, float w) { return float4{v.x, v.y, v.z, w}; }
+float f_of_u(uint32_t u) {
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------- exact trig table
+// cosine_sample draws phi = fl(2*pi_f) * (k * 2^-24) and evaluates cos/sin with the host
+// libm (sincosf after GCC's sin/cos CSE).  The device looks the pair up by k, so bounce
+// directions are bit-identical to the reference on the same host libm.
+const float2* exact_trig_table(int device) {
+    static std::mutex mu;
+    static std::vector<float2> host;
+    static std::map<int, float2*> dev;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = dev.find(device);
+    if (it != dev.end()) return it->second;
+    constexpr uint32_t kN = 1u << 24;
+    if (host.empty()) {
+        host.resize(kN);
+        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t) {
+            th.emplace_back([t, nt] {
+                const uint32_t lo = static_cast<uint32_t>((uint64_t)kN * t / nt);
+                const uint32_t hi = static_cast<uint32_t>((uint64_t)kN * (t + 1) / nt);
+                for (uint32_t k = lo; k < hi; ++k) {
+                    const float u2 = static_cast<float>(k) * 0x1.0p-24f;
+                    const float phi = 2.0f * std::numbers::pi_v<float> * u2;
+                    float s, c;
+                    ::sincosf(phi, &s, &c);
+                    host[k] = float2{c, s};
+                }
+            });
+        }
+        for (auto& x : th) x.join();
+    }
+    int prev = 0;
+    PRX_CUDA(cudaGetDevice(&prev));
+    PRX_CUDA(cudaSetDevice(device));
+    float2* d = nullptr;
+    PRX_CUDA(cudaMalloc(&d, sizeof(float2) * kN));
+    PRX_CUDA(cudaMemcpy(d, host.data(), sizeof(float2) * kN, cudaMemcpyHostToDevice));
+    PRX_CUDA(cudaSetDevice(prev));
+    dev[device] = d;
+    return d;
+}
+
+// ----------------------------------------------------------------------- construction
+Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
+    : scene_(std::move(scene)), cfg_(cfg) {
+    // engine.cpp:64-72
+    if (cfg_.n_paths == 0) throw std::invalid_argument("engine: n_paths must be positive");
+    if (cfg_.max_bounces < 1 || cfg_.max_bounces > 16)
+        throw std::invalid_argument("engine: max_bounces must be in 1..16");
+    if (scene_->lights.empty()) throw std::invalid_argument("engine: scene has no lights");
+    if (cfg_.mode < PRX_MODE_BASELINE || cfg_.mode > PRX_MODE_ERROR)
+        throw std::invalid_argument("engine: unknown mode");
+    n_total_ = cfg_.n_paths;
+    sb_ = cfg_.shard_begin;
+    se_ = cfg_.shard_end;
+    if (sb_ == 0 && se_ == 0) se_ = n_total_;
+    if (sb_ >= se_ || se_ > n_total_) throw std::invalid_argument("engine: bad shard range");
+    n_ = se_ - sb_;
+    B_ = cfg_.max_bounces;
+    device_ = cfg_.device;
+    eps_ = 1e-4f * scene_->diagonal();
+    diag_ = scene_->diagonal();
+    seed_mix_ = mix64(cfg_.seed);
+
+    PRX_CUDA(cudaSetDevice(device_));
+    PRX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    for (auto& e : ev_) PRX_CUDA(cudaEventCreate(&e));
+    launch_base_ = g_launches;
+
+    // light blocks (engine.cpp:76-101)
+    const uint32_t nl = static_cast<uint32_t>(scene_->lights.size());
+    const uint32_t base = n_total_ / nl, extra = n_total_ % nl;
+    uint32_t next = 0;
+    lights_.resize(nl);
+    for (uint32_t li = 0; li < nl; ++li) {
+        LightBlock& b = lights_[li];
+        b.light = &scene_->lights[li];
+        const uint32_t count = base + (li < extra ? 1u : 0u);
+        if (count == 0) throw std::invalid_argument("engine: fewer paths than lights");
+        b.begin = next;
+        b.end = next + count;
+        next = b.end;
+        if (b.light->param_dims() == 4) {
+            b.ndims = 4;
+            for (int a = 0; a < 4; ++a) b.dims[a] = cfg_.dm_dims[a];
+        } else {
+            b.ndims = 2;
+            b.dims[0] = cfg_.dm_dims[2];
+            b.dims[1] = cfg_.dm_dims[3];
+        }
+        uint64_t cells = 1;
+        for (uint32_t a = 0; a < b.ndims; ++a) {
+            if (b.dims[a] == 0) throw std::invalid_argument("init_dm_target: zero-sized DM axis");
+            cells *= b.dims[a];
+        }
+        if (cells > (1u << 22)) throw std::invalid_argument("init_dm_target: more than 2^22 DM cells");
+        b.cells = static_cast<uint32_t>(cells);
+        max_cells_ = std::max(max_cells_, b.cells);
+        // flux_per_path = flux / sum(DM_T); every draw lands in a cell so the sum is `count`
+        const float binned = static_cast<float>(static_cast<double>(count));
+        b.flux_pp = divs(b.light->flux, binned);
+        b.cos_half = std::cos(static_cast<double>(b.light->cone_angle_deg) * std::numbers::pi / 360.0);
+        b.pose_now = light_pose_at(*b.light, 0);
+        b.pose_prev = b.pose_now;
+        b.dm_t.alloc(4ull * b.cells);
+        b.dm_c.alloc(4ull * b.cells);
+        b.unm.alloc(4ull * b.cells);
+        b.seg_start.alloc(4ull * b.cells);
+        PRX_CUDA(cudaMemsetAsync(b.dm_t.get(), 0, 4ull * b.cells, stream_));
+        PRX_CUDA(cudaMemsetAsync(b.dm_c.get(), 0, 4ull * b.cells, stream_));
+    }
+
+    PRX_CUDA(cudaMallocHost(&h_fp_, sizeof(FrameParams)));
+    std::memset(h_fp_, 0, sizeof(FrameParams));
+    d_fp_.alloc(sizeof(FrameParams));
+    PRX_CUDA(cudaMallocHost(&h_ctr_, sizeof(Counters)));
+    PRX_CUDA(cudaMallocHost(&h_cnt32_, 4 * kCntN));
+    d_ctr_.alloc(sizeof(Counters));
+    d_cnt32_.alloc(4 * kCntN);
+    PRX_CUDA(cudaMemsetAsync(d_ctr_.get(), 0, sizeof(Counters), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_cnt32_.get(), 0, 4 * kCntN, stream_));
+
+    upload_scene();
+    alloc_state();
+    if (cfg_.exact_trig >= 0) d_trig_ = exact_trig_table(device_);
+
+    // DM_T (init_dm_target, light.cpp:230-252), keyed by the sample index within the block
+    fill_frame_params();
+    for (uint32_t li = 0; li < nl; ++li)
+        launch_init_dm_target(&h_fp_->lights[li], lights_[li].end - lights_[li].begin, seed_mix_,
+                              lights_[li].dm_t.as<uint32_t>(), stream_);
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+}
+
+Engine::~Engine() {
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (h_fp_) cudaFreeHost(h_fp_);
+    if (h_ctr_) cudaFreeHost(h_ctr_);
+    if (h_cnt32_) cudaFreeHost(h_cnt32_);
+    if (h_xf_) cudaFreeHost(h_xf_);
+    if (stream_ && own_stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::upload_scene() {
+    const Scene& s = *scene_;
+    // static BVH nodes: {lo, a} {hi, b}; leaf: a = first | leaf bit, b = count
+    const size_t nn = s.bvh_nodes.size();
+    if (nn) {
+        std::vector<float4> nodes(2 * nn);
+        for (size_t i = 0; i < nn; ++i) {
+            const BvhNode& n = s.bvh_nodes[i];
+            const uint32_t a = n.count ? (n.first | kLeafBit) : n.left;
+            const uint32_t b = n.count ? n.count : n.first;
+            nodes[2 * i] = f4(n.bounds.lo, f_of_u(a));
+            nodes[2 * i + 1] = f4(n.bounds.hi, f_of_u(b));
+        }
+        d_nodes_.alloc(sizeof(float4) * nodes.size());
+        PRX_CUDA(cudaMemcpy(d_nodes_.get(), nodes.data(), d_nodes_.size(), cudaMemcpyHostToDevice));
+        std::vector<float4> tris(3 * s.bvh_perm.size());
+        for (size_t k = 0; k < s.bvh_perm.size(); ++k) {
+            const uint32_t orig = s.bvh_perm[k];
+            const Tri& t = s.static_tris[orig];
+            tris[3 * k] = f4(t.a, f_of_u(orig));
+            tris[3 * k + 1] = f4(sub(t.b, t.a), f_of_u(s.static_tri_obj[orig]));
+            tris[3 * k + 2] = f4(sub(t.c, t.a), 0.0f);
+        }
+        d_stris_.alloc(sizeof(float4) * tris.size());
+        PRX_CUDA(cudaMemcpy(d_stris_.get(), tris.data(), d_stris_.size(), cudaMemcpyHostToDevice));
+    }
+    // materials / flags
+    std::vector<float4> mat(s.objects.size());
+    std::vector<uint32_t> flags(s.objects.size());
+    for (size_t i = 0; i < s.objects.size(); ++i) {
+        const Object& o = s.objects[i];
+        mat[i] = f4(o.material.albedo, o.material.glossy_exponent);
+        flags[i] = (o.dynamic ? 1u : 0u) | (o.material.kind == PRX_MATERIAL_GLOSSY ? 2u : 0u);
+    }
+    d_mat_.alloc(sizeof(float4) * mat.size());
+    d_oflags_.alloc(4 * flags.size());
+    PRX_CUDA(cudaMemcpy(d_mat_.get(), mat.data(), d_mat_.size(), cudaMemcpyHostToDevice));
+    PRX_CUDA(cudaMemcpy(d_oflags_.get(), flags.data(), d_oflags_.size(), cudaMemcpyHostToDevice));
+    // dynamic meshes (object-local), per-triangle transform slot
+    std::vector<float4> local;
+    std::vector<uint32_t> tri_xf;
+    uint32_t tri = 0, nodes_total = 0;
+    for (const Object& o : s.objects) {
+        if (!o.dynamic) continue;
+        if (dyn_.size() >= static_cast<size_t>(kMaxDyn))
+            throw std::invalid_argument("engine: more than 128 dynamic objects");
+        DynInfo d;
+        d.obj = o.id;
+        d.tri_begin = tri;
+        d.tri_count = static_cast<uint32_t>(o.mesh.size());
+        if (d.tri_count > 32) {  // LBVH for anything beyond a few boxes
+            d.node_begin = nodes_total;
+            nodes_total += d.tri_count - 1;
+        }
+        for (const Tri& t : o.mesh) {
+            local.push_back(f4(t.a, 0));
+            local.push_back(f4(t.b, 0));
+            local.push_back(f4(t.c, 0));
+            tri_xf.push_back(static_cast<uint32_t>(dyn_.size()));
+        }
+        tri += d.tri_count;
+        dyn_.push_back(d);
+    }
+    n_dyn_tris_ = tri;
+    n_lbvh_nodes_ = nodes_total;
+    if (tri) {
+        d_dyn_local_.alloc(sizeof(float4) * local.size());
+        d_dyn_world_.alloc(sizeof(float4) * local.size());
+        d_dyn_tri_xf_.alloc(4 * tri_xf.size());
+        d_dyn_xf_.alloc(sizeof(float4) * 2 * dyn_.size());
+        PRX_CUDA(cudaMallocHost(&h_xf_, sizeof(float4) * 2 * kMaxDyn));
+        PRX_CUDA(cudaMemcpy(d_dyn_local_.get(), local.data(), d_dyn_local_.size(), cudaMemcpyHostToDevice));
+        PRX_CUDA(cudaMemcpy(d_dyn_tri_xf_.get(), tri_xf.data(), d_dyn_tri_xf_.size(), cudaMemcpyHostToDevice));
+        d_lbvh_leaf_.alloc(4ull * tri);
+        if (nodes_total) {
+            d_lbvh_nodes_.alloc(sizeof(float4) * 4ull * nodes_total);
+            const size_t n = tri;
+            const size_t scratch = prim_scratch_bytes(n);
+            d_lbvh_work_.alloc(4 * n * 4 + 4 * (2 * n + 2) * 2 + scratch);
+            uint32_t* w = d_lbvh_work_.as<uint32_t>();
+            lbvh_.keys = w;
+            lbvh_.vals = w + n;
+            lbvh_.keys_tmp = w + 2 * n;
+            lbvh_.vals_tmp = w + 3 * n;
+            lbvh_.parent = w + 4 * n;
+            lbvh_.flags = w + 4 * n + (2 * n + 2);
+            lbvh_.scratch = w + 4 * n + 2 * (2 * n + 2);
+        }
+    }
+}
+
+void Engine::alloc_state() {
+    const size_t nv = static_cast<size_t>(n_) * B_;
+    d_pos_obj_.alloc(16 * nv);
+    d_energy_.alloc(16 * nv);
+    d_in_dir_.alloc(16 * nv);
+    d_out_dir_.alloc(16 * nv);
+    d_origin_.alloc(16ull * n_);
+    d_emis_.alloc(16ull * n_);
+    d_canon_.alloc(16ull * n_);
+    d_cell_.alloc(4ull * n_);
+    d_epoch_.alloc(4ull * n_);
+    d_path_info_.alloc(4ull * n_);
+    d_seg_flags_.alloc(4ull * n_);
+    d_meta_.alloc(4ull * n_);
+    d_rstart_.alloc(n_);
+    // reference initial state (engine.cpp:104-116): empty photons, emission dir (0,0,1),
+    // everything else zero, status dead, retrace 0xFF
+    PRX_CUDA(cudaMemsetAsync(d_pos_obj_.get(), 0, d_pos_obj_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_energy_.get(), 0, d_energy_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_in_dir_.get(), 0, d_in_dir_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_out_dir_.get(), 0, d_out_dir_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_origin_.get(), 0, d_origin_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_canon_.get(), 0, d_canon_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_cell_.get(), 0, d_cell_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_epoch_.get(), 0, d_epoch_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_path_info_.get(), 0, d_path_info_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_seg_flags_.get(), 0, d_seg_flags_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_meta_.get(), 0, d_meta_.size(), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_rstart_.get(), 0xFF, d_rstart_.size(), stream_));
+    {
+        std::vector<float4> emis(n_, float4{0, 0, 1, 0});
+        PRX_CUDA(cudaMemcpy(d_emis_.get(), emis.data(), d_emis_.size(), cudaMemcpyHostToDevice));
+        // empty photon records: object id 0xFFFFFFFF (photon_store.hpp:15)
+        std::vector<float4> po(std::min<size_t>(nv, 1 << 20), float4{0, 0, 0, f_of_u(kInvalidObj)});
+        for (size_t off = 0; off < nv; off += po.size()) {
+            const size_t cnt = std::min(po.size(), nv - off);
+            PRX_CUDA(cudaMemcpyAsync(d_pos_obj_.as<float4>() + off, po.data(), 16 * cnt,
+                                     cudaMemcpyHostToDevice, stream_));
+            PRX_CUDA(cudaStreamSynchronize(stream_));
+        }
+    }
+    // work arrays
+    d_list_.alloc(4ull * n_);
+    d_masks_.alloc(4ull * n_);
+    d_flags8_.alloc(n_);
+    d_flags8b_.alloc(n_);
+    d_keys_.alloc(4ull * n_);
+    d_vals_.alloc(4ull * n_);
+    d_keys_tmp_.alloc(4ull * n_);
+    d_vals_tmp_.alloc(4ull * n_);
+    d_pruned_list_.alloc(4ull * n_);
+    d_need_.alloc(4ull * max_cells_ + 16);
+    d_scratch_.alloc(prim_scratch_bytes(std::max<uint64_t>(n_, max_cells_)));
+    // per-light pointer tables: [0] unm, [1] seg_start, [2] prefix (sharded prune)
+    std::vector<uint32_t*> ptrs(3 * PRX_MAX_LIGHTS, nullptr);
+    for (size_t li = 0; li < lights_.size(); ++li) {
+        ptrs[li] = lights_[li].unm.as<uint32_t>();
+        ptrs[PRX_MAX_LIGHTS + li] = lights_[li].seg_start.as<uint32_t>();
+    }
+    d_light_ptrs_.alloc(sizeof(uint32_t*) * ptrs.size());
+    PRX_CUDA(cudaMemcpy(d_light_ptrs_.get(), ptrs.data(), d_light_ptrs_.size(), cudaMemcpyHostToDevice));
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+}
+
+SceneDev Engine::scene_dev() const {
+    SceneDev S{};
+    S.nodes = d_nodes_.as<float4>();
+    S.n_nodes = static_cast<uint32_t>(scene_->bvh_nodes.size());
+    S.stris = d_stris_.as<float4>();
+    S.dtris = d_dyn_world_.as<float4>();
+    S.dnodes = d_lbvh_nodes_.as<float4>();
+    S.dleaf = d_lbvh_leaf_.as<uint32_t>();
+    S.mat = d_mat_.as<float4>();
+    S.oflags = d_oflags_.as<uint32_t>();
+    S.fp = d_fp_.as<FrameParams>();
+    S.eps = eps_;
+    S.two_diag = 2.0f * diag_;
+    S.seed_mix = seed_mix_;
+    S.gather_radius = cfg_.gather_radius;
+    S.trig = d_trig_;
+    return S;
+}
+
+PathDev Engine::path_dev() const {
+    PathDev P{};
+    P.n = n_;
+    P.base = sb_;
+    P.B = B_;
+    P.pos_obj = d_pos_obj_.as<float4>();
+    P.energy = d_energy_.as<float4>();
+    P.in_dir = d_in_dir_.as<float4>();
+    P.out_dir = d_out_dir_.as<float4>();
+    P.origin = d_origin_.as<float4>();
+    P.emis = d_emis_.as<float4>();
+    P.canon = d_canon_.as<float4>();
+    P.cell = d_cell_.as<uint32_t>();
+    P.epoch = d_epoch_.as<uint32_t>();
+    P.path_info = d_path_info_.as<uint32_t>();
+    P.seg_flags = d_seg_flags_.as<uint32_t>();
+    P.meta = d_meta_.as<uchar4>();
+    P.rstart = d_rstart_.as<uint8_t>();
+    return P;
+}
+
+uint32_t Engine::local_lb(const LightBlock& b) const { return std::max(b.begin, sb_) - sb_; }
+uint32_t Engine::local_le(const LightBlock& b) const {
+    const uint32_t e = std::min(b.end, se_);
+    const uint32_t s = std::max(b.begin, sb_);
+    return e > s ? e - sb_ : local_lb(b);
+}
+
+void Engine::record(int idx) {
+    PRX_CUDA(cudaEventRecord(ev_[idx], stream_));
+    ev_recorded_[idx] = true;
+}
+
+double Engine::elapsed_ms(int a, int b) {
+    if (!ev_recorded_[a] || !ev_recorded_[b]) return 0.0;
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, ev_[a], ev_[b]) != cudaSuccess) return 0.0;
+    return ms;
+}
+
+// ----------------------------------------------------------------------- frame params
+void Engine::fill_frame_params() {
+    FrameParams& fp = *h_fp_;
+    fp.frame = cur_frame_;
+    fp.n_lights = static_cast<uint32_t>(lights_.size());
+    for (size_t li = 0; li < lights_.size(); ++li) {
+        const LightBlock& b = lights_[li];
+        LightDev& L = fp.lights[li];
+        L.kind = b.light->kind;
+        L.begin = b.begin;
+        L.end = b.end;
+        L.moved = b.moved ? 1 : 0;
+        L.position = b.pose_now.position;
+        L.normal = b.pose_now.normal;
+        L.tangent = b.pose_now.tangent;
+        L.bitangent = b.pose_now.bitangent;
+        L.scale = b.pose_now.scale;
+        L.radius = b.light->radius;
+        L.half_x = b.light->half_x;
+        L.half_y = b.light->half_y;
+        L.cos_half = b.cos_half;
+        L.flux_pp = b.flux_pp;
+        L.ndims = b.ndims;
+        L.cells = b.cells;
+        for (int a = 0; a < 4; ++a) L.dims[a] = b.dims[a];
+        L.dm_t = b.dm_t.as<uint32_t>();
+        L.dm_c = b.dm_c.as<uint32_t>();
+    }
+    fp.n_dyn = static_cast<uint32_t>(dyn_.size());
+    PRX_CUDA(cudaMemcpyAsync(d_fp_.get(), h_fp_, sizeof(FrameParams), cudaMemcpyHostToDevice, stream_));
+}
+
+// state_at (scene.cpp:115-134) for the dynamics: host keyframes, device placement + LBVH
+void Engine::place_dynamics(bool force) {
+    if (dyn_.empty()) return;
+    bool changed = force;
+    for (size_t j = 0; j < dyn_.size(); ++j) {
+        const Object& o = scene_->objects[dyn_[j].obj];
+        const Xform now = transform_at(o.kfs, cur_frame_);
+        if (!dyn_[j].placed || !(now == dyn_[j].last_xf)) changed = true;
+        dyn_[j].last_xf = now;
+        dyn_[j].placed = true;
+        h_xf_[2 * j] = float4{now.rot.x, now.rot.y, now.rot.z, now.rot.w};
+        h_xf_[2 * j + 1] = float4{now.trans.x, now.trans.y, now.trans.z, now.scale};
+    }
+    if (!changed) return;
+    PRX_CUDA(cudaMemcpyAsync(d_dyn_xf_.get(), h_xf_, sizeof(float4) * 2 * dyn_.size(),
+                             cudaMemcpyHostToDevice, stream_));
+    launch_transform_dynamic(d_dyn_local_.as<float4>(), d_dyn_tri_xf_.as<uint32_t>(),
+                             d_dyn_xf_.as<float4>(), n_dyn_tris_, d_dyn_world_.as<float4>(), stream_);
+    if (n_lbvh_nodes_)
+        build_dynamic_lbvh(d_dyn_world_.as<float4>(), d_dyn_tri_xf_.as<uint32_t>(), n_dyn_tris_,
+                           h_fp_->dyn, static_cast<uint32_t>(dyn_.size()),
+                           reinterpret_cast<const DynObj*>(d_fp_.as<char>() + offsetof(FrameParams, dyn)),
+                           d_lbvh_nodes_.as<float4>(), d_lbvh_leaf_.as<uint32_t>(), lbvh_, stream_);
+}
+
+// ----------------------------------------------------------------------- stages
+void Engine::frame_update(prx_frame_stats* st) {
+    PRX_CUDA(cudaSetDevice(device_));
+    for (bool& r : ev_recorded_) r = false;
+    record(kEvFrame0);
+    const int frame = frames_run_++;
+    cur_frame_ = frame;
+    PRX_CUDA(cudaMemsetAsync(d_ctr_.get(), 0, sizeof(Counters), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_cnt32_.get(), 0, 4 * kCntN, stream_));
+    n_pruned_ = 0;
+    // light poses (engine.cpp:205-209)
+    for (LightBlock& b : lights_) {
+        b.pose_prev = b.pose_now;
+        b.pose_now = light_pose_at(*b.light, frame);
+        b.moved = frame > 0 && !(b.pose_now == b.pose_prev);
+    }
+    // dynamic placements and occlusion boxes (scene.cpp:115-134, engine.cpp:211-218)
+    FrameParams& fp = *h_fp_;
+    fp.n_boxes = 0;
+    for (size_t j = 0; j < dyn_.size(); ++j) {
+        const Object& o = scene_->objects[dyn_[j].obj];
+        const Xform now = transform_at(o.kfs, frame);
+        const Xform prev = transform_at(o.kfs, frame > 0 ? frame - 1 : 0);
+        const Box cur = transform_box(o.local_bounds, now);
+        const Box prv = transform_box(o.local_bounds, prev);
+        DynObj& D = fp.dyn[j];
+        D.obj = dyn_[j].obj;
+        D.tri_begin = dyn_[j].tri_begin;
+        D.tri_count = dyn_[j].tri_count;
+        D.node_begin = dyn_[j].node_begin;
+        D.cur = cur;
+        if (frame > 0) {
+            Box box = prv;
+            expand(box, cur);
+            inflate(box, eps_);
+            fp.boxes[fp.n_boxes++] = box;
+        }
+    }
+    fill_frame_params();
+    place_dynamics(false);
+    launch_frame_reset(path_dev(), cfg_.record_flags, d_ctr_.as<Counters>(), stream_);
+    if (cfg_.mode == PRX_MODE_BASELINE) {  // engine.cpp:228-232
+        launch_release_all(path_dev(), stream_);
+        for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.dm_c.get(), 0, 4ull * b.cells, stream_));
+    }
+    record(kEvVerify0);
+    if (st) {
+        st->frame = frame;
+        st->mode = cfg_.mode;
+    }
+}
+
+void Engine::stage_update_origins() {
+    bool any = false;
+    for (const LightBlock& b : lights_) any = any || b.moved;
+    if (any) launch_update_origins(scene_dev(), path_dev(), d_ctr_.as<Counters>(), stream_);
+}
+
+void Engine::stage_occlusions() {
+    if (h_fp_->n_boxes == 0) return;  // engine.cpp:308-312
+    launch_occlusion_flags(scene_dev(), path_dev(), cfg_.mode, cfg_.record_flags, d_list_.as<uint32_t>(),
+                           d_masks_.as<uint32_t>(), d_ctr_.as<Counters>(), stream_);
+    if (cfg_.mode == PRX_MODE_ERROR)
+        launch_verify_error(scene_dev(), path_dev(), cfg_.threshold, d_list_.as<uint32_t>(),
+                            d_masks_.as<uint32_t>(), d_ctr_.as<Counters>(), d_ctr_.as<Counters>(), n_,
+                            stream_);
+}
+
+void Engine::stage_compute_dm() {
+    for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.dm_c.get(), 0, 4ull * b.cells, stream_));
+    launch_compute_dm(scene_dev(), path_dev(), d_ctr_.as<Counters>(), stream_);
+}
+
+void Engine::verify_paths(prx_frame_stats* st) {
+    (void)st;
+    PRX_CUDA(cudaSetDevice(device_));
+    record(kEvVerify0);
+    if (cfg_.mode != PRX_MODE_BASELINE && cur_frame_ > 0) {
+        stage_update_origins();
+        record(kEvOccl0);
+        stage_occlusions();
+    } else {
+        record(kEvOccl0);
+    }
+    record(kEvDm0);
+    stage_compute_dm();
+    record(kEvPrune0);
+}
+
+// stage_prune (engine.cpp:473-497) on a single shard: global counts == local counts
+void Engine::stage_prune_local() {
+    uint32_t* const* unm = d_light_ptrs_.as<uint32_t*>();
+    for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.unm.get(), 0, 4ull * b.cells, stream_));
+    const PathDev P = path_dev();
+    launch_prune_mark(scene_dev(), P, static_cast<uint32_t>(cur_frame_), unm, d_flags8_.as<uint8_t>(),
+                      d_flags8b_.as<uint8_t>(), stream_);
+    // candidates that need a trim -> (light, cell)-sorted list, stable in path id
+    uint8_t* trim = reinterpret_cast<uint8_t*>(d_keys_tmp_.as<uint32_t>());  // reuse as n bytes
+    launch_prune_trim_flags(P, d_fp_.as<FrameParams>(), unm, d_flags8b_.as<uint8_t>(), trim, stream_);
+    uint32_t* cnt = d_cnt32_.as<uint32_t>();
+    compact_u8(trim, n_, nullptr, 0, d_list_.as<uint32_t>(), cnt + kCntTrim, d_scratch_.get(), stream_);
+    launch_prune_keys(P, d_fp_.as<FrameParams>(), d_list_.as<uint32_t>(), cnt + kCntTrim,
+                      d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), n_, stream_);
+    int light_bits = 0;
+    while ((1u << light_bits) < lights_.size()) ++light_bits;
+    radix_sort_pairs(d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), d_keys_tmp_.as<uint32_t>(),
+                     d_vals_tmp_.as<uint32_t>(), n_, cnt + kCntTrim, 22 + light_bits, d_scratch_.get(),
+                     stream_);
+    launch_prune_trim(P, d_fp_.as<FrameParams>(), d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(),
+                      cnt + kCntTrim, n_, unm + PRX_MAX_LIGHTS, nullptr, d_flags8_.as<uint8_t>(), stream_);
+    launch_prune_apply(P, d_flags8_.as<uint8_t>(), stream_);
+    for (LightBlock& b : lights_)
+        launch_dm_after_prune(b.dm_c.as<uint32_t>(), b.dm_t.as<uint32_t>(), b.unm.as<uint32_t>(), b.cells,
+                              stream_);
+    compact_u8(d_flags8_.as<uint8_t>(), n_, nullptr, sb_, d_pruned_list_.as<uint32_t>(), cnt + kCntPruned,
+               d_scratch_.get(), stream_);
+}
+
+// stage_fill (engine.cpp:499-546) on a single shard
+void Engine::stage_fill_local() {
+    const PathDev P = path_dev();
+    uint32_t* cnt = d_cnt32_.as<uint32_t>();
+    for (uint32_t li = 0; li < lights_.size(); ++li) {
+        LightBlock& b = lights_[li];
+        const uint32_t lb = local_lb(b), le = local_le(b);
+        launch_fill_need(b.dm_t.as<uint32_t>(), b.dm_c.as<uint32_t>(), d_need_.as<uint32_t>(), b.cells, stream_);
+        scan_exclusive_u32(d_need_.as<uint32_t>(), d_need_.as<uint32_t>(), b.cells, nullptr, cnt + kCntNeed,
+                           d_scratch_.get(), stream_);
+        launch_dead_flags(P, lb, le, d_flags8_.as<uint8_t>(), stream_);
+        compact_u8(d_flags8_.as<uint8_t>(), le - lb, nullptr, lb, d_list_.as<uint32_t>(), cnt + kCntDead,
+                   d_scratch_.get(), stream_);
+        launch_fill_check(cnt + kCntDead, cnt + kCntNeed, d_ctr_.as<Counters>(), stream_);
+        launch_fill_assign(scene_dev(), P, li, d_list_.as<uint32_t>(), cnt + kCntDead, std::max(1u, le - lb), 0,
+                           d_need_.as<uint32_t>(), cnt + kCntNeed, b.cells, d_ctr_.as<Counters>(), stream_);
+        launch_dm_after_fill(b.dm_c.as<uint32_t>(), b.dm_t.as<uint32_t>(), b.cells, stream_);
+    }
+}
+
+void Engine::stage_trace() {
+    const PathDev P = path_dev();
+    uint32_t* cnt = d_cnt32_.as<uint32_t>();
+    launch_retrace_flags(P, d_flags8_.as<uint8_t>(), stream_);
+    compact_u8(d_flags8_.as<uint8_t>(), n_, nullptr, 0, d_list_.as<uint32_t>(), cnt + kCntRetrace,
+               d_scratch_.get(), stream_);
+    launch_trace(scene_dev(), P, d_list_.as<uint32_t>(), cnt + kCntRetrace, n_, d_ctr_.as<Counters>(), stream_);
+    launch_finalize(P, d_ctr_.as<Counters>(), stream_);
+}
+
+void Engine::read_back(prx_frame_stats* st, bool with_times) {
+    PRX_CUDA(cudaMemcpyAsync(h_ctr_, d_ctr_.get(), sizeof(Counters), cudaMemcpyDeviceToHost, stream_));
+    PRX_CUDA(cudaMemcpyAsync(h_cnt32_, d_cnt32_.get(), 4 * kCntN, cudaMemcpyDeviceToHost, stream_));
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+    PRX_CUDA(cudaGetLastError());
+    n_pruned_ = h_cnt32_[kCntPruned];
+    launches_ = g_launches - launch_base_;
+    if (h_ctr_->fill_overflow) throw std::logic_error("fill: ran out of free path slots");
+    if (!st) return;
+    st->frame = cur_frame_;
+    st->mode = cfg_.mode;
+    st->rays_traced = h_ctr_->traced;
+    st->rays_reused = h_ctr_->segments - h_ctr_->traced;
+    st->paths_replaced = h_ctr_->replaced;
+    st->paths_pruned = h_cnt32_[kCntPruned];
+    st->paths_filled = h_ctr_->filled;
+    st->visibility_rays = h_ctr_->vis;
+    st->live_segments_before = h_ctr_->live_segments;
+    st->paths_retraced = h_cnt32_[kCntRetrace];
+    if (with_times) {
+        st->t_update = elapsed_ms(kEvVerify0, kEvOccl0) * 1e-3;
+        st->t_occlusion = elapsed_ms(kEvOccl0, kEvDm0) * 1e-3;
+        st->t_dm = elapsed_ms(kEvDm0, kEvPrune0) * 1e-3;
+        st->t_prune = elapsed_ms(kEvPrune0, kEvFill0) * 1e-3;
+        st->t_fill = elapsed_ms(kEvFill0, kEvTrace0) * 1e-3;
+        st->t_trace = elapsed_ms(kEvTrace0, kEvEnd) * 1e-3;
+        st->ms_frame_update = elapsed_ms(kEvFrame0, kEvVerify0);
+        st->ms_verify = elapsed_ms(kEvVerify0, kEvPrune0);
+        st->ms_retrace = elapsed_ms(kEvPrune0, kEvEnd);
+    }
+}
+
+void Engine::retrace_invalid(prx_frame_stats* st) {
+    PRX_CUDA(cudaSetDevice(device_));
+    record(kEvPrune0);
+    if (cfg_.mode != PRX_MODE_BASELINE) stage_prune_local();
+    record(kEvFill0);
+    stage_fill_local();
+    record(kEvTrace0);
+    stage_trace();
+    record(kEvEnd);
+    read_back(st, true);
+}
+
+void Engine::run_frame(prx_frame_stats* st) {
+    if (st) std::memset(st, 0, sizeof(*st));
+    frame_update(st);
+    verify_paths(st);
+    retrace_invalid(st);
+}
+
+void Engine::run_stage(int stage, prx_frame_stats* st) {
+    PRX_CUDA(cudaSetDevice(device_));
+    const bool active = cfg_.mode != PRX_MODE_BASELINE && cur_frame_ > 0;
+    prx_frame_stats tmp{};
+    switch (stage) {
+        case PRX_STAGE_UPDATE_ORIGINS:
+            if (active) stage_update_origins();
+            break;
+        case PRX_STAGE_OCCLUSIONS:
+            if (active) stage_occlusions();
+            break;
+        case PRX_STAGE_COMPUTE_DM: stage_compute_dm(); break;
+        case PRX_STAGE_PRUNE:
+            if (cfg_.mode != PRX_MODE_BASELINE) stage_prune_local();
+            break;
+        case PRX_STAGE_FILL: stage_fill_local(); break;
+        case PRX_STAGE_TRACE: stage_trace(); break;
+        case PRX_STAGE_RELEASE_ALL:
+            launch_release_all(path_dev(), stream_);
+            for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.dm_c.get(), 0, 4ull * b.cells, stream_));
+            break;
+        default: throw std::invalid_argument("unknown stage");
+    }
+    read_back(&tmp, false);
+    if (st) {  // counters accumulate over the frame; report the running totals
+        st->frame = tmp.frame;
+        st->mode = tmp.mode;
+        st->rays_traced = tmp.rays_traced;
+        st->rays_reused = stage == PRX_STAGE_TRACE ? tmp.rays_reused : 0;
+        st->paths_replaced = tmp.paths_replaced;
+        st->paths_pruned = tmp.paths_pruned;
+        st->paths_filled = tmp.paths_filled;
+        st->visibility_rays = tmp.visibility_rays;
+        st->paths_retraced = tmp.paths_retraced;
+        st->live_segments_before = tmp.live_segments_before;
+    }
+}
+
+// ----------------------------------------------------------------------- sharded exchange
+void Engine::dm_current_ptr(uint32_t light, void** ptr, uint32_t* cells) {
+    if (light >= lights_.size()) throw std::out_of_range("light index");
+    *ptr = lights_[light].dm_c.get();
+    *cells = lights_[light].cells;
+}
+
+void Engine::prune_count(uint32_t light, uint32_t* unmarked_out_dev) {
+    // marks for every light are produced together; copy this light's unmarked counts
+    if (light >= lights_.size()) throw std::out_of_range("light index");
+    if (light == 0) {
+        for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.unm.get(), 0, 4ull * b.cells, stream_));
+        launch_prune_mark(scene_dev(), path_dev(), static_cast<uint32_t>(cur_frame_),
+                          d_light_ptrs_.as<uint32_t*>(), d_flags8_.as<uint8_t>(), d_flags8b_.as<uint8_t>(),
+                          stream_);
+    }
+    PRX_CUDA(cudaMemcpyAsync(unmarked_out_dev, lights_[light].unm.get(), 4ull * lights_[light].cells,
+                             cudaMemcpyDeviceToDevice, stream_));
+}
+
+void Engine::prune_apply(uint32_t light, const uint32_t* prefix_dev, const uint32_t* total_dev,
+                         prx_frame_stats* st) {
+    (void)light;
+    (void)prefix_dev;
+    (void)total_dev;
+    (void)st;
+    throw std::logic_error("prune_apply: sharded prune is driven per frame (not yet wired)");
+}
+
+void Engine::fill_count(uint32_t light, uint32_t* dead_out) {
+    (void)light;
+    (void)dead_out;
+    throw std::logic_error("fill_count: sharded fill is driven per frame (not yet wired)");
+}
+
+void Engine::fill_apply(uint32_t light, uint64_t dead_prefix, uint64_t dead_total, prx_frame_stats* st) {
+    (void)light;
+    (void)dead_prefix;
+    (void)dead_total;
+    (void)st;
+    throw std::logic_error("fill_apply: sharded fill is driven per frame (not yet wired)");
+}
+
+// ----------------------------------------------------------------------- splat
+void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_host, float* rgb_dev,
+                   prx_frame_stats* st) {
+    PRX_CUDA(cudaSetDevice(device_));
+    if (!(radius > 0.0f)) throw std::invalid_argument("gather: radius must be positive");
+    if (mode != 0) throw std::invalid_argument("splat: only mode 0 (atomic splat) is available");
+    Camera c = scene_->camera;
+    if (cam) {
+        c.position = V3{cam->position.x, cam->position.y, cam->position.z};
+        c.look_at = V3{cam->look_at.x, cam->look_at.y, cam->look_at.z};
+        c.fov_deg = cam->fov_deg;
+        c.width = cam->width;
+        c.height = cam->height;
+    }
+    if (c.width == 0 || c.height == 0) throw std::invalid_argument("splat: empty image");
+    // camera_ray (gather.cpp:22-33): per-image constants on the host libm
+    CamDev C{};
+    C.pos = c.position;
+    C.fwd = normalized(sub(c.look_at, c.position));
+    V3 up{0, 1, 0};
+    if (std::abs(dot(C.fwd, up)) > 0.999f) up = V3{1, 0, 0};
+    C.right = normalized(cross(C.fwd, up));
+    C.up = cross(C.right, C.fwd);
+    C.tan_half = std::tan(c.fov_deg * static_cast<float>(M_PI) / 360.0f);
+    C.aspect = static_cast<float>(c.width) / static_cast<float>(c.height);
+    C.w = c.width;
+    C.h = c.height;
+    const uint32_t npx = c.width * c.height;
+    if (c.width != img_w_ || c.height != img_h_) {
+        d_gbuf_.alloc(16ull * npx);
+        d_img_.alloc(12ull * npx);
+        img_w_ = c.width;
+        img_h_ = c.height;
+    }
+    const float inv_area = 1.0f / (static_cast<float>(M_PI) * radius * radius);
+    const float inv_pi = 1.0f / static_cast<float>(M_PI);
+    record(kEvSplat0);
+    float* out = rgb_dev ? rgb_dev : d_img_.as<float>();
+    launch_splat(scene_dev(), path_dev(), C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, stream_);
+    record(kEvSplat1);
+    if (rgb_host)
+        PRX_CUDA(cudaMemcpyAsync(rgb_host, out, 12ull * npx, cudaMemcpyDeviceToHost, stream_));
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+    PRX_CUDA(cudaGetLastError());
+    launches_ = g_launches - launch_base_;
+    if (st) {
+        st->ms_splat = elapsed_ms(kEvSplat0, kEvSplat1);
+        st->t_gather = st->ms_splat * 1e-3;
+    }
+}
+
+// ----------------------------------------------------------------------- field I/O
+size_t Engine::field_bytes(int field, uint32_t index) const {
+    const size_t nv = static_cast<size_t>(n_) * B_;
+    switch (field) {
+        case PRX_FIELD_PHOTONS: return nv * 32;
+        case PRX_FIELD_AUX: return nv * 24;
+        case PRX_FIELD_POS_OBJ:
+        case PRX_FIELD_ENERGY:
+        case PRX_FIELD_IN_DIR:
+        case PRX_FIELD_OUT_DIR: return nv * 16;
+        case PRX_FIELD_ORIGIN:
+        case PRX_FIELD_EMISSION_DIR:
+        case PRX_FIELD_CANONICAL: return 16ull * n_;
+        case PRX_FIELD_CELL:
+        case PRX_FIELD_EPOCH:
+        case PRX_FIELD_PATH_INFO:
+        case PRX_FIELD_META:
+        case PRX_FIELD_SEGMENT_FLAGS: return 4ull * n_;
+        case PRX_FIELD_RETRACE_START: return n_;
+        case PRX_FIELD_DM_TARGET:
+        case PRX_FIELD_DM_CURRENT:
+            if (index >= lights_.size()) throw std::out_of_range("light index out of range");
+            return 4ull * lights_[index].cells;
+        case PRX_FIELD_PRUNED: return 4ull * n_pruned_;
+    }
+    throw std::invalid_argument("unknown field");
+}
+
+namespace {
+struct FieldPtr {
+    void* p;
+    bool convert;
+};
+}  // namespace
+
+void Engine::download(int field, uint32_t index, void* dst, size_t bytes) {
+    PRX_CUDA(cudaSetDevice(device_));
+    if (bytes != field_bytes(field, index)) throw std::invalid_argument("download: size mismatch");
+    if (bytes == 0) return;
+    void* src = nullptr;
+    DevBuf tmp;
+    switch (field) {
+        case PRX_FIELD_PHOTONS:
+            tmp.alloc(bytes);
+            launch_pack_photons(path_dev(), tmp.get(), nullptr, stream_);
+            src = tmp.get();
+            break;
+        case PRX_FIELD_AUX:
+            tmp.alloc(bytes);
+            launch_pack_photons(path_dev(), nullptr, tmp.get(), stream_);
+            src = tmp.get();
+            break;
+        case PRX_FIELD_POS_OBJ: src = d_pos_obj_.get(); break;
+        case PRX_FIELD_ENERGY: src = d_energy_.get(); break;
+        case PRX_FIELD_IN_DIR: src = d_in_dir_.get(); break;
+        case PRX_FIELD_OUT_DIR: src = d_out_dir_.get(); break;
+        case PRX_FIELD_ORIGIN: src = d_origin_.get(); break;
+        case PRX_FIELD_EMISSION_DIR: src = d_emis_.get(); break;
+        case PRX_FIELD_CANONICAL: src = d_canon_.get(); break;
+        case PRX_FIELD_CELL: src = d_cell_.get(); break;
+        case PRX_FIELD_EPOCH: src = d_epoch_.get(); break;
+        case PRX_FIELD_PATH_INFO: src = d_path_info_.get(); break;
+        case PRX_FIELD_META: src = d_meta_.get(); break;
+        case PRX_FIELD_RETRACE_START: src = d_rstart_.get(); break;
+        case PRX_FIELD_SEGMENT_FLAGS: src = d_seg_flags_.get(); break;
+        case PRX_FIELD_DM_TARGET: src = lights_[index].dm_t.get(); break;
+        case PRX_FIELD_DM_CURRENT: src = lights_[index].dm_c.get(); break;
+        case PRX_FIELD_PRUNED: src = d_pruned_list_.get(); break;
+        default: throw std::invalid_argument("unknown field");
+    }
+    PRX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_));
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::upload(int field, uint32_t index, const void* src, size_t bytes) {
+    PRX_CUDA(cudaSetDevice(device_));
+    if (bytes != field_bytes(field, index)) throw std::invalid_argument("upload: size mismatch");
+    if (bytes == 0) return;
+    void* dst = nullptr;
+    DevBuf tmp;
+    switch (field) {
+        case PRX_FIELD_PHOTONS:
+        case PRX_FIELD_AUX: {
+            tmp.alloc(bytes);
+            PRX_CUDA(cudaMemcpyAsync(tmp.get(), src, bytes, cudaMemcpyHostToDevice, stream_));
+            if (field == PRX_FIELD_PHOTONS) launch_unpack_photons(path_dev(), tmp.get(), nullptr, stream_);
+            else launch_unpack_photons(path_dev(), nullptr, tmp.get(), stream_);
+            PRX_CUDA(cudaStreamSynchronize(stream_));
+            return;
+        }
+        case PRX_FIELD_POS_OBJ: dst = d_pos_obj_.get(); break;
+        case PRX_FIELD_ENERGY: dst = d_energy_.get(); break;
+        case PRX_FIELD_IN_DIR: dst = d_in_dir_.get(); break;
+        case PRX_FIELD_OUT_DIR: dst = d_out_dir_.get(); break;
+        case PRX_FIELD_ORIGIN: dst = d_origin_.get(); break;
+        case PRX_FIELD_EMISSION_DIR: dst = d_emis_.get(); break;
+        case PRX_FIELD_CANONICAL: dst = d_canon_.get(); break;
+        case PRX_FIELD_CELL: dst = d_cell_.get(); break;
+        case PRX_FIELD_EPOCH: dst = d_epoch_.get(); break;
+        case PRX_FIELD_PATH_INFO: dst = d_path_info_.get(); break;
+        case PRX_FIELD_META: dst = d_meta_.get(); break;
+        case PRX_FIELD_RETRACE_START: dst = d_rstart_.get(); break;
+        case PRX_FIELD_SEGMENT_FLAGS: dst = d_seg_flags_.get(); break;
+        case PRX_FIELD_DM_TARGET: dst = lights_[index].dm_t.get(); break;
+        case PRX_FIELD_DM_CURRENT: dst = lights_[index].dm_c.get(); break;
+        case PRX_FIELD_PRUNED: throw std::invalid_argument("upload: the pruned list is read-only");
+        default: throw std::invalid_argument("unknown field");
+    }
+    PRX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::set_frame_counter(int frames_run) {
+    if (frames_run < 0) throw std::invalid_argument("frames_run must be >= 0");
+    frames_run_ = frames_run;
+    cur_frame_ = frames_run > 0 ? frames_run - 1 : 0;
+    for (LightBlock& b : lights_) {
+        b.pose_now = light_pose_at(*b.light, cur_frame_);
+        b.pose_prev = b.pose_now;
+        b.moved = false;
+    }
+    fill_frame_params();
+    place_dynamics(true);
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::set_stream(cudaStream_t s) {
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+    if (own_stream_ && stream_) cudaStreamDestroy(stream_);
+    if (s) {
+        stream_ = s;
+        own_stream_ = false;
+    } else {
+        PRX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        own_stream_ = true;
+    }
+}
+
+void Engine::synchronize() { PRX_CUDA(cudaStreamSynchronize(stream_)); }
+
+void Engine::info(prx_engine_info* out) const {
+    std::memset(out, 0, sizeof(*out));
+    out->n_paths = n_total_;
+    out->max_bounces = B_;
+    out->n_lights = static_cast<uint32_t>(lights_.size());
+    out->shard_begin = sb_;
+    out->shard_end = se_;
+    out->eps_world = eps_;
+    out->diagonal = diag_;
+    out->frames_run = frames_run_;
+    out->n_pruned = n_pruned_;
+    for (size_t li = 0; li < lights_.size(); ++li) {
+        const LightBlock& b = lights_[li];
+        out->light_path_begin[li] = b.begin;
+        out->light_path_end[li] = b.end;
+        out->dm_ndims[li] = b.ndims;
+        for (int a = 0; a < 4; ++a) out->dm_dims[li][a] = b.dims[a];
+        out->dm_cells[li] = b.cells;
+        out->flux_per_path[li][0] = b.flux_pp.x;
+        out->flux_per_path[li][1] = b.flux_pp.y;
+        out->flux_per_path[li][2] = b.flux_pp.z;
+    }
+    uint64_t bytes = 0;
+    for (const DevBuf* b : {&d_nodes_, &d_stris_, &d_dyn_local_, &d_dyn_world_, &d_lbvh_nodes_, &d_pos_obj_,
+                            &d_energy_, &d_in_dir_, &d_out_dir_, &d_origin_, &d_emis_, &d_canon_, &d_cell_,
+                            &d_epoch_, &d_path_info_, &d_seg_flags_, &d_meta_, &d_rstart_, &d_list_, &d_masks_,
+                            &d_keys_, &d_vals_, &d_keys_tmp_, &d_vals_tmp_, &d_pruned_list_})
+        bytes += b->size();
+    out->device_bytes = bytes;
+}
+
+}  // namespace prx

@@ -1,0 +1,179 @@
+// engine.h -- host side of one B200 path-reuse engine (one GPU, one path shard).
+//
+// Mirrors pathreuse::Engine (engine.hpp:69-179): owns the device path store, the scene's
+// device copy, per-light distribution maps, and orchestrates the frame as the north_star
+// stages frame_update / verify_paths / retrace_invalid, all enqueued on
+// one CUDA stream with no host round trip until the frame's statistics are read back.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dev_types.h"
+#include "host_scene.h"
+#include "kernels.h"
+#include "prx.h"
+
+namespace prx {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define PRX_CUDA(x) ::prx::cuda_check((x), #x)
+
+// RAII device allocation
+class DevBuf {
+public:
+    DevBuf() = default;
+    explicit DevBuf(size_t bytes) { alloc(bytes); }
+    ~DevBuf() { reset(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        reset();
+        p_ = o.p_;
+        n_ = o.n_;
+        o.p_ = nullptr;
+        o.n_ = 0;
+        return *this;
+    }
+    void alloc(size_t bytes);
+    void reset();
+    template <typename T>
+    T* as() const { return static_cast<T*>(p_); }
+    void* get() const { return p_; }
+    size_t size() const { return n_; }
+
+private:
+    void* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+class Engine {
+public:
+    Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    void frame_update(prx_frame_stats* st);
+    void verify_paths(prx_frame_stats* st);
+    void retrace_invalid(prx_frame_stats* st);
+    void run_frame(prx_frame_stats* st);
+    void run_stage(int stage, prx_frame_stats* st);
+
+    // sharded exchange points
+    void dm_current_ptr(uint32_t light, void** ptr, uint32_t* cells);
+    void prune_count(uint32_t light, uint32_t* unmarked_out_dev);
+    void prune_apply(uint32_t light, const uint32_t* prefix_dev, const uint32_t* total_dev,
+                     prx_frame_stats* st);
+    void fill_count(uint32_t light, uint32_t* dead_out);
+    void fill_apply(uint32_t light, uint64_t dead_prefix, uint64_t dead_total, prx_frame_stats* st);
+
+    void splat(const prx_camera* cam, float radius, int mode, float* rgb_host, float* rgb_dev,
+               prx_frame_stats* st);
+
+    size_t field_bytes(int field, uint32_t index) const;
+    void download(int field, uint32_t index, void* dst, size_t bytes);
+    void upload(int field, uint32_t index, const void* src, size_t bytes);
+    void set_frame_counter(int frames_run);
+    void set_stream(cudaStream_t s);
+    void synchronize();
+    void info(prx_engine_info* out) const;
+    uint64_t launches() const { return launches_; }
+
+private:
+    struct LightBlock {
+        const Light* light = nullptr;
+        uint32_t begin = 0, end = 0;  // global path range
+        uint32_t ndims = 0, dims[4] = {0, 0, 0, 0}, cells = 0;
+        V3 flux_pp{0, 0, 0};
+        double cos_half = 0.0;
+        LightPose pose_prev, pose_now;
+        bool moved = false;
+        DevBuf dm_t, dm_c, unm, seg_start;
+    };
+    struct DynInfo {
+        uint32_t obj = 0, tri_begin = 0, tri_count = 0, node_begin = kLbvhBrute;
+        Xform last_xf;
+        bool placed = false;
+    };
+
+    void upload_scene();
+    void alloc_state();
+    void fill_frame_params();
+    void place_dynamics(bool force);
+    void stage_update_origins();
+    void stage_occlusions();
+    void stage_compute_dm();
+    void stage_prune_local();
+    void stage_fill_local();
+    void stage_trace();
+    void read_back(prx_frame_stats* st, bool with_times);
+    void record(int idx);
+    double elapsed_ms(int a, int b);
+    SceneDev scene_dev() const;
+    PathDev path_dev() const;
+    uint32_t local_lb(const LightBlock& b) const;
+    uint32_t local_le(const LightBlock& b) const;
+
+    std::shared_ptr<const Scene> scene_;
+    prx_config cfg_;
+    int device_ = 0;
+    cudaStream_t stream_ = nullptr;
+    bool own_stream_ = true;
+    uint32_t n_total_ = 0, sb_ = 0, se_ = 0, n_ = 0, B_ = 0;
+    float eps_ = 0.0f, diag_ = 0.0f;
+    uint64_t seed_mix_ = 0;
+    int frames_run_ = 0;
+    int cur_frame_ = 0;
+    uint64_t launches_ = 0;
+    uint64_t launch_base_ = 0;
+
+    std::vector<LightBlock> lights_;
+    std::vector<DynInfo> dyn_;
+    uint32_t n_dyn_tris_ = 0, n_lbvh_nodes_ = 0;
+
+    // scene device data
+    DevBuf d_nodes_, d_stris_, d_mat_, d_oflags_, d_dyn_local_, d_dyn_world_, d_dyn_xf_, d_dyn_tri_xf_,
+        d_lbvh_nodes_, d_lbvh_leaf_, d_lbvh_work_;
+    LbvhBuffers lbvh_{};
+    const float2* d_trig_ = nullptr;
+
+    // frame params (pinned host + device)
+    FrameParams* h_fp_ = nullptr;
+    DevBuf d_fp_;
+    float4* h_xf_ = nullptr;
+    DevBuf d_light_ptrs_;  // uint32_t*[3][PRX_MAX_LIGHTS]: unm, seg_start, prefix
+
+    // path state
+    DevBuf d_pos_obj_, d_energy_, d_in_dir_, d_out_dir_, d_origin_, d_emis_, d_canon_, d_cell_,
+        d_epoch_, d_path_info_, d_seg_flags_, d_meta_, d_rstart_;
+    // work arrays
+    DevBuf d_list_, d_masks_, d_flags8_, d_flags8b_, d_keys_, d_vals_, d_keys_tmp_, d_vals_tmp_,
+        d_pruned_list_, d_need_, d_scratch_;
+    DevBuf d_ctr_, d_cnt32_;
+    Counters* h_ctr_ = nullptr;
+    uint32_t* h_cnt32_ = nullptr;
+    uint32_t n_pruned_ = 0;
+    uint32_t max_cells_ = 1;
+
+    // splat buffers
+    DevBuf d_gbuf_, d_img_;
+    uint32_t img_w_ = 0, img_h_ = 0;
+
+    cudaEvent_t ev_[12] = {};
+    bool ev_recorded_[12] = {};
+};
+
+// host-libm cos/sin table for cosine_sample's 2^24 possible angles (device copy, cached)
+const float2* exact_trig_table(int device);
+
+}  // namespace prx

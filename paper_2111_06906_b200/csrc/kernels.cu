@@ -1,0 +1,663 @@
+// kernels.cu -- per-frame stage kernels of the B200 path-reuse engine.
+//
+// One thread per path (grid-stride), bounce-major vertex streams so that every warp
+// access to bounce b of 32 consecutive paths is one coalesced 512-byte float4 load.
+// Citations: reference function each kernel restates (paths under /root/reference/proj).
+#include "device_scene.cuh"
+#include "kernels.h"
+
+namespace prx {
+
+uint64_t g_launches = 0;
+
+int launch_grid(uint64_t n, int threads) {
+    const uint64_t blocks = (n + threads - 1) / threads;
+    const uint64_t cap = 148ull * 16ull;  // 16 resident 256-thread CTAs per SM
+    return static_cast<int>(blocks == 0 ? 1 : (blocks < cap ? blocks : cap));
+}
+
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+__device__ __forceinline__ size_t vix(const PathDev& P, uint32_t b, uint32_t i) {
+    return (size_t)b * P.n + i;
+}
+
+// Engine::truncate_path (engine.cpp:141-147): photon records >= new_count become empty
+// Photon{} (aux untouched), count/escaped updated.
+__device__ __forceinline__ void truncate_path(const PathDev& P, uint32_t i, uint32_t new_count,
+                                              bool escaped, uchar4& m) {
+    for (uint32_t b = new_count; b < P.B; ++b) {
+        const size_t v = vix(P, b, i);
+        P.in_dir[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        P.pos_obj[v].w = __uint_as_float(kInvalidObj);
+        P.energy[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    m.x = (unsigned char)new_count;
+    m.y = escaped ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- init / placement
+__global__ void k_init_dm_target(LightDev L, uint32_t n, uint64_t seed_mix, uint32_t* dm_t) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        float c[4] = {0, 0, 0, 0};
+        for (uint32_t a = 0; a < L.ndims; ++a)
+            c[a] = (float)rng_uniform_d_m(seed_mix, i, 0, 0, kDmTargetInit, a);
+        atomicAdd(&dm_t[cell_of(L, c)], 1u);
+    }
+}
+
+// transform.hpp:72,98-100: p' = rotate(q, p * s) + t, then (a, b - a, c - a)
+__global__ void k_transform_dynamic(const float4* __restrict__ local, const uint32_t* __restrict__ tri_xf,
+                                    const float4* __restrict__ xf, uint32_t n, float4* __restrict__ world) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = tri_xf[i];
+        const float4 q = xf[2 * k], ts = xf[2 * k + 1];
+        const V3 u{q.x, q.y, q.z};
+        V3 w[3];
+        for (int j = 0; j < 3; ++j) {
+            const float4 p4 = local[3 * i + j];
+            const V3 v = mul(V3{p4.x, p4.y, p4.z}, ts.w);
+            const V3 t = mul(cross(u, v), 2.0f);
+            w[j] = add(add(add(v, mul(t, q.w)), cross(u, t)), V3{ts.x, ts.y, ts.z});
+        }
+        const V3 e1 = sub(w[1], w[0]), e2 = sub(w[2], w[0]);
+        world[3 * i] = make_float4(w[0].x, w[0].y, w[0].z, 0.f);
+        world[3 * i + 1] = make_float4(e1.x, e1.y, e1.z, 0.f);
+        world[3 * i + 2] = make_float4(e2.x, e2.y, e2.z, 0.f);
+    }
+}
+
+__global__ void k_frame_reset(PathDev P, int record, Counters* ctr) {
+    unsigned long long segs = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        uchar4 m = P.meta[i];
+        if (m.z == kLive) segs += m.x + m.y;
+        m.w = 0;
+        P.meta[i] = m;
+        P.rstart[i] = kNoRetrace;
+        if (record) P.seg_flags[i] = 0;
+    }
+    warp_add(&ctr->live_segments, segs);
+}
+
+__global__ void k_release_all(PathDev P) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        uchar4 m = P.meta[i];
+        truncate_path(P, i, 0, false, m);
+        m.z = kDead;
+        P.meta[i] = m;
+    }
+}
+
+// ---------------------------------------------------------------- verify_paths
+__global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Counters* ctr) {
+    const FrameParams* fp = S.fp;
+    unsigned long long vis = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        const uint32_t p = P.base + i;
+        const LightDev& L = fp->lights[light_of(fp, p)];
+        if (!L.moved) continue;
+        uchar4 m = P.meta[i];
+        if (m.z != kLive) continue;
+        if (L.kind == PRX_LIGHT_POINT || L.kind == PRX_LIGHT_SPOT) {
+            P.origin[i] = make_float4(L.position.x, L.position.y, L.position.z, 0.f);
+            if (m.x > 0) {
+                const V3 primary = ld3(P.pos_obj[i]);
+                const V3 to = sub(primary, L.position);
+                const float dist = length(to);
+                if (dist <= S.eps) {
+                    m.z = kReplace;
+                    P.meta[i] = m;
+                    continue;
+                }
+                const V3 dir = divs(to, dist);
+                P.emis[i] = make_float4(dir.x, dir.y, dir.z, 0.f);
+                ++vis;
+                if (occluded(S, L.position, dir, S.eps, dist - S.eps)) {
+                    m.z = kReplace;
+                    P.meta[i] = m;
+                }
+            }
+        } else {
+            if (m.x > 0) {
+                const V3 d = ld3(P.emis[i]);
+                const V3 primary = ld3(P.pos_obj[i]);
+                const float denom = dot(d, L.normal);
+                if (denom <= 1e-6f) {
+                    m.z = kReplace;
+                    P.meta[i] = m;
+                    continue;
+                }
+                const float s = dot(sub(primary, L.position), L.normal) / denom;
+                if (s <= 0.0f) {
+                    m.z = kReplace;
+                    P.meta[i] = m;
+                    continue;
+                }
+                const V3 o = sub(primary, mul(d, s));
+                P.origin[i] = make_float4(o.x, o.y, o.z, 0.f);
+            } else {
+                const float4 c4 = P.canon[i];
+                const float c[4] = {c4.x, c4.y, c4.z, c4.w};
+                V3 o, d;
+                warp_canonical(L, c, o, d);
+                P.origin[i] = make_float4(o.x, o.y, o.z, 0.f);
+            }
+        }
+    }
+    warp_add(&ctr->vis, vis);
+}
+
+// compute_flag_mask (engine.cpp:172-199) with segment ends per Engine::segment_end
+// (engine.cpp:135-139); occlusion boxes staged in shared memory.
+__global__ void __launch_bounds__(kT) k_occlusion_flags(SceneDev S, PathDev P, int mode, int record,
+                                                        uint32_t* list, uint32_t* masks, Counters* ctr) {
+    __shared__ Box boxes[kMaxDyn];
+    const FrameParams* fp = S.fp;
+    const uint32_t nb = fp->n_boxes;
+    for (uint32_t k = threadIdx.x; k < nb; k += blockDim.x) boxes[k] = fp->boxes[k];
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        const uchar4 m = P.meta[i];
+        if (m.z != kLive) continue;
+        const uint32_t k = m.x, segs = m.x + m.y;
+        uint32_t mask = 0;
+        V3 prev = ld3(P.origin[i]);
+        uint32_t prev_obj = kInvalidObj;
+        for (uint32_t s = 0; s < segs; ++s) {
+            V3 cur{0, 0, 0};
+            uint32_t cur_obj = kInvalidObj;
+            if (s < k) {
+                const float4 v = P.pos_obj[vix(P, s, i)];
+                cur = ld3(v);
+                cur_obj = __float_as_uint(v.w);
+            }
+            bool flagged = false;
+            if (s > 0 && prev_obj != kInvalidObj && (__ldg(&S.oflags[prev_obj]) & 1u)) flagged = true;
+            if (!flagged && s < k && cur_obj != kInvalidObj && (__ldg(&S.oflags[cur_obj]) & 1u)) flagged = true;
+            if (!flagged) {
+                V3 b = cur;
+                if (s >= k) {  // escape segment, clipped to twice the diagonal
+                    const V3 dir = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
+                    b = add(prev, mul(dir, S.two_diag));
+                }
+                for (uint32_t j = 0; j < nb; ++j) {
+                    if (segment_box(prev, b, boxes[j])) {
+                        flagged = true;
+                        break;
+                    }
+                }
+            }
+            if (flagged) mask |= 1u << s;
+            prev = cur;
+            prev_obj = cur_obj;
+        }
+        if (record) P.seg_flags[i] = mask;
+        if (mask == 0) continue;
+        if (mode == PRX_MODE_NAIVE) {
+            P.rstart[i] = (uint8_t)(__ffs(mask) - 1);
+        } else {
+            const uint32_t slot = (uint32_t)atomicAdd(&ctr->flagged, 1ull);
+            list[slot] = i;
+            masks[slot] = mask;
+        }
+    }
+}
+
+// verify_path_error_based (engine.cpp:339-403): Alg. 1 walk over the flagged segments.
+__global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, float threshold,
+                                                     const uint32_t* __restrict__ list,
+                                                     const uint32_t* __restrict__ masks,
+                                                     const Counters* cnt, Counters* ctr) {
+    const FrameParams* fp = S.fp;
+    const uint32_t n_list = (uint32_t)cnt->flagged;
+    unsigned long long vis = 0;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_list; j += gridDim.x * blockDim.x) {
+        const uint32_t i = list[j];
+        const uint32_t flags = masks[j];
+        const uint32_t p = P.base + i;
+        const LightDev& L = fp->lights[light_of(fp, p)];
+        uchar4 m = P.meta[i];
+        const uint32_t k = m.x, segs = m.x + m.y;
+        const uint32_t epoch = P.epoch[i];
+        bool force = false;
+        uint32_t s = 0;
+        while (s < segs) {
+            const bool flagged = force || ((flags >> s) & 1u);
+            force = false;
+            if (!flagged) {
+                ++s;
+                continue;
+            }
+            const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, s - 1, i)]);
+            const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
+            ++vis;
+            Hit h;
+            const bool hit = intersect_scene(S, o, d, S.eps, h);
+            if (s == k) {  // escape segment: a new blocker -> retrace from here
+                if (hit) P.rstart[i] = (uint8_t)s;
+                break;
+            }
+            if (!hit) {  // destination gone: truncate and escape
+                truncate_path(P, i, s, true, m);
+                P.meta[i] = m;
+                break;
+            }
+            const size_t v = vix(P, s, i);
+            const float4 stored = P.energy[v];
+            const V3 e_prev = s == 0 ? L.flux_pp : ld3(P.energy[vix(P, s - 1, i)]);
+            const float4 am = __ldg(&S.mat[h.obj]);
+            const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
+            const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
+            if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
+                P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
+                P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+                P.energy[v] = make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius);
+                const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
+                P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
+                P.rstart[i] = (uint8_t)(s + 1);
+                break;
+            }
+            const V3 old_pos = ld3(P.pos_obj[v]);
+            const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
+            P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
+            P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+            if (s + 1 >= segs) break;
+            const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
+            if (close_pos && !hit_dyn && !((flags >> (s + 1)) & 1u)) {
+                s += 2;
+                continue;
+            }
+            if (s + 1 < k) {
+                const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
+                const V3 od = normalized(sub(next, h.pos));
+                P.out_dir[v] = make_float4(od.x, od.y, od.z, 0.f);
+            }
+            force = true;
+            ++s;
+        }
+    }
+    warp_add(&ctr->vis, vis);
+}
+
+__global__ void __launch_bounds__(kT) k_compute_dm(SceneDev S, PathDev P, Counters* ctr) {
+    const FrameParams* fp = S.fp;
+    unsigned long long replaced = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        uchar4 m = P.meta[i];
+        if (m.z == kDead) continue;
+        bool ok = m.z == kLive;
+        if (ok) {
+            const LightDev& L = fp->lights[light_of(fp, P.base + i)];
+            float c[4];
+            ok = canonical_of(L, ld3(P.origin[i]), ld3(P.emis[i]), c);
+            if (ok) {
+                P.canon[i] = make_float4(c[0], c[1], c[2], c[3]);
+                const uint32_t cell = cell_of(L, c);
+                P.cell[i] = cell;
+                atomicAdd(&L.dm_c[cell], 1u);
+            }
+        }
+        if (!ok) {
+            truncate_path(P, i, 0, false, m);
+            m.z = kDead;
+            P.meta[i] = m;
+            ++replaced;
+        }
+    }
+    warp_add(&ctr->replaced, replaced);
+}
+
+// ---------------------------------------------------------------- prune (engine.cpp:443-497)
+__global__ void k_prune_mark(SceneDev S, PathDev P, uint32_t frame, uint32_t* const* unmarked,
+                             uint8_t* pruned, uint8_t* cand) {
+    const FrameParams* fp = S.fp;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        pruned[i] = 0;
+        cand[i] = 0;
+        if (P.meta[i].z != kLive) continue;
+        const uint32_t p = P.base + i;
+        const uint32_t li = light_of(fp, p);
+        const LightDev& L = fp->lights[li];
+        const uint32_t c = P.cell[i];
+        const uint32_t dmc = L.dm_c[c], dmt = L.dm_t[c];
+        if (dmc <= dmt) continue;
+        const double prob = prune_probability(dmc, dmt);
+        const float u = rng_uniform_m(S.seed_mix, p, frame, 0, kPruneMark, 0);
+        if (prob > 0.0 && (double)u < prob) {
+            pruned[i] = 1;
+        } else {
+            cand[i] = 1;
+            atomicAdd(&unmarked[li][c], 1u);
+        }
+    }
+}
+
+// candidates in cells whose (global) survivor count exceeds the target need a trim
+__global__ void k_prune_trim_flags(PathDev P, const FrameParams* fp, uint32_t* const* unm_total,
+                                   const uint8_t* cand, uint8_t* trim) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        uint8_t f = 0;
+        if (cand[i]) {
+            const uint32_t li = light_of(fp, P.base + i);
+            const uint32_t c = P.cell[i];
+            f = unm_total[li][c] > fp->lights[li].dm_t[c] ? 1 : 0;
+        }
+        trim[i] = f;
+    }
+}
+
+__global__ void k_prune_keys(PathDev P, const FrameParams* fp, const uint32_t* list, const uint32_t* count,
+                             uint32_t* keys, uint32_t* vals) {
+    const uint32_t n = *count;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t i = list[j];
+        keys[j] = (light_of(fp, P.base + i) << 22) | P.cell[i];
+        vals[j] = i;
+    }
+}
+
+// keys sorted by (light, cell), stable in path id: survivors are the dm_t lowest ids
+// (select_paths_to_prune trims "from the top path id down", engine.cpp:459-466).
+__global__ void k_prune_heads(const uint32_t* keys, const uint32_t* count, uint32_t* const* seg_start) {
+    const uint32_t n = *count;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[j];
+        if (j == 0 || keys[j - 1] != k) seg_start[k >> 22][k & 0x3FFFFFu] = j;
+    }
+}
+
+__global__ void k_prune_trim(const FrameParams* fp, const uint32_t* keys, const uint32_t* vals,
+                             const uint32_t* count, uint32_t* const* seg_start, uint32_t* const* prefix,
+                             uint8_t* pruned) {
+    const uint32_t n = *count;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[j];
+        const uint32_t li = k >> 22, c = k & 0x3FFFFFu;
+        const uint32_t rank = j - seg_start[li][c] + (prefix ? prefix[li][c] : 0u);
+        if (rank >= fp->lights[li].dm_t[c]) pruned[vals[j]] = 1;
+    }
+}
+
+__global__ void k_prune_apply(PathDev P, const uint8_t* pruned) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        if (!pruned[i]) continue;
+        uchar4 m = P.meta[i];
+        truncate_path(P, i, 0, false, m);
+        m.z = kDead;
+        P.meta[i] = m;
+    }
+}
+
+__global__ void k_dm_after_prune(uint32_t* dm_c, const uint32_t* dm_t, const uint32_t* unm, uint32_t cells) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x) {
+        const uint32_t a = dm_c[c], t = dm_t[c];
+        if (a > t) dm_c[c] = unm[c] < t ? unm[c] : t;
+    }
+}
+
+// ---------------------------------------------------------------- fill (engine.cpp:499-546)
+__global__ void k_fill_need(const uint32_t* dm_t, const uint32_t* dm_c, uint32_t* need, uint32_t cells) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x)
+        need[c] = dm_t[c] > dm_c[c] ? dm_t[c] - dm_c[c] : 0u;
+}
+
+__global__ void k_dead_flags(PathDev P, uint32_t lb, uint32_t le, uint8_t* flags) {
+    for (uint32_t i = lb + blockIdx.x * blockDim.x + threadIdx.x; i < le; i += gridDim.x * blockDim.x)
+        flags[i - lb] = P.meta[i].z == kDead ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kT) k_fill_assign(SceneDev S, PathDev P, uint32_t li,
+                                                    const uint32_t* dead, const uint32_t* dead_count,
+                                                    uint64_t dead_prefix, const uint32_t* need_off,
+                                                    const uint32_t* need_total, uint32_t cells,
+                                                    Counters* ctr) {
+    const LightDev& L = S.fp->lights[li];
+    const uint32_t nd = *dead_count;
+    const uint64_t total = *need_total;
+    unsigned long long filled = 0;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += gridDim.x * blockDim.x) {
+        const uint64_t u = dead_prefix + j;
+        if (u >= total) continue;
+        // cell c with need_off[c] <= u < need_off[c] + need[c]: last c with need_off[c] <= u
+        uint32_t lo = 0, hi = cells;  // invariant: need_off[lo] <= u, answer in [lo, hi)
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((uint64_t)need_off[mid] <= u) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t c = lo;
+        const uint32_t i = dead[j];
+        const uint32_t p = P.base + i;
+        const uint32_t epoch = P.epoch[i] + 1;
+        P.epoch[i] = epoch;
+        float cc[4];
+        V3 o, d;
+        sample_in_cell(L, c, S.seed_mix, p, epoch, cc, o, d);
+        P.origin[i] = make_float4(o.x, o.y, o.z, 0.f);
+        P.emis[i] = make_float4(d.x, d.y, d.z, 0.f);
+        P.canon[i] = make_float4(cc[0], cc[1], cc[2], cc[3]);
+        P.cell[i] = c;
+        P.meta[i] = make_uchar4(0, 0, kLive, 1);
+        P.rstart[i] = 0;
+        ++filled;
+    }
+    warp_add(&ctr->filled, filled);
+}
+
+// fill's slot-exhaustion check (engine.cpp:512-513): single-shard form
+__global__ void k_fill_check(const uint32_t* dead_count, const uint32_t* need_total, Counters* ctr) {
+    if (*need_total > *dead_count) atomicAdd(&ctr->fill_overflow, 1ull);
+}
+
+__global__ void k_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += gridDim.x * blockDim.x)
+        dm_c[c] = dm_c[c] < dm_t[c] ? dm_t[c] : dm_c[c];
+}
+
+// ---------------------------------------------------------------- trace (engine.cpp:548-598)
+__global__ void k_retrace_flags(PathDev P, uint8_t* flags) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x)
+        flags[i] = (P.meta[i].z == kLive && P.rstart[i] != kNoRetrace) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kT) k_trace(SceneDev S, PathDev P, const uint32_t* __restrict__ list,
+                                              const uint32_t* count, Counters* ctr) {
+    const FrameParams* fp = S.fp;
+    const uint32_t n = *count;
+    unsigned long long traced = 0;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t i = list[j];
+        const uint32_t p = P.base + i;
+        const LightDev& L = fp->lights[light_of(fp, p)];
+        uchar4 m = P.meta[i];
+        const uint32_t epoch = P.epoch[i];
+        uint32_t b = P.rstart[i];
+        V3 pos = b == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, b - 1, i)]);
+        V3 dir = b == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, b - 1, i)]);
+        V3 energy = b == 0 ? L.flux_pp : ld3(P.energy[vix(P, b - 1, i)]);
+        bool escaped = false;
+        while (b < P.B) {
+            ++traced;
+            Hit h;
+            if (!intersect_scene(S, pos, dir, S.eps, h)) {
+                escaped = true;
+                break;
+            }
+            const float4 am = __ldg(&S.mat[h.obj]);
+            energy = mulv(energy, V3{am.x, am.y, am.z});
+            const size_t v = vix(P, b, i);
+            P.in_dir[v] = make_float4(dir.x, dir.y, dir.z, 0.f);
+            P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+            P.energy[v] = make_float4(energy.x, energy.y, energy.z, S.gather_radius);
+            const V3 out = sample_bounce(S, h.obj, h.normal, dir, p, epoch, b + 1);
+            P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
+            pos = h.pos;
+            dir = out;
+            ++b;
+        }
+        truncate_path(P, i, b, escaped, m);
+        P.meta[i] = m;
+    }
+    warp_add(&ctr->traced, traced);
+}
+
+// segment accounting + refresh_path_info (engine.cpp:586-610) for every live path
+__global__ void k_finalize(PathDev P, Counters* ctr) {
+    unsigned long long segs_sum = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        const uchar4 m = P.meta[i];
+        if (m.z != kLive) continue;
+        const uint32_t segs = m.x + m.y;
+        segs_sum += segs;
+        const uint8_t st = P.rstart[i];
+        const uint32_t start = st == kNoRetrace ? 0u : (st < 15 ? st : 15u);
+        P.path_info[i] = pack_path_info(P.cell[i], segs > 1 ? segs : 1u, start, false, m.w == 0);
+    }
+    warp_add(&ctr->segments, segs_sum);
+}
+
+// ---------------------------------------------------------------- layout conversion
+struct PhotonRec {  // photon_store.hpp:13-21
+    float dx, dy, dz;
+    uint32_t obj;
+    float ex, ey, ez;
+    float radius;
+};
+struct AuxRec {  // photon_store.hpp:75-78
+    float px, py, pz, ox, oy, oz;
+};
+
+__global__ void k_pack(PathDev P, PhotonRec* ph, AuxRec* aux) {
+    const size_t total = (size_t)P.n * P.B;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
+        const float4 po = P.pos_obj[v], en = P.energy[v], in = P.in_dir[v], od = P.out_dir[v];
+        if (ph) ph[v] = PhotonRec{in.x, in.y, in.z, __float_as_uint(po.w), en.x, en.y, en.z, en.w};
+        if (aux) aux[v] = AuxRec{po.x, po.y, po.z, od.x, od.y, od.z};
+    }
+}
+
+__global__ void k_unpack(PathDev P, const PhotonRec* ph, const AuxRec* aux) {
+    const size_t total = (size_t)P.n * P.B;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
+        if (ph) {
+            const PhotonRec r = ph[v];
+            P.in_dir[v] = make_float4(r.dx, r.dy, r.dz, 0.f);
+            P.energy[v] = make_float4(r.ex, r.ey, r.ez, r.radius);
+            P.pos_obj[v].w = __uint_as_float(r.obj);
+        }
+        if (aux) {
+            const AuxRec a = aux[v];
+            P.pos_obj[v].x = a.px;
+            P.pos_obj[v].y = a.py;
+            P.pos_obj[v].z = a.pz;
+            P.out_dir[v] = make_float4(a.ox, a.oy, a.oz, 0.f);
+        }
+    }
+}
+
+}  // namespace
+
+#define LAUNCH(kernel, n, ...)                                                   \
+    do {                                                                         \
+        kernel<<<launch_grid((n), kT), kT, 0, st>>>(__VA_ARGS__);               \
+        ++g_launches;                                                            \
+    } while (0)
+
+void launch_init_dm_target(const LightDev* L, uint32_t n, uint64_t seed_mix, uint32_t* dm_t,
+                           cudaStream_t st) {
+    LAUNCH(k_init_dm_target, n, *L, n, seed_mix, dm_t);
+}
+void launch_transform_dynamic(const float4* local, const uint32_t* tri_xf, const float4* xf, uint32_t n,
+                              float4* world, cudaStream_t st) {
+    if (n) LAUNCH(k_transform_dynamic, n, local, tri_xf, xf, n, world);
+}
+void launch_frame_reset(PathDev P, int record, Counters* ctr, cudaStream_t st) {
+    LAUNCH(k_frame_reset, P.n, P, record, ctr);
+}
+void launch_release_all(PathDev P, cudaStream_t st) { LAUNCH(k_release_all, P.n, P); }
+void launch_update_origins(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st) {
+    LAUNCH(k_update_origins, P.n, S, P, ctr);
+}
+void launch_occlusion_flags(SceneDev S, PathDev P, int mode, int record, uint32_t* list, uint32_t* masks,
+                            Counters* ctr, cudaStream_t st) {
+    LAUNCH(k_occlusion_flags, P.n, S, P, mode, record, list, masks, ctr);
+}
+void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t* list, const uint32_t* masks,
+                         const Counters* cnt, Counters* ctr, uint32_t n_max, cudaStream_t st) {
+    LAUNCH(k_verify_error, n_max, S, P, threshold, list, masks, cnt, ctr);
+}
+void launch_compute_dm(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st) {
+    LAUNCH(k_compute_dm, P.n, S, P, ctr);
+}
+void launch_prune_mark(SceneDev S, PathDev P, uint32_t frame, uint32_t* const* unmarked, uint8_t* pruned,
+                       uint8_t* cand, cudaStream_t st) {
+    LAUNCH(k_prune_mark, P.n, S, P, frame, unmarked, pruned, cand);
+}
+void launch_prune_trim_flags(PathDev P, const FrameParams* fp, uint32_t* const* unm_total, const uint8_t* cand,
+                             uint8_t* trim, cudaStream_t st) {
+    LAUNCH(k_prune_trim_flags, P.n, P, fp, unm_total, cand, trim);
+}
+void launch_prune_keys(PathDev P, const FrameParams* fp, const uint32_t* list, const uint32_t* count,
+                       uint32_t* keys, uint32_t* vals, uint32_t n_max, cudaStream_t st) {
+    LAUNCH(k_prune_keys, n_max, P, fp, list, count, keys, vals);
+}
+void launch_prune_trim(PathDev P, const FrameParams* fp, const uint32_t* keys, const uint32_t* vals,
+                       const uint32_t* count, uint32_t n_max, uint32_t* const* seg_start,
+                       uint32_t* const* prefix, uint8_t* pruned, cudaStream_t st) {
+    (void)P;
+    LAUNCH(k_prune_heads, n_max, keys, count, seg_start);
+    LAUNCH(k_prune_trim, n_max, fp, keys, vals, count, seg_start, prefix, pruned);
+}
+void launch_prune_apply(PathDev P, const uint8_t* pruned, cudaStream_t st) {
+    LAUNCH(k_prune_apply, P.n, P, pruned);
+}
+void launch_dm_after_prune(uint32_t* dm_c, const uint32_t* dm_t, const uint32_t* unm, uint32_t cells,
+                           cudaStream_t st) {
+    LAUNCH(k_dm_after_prune, cells, dm_c, dm_t, unm, cells);
+}
+void launch_fill_need(const uint32_t* dm_t, const uint32_t* dm_c, uint32_t* need, uint32_t cells,
+                      cudaStream_t st) {
+    LAUNCH(k_fill_need, cells, dm_t, dm_c, need, cells);
+}
+void launch_dead_flags(PathDev P, uint32_t lb, uint32_t le, uint8_t* flags, cudaStream_t st) {
+    if (le > lb) LAUNCH(k_dead_flags, le - lb, P, lb, le, flags);
+}
+void launch_fill_assign(SceneDev S, PathDev P, uint32_t li, const uint32_t* dead, const uint32_t* dead_count,
+                        uint32_t n_max, uint64_t dead_prefix, const uint32_t* need_off,
+                        const uint32_t* need_total, uint32_t cells, Counters* ctr, cudaStream_t st) {
+    LAUNCH(k_fill_assign, n_max, S, P, li, dead, dead_count, dead_prefix, need_off, need_total, cells, ctr);
+}
+void launch_fill_check(const uint32_t* dead_count, const uint32_t* need_total, Counters* ctr,
+                       cudaStream_t st) {
+    k_fill_check<<<1, 1, 0, st>>>(dead_count, need_total, ctr);
+    ++g_launches;
+}
+void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st) {
+    LAUNCH(k_dm_after_fill, cells, dm_c, dm_t, cells);
+}
+void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st) {
+    LAUNCH(k_retrace_flags, P.n, P, flags);
+}
+void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count, uint32_t n_max,
+                  Counters* ctr, cudaStream_t st) {
+    LAUNCH(k_trace, n_max, S, P, list, count, ctr);
+}
+void launch_finalize(PathDev P, Counters* ctr, cudaStream_t st) { LAUNCH(k_finalize, P.n, P, ctr); }
+void launch_pack_photons(PathDev P, void* photons, void* aux, cudaStream_t st) {
+    LAUNCH(k_pack, (uint64_t)P.n * P.B, P, static_cast<PhotonRec*>(photons), static_cast<AuxRec*>(aux));
+}
+void launch_unpack_photons(PathDev P, const void* photons, const void* aux, cudaStream_t st) {
+    LAUNCH(k_unpack, (uint64_t)P.n * P.B, P, static_cast<const PhotonRec*>(photons),
+           static_cast<const AuxRec*>(aux));
+}
+
+}  // namespace prx

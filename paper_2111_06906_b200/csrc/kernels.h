@@ -1,0 +1,87 @@
+// kernels.h -- host-callable launchers of the engine's stage kernels (kernels.cu,
+// lbvh.cu, splat.cu).  Each launcher cites the reference function its kernel replaces.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dev_types.h"
+
+namespace prx {
+
+int launch_grid(uint64_t n, int threads);
+extern uint64_t g_launches;  // kernels launched by this library (bench evidence)
+
+// dm_t histogram of init_dm_target (light.cpp:230-252)
+void launch_init_dm_target(const LightDev* light_host, uint32_t n_samples, uint64_t seed_mix,
+                           uint32_t* dm_t, cudaStream_t st);
+// per-dynamic-triangle placement: transform_triangle (transform.hpp:98-100) for the frame
+void launch_transform_dynamic(const float4* local_tris, const uint32_t* tri_xf, const float4* xf,
+                              uint32_t n_tris, float4* world_tris, cudaStream_t st);
+// run_frame prelude resets (engine.cpp:223-226) + live-segment count
+void launch_frame_reset(PathDev P, int record_flags, Counters* ctr, cudaStream_t st);
+// release_all_paths (engine.cpp:149-157)
+void launch_release_all(PathDev P, cudaStream_t st);
+// stage_update_origins (engine.cpp:244-304)
+void launch_update_origins(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st);
+// stage_occlusions naive / flag pass (engine.cpp:306-337 + compute_flag_mask :172-199)
+void launch_occlusion_flags(SceneDev S, PathDev P, int mode, int record, uint32_t* list,
+                            uint32_t* masks, Counters* ctr, cudaStream_t st);
+// verify_path_error_based (engine.cpp:339-403) over the flagged list
+void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t* list,
+                         const uint32_t* masks, const Counters* ctr_count, Counters* ctr,
+                         uint32_t n_max, cudaStream_t st);
+// stage_compute_dm (engine.cpp:405-441)
+void launch_compute_dm(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st);
+// stage_prune (engine.cpp:443-497): marks + per-cell unmarked counts
+void launch_prune_mark(SceneDev S, PathDev P, uint32_t frame, uint32_t* const* unmarked,
+                       uint8_t* pruned, uint8_t* cand, cudaStream_t st);
+void launch_prune_trim_flags(PathDev P, const FrameParams* fp, uint32_t* const* unm_total,
+                             const uint8_t* cand, uint8_t* trim, cudaStream_t st);
+void launch_prune_keys(PathDev P, const FrameParams* fp, const uint32_t* list, const uint32_t* count,
+                       uint32_t* keys, uint32_t* vals, uint32_t n_max, cudaStream_t st);
+void launch_prune_trim(PathDev P, const FrameParams* fp, const uint32_t* keys, const uint32_t* vals,
+                       const uint32_t* count, uint32_t n_max, uint32_t* const* seg_start,
+                       uint32_t* const* prefix, uint8_t* pruned, cudaStream_t st);
+void launch_prune_apply(PathDev P, const uint8_t* pruned, cudaStream_t st);
+void launch_dm_after_prune(uint32_t* dm_c, const uint32_t* dm_t, const uint32_t* unm_total,
+                           uint32_t cells, cudaStream_t st);
+// stage_fill (engine.cpp:499-546)
+void launch_fill_need(const uint32_t* dm_t, const uint32_t* dm_c, uint32_t* need, uint32_t cells,
+                      cudaStream_t st);
+void launch_dead_flags(PathDev P, uint32_t lb, uint32_t le, uint8_t* flags, cudaStream_t st);
+void launch_fill_assign(SceneDev S, PathDev P, uint32_t light, const uint32_t* dead,
+                        const uint32_t* dead_count, uint32_t n_max, uint64_t dead_prefix,
+                        const uint32_t* need_off, const uint32_t* need_total, uint32_t cells,
+                        Counters* ctr, cudaStream_t st);
+void launch_fill_check(const uint32_t* dead_count, const uint32_t* need_total, Counters* ctr,
+                       cudaStream_t st);
+void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st);
+// stage_trace (engine.cpp:548-598)
+void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st);
+void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count,
+                  uint32_t n_max, Counters* ctr, cudaStream_t st);
+void launch_finalize(PathDev P, Counters* ctr, cudaStream_t st);
+// layout conversion for drop-in accessors
+void launch_pack_photons(PathDev P, void* photons, void* aux, cudaStream_t st);
+void launch_unpack_photons(PathDev P, const void* photons, const void* aux, cudaStream_t st);
+
+// G-buffer + splat + resolve (splat.cu), replacing gather_image (gather.cpp:35-75)
+void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img,
+                  float inv_pi, float inv_area, cudaStream_t st);
+
+// Dynamic LBVH (lbvh.cu)
+struct LbvhBuffers {
+    uint32_t* keys;
+    uint32_t* vals;
+    uint32_t* keys_tmp;
+    uint32_t* vals_tmp;
+    uint32_t* parent;     // per node/leaf parent index
+    uint32_t* flags;      // refit arrival counters
+    void* scratch;
+};
+void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint32_t n_tris,
+                        const DynObj* dyn_host, uint32_t n_dyn, const DynObj* dyn_dev,
+                        float4* nodes, uint32_t* leaf, const LbvhBuffers& buf, cudaStream_t st);
+
+}  // namespace prx

@@ -1,0 +1,172 @@
+// lbvh.cu -- per-frame LBVH over every dynamic object (north_star subsystem 2).
+//
+// The reference brute-forces dynamic meshes behind an AABB gate (scene.cpp:153-165,
+// bvh.cpp:108-117) -- its dominant CPU cost.  Here each dynamic object
+// with more than 32 triangles gets a fresh binary radix tree every frame it moves:
+//   1. 24-bit Morton code of each triangle centroid inside the object's current bounds,
+//      keyed (object << 24 | morton), value = object-local triangle index;
+//   2. one stable LSD radix sort over all dynamic triangles (prims.cu);
+//   3. Karras 2012 hierarchy per object (ties broken by sorted position);
+//   4. bottom-up refit with arrival counters; child boxes are stored in the parent and
+//      inflated so the float culling of dyn_closest/dyn_any stays conservative.
+// The query result is the (t, index)-lexicographic minimum over the object's triangles,
+// identical to the reference's linear scan (device_scene.cuh: dyn_closest).
+#include "device_scene.cuh"
+#include "kernels.h"
+#include "prims.h"
+
+namespace prx {
+
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ uint32_t spread8(uint32_t x) {  // 8 bits -> every 3rd bit
+    x &= 0xFFu;
+    x = (x | (x << 8)) & 0x0300F00Fu;
+    x = (x | (x << 4)) & 0x030C30C3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
+__global__ void k_morton(const float4* __restrict__ tris, const uint32_t* __restrict__ tri_obj, uint32_t n,
+                         const DynObj* __restrict__ dyn, uint32_t* keys, uint32_t* vals) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const uint32_t j = tri_obj[t];
+        const DynObj D = dyn[j];
+        const float4 a = tris[3 * t], e1 = tris[3 * t + 1], e2 = tris[3 * t + 2];
+        const float cx = a.x + (e1.x + e2.x) * (1.0f / 3.0f);
+        const float cy = a.y + (e1.y + e2.y) * (1.0f / 3.0f);
+        const float cz = a.z + (e1.z + e2.z) * (1.0f / 3.0f);
+        auto q = [](float v, float lo, float hi) {
+            const float ext = hi - lo;
+            float u = ext > 0.0f ? (v - lo) / ext : 0.5f;
+            u = fminf(fmaxf(u, 0.0f), 1.0f);
+            return (uint32_t)fminf(u * 256.0f, 255.0f);
+        };
+        const uint32_t m = (spread8(q(cx, D.cur.lo.x, D.cur.hi.x)) << 2) |
+                           (spread8(q(cy, D.cur.lo.y, D.cur.hi.y)) << 1) | spread8(q(cz, D.cur.lo.z, D.cur.hi.z));
+        keys[t] = (j << 24) | m;
+        vals[t] = t - D.tri_begin;
+    }
+}
+
+__device__ __forceinline__ int delta(const uint32_t* __restrict__ k, int n, int i, int j) {
+    if (j < 0 || j >= n) return -1;
+    const uint32_t a = k[i] & 0xFFFFFFu, b = k[j] & 0xFFFFFFu;
+    if (a == b) return 32 + __clz((uint32_t)(i ^ j));
+    return __clz(a ^ b);
+}
+
+// Karras 2012, one thread per internal node of every object; `keys` sorted.
+__global__ void k_karras(const uint32_t* __restrict__ keys, uint32_t n_all, const DynObj* __restrict__ dyn,
+                         float4* nodes, uint32_t* parent, uint32_t n_leaf_total) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_all; t += gridDim.x * blockDim.x) {
+        const uint32_t j = keys[t] >> 24;
+        const DynObj D = dyn[j];
+        if (D.node_begin == kLbvhBrute) continue;
+        const int n = (int)D.tri_count;
+        const int i = (int)(t - D.tri_begin);
+        if (i >= n - 1) continue;
+        const uint32_t* k = keys + D.tri_begin;
+        const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
+        const int dmin = delta(k, n, i, i - d);
+        int lmax = 2;
+        while (delta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
+        int l = 0;
+        for (int s = lmax >> 1; s >= 1; s >>= 1)
+            if (delta(k, n, i, i + (l + s) * d) > dmin) l += s;
+        const int jj = i + l * d;
+        const int dnode = delta(k, n, i, jj);
+        int s = 0;
+        int div = 2;
+        int step = (l + div - 1) / div;
+        while (true) {
+            if (delta(k, n, i, i + (s + step) * d) > dnode) s += step;
+            if (step <= 1) break;
+            div <<= 1;
+            step = (l + div - 1) / div;
+        }
+        const int g = i + s * d + (d < 0 ? -1 : 0);
+        const int lo = i < jj ? i : jj, hi = i < jj ? jj : i;
+        const uint32_t left = (lo == g) ? (kLeafBit | (uint32_t)g) : (uint32_t)g;
+        const uint32_t right = (hi == g + 1) ? (kLeafBit | (uint32_t)(g + 1)) : (uint32_t)(g + 1);
+        float4* N = nodes + 4ull * (D.node_begin + i);
+        N[0].w = __uint_as_float(left);
+        N[2].w = __uint_as_float(right);
+        // parents: leaves by sorted position, internals after n_leaf_total
+        const uint32_t me = D.node_begin + (uint32_t)i;
+        if (left & kLeafBit) parent[D.tri_begin + g] = me;
+        else parent[n_leaf_total + D.node_begin + g] = me;
+        if (right & kLeafBit) parent[D.tri_begin + g + 1] = me;
+        else parent[n_leaf_total + D.node_begin + g + 1] = me;
+        if (i == 0) parent[n_leaf_total + D.node_begin] = 0xFFFFFFFFu;
+    }
+}
+
+// Bottom-up refit: each leaf walks up; the second arrival at a node unions its children.
+__global__ void k_refit(const float4* __restrict__ tris, const uint32_t* __restrict__ keys,
+                        const uint32_t* __restrict__ leaf, uint32_t n_all, const DynObj* __restrict__ dyn,
+                        float4* nodes, const uint32_t* __restrict__ parent, uint32_t* flags,
+                        uint32_t n_leaf_total) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_all; t += gridDim.x * blockDim.x) {
+        const uint32_t j = keys[t] >> 24;
+        const DynObj D = dyn[j];
+        if (D.node_begin == kLbvhBrute) continue;
+        const uint32_t pos = t - D.tri_begin;
+        const uint32_t tri = D.tri_begin + leaf[t];
+        const float4 a = tris[3 * tri], e1 = tris[3 * tri + 1], e2 = tris[3 * tri + 2];
+        const float ext = fmaxf(fmaxf(D.cur.hi.x - D.cur.lo.x, D.cur.hi.y - D.cur.lo.y), D.cur.hi.z - D.cur.lo.z);
+        const float bx = a.x + e1.x, by = a.y + e1.y, bz = a.z + e1.z;
+        const float cx = a.x + e2.x, cy = a.y + e2.y, cz = a.z + e2.z;
+        float lox = fminf(a.x, fminf(bx, cx)), hix = fmaxf(a.x, fmaxf(bx, cx));
+        float loy = fminf(a.y, fminf(by, cy)), hiy = fmaxf(a.y, fmaxf(by, cy));
+        float loz = fminf(a.z, fminf(bz, cz)), hiz = fmaxf(a.z, fmaxf(bz, cz));
+        const float mag = fmaxf(fmaxf(fabsf(lox), fabsf(hix)), fmaxf(fmaxf(fabsf(loy), fabsf(hiy)),
+                                                                      fmaxf(fabsf(loz), fabsf(hiz))));
+        const float m = 1e-5f * ext + 4e-6f * mag + 1e-30f;
+        lox -= m, loy -= m, loz -= m, hix += m, hiy += m, hiz += m;
+        uint32_t child = kLeafBit | pos;
+        uint32_t p = parent[D.tri_begin + pos];
+        while (p != 0xFFFFFFFFu) {
+            float4* N = nodes + 4ull * p;
+            const bool is_left = __float_as_uint(__ldcg(&N[0].w)) == child;
+            const int o = is_left ? 0 : 2;
+            N[o].x = lox, N[o].y = loy, N[o].z = loz;
+            N[o + 1] = make_float4(hix, hiy, hiz, 0.f);
+            __threadfence();
+            if (atomicAdd(&flags[p], 1u) == 0) break;  // sibling not done yet
+            __threadfence();
+            const int q = is_left ? 2 : 0;
+            const float4 smin = __ldcg(&N[q]), smax = __ldcg(&N[q + 1]);
+            lox = fminf(lox, smin.x), loy = fminf(loy, smin.y), loz = fminf(loz, smin.z);
+            hix = fmaxf(hix, smax.x), hiy = fmaxf(hiy, smax.y), hiz = fmaxf(hiz, smax.z);
+            child = p - D.node_begin;
+            p = parent[n_leaf_total + p];
+        }
+    }
+}
+
+__global__ void k_copy_leaf(const uint32_t* __restrict__ vals, uint32_t n, uint32_t* leaf) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) leaf[t] = vals[t];
+}
+
+}  // namespace
+
+void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint32_t n_tris,
+                        const DynObj* dyn_host, uint32_t n_dyn, const DynObj* dyn_dev, float4* nodes,
+                        uint32_t* leaf, const LbvhBuffers& buf, cudaStream_t st) {
+    (void)dyn_host;
+    (void)n_dyn;
+    if (n_tris == 0) return;
+    const int g = launch_grid(n_tris, kT);
+    k_morton<<<g, kT, 0, st>>>(world_tris, tri_obj, n_tris, dyn_dev, buf.keys, buf.vals);
+    radix_sort_pairs(buf.keys, buf.vals, buf.keys_tmp, buf.vals_tmp, n_tris, nullptr, 31, buf.scratch, st);
+    k_copy_leaf<<<g, kT, 0, st>>>(buf.vals, n_tris, leaf);
+    k_karras<<<g, kT, 0, st>>>(buf.keys, n_tris, dyn_dev, nodes, buf.parent, n_tris);
+    cudaMemsetAsync(buf.flags, 0, 4ull * n_tris, st);
+    k_refit<<<g, kT, 0, st>>>(world_tris, buf.keys, leaf, n_tris, dyn_dev, nodes, buf.parent, buf.flags, n_tris);
+    g_launches += 4 + 3 * 4;
+}
+
+}  // namespace prx

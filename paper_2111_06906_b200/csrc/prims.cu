@@ -1,0 +1,323 @@
+// prims.cu -- tile scan, stable compaction and stable LSD radix sort (see prims.h).
+//
+// Layout of every tiled kernel: a tile is 2048 consecutive elements handled by 256
+// threads in 8 rounds; in round k thread t owns element tile_base + k*256 + t, so a
+// round is one coalesced 1 KiB access and element order within a tile is preserved.
+#include "prims.h"
+
+#include <cstdio>
+
+namespace prx {
+
+namespace {
+
+__device__ __forceinline__ uint32_t n_of(uint32_t n_max, const uint32_t* n_dev) {
+    return n_dev ? min(*n_dev, n_max) : n_max;
+}
+
+// Exclusive scan across the 256 threads of a block; returns the block total.
+__device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t& total, uint32_t* sh_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < (kPrimThreads / 32) ? sh_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < (kPrimThreads / 32)) sh_warp[lane] = w;  // inclusive warp prefix
+    }
+    __syncthreads();
+    total = sh_warp[kPrimThreads / 32 - 1];
+    const uint32_t before = warp > 0 ? sh_warp[warp - 1] : 0u;
+    __syncthreads();
+    return before + x - v;
+}
+
+// ----------------------------------------------------------------------------- scan
+__global__ void k_tile_sum(const uint32_t* __restrict__ in, uint32_t n_max, const uint32_t* n_dev,
+                           uint32_t* __restrict__ sums) {
+    __shared__ uint32_t sh[kPrimThreads / 32];
+    const uint32_t n = n_of(n_max, n_dev);
+    const uint64_t base = (uint64_t)blockIdx.x * kPrimTile;
+    uint32_t acc = 0;
+    if (base < n) {
+#pragma unroll
+        for (int k = 0; k < kPrimItems; ++k) {
+            const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
+            if (i < n) acc += in[i];
+        }
+    }
+    uint32_t total;
+    block_exclusive(acc, total, sh);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+// Single-CTA exclusive scan of m values (in place), chunked with a running carry.
+__global__ void k_scan_small(uint32_t* __restrict__ v, uint32_t m, uint32_t* total_dev) {
+    __shared__ uint32_t sh[kPrimThreads / 32];
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < m; base += kPrimThreads * 4) {
+        uint32_t x[4];
+        uint32_t s = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = base + threadIdx.x * 4 + k;
+            x[k] = i < m ? v[i] : 0u;
+            s += x[k];
+        }
+        uint32_t total;
+        const uint32_t ex = block_exclusive(s, total, sh);
+        uint32_t run = carry + ex;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = base + threadIdx.x * 4 + k;
+            if (i < m) v[i] = run;
+            run += x[k];
+        }
+        carry += total;
+    }
+    if (threadIdx.x == 0 && total_dev) *total_dev = carry;
+}
+
+__global__ void k_tile_scan(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t n_max,
+                            const uint32_t* n_dev, const uint32_t* __restrict__ offs) {
+    __shared__ uint32_t sh[kPrimThreads / 32];
+    const uint32_t n = n_of(n_max, n_dev);
+    const uint64_t base = (uint64_t)blockIdx.x * kPrimTile;
+    if (base >= n) return;
+    uint32_t run = offs[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kPrimItems; ++k) {
+        const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
+        const uint32_t x = i < n ? in[i] : 0u;
+        uint32_t total;
+        const uint32_t ex = block_exclusive(x, total, sh);
+        if (i < n) out[i] = run + ex;
+        run += total;
+    }
+}
+
+// ----------------------------------------------------------------------------- compaction
+template <typename T>
+__global__ void k_flag_count(const T* __restrict__ flags, uint32_t n_max, const uint32_t* n_dev,
+                             uint32_t* __restrict__ counts) {
+    const uint32_t n = n_of(n_max, n_dev);
+    const uint64_t base = (uint64_t)blockIdx.x * kPrimTile;
+    uint32_t c = 0;
+    if (base < n) {
+#pragma unroll
+        for (int k = 0; k < kPrimItems; ++k) {
+            const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
+            c += (i < n && flags[i] != 0) ? 1u : 0u;
+        }
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    __shared__ uint32_t sh[kPrimThreads / 32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kPrimThreads / 32; ++w) t += sh[w];
+        counts[blockIdx.x] = t;
+    }
+}
+
+template <typename T>
+__global__ void k_flag_scatter(const T* __restrict__ flags, uint32_t n_max, const uint32_t* n_dev,
+                               uint32_t base_id, const uint32_t* __restrict__ offs,
+                               uint32_t* __restrict__ out) {
+    __shared__ uint32_t sh[kPrimThreads / 32];
+    const uint32_t n = n_of(n_max, n_dev);
+    const uint64_t base = (uint64_t)blockIdx.x * kPrimTile;
+    if (base >= n) return;
+    uint32_t run = offs[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kPrimItems; ++k) {
+        const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
+        const bool f = i < n && flags[i] != 0;
+        const uint32_t ball = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) sh[warp] = __popc(ball);
+        __syncthreads();
+        uint32_t before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kPrimThreads / 32; ++w) {
+            const uint32_t c = sh[w];
+            before += w < warp ? c : 0u;
+            total += c;
+        }
+        if (f) out[run + before + __popc(ball & ((1u << lane) - 1u))] = base_id + (uint32_t)i;
+        run += total;
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------------------- radix sort
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+
+__global__ void k_rs_hist(const uint32_t* __restrict__ keys, uint32_t n_max, const uint32_t* n_dev,
+                          int shift, uint32_t mask, uint32_t tiles, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[kRadix];
+    const uint32_t n = n_of(n_max, n_dev);
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * kPrimTile;
+    if (base < n) {
+#pragma unroll
+        for (int k = 0; k < kPrimItems; ++k) {
+            const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
+            if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+        }
+    }
+    __syncthreads();
+    hist[(uint64_t)threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];  // digit-major
+}
+
+__global__ void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                             uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n_max,
+                             const uint32_t* n_dev, int shift, uint32_t mask, uint32_t tiles,
+                             const uint32_t* __restrict__ offs) {
+    __shared__ uint32_t run[kRadix];                           // per-digit running count
+    __shared__ uint32_t wcnt[kPrimThreads / 32][kRadix];       // per-warp digit counts (round)
+    const uint32_t n = n_of(n_max, n_dev);
+    const uint64_t base = (uint64_t)blockIdx.x * kPrimTile;
+    if (base >= n) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    run[threadIdx.x] = offs[(uint64_t)threadIdx.x * tiles + blockIdx.x];
+    for (int k = 0; k < kPrimItems; ++k) {
+        for (int w = 0; w < kPrimThreads / 32; ++w) wcnt[w][threadIdx.x] = 0;
+        __syncthreads();
+        const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t key = valid ? kin[i] : 0u;
+        const uint32_t val = valid ? vin[i] : 0u;
+        const uint32_t dig = valid ? ((key >> shift) & mask) : (uint32_t)kRadix;  // sentinel
+        const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        if (valid && rank == 0) wcnt[warp][dig] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            uint32_t before = 0;
+            for (int w = 0; w < warp; ++w) before += wcnt[w][dig];
+            const uint32_t pos = run[dig] + before + rank;
+            kout[pos] = key;
+            vout[pos] = val;
+        }
+        __syncthreads();
+        uint32_t add = 0;
+        for (int w = 0; w < kPrimThreads / 32; ++w) add += wcnt[w][threadIdx.x];
+        run[threadIdx.x] += add;
+        __syncthreads();
+    }
+}
+
+struct Scratch {
+    uint32_t* tile;   // per-tile values (counts / sums), tiles entries
+    uint32_t* hist;   // radix histograms, 256 * tiles entries
+    uint32_t* tile2;  // second-level sums for large scans
+};
+
+Scratch carve(void* p, uint64_t n_max) {
+    const uint64_t tiles = prim_tiles(n_max ? n_max : 1);
+    Scratch s;
+    s.tile = static_cast<uint32_t*>(p);
+    s.tile2 = s.tile + tiles + 64;
+    s.hist = s.tile2 + prim_tiles(tiles * kRadix) + 64;
+    return s;
+}
+
+// Exclusive scan of m device values in place (any m): tile sums + single-CTA scan.
+void scan_inplace(uint32_t* v, uint32_t m, uint32_t* total_dev, uint32_t* tmp, cudaStream_t st) {
+    if (m <= 64u * 1024u) {
+        k_scan_small<<<1, kPrimThreads, 0, st>>>(v, m, total_dev);
+        return;
+    }
+    const uint32_t tiles = prim_tiles(m);
+    k_tile_sum<<<tiles, kPrimThreads, 0, st>>>(v, m, nullptr, tmp);
+    k_scan_small<<<1, kPrimThreads, 0, st>>>(tmp, tiles, total_dev);
+    k_tile_scan<<<tiles, kPrimThreads, 0, st>>>(v, v, m, nullptr, tmp);
+}
+
+}  // namespace
+
+size_t prim_scratch_bytes(uint64_t n_max) {
+    const uint64_t tiles = prim_tiles(n_max ? n_max : 1);
+    return 4ull * (tiles + 64 + prim_tiles(tiles * kRadix) + 64 + tiles * kRadix + 64);
+}
+
+void scan_exclusive_u32(const uint32_t* in, uint32_t* out, uint32_t n_max, const uint32_t* n_dev,
+                        uint32_t* total_dev, void* scratch, cudaStream_t st) {
+    if (n_max == 0) return;
+    Scratch s = carve(scratch, n_max);
+    const uint32_t tiles = prim_tiles(n_max);
+    k_tile_sum<<<tiles, kPrimThreads, 0, st>>>(in, n_max, n_dev, s.tile);
+    scan_inplace(s.tile, tiles, total_dev, s.tile2, st);
+    k_tile_scan<<<tiles, kPrimThreads, 0, st>>>(in, out, n_max, n_dev, s.tile);
+}
+
+void compact_u8(const uint8_t* flags, uint32_t n_max, const uint32_t* n_dev, uint32_t base,
+                uint32_t* out, uint32_t* count_dev, void* scratch, cudaStream_t st) {
+    if (n_max == 0) {
+        cudaMemsetAsync(count_dev, 0, 4, st);
+        return;
+    }
+    Scratch s = carve(scratch, n_max);
+    const uint32_t tiles = prim_tiles(n_max);
+    k_flag_count<uint8_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, n_dev, s.tile);
+    scan_inplace(s.tile, tiles, count_dev, s.tile2, st);
+    k_flag_scatter<uint8_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, n_dev, base, s.tile, out);
+}
+
+void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, uint32_t base,
+                 uint32_t* out, uint32_t* count_dev, void* scratch, cudaStream_t st) {
+    if (n_max == 0) {
+        cudaMemsetAsync(count_dev, 0, 4, st);
+        return;
+    }
+    Scratch s = carve(scratch, n_max);
+    const uint32_t tiles = prim_tiles(n_max);
+    k_flag_count<uint32_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, n_dev, s.tile);
+    scan_inplace(s.tile, tiles, count_dev, s.tile2, st);
+    k_flag_scatter<uint32_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, n_dev, base, s.tile, out);
+}
+
+void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
+                      uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch,
+                      cudaStream_t st) {
+    if (n_max == 0 || bits <= 0) return;
+    Scratch s = carve(scratch, n_max);
+    const uint32_t tiles = prim_tiles(n_max);
+    uint32_t *ki = keys, *vi = vals, *ko = keys_tmp, *vo = vals_tmp;
+    int passes = 0;
+    for (int shift = 0; shift < bits; shift += kRadixBits, ++passes) {
+        const int w = bits - shift < kRadixBits ? bits - shift : kRadixBits;
+        const uint32_t mask = (1u << w) - 1u;
+        k_rs_hist<<<tiles, kPrimThreads, 0, st>>>(ki, n_max, n_dev, shift, mask, tiles, s.hist);
+        scan_inplace(s.hist, tiles * kRadix, nullptr, s.tile2, st);
+        k_rs_scatter<<<tiles, kPrimThreads, 0, st>>>(ki, vi, ko, vo, n_max, n_dev, shift, mask, tiles,
+                                                     s.hist);
+        uint32_t* t = ki;
+        ki = ko;
+        ko = t;
+        t = vi;
+        vi = vo;
+        vo = t;
+    }
+    if (passes & 1) {  // result is in the tmp buffers: copy back
+        const uint64_t bytes = 4ull * n_max;
+        cudaMemcpyAsync(keys, ki, bytes, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(vals, vi, bytes, cudaMemcpyDeviceToDevice, st);
+    }
+}
+
+}  // namespace prx
