@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark of the per-frame photon-path verification + reuse pipeline (BASELINE.json).
+
+One step = one animated frame of the north_star hot path on the configured workload:
+frame_update -> verify_paths -> retrace_invalid -> splat (120x90), i.e. Engine::run_frame
+(engine.cpp:201-242) + gather_image (gather.cpp:35-75) of the reference.
+
+  value   whole-job paths/s = n_paths * steps / device time of the timed steps (CUDA events
+          on the engine's stream, max over ranks); every live path is verified each frame
+          and the invalid ones are retraced.
+  e2e     the same metric through the public Python API (Engine.run_frame + Engine.splat
+          returning the host image), wall clock, host<->device copies included.
+  --impl reference: the reference CPU engine (oracle/_ref, built from /root/reference) on a
+          bounded path-prefix sample of the same workload, all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "C1": dict(desc="Cornell box (~1K static tris), point light, translating 992-tri sphere",
+               mode="naive", paths=65536, bounces=3, threshold=0.001),
+    "C2": dict(desc="Cornell box, rect area light translating in its plane (DM remap)",
+               mode="naive", paths=1048576, bounces=5, threshold=0.001),
+    "C3": dict(desc="Sponza-scale synthetic (282K static tris + 4 x 20K dynamic), disc light",
+               mode="error", paths=2097152, bounces=7, threshold=0.01),
+    "C4": dict(desc="Villa-scale synthetic (1.02M static tris + 8 x 20K dynamic + 2 moving lights)",
+               mode="error", paths=5000000, bounces=7, threshold=0.001),
+}
+CPU_SAMPLE_PATHS = {"C1": 65536, "C2": 131072, "C3": 16384, "C4": 16384}
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--paths", type=int, default=0, help="override n_paths")
+    ap.add_argument("--splat-mode", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        loaded = [s for s in sm if smax and s > 0.3 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def scene_for(pr, name):
+    return pr.Scene.synthetic(name)
+
+
+def run_reference(args, name, n_paths, steps, warmup):
+    """The reference CPU engine on a path-prefix sample; returns (paths/s, detail)."""
+    from oracle import ref
+    from paper_2111_06906_b200 import pathreuse as pr
+
+    w = WORKLOADS[name]
+    scene = scene_for(pr, name)
+    rscene = ref.RefScene.from_desc(scene.describe())
+    cfg = pr.make_config(mode=w["mode"], paths=n_paths, bounces=w["bounces"],
+                         dm=[8, 8, 64, 64], threshold=w["threshold"], seed=1, workers=0)
+    eng = ref.RefEngine(rscene, cfg)
+    eng.set_workers(0)
+    for _ in range(warmup):
+        eng.run_frame()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        eng.run_frame()
+        eng.gather(radius=0.25, workers=0)
+        times.append(time.perf_counter() - t0)
+    mean = sum(times) / len(times)
+    return n_paths / mean, {"frame_s_mean": mean, "frames": steps, "warmup": warmup}
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    name = args.workload
+    w = WORKLOADS[name]
+    n_paths = args.paths or w["paths"]
+    unit = "paths/s"
+    metric = "verified+retraced photon paths/s (frame = verify+retrace+splat)"
+    config = {"workload": f"{name}: {w['desc']}", "n_paths": n_paths, "max_bounces": w["bounces"],
+              "mode": w["mode"], "threshold": w["threshold"], "dm_dims": [8, 8, 64, 64],
+              "image": "120x90", "gather_radius": 0.25,
+              "l2": "inputs larger than L2 (path store >= 1 GB for C2-C4)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        sample = args.cpu_sample or CPU_SAMPLE_PATHS[name]
+        value, det = run_reference(args, name, sample, args.steps, args.warmup)
+        cores = os.cpu_count()
+        line = {"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": det["frame_s_mean"] * 1e3 * (n_paths / sample),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": dict(config, cpu_sample_paths=sample),
+                "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "reference",
+                                 "sample": f"first {sample} of {n_paths} paths (path-prefix; per-path "
+                                           f"work is independent), {args.warmup} warm-up + "
+                                           f"{args.steps} timed frames incl. gather_image"},
+                "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2111_06906_b200 import pathreuse as pr
+    from paper_2111_06906_b200 import _lib as L
+
+    scene = scene_for(pr, name)
+    counts = scene.counts()
+    config.update(static_tris=counts["static_triangles"], dynamic_tris=counts["dynamic_triangles"])
+    shard = (0, 0)
+    if world > 1:
+        shard = (n_paths * rank // world, n_paths * (rank + 1) // world)
+    cfg = pr.make_config(mode=w["mode"], paths=n_paths, bounces=w["bounces"], dm=[8, 8, 64, 64],
+                         threshold=w["threshold"], seed=1, device=local, shard=shard)
+    eng = pr.Engine(scene, cfg)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    cam = scene.describe().camera
+    img_dev = torch.zeros(cam.height * cam.width * 3, dtype=torch.float32, device="cuda")
+
+    def step(collect=None):
+        st = L.FrameStats()
+        L.check(L.lib().prx_run_frame(eng.handle, C.byref(st)))
+        sst = L.FrameStats()
+        L.check(L.lib().prx_splat(eng.handle, C.byref(cam), 0.25, args.splat_mode, None,
+                                  C.c_void_p(img_dev.data_ptr()), C.byref(sst)))
+        if collect is not None:
+            collect.append((st, sst))
+
+    import ctypes as C
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    stats = []
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = eng.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(stats)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    launches = eng.launch_count() - launches0
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = n_paths * args.steps / (elapsed_ms * 1e-3)
+
+    # stage breakdown (device events inside the engine)
+    def med(f):
+        return statistics.median(f(a, b) for a, b in stats)
+
+    verify_ms = med(lambda a, b: a.ms_verify)
+    retrace_ms = med(lambda a, b: a.ms_retrace)
+    splat_ms = med(lambda a, b: b.ms_splat)
+    update_ms = med(lambda a, b: a.ms_frame_update)
+    trace_ms = med(lambda a, b: a.t_trace * 1e3)
+    occl_ms = med(lambda a, b: a.t_occlusion * 1e3)
+    seg_before = med(lambda a, b: a.live_segments_before)
+    retraced = med(lambda a, b: a.paths_retraced)
+    traced = med(lambda a, b: a.rays_traced)
+    vis = med(lambda a, b: a.visibility_rays)
+
+    # e2e through the public API with host buffers (stats + image read back every step)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        eng.run_frame()
+        eng.splat(radius=0.25, mode=args.splat_mode)
+    e2e_s = time.perf_counter() - t0
+    e2e_value = n_paths * args.steps / e2e_s
+    h2d = 4 + 16 * 4 + 40 * 128 + 24 * 128 + 176 * 16 + 32 * 128  # FrameParams + transforms
+    d2h = 12 * cam.width * cam.height + 96 + 32 + 8 * 21
+
+    # roofline of the dominant kernel stage (trace): algorithmic bytes per traced segment =
+    # 64 B written (4 x float4 vertex streams) + 64 B per retraced path start (meta, rstart,
+    # epoch, origin/emission or previous vertex, truncation of the tail records).
+    hbm, peak_src = peaks()
+    trace_bytes = traced * 64 + retraced * 64
+    achieved = trace_bytes / (trace_ms * 1e-3) / 1e9 if trace_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": "k_trace (stage_trace: compaction + trace + finalize)",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "peak_source": peak_src,
+                "note": "traversal is latency/issue-bound: BVH reads are implementation-defined "
+                        "and not in the algorithmic bytes"}
+
+    line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (procedural scene, seed 1)", "config": config,
+            "stages_ms": {"frame_update": update_ms, "verify": verify_ms, "occlusions": occl_ms,
+                          "retrace": retrace_ms, "trace": trace_ms, "splat": splat_ms},
+            "verified_segments_per_s": seg_before / (verify_ms * 1e-3) if verify_ms else None,
+            "retraced_paths_per_frame": retraced, "rays_traced_per_frame": traced,
+            "visibility_rays_per_frame": vis,
+            "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches, "clocks": clk, "roofline": roofline}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = args.cpu_sample or CPU_SAMPLE_PATHS[name]
+        try:
+            cpu_value, det = run_reference(args, name, sample, 2, 1)
+            line["cpu_baseline"] = {"value": cpu_value, "unit": unit, "cores": os.cpu_count(),
+                                    "kind": "reference",
+                                    "sample": f"first {sample} of {n_paths} paths, 1 warm-up + 2 "
+                                              f"timed frames incl. gather_image"}
+        except Exception as exc:  # oracle not built on this box
+            line["cpu_baseline"] = {"value": None, "unit": unit, "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"unavailable: {exc}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

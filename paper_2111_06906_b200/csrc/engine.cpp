@@ -786,6 +786,7 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
     if (c.width != img_w_ || c.height != img_h_) {
         d_gbuf_.alloc(16ull * npx);
         d_img_.alloc(12ull * npx);
+        d_splat_work_.alloc(splat_work_bytes(npx));
         img_w_ = c.width;
         img_h_ = c.height;
     }
@@ -793,7 +794,8 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
     const float inv_pi = 1.0f / static_cast<float>(M_PI);
     record(kEvSplat0);
     float* out = rgb_dev ? rgb_dev : d_img_.as<float>();
-    launch_splat(scene_dev(), path_dev(), C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, stream_);
+    launch_splat(scene_dev(), path_dev(), C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area,
+                 d_splat_work_.get(), stream_);
     record(kEvSplat1);
     if (rgb_host)
         PRX_CUDA(cudaMemcpyAsync(rgb_host, out, 12ull * npx, cudaMemcpyDeviceToHost, stream_));

@@ -67,8 +67,10 @@ void launch_pack_photons(PathDev P, void* photons, void* aux, cudaStream_t st);
 void launch_unpack_photons(PathDev P, const void* photons, const void* aux, cudaStream_t st);
 
 // G-buffer + splat + resolve (splat.cu), replacing gather_image (gather.cpp:35-75)
+int splat_table_bits(uint32_t npx);
+size_t splat_work_bytes(uint32_t npx);
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img,
-                  float inv_pi, float inv_area, cudaStream_t st);
+                  float inv_pi, float inv_area, void* work, cudaStream_t st);
 
 // Dynamic LBVH (lbvh.cu)
 struct LbvhBuffers {

@@ -1,30 +1,50 @@
-// splat.cu -- screen-space photon splatting (north_star subsystem 6), replacing the
+// splat.cu -- photon splatting into an fp32 image (north_star subsystem 6), replacing the
 // reference's per-pixel gather_image (gather.cpp:35-75).
 //
-//   K11 gbuffer:  per pixel, camera_ray (gather.cpp:22-33) + intersect_scene -> hit
-//                 position and object (same float ops as the reference).
-//   K12 splat:    per live photon, the screen rectangle that can contain pixels whose
-//                 hit point lies within r is derived from the photon's bounding box in
-//                 camera space; every pixel in it passes the reference's own filters
-//                 (same object, |x_ph - x_px|^2 <= r^2, photon in the 27-cell grid
-//                 neighbourhood of the pixel, gather.hpp:45-58) and atomically adds the
-//                 photon energy -- into a CTA-private shared-memory image when the frame
-//                 fits (120x90x3 fp32 = 130 KB), else straight into global memory.
-//   resolve:      L = sum(E) * albedo / pi / (pi r^2) (gather.cpp:71).
-// Only the fp32 summation order differs from the reference (tolerance class C).
+// The reference, per pixel: primary hit x (camera_ray + intersect_scene), then every live
+// photon in the 27 grid cells around cell(x) (cell edge = r, 21-bit wrapped keys,
+// gather.hpp:38-74) with the same object and |x_ph - x|^2 <= r^2 adds its energy.
+// Inverting that relation, photon ph contributes to pixel p iff key(cell(ph)) is one of
+// the 27 keys key(cell(x_p) + o).  So:
+//   K11 gbuffer     primary hits (same float ops as camera_ray / intersect_scene);
+//   K12a pixcells   each hit pixel inserts its 27 neighbour-cell keys into an
+//                   open-addressing hash table -> per-key pixel lists (count, scan, fill);
+//   K12b splat      every photon streams once through HBM (16 B {pos, obj}), probes the
+//                   table with its own cell key (an L2-resident table), and for each listed
+//                   pixel applies the reference filters and adds its energy with shared-memory
+//                   atomics into a CTA-private image (global atomics when the image does not
+//                   fit in shared memory);
+//   resolve         L = sum(E) * albedo / pi / (pi r^2) (gather.cpp:71).
+// The contributing (photon, pixel) set is identical to the reference's; only the fp32
+// summation order differs (tolerance class C).
 #include "device_scene.cuh"
 #include "kernels.h"
+#include "prims.h"
 
 namespace prx {
 
 namespace {
 
 constexpr int kT = 256;
+constexpr unsigned long long kEmptyKey = ~0ull;
+
+__device__ __forceinline__ long long cell_coord(float v, float r) { return (long long)floorf(v / r); }
+
+// GatherGrid::key (gather.hpp:64-69): three 21-bit wrapped coordinates
+__device__ __forceinline__ unsigned long long grid_key(long long x, long long y, long long z) {
+    return (((unsigned long long)x & 0x1FFFFFull) << 42) | (((unsigned long long)y & 0x1FFFFFull) << 21) |
+           ((unsigned long long)z & 0x1FFFFFull);
+}
+
+__device__ __forceinline__ uint32_t slot_of(unsigned long long key, int bits) {
+    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - bits));
+}
 
 __global__ void k_gbuffer(SceneDev S, CamDev C, float4* gbuf) {
     const uint32_t n = C.w * C.h;
     for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < n; pix += gridDim.x * blockDim.x) {
         const uint32_t px = pix % C.w, py = pix / C.w;
+        // camera_ray (gather.cpp:22-33)
         const float sx = (2.0f * ((float)px + 0.5f) / (float)C.w - 1.0f) * C.tan_half * C.aspect;
         const float sy = (1.0f - 2.0f * ((float)py + 0.5f) / (float)C.h) * C.tan_half;
         const V3 dir = normalized(add(add(C.fwd, mul(C.right, sx)), mul(C.up, sy)));
@@ -36,73 +56,89 @@ __global__ void k_gbuffer(SceneDev S, CamDev C, float4* gbuf) {
     }
 }
 
-__device__ __forceinline__ long long cell_coord(float v, float r) { return (long long)floorf(v / r); }
+// pass 0: count (fill == false) / pass 1: fill per-key pixel lists
+template <bool kFill>
+__global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float r, unsigned long long* keys,
+                           uint32_t* cnt, const uint32_t* __restrict__ off, uint32_t* cursor, uint32_t* list,
+                           int bits) {
+    const uint32_t mask = (1u << bits) - 1u;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < 27u * npx; w += gridDim.x * blockDim.x) {
+        const uint32_t pix = w / 27u, o = w % 27u;
+        const float4 g = gbuf[pix];
+        if (__float_as_uint(g.w) == kInvalidObj) continue;
+        const long long cx = cell_coord(g.x, r) + (long long)(o % 3) - 1;
+        const long long cy = cell_coord(g.y, r) + (long long)((o / 3) % 3) - 1;
+        const long long cz = cell_coord(g.z, r) + (long long)(o / 9) - 1;
+        const unsigned long long key = grid_key(cx, cy, cz);
+        uint32_t s = slot_of(key, bits);
+        if (!kFill) {
+            while (true) {
+                const unsigned long long prev = atomicCAS(&keys[s], kEmptyKey, key);
+                if (prev == kEmptyKey || prev == key) break;
+                s = (s + 1) & mask;
+            }
+            atomicAdd(&cnt[s], 1u);
+        } else {
+            while (keys[s] != key) s = (s + 1) & mask;
+            list[off[s] + atomicAdd(&cursor[s], 1u)] = pix;
+        }
+    }
+}
 
 template <bool kShared>
-__global__ void __launch_bounds__(kT) k_splat(PathDev P, CamDev C, float radius,
-                                              const float4* __restrict__ gbuf, float* __restrict__ img) {
+__global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float radius,
+                                              const float4* __restrict__ gbuf,
+                                              const unsigned long long* __restrict__ keys,
+                                              const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                                              const uint32_t* __restrict__ list, int bits, float* __restrict__ img) {
     extern __shared__ float simg[];
-    const uint32_t npx = C.w * C.h;
     if (kShared) {
         for (uint32_t k = threadIdx.x; k < 3 * npx; k += blockDim.x) simg[k] = 0.0f;
         __syncthreads();
     }
     float* acc = kShared ? simg : img;
+    const uint32_t mask = (1u << bits) - 1u;
     const float r2 = radius * radius;
-    const float ta = C.tan_half * C.aspect;
     const size_t total = (size_t)P.n * P.B;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const float4 po = P.pos_obj[v];
+        const float4 po = __ldcs(&P.pos_obj[v]);
         const uint32_t obj = __float_as_uint(po.w);
         if (obj == kInvalidObj) continue;
-        const float4 en = P.energy[v];
-        const V3 ph{po.x, po.y, po.z};
-        const V3 q = sub(ph, C.pos);
-        const float z = dot(q, C.fwd), x = dot(q, C.right), y = dot(q, C.up);
-        int x0 = 0, x1 = (int)C.w - 1, y0 = 0, y1 = (int)C.h - 1;
-        if (z > radius * 1.001f + 1e-4f) {
-            const float zl = z - radius, zh = z + radius;
-            const float sxa = fminf((x - radius) / zl, (x - radius) / zh);
-            const float sxb = fmaxf((x + radius) / zl, (x + radius) / zh);
-            const float sya = fminf((y - radius) / zl, (y - radius) / zh);
-            const float syb = fmaxf((y + radius) / zl, (y + radius) / zh);
-            const float fx0 = (sxa / ta + 1.0f) * 0.5f * (float)C.w - 0.5f;
-            const float fx1 = (sxb / ta + 1.0f) * 0.5f * (float)C.w - 0.5f;
-            const float fy0 = (1.0f - syb / C.tan_half) * 0.5f * (float)C.h - 0.5f;
-            const float fy1 = (1.0f - sya / C.tan_half) * 0.5f * (float)C.h - 0.5f;
-            if (fx1 < -2.0f || fy1 < -2.0f || fx0 > (float)C.w + 1.0f || fy0 > (float)C.h + 1.0f) continue;
-            x0 = max(0, (int)floorf(fx0) - 1);
-            x1 = min((int)C.w - 1, (int)ceilf(fx1) + 1);
-            y0 = max(0, (int)floorf(fy0) - 1);
-            y1 = min((int)C.h - 1, (int)ceilf(fy1) + 1);
-        }
-        const long long cx = cell_coord(ph.x, radius), cy = cell_coord(ph.y, radius), cz = cell_coord(ph.z, radius);
-        for (int py = y0; py <= y1; ++py) {
-            for (int px = x0; px <= x1; ++px) {
-                const uint32_t pix = (uint32_t)py * C.w + (uint32_t)px;
-                const float4 g = __ldg(&gbuf[pix]);
-                if (__float_as_uint(g.w) != obj) continue;
-                const V3 d = sub(ph, V3{g.x, g.y, g.z});
-                if (dot(d, d) > r2) continue;
-                const long long gx = cell_coord(g.x, radius), gy = cell_coord(g.y, radius), gz = cell_coord(g.z, radius);
-                if (llabs(cx - gx) > 1 || llabs(cy - gy) > 1 || llabs(cz - gz) > 1) continue;
-                atomicAdd(&acc[3 * pix], en.x);
-                atomicAdd(&acc[3 * pix + 1], en.y);
-                atomicAdd(&acc[3 * pix + 2], en.z);
+        const unsigned long long key =
+            grid_key(cell_coord(po.x, radius), cell_coord(po.y, radius), cell_coord(po.z, radius));
+        uint32_t s = slot_of(key, bits);
+        unsigned long long k;
+        while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
+        if (k != key) continue;
+        const uint32_t n = __ldg(&cnt[s]), o = __ldg(&off[s]);
+        float4 en;
+        bool have_en = false;
+        for (uint32_t j = 0; j < n; ++j) {
+            const uint32_t pix = __ldg(&list[o + j]);
+            const float4 g = __ldg(&gbuf[pix]);
+            if (__float_as_uint(g.w) != obj) continue;
+            const V3 d = sub(V3{po.x, po.y, po.z}, V3{g.x, g.y, g.z});  // gather.hpp:54
+            if (dot(d, d) > r2) continue;
+            if (!have_en) {
+                en = __ldcs(&P.energy[v]);
+                have_en = true;
             }
+            atomicAdd(&acc[3 * pix], en.x);
+            atomicAdd(&acc[3 * pix + 1], en.y);
+            atomicAdd(&acc[3 * pix + 2], en.z);
         }
     }
     if (kShared) {
         __syncthreads();
-        for (uint32_t k = threadIdx.x; k < 3 * npx; k += blockDim.x) {
-            const float s = simg[k];
-            if (s != 0.0f) atomicAdd(&img[k], s);
+        for (uint32_t k2 = threadIdx.x; k2 < 3 * npx; k2 += blockDim.x) {
+            const float s2 = simg[k2];
+            if (s2 != 0.0f) atomicAdd(&img[k2], s2);
         }
     }
 }
 
-__global__ void k_resolve(const float4* __restrict__ gbuf, const float4* __restrict__ mat, float* img,
-                          uint32_t n, float inv_pi, float inv_area) {
+__global__ void k_resolve(const float4* __restrict__ gbuf, const float4* __restrict__ mat, float* img, uint32_t n,
+                          float inv_pi, float inv_area) {
     for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < n; pix += gridDim.x * blockDim.x) {
         const uint32_t obj = __float_as_uint(gbuf[pix].w);
         if (obj == kInvalidObj) {
@@ -111,7 +147,7 @@ __global__ void k_resolve(const float4* __restrict__ gbuf, const float4* __restr
         }
         const float4 a = mat[obj];
         const V3 rad{img[3 * pix], img[3 * pix + 1], img[3 * pix + 2]};
-        const V3 out = mul(mul(mulv(rad, V3{a.x, a.y, a.z}), inv_pi), inv_area);
+        const V3 out = mul(mul(mulv(rad, V3{a.x, a.y, a.z}), inv_pi), inv_area);  // gather.cpp:71
         img[3 * pix] = out.x;
         img[3 * pix + 1] = out.y;
         img[3 * pix + 2] = out.z;
@@ -120,24 +156,53 @@ __global__ void k_resolve(const float4* __restrict__ gbuf, const float4* __restr
 
 }  // namespace
 
-void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img,
-                  float inv_pi, float inv_area, cudaStream_t st) {
+int splat_table_bits(uint32_t npx) {
+    uint64_t want = 2ull * 27ull * npx;
+    int bits = 10;
+    while ((1ull << bits) < want && bits < 30) ++bits;
+    return bits;
+}
+
+size_t splat_work_bytes(uint32_t npx) {
+    const uint64_t slots = 1ull << splat_table_bits(npx);
+    return slots * (8 + 4 + 4 + 4) + 4ull * 27 * npx + prim_scratch_bytes(slots) + 64;
+}
+
+void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
+                  float inv_area, void* work, cudaStream_t st) {
     const uint32_t npx = C.w * C.h;
+    const int bits = splat_table_bits(npx);
+    const uint64_t slots = 1ull << bits;
+    auto* keys = static_cast<unsigned long long*>(work);
+    auto* cnt = reinterpret_cast<uint32_t*>(keys + slots);
+    uint32_t* off = cnt + slots;
+    uint32_t* cursor = off + slots;
+    uint32_t* list = cursor + slots;
+    void* scratch = list + 27ull * npx;
+
     k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
+    cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
+    cudaMemsetAsync(cnt, 0, 4 * slots, st);
+    cudaMemsetAsync(cursor, 0, 4 * slots, st);
+    k_pixcells<false><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, nullptr, nullptr,
+                                                                  nullptr, bits);
+    scan_exclusive_u32(cnt, off, (uint32_t)slots, nullptr, nullptr, scratch, st);
+    k_pixcells<true><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, off, cursor, list,
+                                                                 bits);
     cudaMemsetAsync(img, 0, 12ull * npx, st);
     const size_t smem = 12ull * npx;
-    int dev = 0;
+    int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
-    int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (smem <= 200u * 1024u) {
         cudaFuncSetAttribute(k_splat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_splat<true><<<n_sm, kT, smem, st>>>(P, C, radius, gbuf, img);
+        k_splat<true><<<n_sm, kT, smem, st>>>(P, npx, radius, gbuf, keys, cnt, off, list, bits, img);
     } else {
-        k_splat<false><<<launch_grid((uint64_t)P.n * P.B, kT), kT, 0, st>>>(P, C, radius, gbuf, img);
+        k_splat<false><<<launch_grid((uint64_t)P.n * P.B, kT), kT, 0, st>>>(P, npx, radius, gbuf, keys, cnt, off,
+                                                                           list, bits, img);
     }
     k_resolve<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, S.mat, img, npx, inv_pi, inv_area);
-    g_launches += 3;
+    g_launches += 6 + 3;
 }
 
 }  // namespace prx
