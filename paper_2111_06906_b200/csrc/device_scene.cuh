@@ -275,20 +275,188 @@ __device__ __forceinline__ bool dyn_any(const SceneDev& S, const DynObj& D, cons
     return false;
 }
 
-// intersect_scene (scene.cpp:136-168)
-__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min,
-                                                Hit& h) {
+// --------------------------------------------------------------------------- resumable traversal
+// One ray query of intersect_scene (scene.cpp:136-168) or occluded (:170-177) as a state
+// machine advanced one BVH node (or one leaf) per trav_step().  Persistent kernels step
+// many rays per lane and refill finished lanes, keeping SIMD lanes busy; visit order and
+// culling are exactly those of the one-shot functions above, so results are identical.
+struct Trav {
+    RayPre r;
+    float t_min, t_max;   // acceptance window (t_max shrinks in closest-hit mode)
+    float t_in;           // dynamic object: window bound when the object started
+    float obj_t;          // dynamic object: best t so far (lexicographic with obj_i)
+    uint32_t obj_i;
+    uint32_t best;        // static: BVH-order triangle; dynamic: object-local triangle
+    uint32_t dj;          // dynamic object of `best`
+    int32_t kind;         // -1 none, 0 static, 1 dynamic
+    int32_t phase;        // -1 static BVH, j >= 0 dynamic object j, n_dyn = finished
+    int32_t gate;         // dynamic: 0 = gate pending, 1 = inside the object's LBVH
+    int32_t any;          // any-hit (occluded) mode
+    int32_t sp;
+    uint32_t stack[64];
+};
+
+__device__ __forceinline__ void trav_init(const SceneDev& S, Trav& T, V3 o, V3 d, float t_min, float t_max,
+                                          bool any) {
+    T.r = make_ray(o, d);
+    T.t_min = t_min;
+    T.t_max = t_max;
+    T.kind = -1;
+    T.any = any ? 1 : 0;
+    T.gate = 0;
+    T.sp = 0;
+    if (S.n_nodes) {
+        T.phase = -1;
+        T.stack[T.sp++] = 0;
+    } else {
+        T.phase = 0;
+    }
+}
+
+// Returns true when the query is finished (any-hit: T.kind >= 0 means occluded).
+__device__ __forceinline__ bool trav_step(const SceneDev& S, Trav& T) {
+    if (T.phase < 0) {  // static BVH, left-first DFS (bvh.cpp:79-106)
+        if (T.sp == 0) {
+            T.phase = 0;
+            T.gate = 0;
+            return S.fp->n_dyn == 0;
+        }
+        const uint32_t ni = T.stack[--T.sp];
+        const float4 A = __ldg(&S.nodes[2 * ni]);
+        const float4 B = __ldg(&S.nodes[2 * ni + 1]);
+        const Box box{{A.x, A.y, A.z}, {B.x, B.y, B.z}};
+        if (!ray_box(T.r, T.t_min, T.t_max, box)) return false;
+        const uint32_t a = __float_as_uint(A.w), b = __float_as_uint(B.w);
+        if (a & kLeafBit) {
+            const uint32_t first = a & ~kLeafBit;
+            for (uint32_t i = first; i < first + b; ++i) {
+                const float4 ta = __ldg(&S.stris[3 * i]);
+                const float4 t1 = __ldg(&S.stris[3 * i + 1]);
+                const float4 t2 = __ldg(&S.stris[3 * i + 2]);
+                float t;
+                if (intersect_tri(T.r.o, T.r.d, T.t_min, T.t_max, ld3(ta), ld3(t1), ld3(t2), t)) {
+                    T.kind = 0;
+                    T.best = i;
+                    if (T.any) return true;
+                    T.t_max = t;
+                }
+            }
+        } else {
+            T.stack[T.sp++] = b;  // right child
+            T.stack[T.sp++] = a;  // left child, popped first
+        }
+        return false;
+    }
+    const FrameParams* fp = S.fp;
+    if ((uint32_t)T.phase >= fp->n_dyn) return true;
+    const DynObj& D = fp->dyn[T.phase];
+    const float4* Tr = S.dtris + 3ull * D.tri_begin;
+    if (T.gate == 0) {  // scene.cpp:153-155 gate with the already-shrunk t_max
+        if (!ray_box(T.r, T.t_min, T.t_max, D.cur)) {
+            ++T.phase;
+            return (uint32_t)T.phase >= fp->n_dyn;
+        }
+        if (D.node_begin == kLbvhBrute) {  // brute_force_intersect (bvh.cpp:108-117)
+            for (uint32_t i = 0; i < D.tri_count; ++i) {
+                float t;
+                if (intersect_tri(T.r.o, T.r.d, T.t_min, T.t_max, ld3(__ldg(&Tr[3 * i])),
+                                  ld3(__ldg(&Tr[3 * i + 1])), ld3(__ldg(&Tr[3 * i + 2])), t)) {
+                    T.kind = 1;
+                    T.dj = (uint32_t)T.phase;
+                    T.best = i;
+                    if (T.any) return true;
+                    T.t_max = t;
+                }
+            }
+            ++T.phase;
+            return (uint32_t)T.phase >= fp->n_dyn;
+        }
+        T.gate = 1;
+        T.sp = 0;
+        T.stack[T.sp++] = D.tri_count == 1 ? (kLeafBit | 0u) : 0u;
+        T.t_in = T.t_max;
+        T.obj_t = T.t_max;
+        T.obj_i = 0xFFFFFFFFu;
+        return false;
+    }
+    if (T.sp == 0) {  // object finished: lexicographic (t, index) minimum
+        if (T.obj_i != 0xFFFFFFFFu) {
+            T.kind = 1;
+            T.dj = (uint32_t)T.phase;
+            T.best = T.obj_i;
+            T.t_max = T.obj_t;
+        }
+        ++T.phase;
+        T.gate = 0;
+        return (uint32_t)T.phase >= fp->n_dyn;
+    }
+    const uint32_t c = T.stack[--T.sp];
+    if (c & kLeafBit) {
+        const uint32_t i = __ldg(&S.dleaf[D.tri_begin + (c & ~kLeafBit)]);
+        float t;
+        if (intersect_tri(T.r.o, T.r.d, T.t_min, T.t_in, ld3(__ldg(&Tr[3 * i])), ld3(__ldg(&Tr[3 * i + 1])),
+                          ld3(__ldg(&Tr[3 * i + 2])), t)) {
+            if (T.any) {
+                T.kind = 1;
+                T.dj = (uint32_t)T.phase;
+                T.best = i;
+                return true;
+            }
+            if (t < T.obj_t || (t == T.obj_t && i < T.obj_i)) {
+                T.obj_t = t;
+                T.obj_i = i;
+            }
+        }
+        return false;
+    }
+    const float4* N = S.dnodes + 4ull * (D.node_begin + c);
+    const float4 lmin = __ldg(&N[0]), lmax = __ldg(&N[1]);
+    const float4 rmin = __ldg(&N[2]), rmax = __ldg(&N[3]);
+    const float tb = T.any ? T.t_max : T.obj_t;
+    if (ray_box_conservative(T.r, T.t_min, tb, rmin, rmax)) T.stack[T.sp++] = __float_as_uint(rmin.w);
+    if (ray_box_conservative(T.r, T.t_min, tb, lmin, lmax)) T.stack[T.sp++] = __float_as_uint(lmin.w);
+    return false;
+}
+
+// Hit record of a finished closest-hit query (scene.cpp:144-167)
+__device__ __forceinline__ bool trav_hit(const SceneDev& S, const Trav& T, Hit& h) {
+    if (T.kind < 0) return false;
+    V3 e1, e2;
+    if (T.kind == 0) {
+        const float4 q1 = __ldg(&S.stris[3 * T.best + 1]);
+        const float4 q2 = __ldg(&S.stris[3 * T.best + 2]);
+        e1 = ld3(q1);
+        e2 = ld3(q2);
+        h.obj = __float_as_uint(q1.w);
+    } else {
+        const DynObj& D = S.fp->dyn[T.dj];
+        const float4* Tr = S.dtris + 3ull * (D.tri_begin + T.best);
+        e1 = ld3(__ldg(&Tr[1]));
+        e2 = ld3(__ldg(&Tr[2]));
+        h.obj = D.obj;
+    }
+    h.t = T.t_max;
+    h.pos = add(T.r.o, mul(T.r.d, T.t_max));
+    V3 n = normalized(cross(e1, e2));  // Triangle::geometric_normal (geometry.hpp:64)
+    if (dot(n, T.r.d) > 0.0f) n = neg(n);
+    h.normal = n;
+    return true;
+}
+
+// intersect_scene (scene.cpp:136-168), one-shot form: tight static loop, then each dynamic
+// object behind its gate.
+__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h) {
     const RayPre r = make_ray(o, d);
     float t_max = FLT_MAX;
     uint32_t sbest = 0;
-    bool found = static_closest(S, r, t_min, t_max, sbest);
-    int kind = found ? 0 : -1;  // 0 static, 1 dynamic
+    const bool found = static_closest(S, r, t_min, t_max, sbest);
+    int kind = found ? 0 : -1;
     uint32_t dj = 0, dtri = 0;
     const FrameParams* fp = S.fp;
     const uint32_t n_dyn = fp->n_dyn;
     for (uint32_t j = 0; j < n_dyn; ++j) {
-        const DynObj D = fp->dyn[j];
-        if (!ray_box_exact(o, d, t_min, t_max, D.cur)) continue;
+        const DynObj& D = fp->dyn[j];
+        if (!ray_box(r, t_min, t_max, D.cur)) continue;
         uint32_t bt;
         if (dyn_closest(S, D, r, t_min, t_max, bt)) {
             kind = 1;
@@ -325,8 +493,8 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
     if (static_any(S, r, t_min, t_max)) return true;
     const FrameParams* fp = S.fp;
     for (uint32_t j = 0; j < fp->n_dyn; ++j) {
-        const DynObj D = fp->dyn[j];
-        if (!ray_box_exact(o, d, t_min, t_max, D.cur)) continue;
+        const DynObj& D = fp->dyn[j];
+        if (!ray_box(r, t_min, t_max, D.cur)) continue;
         if (dyn_any(S, D, r, t_min, t_max)) return true;
     }
     return false;

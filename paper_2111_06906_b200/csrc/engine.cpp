@@ -178,6 +178,7 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     PRX_CUDA(cudaMallocHost(&h_cnt32_, 4 * kCntN));
     d_ctr_.alloc(sizeof(Counters));
     d_cnt32_.alloc(4 * kCntN);
+    d_work_.alloc(64);
     PRX_CUDA(cudaMemsetAsync(d_ctr_.get(), 0, sizeof(Counters), stream_));
     PRX_CUDA(cudaMemsetAsync(d_cnt32_.get(), 0, 4 * kCntN, stream_));
 
@@ -539,8 +540,8 @@ void Engine::stage_occlusions() {
                            d_masks_.as<uint32_t>(), d_ctr_.as<Counters>(), stream_);
     if (cfg_.mode == PRX_MODE_ERROR)
         launch_verify_error(scene_dev(), path_dev(), cfg_.threshold, d_list_.as<uint32_t>(),
-                            d_masks_.as<uint32_t>(), d_ctr_.as<Counters>(), d_ctr_.as<Counters>(), n_,
-                            stream_);
+                            d_masks_.as<uint32_t>(), d_ctr_.as<Counters>(), d_work_.as<uint32_t>(),
+                            d_ctr_.as<Counters>(), stream_);
 }
 
 void Engine::stage_compute_dm() {
@@ -619,7 +620,8 @@ void Engine::stage_trace() {
     launch_retrace_flags(P, d_flags8_.as<uint8_t>(), stream_);
     compact_u8(d_flags8_.as<uint8_t>(), n_, nullptr, 0, d_list_.as<uint32_t>(), cnt + kCntRetrace,
                d_scratch_.get(), stream_);
-    launch_trace(scene_dev(), P, d_list_.as<uint32_t>(), cnt + kCntRetrace, n_, d_ctr_.as<Counters>(), stream_);
+    launch_trace(scene_dev(), P, d_list_.as<uint32_t>(), cnt + kCntRetrace, d_work_.as<uint32_t>(),
+                 d_ctr_.as<Counters>(), stream_);
     launch_finalize(P, d_ctr_.as<Counters>(), stream_);
 }
 

@@ -159,7 +159,7 @@ private:
     // work arrays
     DevBuf d_list_, d_masks_, d_flags8_, d_flags8b_, d_keys_, d_vals_, d_keys_tmp_, d_vals_tmp_,
         d_pruned_list_, d_need_, d_scratch_;
-    DevBuf d_ctr_, d_cnt32_;
+    DevBuf d_ctr_, d_cnt32_, d_work_;
     Counters* h_ctr_ = nullptr;
     uint32_t* h_cnt32_ = nullptr;
     uint32_t n_pruned_ = 0;

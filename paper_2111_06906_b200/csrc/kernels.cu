@@ -212,78 +212,119 @@ __global__ void __launch_bounds__(kT) k_occlusion_flags(SceneDev S, PathDev P, i
     }
 }
 
-// verify_path_error_based (engine.cpp:339-403): Alg. 1 walk over the flagged segments.
+// Warp-aggregated work fetch for persistent kernels: every lane that needs work gets the
+// next index of a global queue; one atomic per warp and call.
+__device__ __forceinline__ uint32_t fetch_work(uint32_t* counter) {
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    const unsigned rank = __popc(m & ((1u << lane) - 1u));
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    return base + rank;
+}
+
+// verify_path_error_based (engine.cpp:339-403): Alg. 1 walk over the flagged segments,
+// persistent: each lane walks one path at a time and advances its visibility ray one BVH
+// node per iteration, fetching the next flagged path as soon as its walk ends.
 __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, float threshold,
                                                      const uint32_t* __restrict__ list,
                                                      const uint32_t* __restrict__ masks,
-                                                     const Counters* cnt, Counters* ctr) {
+                                                     const Counters* cnt, uint32_t* work, Counters* ctr) {
     const FrameParams* fp = S.fp;
     const uint32_t n_list = (uint32_t)cnt->flagged;
     unsigned long long vis = 0;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_list; j += gridDim.x * blockDim.x) {
-        const uint32_t i = list[j];
-        const uint32_t flags = masks[j];
-        const uint32_t p = P.base + i;
-        const LightDev& L = fp->lights[light_of(fp, p)];
-        uchar4 m = P.meta[i];
-        const uint32_t k = m.x, segs = m.x + m.y;
-        const uint32_t epoch = P.epoch[i];
-        bool force = false;
-        uint32_t s = 0;
-        while (s < segs) {
-            const bool flagged = force || ((flags >> s) & 1u);
+    bool has = false, ray = false, force = false;
+    uint32_t i = 0, p = 0, flags = 0, k = 0, segs = 0, s = 0, epoch = 0, li = 0;
+    uchar4 m = make_uchar4(0, 0, 0, 0);
+    Trav T;
+    while (true) {
+        if (!has) {
+            const uint32_t j = fetch_work(work);
+            if (j >= n_list) break;
+            i = list[j];
+            flags = masks[j];
+            p = P.base + i;
+            li = light_of(fp, p);
+            m = P.meta[i];
+            k = m.x;
+            segs = m.x + m.y;
+            epoch = P.epoch[i];
+            s = 0;
             force = false;
-            if (!flagged) {
+            ray = false;
+            has = true;
+        }
+        if (!ray) {  // next flagged segment (engine.cpp:345-351)
+            while (s < segs) {
+                const bool flagged = force || ((flags >> s) & 1u);
+                force = false;
+                if (flagged) break;
                 ++s;
+            }
+            if (s >= segs) {
+                has = false;
                 continue;
             }
             const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, s - 1, i)]);
             const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
             ++vis;
-            Hit h;
-            const bool hit = intersect_scene(S, o, d, S.eps, h);
-            if (s == k) {  // escape segment: a new blocker -> retrace from here
-                if (hit) P.rstart[i] = (uint8_t)s;
-                break;
-            }
-            if (!hit) {  // destination gone: truncate and escape
-                truncate_path(P, i, s, true, m);
-                P.meta[i] = m;
-                break;
-            }
-            const size_t v = vix(P, s, i);
-            const float4 stored = P.energy[v];
-            const V3 e_prev = s == 0 ? L.flux_pp : ld3(P.energy[vix(P, s - 1, i)]);
-            const float4 am = __ldg(&S.mat[h.obj]);
-            const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
-            const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
-            if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
-                P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
-                P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
-                P.energy[v] = make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius);
-                const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
-                P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
-                P.rstart[i] = (uint8_t)(s + 1);
-                break;
-            }
-            const V3 old_pos = ld3(P.pos_obj[v]);
-            const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
+            trav_init(S, T, o, d, S.eps, FLT_MAX, false);
+            ray = true;
+        }
+        if (!trav_step(S, T)) continue;
+        ray = false;
+        Hit h;
+        const bool hit = trav_hit(S, T, h);
+        const V3 d = T.r.d;
+        if (s == k) {  // escape segment: a new blocker -> retrace from here
+            if (hit) P.rstart[i] = (uint8_t)s;
+            has = false;
+            continue;
+        }
+        if (!hit) {  // destination gone: truncate and escape
+            truncate_path(P, i, s, true, m);
+            P.meta[i] = m;
+            has = false;
+            continue;
+        }
+        const size_t v = vix(P, s, i);
+        const float4 stored = P.energy[v];
+        const V3 e_prev = s == 0 ? fp->lights[li].flux_pp : ld3(P.energy[vix(P, s - 1, i)]);
+        const float4 am = __ldg(&S.mat[h.obj]);
+        const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
+        const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
+        if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
             P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
             P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
-            if (s + 1 >= segs) break;
-            const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
-            if (close_pos && !hit_dyn && !((flags >> (s + 1)) & 1u)) {
-                s += 2;
-                continue;
-            }
-            if (s + 1 < k) {
-                const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
-                const V3 od = normalized(sub(next, h.pos));
-                P.out_dir[v] = make_float4(od.x, od.y, od.z, 0.f);
-            }
-            force = true;
-            ++s;
+            P.energy[v] = make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius);
+            const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
+            P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
+            P.rstart[i] = (uint8_t)(s + 1);
+            has = false;
+            continue;
         }
+        const V3 old_pos = ld3(P.pos_obj[v]);
+        const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
+        P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
+        P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+        if (s + 1 >= segs) {
+            has = false;
+            continue;
+        }
+        const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
+        if (close_pos && !hit_dyn && !((flags >> (s + 1)) & 1u)) {
+            s += 2;  // the next segment is provably unchanged
+            continue;
+        }
+        if (s + 1 < k) {
+            const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
+            const V3 od = normalized(sub(next, h.pos));
+            P.out_dir[v] = make_float4(od.x, od.y, od.z, 0.f);
+        }
+        force = true;
+        ++s;
     }
     warp_add(&ctr->vis, vis);
 }
@@ -469,21 +510,22 @@ __global__ void k_retrace_flags(PathDev P, uint8_t* flags) {
         flags[i] = (P.meta[i].z == kLive && P.rstart[i] != kNoRetrace) ? 1 : 0;
 }
 
+// stage_trace's per-path bounce loop (engine.cpp:557-586): one path per thread.
 __global__ void __launch_bounds__(kT) k_trace(SceneDev S, PathDev P, const uint32_t* __restrict__ list,
-                                              const uint32_t* count, Counters* ctr) {
+                                              const uint32_t* count, uint32_t* work, Counters* ctr) {
+    (void)work;
     const FrameParams* fp = S.fp;
     const uint32_t n = *count;
     unsigned long long traced = 0;
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const uint32_t i = list[j];
         const uint32_t p = P.base + i;
-        const LightDev& L = fp->lights[light_of(fp, p)];
         uchar4 m = P.meta[i];
         const uint32_t epoch = P.epoch[i];
         uint32_t b = P.rstart[i];
         V3 pos = b == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, b - 1, i)]);
         V3 dir = b == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, b - 1, i)]);
-        V3 energy = b == 0 ? L.flux_pp : ld3(P.energy[vix(P, b - 1, i)]);
+        V3 energy = b == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[vix(P, b - 1, i)]);
         bool escaped = false;
         while (b < P.B) {
             ++traced;
@@ -591,9 +633,21 @@ void launch_occlusion_flags(SceneDev S, PathDev P, int mode, int record, uint32_
                             Counters* ctr, cudaStream_t st) {
     LAUNCH(k_occlusion_flags, P.n, S, P, mode, record, list, masks, ctr);
 }
+template <typename K>
+static int persistent_grid(K kernel) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kT, 0);
+    return sms * (per_sm > 0 ? per_sm : 1);
+}
+
 void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t* list, const uint32_t* masks,
-                         const Counters* cnt, Counters* ctr, uint32_t n_max, cudaStream_t st) {
-    LAUNCH(k_verify_error, n_max, S, P, threshold, list, masks, cnt, ctr);
+                         const Counters* cnt, uint32_t* work, Counters* ctr, cudaStream_t st) {
+    static int grid = persistent_grid(k_verify_error);
+    cudaMemsetAsync(work, 0, 4, st);
+    k_verify_error<<<grid, kT, 0, st>>>(S, P, threshold, list, masks, cnt, work, ctr);
+    ++g_launches;
 }
 void launch_compute_dm(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st) {
     LAUNCH(k_compute_dm, P.n, S, P, ctr);
@@ -647,9 +701,11 @@ void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, 
 void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st) {
     LAUNCH(k_retrace_flags, P.n, P, flags);
 }
-void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count, uint32_t n_max,
+void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count, uint32_t* work,
                   Counters* ctr, cudaStream_t st) {
-    LAUNCH(k_trace, n_max, S, P, list, count, ctr);
+    static int grid = persistent_grid(k_trace);
+    k_trace<<<grid, kT, 0, st>>>(S, P, list, count, work, ctr);
+    ++g_launches;
 }
 void launch_finalize(PathDev P, Counters* ctr, cudaStream_t st) { LAUNCH(k_finalize, P.n, P, ctr); }
 void launch_pack_photons(PathDev P, void* photons, void* aux, cudaStream_t st) {

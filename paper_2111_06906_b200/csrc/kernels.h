@@ -29,8 +29,8 @@ void launch_occlusion_flags(SceneDev S, PathDev P, int mode, int record, uint32_
                             uint32_t* masks, Counters* ctr, cudaStream_t st);
 // verify_path_error_based (engine.cpp:339-403) over the flagged list
 void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t* list,
-                         const uint32_t* masks, const Counters* ctr_count, Counters* ctr,
-                         uint32_t n_max, cudaStream_t st);
+                         const uint32_t* masks, const Counters* ctr_count, uint32_t* work,
+                         Counters* ctr, cudaStream_t st);
 // stage_compute_dm (engine.cpp:405-441)
 void launch_compute_dm(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st);
 // stage_prune (engine.cpp:443-497): marks + per-cell unmarked counts
@@ -60,7 +60,7 @@ void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, 
 // stage_trace (engine.cpp:548-598)
 void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st);
 void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count,
-                  uint32_t n_max, Counters* ctr, cudaStream_t st);
+                  uint32_t* work, Counters* ctr, cudaStream_t st);
 void launch_finalize(PathDev P, Counters* ctr, cudaStream_t st);
 // layout conversion for drop-in accessors
 void launch_pack_photons(PathDev P, void* photons, void* aux, cudaStream_t st);
