@@ -255,25 +255,27 @@ typedef enum prx_stage {
 } prx_stage;
 prx_status prx_run_stage(prx_engine* engine, int stage, prx_frame_stats* stats);
 
-/* Sharded prune/fill exchange points.  All buffers are DEVICE pointers
- * on the engine's device, ordered on the engine stream.
- *  - after COMPUTE_DM: the caller all-reduces DM_C of each light (prx_engine_dm_current
- *    gives its device address) across shards;
- *  - prx_prune_count: marks paths, writes per-cell unmarked counts for light `li` into
- *    `unmarked_out[cells]`;
- *  - caller all-gathers those; passes (sum over shards < this, total over shards);
- *  - prx_prune_apply: trims survivors, updates DM_C, builds the pruned list;
- *  - prx_fill_count: writes the number of dead slots of light `li` into *dead_out (host);
- *  - prx_fill_apply: with the global exclusive prefix of dead slots and the global
- *    total, assigns deficit units to this shard's slots and samples them.          */
+/* Sharded prune/fill exchange points.  Per-light arrays are indexed by
+ * light; every `*_dev` buffer is a DEVICE pointer on the engine's device, ordered on the
+ * engine stream.  A sharded frame is:
+ *   frame_update; verify_paths (local DM_C histogram);
+ *   all-reduce(sum) DM_C of every light (prx_engine_dm_current gives its address);
+ *   prx_prune_count -> per-cell unmarked counts of this shard; all-gather them; pass the
+ *     exclusive prefix over lower shards and the total over all shards to prx_prune_apply
+ *     (survivors are the dm_t lowest path ids of a cell, engine.cpp:459-466);
+ *   prx_fill_count -> dead slots of this shard per light (host); all-gather; pass the
+ *     exclusive prefix and the total to prx_fill_apply (deficit cells ascending <-> dead
+ *     slots ascending over the whole path range, engine.cpp:503-519);
+ *   prx_run_stage(PRX_STAGE_TRACE); all-reduce the counters.
+ * With one shard, prefix = 0 and total = local reproduce run_frame exactly. */
 prx_status prx_engine_dm_current(prx_engine* engine, uint32_t light, void** dev_ptr,
                                  uint32_t* cells);
-prx_status prx_prune_count(prx_engine* engine, uint32_t light, uint32_t* unmarked_out_dev);
-prx_status prx_prune_apply(prx_engine* engine, uint32_t light, const uint32_t* prefix_dev,
-                           const uint32_t* total_dev, prx_frame_stats* stats);
-prx_status prx_fill_count(prx_engine* engine, uint32_t light, uint32_t* dead_out);
-prx_status prx_fill_apply(prx_engine* engine, uint32_t light, uint64_t dead_prefix,
-                          uint64_t dead_total, prx_frame_stats* stats);
+prx_status prx_prune_count(prx_engine* engine, uint32_t* const* unmarked_dev);
+prx_status prx_prune_apply(prx_engine* engine, const uint32_t* const* prefix_dev,
+                           const uint32_t* const* total_dev, prx_frame_stats* stats);
+prx_status prx_fill_count(prx_engine* engine, uint32_t* dead_out);
+prx_status prx_fill_apply(prx_engine* engine, const uint64_t* dead_prefix,
+                          const uint64_t* dead_total, prx_frame_stats* stats);
 /* Stream the engine orders its work on (cudaStream_t as void*); NULL = engine-owned. */
 prx_status prx_engine_set_stream(prx_engine* engine, void* cuda_stream);
 prx_status prx_engine_synchronize(prx_engine* engine);

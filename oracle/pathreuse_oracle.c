@@ -898,7 +898,13 @@ struct po_engine {
     Placed placed;
     Box occ[256];
     uint32_t n_occ;
+    uint32_t sb, se;   /* shard [sb, se) of the global path range (all paths by default) */
+    uint8_t* mark;     /* sharded prune: 1 = marked, 2 = unmarked candidate */
 };
+
+/* block range intersected with the shard */
+static uint32_t lo_of(const po_engine* e, const Block* b) { return b->begin > e->sb ? b->begin : e->sb; }
+static uint32_t hi_of(const po_engine* e, const Block* b) { return b->end < e->se ? b->end : e->se; }
 
 static size_t vi(const po_engine* e, uint32_t b, uint32_t p) { return (size_t)b * e->N + p; }
 static V f4v(F4 f) { return v3(f.x, f.y, f.z); }
@@ -912,7 +918,7 @@ void po_engine_destroy(po_engine* e) {
     for (uint32_t i = 0; i < e->n_blk; ++i) { free(e->blk[i].dm_t); free(e->blk[i].dm_c); }
     free(e->pos_obj); free(e->energy); free(e->in_dir); free(e->out_dir); free(e->origin); free(e->emis);
     free(e->canon); free(e->cell); free(e->epoch); free(e->path_info); free(e->seg_flags); free(e->pruned);
-    free(e->meta); free(e->rstart);
+    free(e->meta); free(e->rstart); free(e->mark);
     placed_free(&e->placed);
     free(e);
 }
@@ -977,6 +983,9 @@ int po_engine_create(const po_scene* s, const prx_config* cfg, po_engine** out) 
     e->meta = (uint8_t*)calloc(e->N, 4);
     e->rstart = (uint8_t*)malloc(e->N);
     memset(e->rstart, 0xFF, e->N);
+    e->mark = (uint8_t*)calloc(e->N, 1);
+    e->sb = cfg->shard_begin;
+    e->se = (cfg->shard_begin == 0 && cfg->shard_end == 0) ? e->N : cfg->shard_end;
     *out = e;
     return 0;
 }
@@ -1077,13 +1086,13 @@ int po_frame_update(po_engine* e, prx_frame_stats* st) {
         }
     }
     e->n_pruned = 0;
-    for (uint32_t p = 0; p < e->N; ++p) {
+    for (uint32_t p = e->sb; p < e->se; ++p) {
         e->meta[4 * p + 3] = 0;
         e->rstart[p] = 0xFF;
         if (e->cfg.record_flags) e->seg_flags[p] = 0;
     }
     if (e->cfg.mode == PRX_MODE_BASELINE) {                                                /* release_all_paths :149-157 */
-        for (uint32_t p = 0; p < e->N; ++p) {
+        for (uint32_t p = e->sb; p < e->se; ++p) {
             truncate_path(e, p, 0, 0);
             e->meta[4 * p + 2] = DEAD;
         }
@@ -1103,7 +1112,7 @@ static void update_origins(po_engine* e, prx_frame_stats* st) {
         Block* b = &e->blk[li];
         if (!b->moved) continue;
         const Pose ps = b->now;
-        for (uint32_t p = b->begin; p < b->end; ++p) {
+        for (uint32_t p = lo_of(e, b); p < hi_of(e, b); ++p) {
             if (e->meta[4 * p + 2] != LIVE) continue;
             if (!is_area(b->L->kind)) {
                 e->origin[p] = vf4(ps.pos, 0);
@@ -1178,7 +1187,7 @@ static void occlusions(po_engine* e, prx_frame_stats* st) {
     if (e->n_occ == 0) return;
     for (uint32_t li = 0; li < e->n_blk; ++li) {
         const Block* b = &e->blk[li];
-        for (uint32_t p = b->begin; p < b->end; ++p) {
+        for (uint32_t p = lo_of(e, b); p < hi_of(e, b); ++p) {
             if (e->meta[4 * p + 2] != LIVE) continue;
             const uint32_t flags = flag_mask(e, p);
             if (e->cfg.record_flags) e->seg_flags[p] = flags;
@@ -1199,7 +1208,7 @@ static void compute_dm(po_engine* e, prx_frame_stats* st) {
     for (uint32_t li = 0; li < e->n_blk; ++li) {
         Block* b = &e->blk[li];
         memset(b->dm_c, 0, 4 * b->cells);
-        for (uint32_t p = b->begin; p < b->end; ++p) {
+        for (uint32_t p = lo_of(e, b); p < hi_of(e, b); ++p) {
             const uint8_t status = e->meta[4 * p + 2];
             if (status == DEAD) continue;
             int ok = status == LIVE;
@@ -1295,7 +1304,7 @@ static void trace(po_engine* e, prx_frame_stats* st) {
     uint64_t traced = 0, segments = 0;
     for (uint32_t li = 0; li < e->n_blk; ++li) {
         const Block* blk = &e->blk[li];
-        for (uint32_t p = blk->begin; p < blk->end; ++p) {
+        for (uint32_t p = lo_of(e, blk); p < hi_of(e, blk); ++p) {
             if (e->meta[4 * p + 2] != LIVE) continue;
             const uint8_t start = e->rstart[p];
             if (start != 0xFF) {
@@ -1521,5 +1530,96 @@ int po_gather(po_engine* e, const prx_camera* cam, float radius, float* rgb) {
         rgb[3 * pix + 2] = out.z;
     }
     free(pos); free(en); free(ob); free(ki);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ sharded prune / fill
+ * The single-engine stage_prune / stage_fill (engine.cpp:443-546) split at the exchange
+ * points of SURVEY.md s8e; with one shard (prefix 0, total = local) they reduce to them. */
+int po_prune_count(po_engine* e, uint32_t** unmarked) {
+    const uint32_t frame = (uint32_t)(e->frames_run - 1);
+    for (uint32_t li = 0; li < e->n_blk; ++li) {
+        const Block* b = &e->blk[li];
+        memset(unmarked[li], 0, 4 * b->cells);
+        for (uint32_t p = lo_of(e, b); p < hi_of(e, b); ++p) {
+            e->mark[p] = 0;
+            if (e->meta[4 * p + 2] != LIVE) continue;
+            const uint32_t c = e->cell[p];
+            if (b->dm_c[c] <= b->dm_t[c]) continue;
+            const double prob = po_prune_probability(b->dm_c[c], b->dm_t[c]);
+            const float u = rng_f(e->cfg.seed, p, frame, 0, P_PRUNE, 0);
+            if (prob > 0.0 && u < prob) e->mark[p] = 1;
+            else { e->mark[p] = 2; unmarked[li][c]++; }
+        }
+    }
+    return 0;
+}
+
+int po_prune_apply(po_engine* e, const uint32_t** prefix, const uint32_t** total, prx_frame_stats* st) {
+    e->n_pruned = 0;
+    for (uint32_t li = 0; li < e->n_blk; ++li) {
+        Block* b = &e->blk[li];
+        uint32_t* seen = (uint32_t*)calloc(b->cells, 4);
+        for (uint32_t p = lo_of(e, b); p < hi_of(e, b); ++p) {  /* ascending ids = per-cell rank */
+            if (e->mark[p] != 2) continue;
+            const uint32_t c = e->cell[p];
+            const uint32_t rank = prefix[li][c] + seen[c]++;
+            if (total[li][c] > b->dm_t[c] && rank >= b->dm_t[c]) e->mark[p] = 1;
+        }
+        free(seen);
+        for (uint32_t p = lo_of(e, b); p < hi_of(e, b); ++p) {
+            if (e->mark[p] != 1) continue;
+            truncate_path(e, p, 0, 0);
+            e->meta[4 * p + 2] = DEAD;
+            e->pruned[e->n_pruned++] = p;
+        }
+        for (uint32_t c = 0; c < b->cells; ++c)
+            if (b->dm_c[c] > b->dm_t[c]) b->dm_c[c] = total[li][c] < b->dm_t[c] ? total[li][c] : b->dm_t[c];
+    }
+    qsort(e->pruned, e->n_pruned, 4, cmp_u32);
+    st->paths_pruned = e->n_pruned;
+    return 0;
+}
+
+int po_fill_count(po_engine* e, uint32_t* dead) {
+    for (uint32_t li = 0; li < e->n_blk; ++li) {
+        const Block* b = &e->blk[li];
+        dead[li] = 0;
+        for (uint32_t p = lo_of(e, b); p < hi_of(e, b); ++p) dead[li] += e->meta[4 * p + 2] == DEAD;
+    }
+    return 0;
+}
+
+int po_fill_apply(po_engine* e, const uint64_t* prefix, const uint64_t* total, prx_frame_stats* st) {
+    for (uint32_t li = 0; li < e->n_blk; ++li) {
+        Block* b = &e->blk[li];
+        uint64_t need_total = 0;
+        for (uint32_t c = 0; c < b->cells; ++c) need_total += b->dm_t[c] > b->dm_c[c] ? b->dm_t[c] - b->dm_c[c] : 0;
+        if (need_total > total[li]) return fail(PRX_E_LOGIC, "fill: ran out of free path slots");
+        uint64_t u = 0;  /* global unit index */
+        uint32_t slot = lo_of(e, b);
+        for (uint32_t c = 0; c < b->cells; ++c) {
+            const uint32_t need = b->dm_t[c] > b->dm_c[c] ? b->dm_t[c] - b->dm_c[c] : 0;
+            for (uint32_t k = 0; k < need; ++k, ++u) {
+                if (u < prefix[li]) continue;            /* unit owned by a lower shard */
+                while (slot < hi_of(e, b) && e->meta[4 * slot + 2] != DEAD) ++slot;
+                if (slot >= hi_of(e, b)) break;          /* owned by a higher shard */
+                const uint32_t p = slot++;
+                e->epoch[p] += 1;
+                float cc[4];
+                V o, d;
+                sample_cell(b->L, b->now, b->dims, b->nd, c, e->cfg.seed, p, e->epoch[p], cc, &o, &d);
+                e->origin[p] = vf4(o, 0);
+                e->emis[p] = vf4(d, 0);
+                e->canon[p].x = cc[0]; e->canon[p].y = cc[1]; e->canon[p].z = cc[2]; e->canon[p].w = cc[3];
+                e->cell[p] = c;
+                e->meta[4 * p] = 0; e->meta[4 * p + 1] = 0; e->meta[4 * p + 2] = LIVE; e->meta[4 * p + 3] = 1;
+                e->rstart[p] = 0;
+                st->paths_filled++;
+            }
+        }
+        for (uint32_t c = 0; c < b->cells; ++c)
+            if (b->dm_c[c] < b->dm_t[c]) b->dm_c[c] = b->dm_t[c];
+    }
     return 0;
 }

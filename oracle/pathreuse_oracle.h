@@ -50,6 +50,11 @@ int po_download(const po_engine* e, int field, uint32_t index, void* dst, size_t
 int po_upload(po_engine* e, int field, uint32_t index, const void* src, size_t bytes);
 int po_set_frame_counter(po_engine* e, int frames_run);
 int po_gather(po_engine* e, const prx_camera* cam, float radius, float* rgb_out);
+/* sharded prune/fill exchange points (cfg.shard_begin/end select the shard) */
+int po_prune_count(po_engine* e, uint32_t** unmarked);
+int po_prune_apply(po_engine* e, const uint32_t** prefix, const uint32_t** total, prx_frame_stats* st);
+int po_fill_count(po_engine* e, uint32_t* dead);
+int po_fill_apply(po_engine* e, const uint64_t* prefix, const uint64_t* total, prx_frame_stats* st);
 /* closest hit at `frame`: rays [n][8] {o, d, t_min, t_max} -> hits [n][9] as prxref_intersect_batch */
 int po_intersect_batch(const po_scene* s, int frame, const float* rays, size_t n, float* hits);
 

@@ -158,3 +158,96 @@ class PortEngine:
         out = np.zeros((cam.height, cam.width, 3), dtype=np.float32)
         check(lib().po_gather(self._h, C.byref(cam), float(radius), out.ctypes.data_as(C.POINTER(C.c_float))))
         return out, 0.0
+
+
+_SHARD_SIGS = [
+    ("po_prune_count", C.c_int, [_P, C.POINTER(C.POINTER(C.c_uint32))]),
+    ("po_prune_apply", C.c_int, [_P, C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.POINTER(C.c_uint32)),
+                                 C.POINTER(L.FrameStats)]),
+    ("po_fill_count", C.c_int, [_P, C.POINTER(C.c_uint32)]),
+    ("po_fill_apply", C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(L.FrameStats)]),
+]
+
+
+def _shard_lib():
+    h = lib()
+    for name, res, args in _SHARD_SIGS:
+        fn = getattr(h, name)
+        fn.restype = res
+        fn.argtypes = args
+    return h
+
+
+class PortShardExecutor:
+    """One path shard of the C oracle behind the executor interface of
+    paper_2111_06906_b200.distributed (CPU torch tensors, for gloo tests)."""
+
+    def __init__(self, scene: PortScene, config: L.Config):
+        import torch
+
+        self.torch = torch
+        self.engine = PortEngine(scene, config)
+        self.sb, self.se = config.shard_begin, config.shard_end
+        self.mode = config.mode
+        self.n_lights = scene.describe().n_lights
+        self.cells = [self.engine.download("dm_target", li).size for li in range(self.n_lights)]
+        self.st = L.FrameStats()
+        self.lib = _shard_lib()
+
+    def _meta(self):
+        return self.engine.download("meta")[self.sb:self.se]
+
+    def frame_update(self):
+        m = self._meta()
+        live = m[:, 2] == 1
+        self.live_segments = int((m[live, 0].astype(np.int64) + m[live, 1]).sum())
+        self.st = self.engine.frame_update()
+
+    def verify(self):
+        for s in ("update_origins", "occlusions", "compute_dm"):
+            self.engine.run_stage(s, self.st)
+
+    def dm_buffers(self):
+        return [self.torch.from_numpy(self.engine.download("dm_current", li).view(np.int32).copy())
+                for li in range(self.n_lights)]
+
+    def dm_commit(self, bufs):
+        for li, t in enumerate(bufs):
+            self.engine.upload("dm_current", t.numpy().view(np.uint32), li)
+
+    def prune_count(self):
+        outs = [np.zeros(c, dtype=np.uint32) for c in self.cells]
+        arr = (C.POINTER(C.c_uint32) * self.n_lights)(*[o.ctypes.data_as(C.POINTER(C.c_uint32)) for o in outs])
+        check(self.lib.po_prune_count(self.engine._h, arr))
+        return [self.torch.from_numpy(o.view(np.int32)) for o in outs]
+
+    def prune_apply(self, prefix, total):
+        pn = [np.ascontiguousarray(p.numpy()).view(np.uint32) for p in prefix]
+        tn = [np.ascontiguousarray(t.numpy()).view(np.uint32) for t in total]
+        pa = (C.POINTER(C.c_uint32) * self.n_lights)(*[a.ctypes.data_as(C.POINTER(C.c_uint32)) for a in pn])
+        ta = (C.POINTER(C.c_uint32) * self.n_lights)(*[a.ctypes.data_as(C.POINTER(C.c_uint32)) for a in tn])
+        check(self.lib.po_prune_apply(self.engine._h, pa, ta, C.byref(self.st)))
+
+    def fill_count(self):
+        out = (C.c_uint32 * self.n_lights)()
+        check(self.lib.po_fill_count(self.engine._h, out))
+        return list(out)
+
+    def fill_apply(self, prefix, total):
+        pa = (C.c_uint64 * self.n_lights)(*prefix)
+        ta = (C.c_uint64 * self.n_lights)(*total)
+        check(self.lib.po_fill_apply(self.engine._h, pa, ta, C.byref(self.st)))
+
+    def trace(self):
+        m = self._meta()
+        rs = self.engine.download("retrace_start")[self.sb:self.se]
+        retraced = int(((m[:, 2] == 1) & (rs != 0xFF)).sum())
+        self.engine.run_stage("trace", self.st)
+        st = self.st
+        return {"rays_traced": st.rays_traced, "paths_replaced": st.paths_replaced,
+                "paths_pruned": st.paths_pruned, "paths_filled": st.paths_filled,
+                "visibility_rays": st.visibility_rays, "live_segments_before": self.live_segments,
+                "paths_retraced": retraced, "segments": st.rays_traced + st.rays_reused}
+
+    def new_tensor(self, values, dtype="int64"):
+        return self.torch.tensor(values, dtype=getattr(self.torch, dtype))

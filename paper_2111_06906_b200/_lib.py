@@ -153,10 +153,11 @@ SIGNATURES = [
     ("prx_retrace_invalid", C.c_int, [P, C.POINTER(FrameStats)]),
     ("prx_run_stage", C.c_int, [P, C.c_int, C.POINTER(FrameStats)]),
     ("prx_engine_dm_current", C.c_int, [P, C.c_uint32, C.POINTER(P), C.POINTER(C.c_uint32)]),
-    ("prx_prune_count", C.c_int, [P, C.c_uint32, P]),
-    ("prx_prune_apply", C.c_int, [P, C.c_uint32, P, P, C.POINTER(FrameStats)]),
-    ("prx_fill_count", C.c_int, [P, C.c_uint32, C.POINTER(C.c_uint32)]),
-    ("prx_fill_apply", C.c_int, [P, C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(FrameStats)]),
+    ("prx_prune_count", C.c_int, [P, C.POINTER(C.POINTER(C.c_uint32))]),
+    ("prx_prune_apply", C.c_int, [P, C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.POINTER(C.c_uint32)),
+                                  C.POINTER(FrameStats)]),
+    ("prx_fill_count", C.c_int, [P, C.POINTER(C.c_uint32)]),
+    ("prx_fill_apply", C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(FrameStats)]),
     ("prx_engine_set_stream", C.c_int, [P, P]),
     ("prx_engine_synchronize", C.c_int, [P]),
     ("prx_splat", C.c_int, [P, C.POINTER(Camera), C.c_float, C.c_int, P, P,

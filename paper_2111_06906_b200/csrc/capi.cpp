@@ -227,19 +227,33 @@ prx_status prx_run_stage(prx_engine* engine, int stage, prx_frame_stats* stats) 
 prx_status prx_engine_dm_current(prx_engine* engine, uint32_t light, void** dev_ptr, uint32_t* cells) {
     return guarded([&] { eng(engine).dm_current_ptr(light, dev_ptr, cells); });
 }
-prx_status prx_prune_count(prx_engine* engine, uint32_t light, uint32_t* unmarked_out_dev) {
-    return guarded([&] { eng(engine).prune_count(light, unmarked_out_dev); });
+prx_status prx_prune_count(prx_engine* engine, uint32_t* const* unmarked_dev) {
+    return guarded([&] {
+        need(unmarked_dev, "unmarked_dev");
+        eng(engine).prune_count(unmarked_dev);
+    });
 }
-prx_status prx_prune_apply(prx_engine* engine, uint32_t light, const uint32_t* prefix_dev,
-                           const uint32_t* total_dev, prx_frame_stats* stats) {
-    return guarded([&] { eng(engine).prune_apply(light, prefix_dev, total_dev, stats); });
+prx_status prx_prune_apply(prx_engine* engine, const uint32_t* const* prefix_dev, const uint32_t* const* total_dev,
+                           prx_frame_stats* stats) {
+    return guarded([&] {
+        need(prefix_dev, "prefix_dev");
+        need(total_dev, "total_dev");
+        eng(engine).prune_apply(prefix_dev, total_dev, stats);
+    });
 }
-prx_status prx_fill_count(prx_engine* engine, uint32_t light, uint32_t* dead_out) {
-    return guarded([&] { eng(engine).fill_count(light, dead_out); });
+prx_status prx_fill_count(prx_engine* engine, uint32_t* dead_out) {
+    return guarded([&] {
+        need(dead_out, "dead_out");
+        eng(engine).fill_count(dead_out);
+    });
 }
-prx_status prx_fill_apply(prx_engine* engine, uint32_t light, uint64_t dead_prefix, uint64_t dead_total,
+prx_status prx_fill_apply(prx_engine* engine, const uint64_t* dead_prefix, const uint64_t* dead_total,
                           prx_frame_stats* stats) {
-    return guarded([&] { eng(engine).fill_apply(light, dead_prefix, dead_total, stats); });
+    return guarded([&] {
+        need(dead_prefix, "dead_prefix");
+        need(dead_total, "dead_total");
+        eng(engine).fill_apply(dead_prefix, dead_total, stats);
+    });
 }
 prx_status prx_engine_set_stream(prx_engine* engine, void* cuda_stream) {
     return guarded([&] { eng(engine).set_stream(static_cast<cudaStream_t>(cuda_stream)); });

@@ -36,7 +36,7 @@ void DevBuf::reset() {
 
 namespace {
 
-enum { kCntTrim = 0, kCntPruned = 1, kCntRetrace = 2, kCntDead = 3, kCntNeed = 4, kCntN = 8 };
+enum { kCntTrim = 0, kCntPruned = 1, kCntRetrace = 2, kCntDead0 = 8, kCntNeed0 = 24, kCntN = 40 };
 enum {
     kEvFrame0 = 0,
     kEvVerify0 = 1,
@@ -349,8 +349,8 @@ void Engine::alloc_state() {
     d_pruned_list_.alloc(4ull * n_);
     d_need_.alloc(4ull * max_cells_ + 16);
     d_scratch_.alloc(prim_scratch_bytes(std::max<uint64_t>(n_, max_cells_)));
-    // per-light pointer tables: [0] unm, [1] seg_start, [2] prefix (sharded prune)
-    std::vector<uint32_t*> ptrs(3 * PRX_MAX_LIGHTS, nullptr);
+    // per-light pointer tables: [0] unm, [1] seg_start, [2] prefix, [3] total (sharded prune)
+    std::vector<uint32_t*> ptrs(4 * PRX_MAX_LIGHTS, nullptr);
     for (size_t li = 0; li < lights_.size(); ++li) {
         ptrs[li] = lights_[li].unm.as<uint32_t>();
         ptrs[PRX_MAX_LIGHTS + li] = lights_[li].seg_start.as<uint32_t>();
@@ -565,53 +565,86 @@ void Engine::verify_paths(prx_frame_stats* st) {
     record(kEvPrune0);
 }
 
-// stage_prune (engine.cpp:473-497) on a single shard: global counts == local counts
-void Engine::stage_prune_local() {
-    uint32_t* const* unm = d_light_ptrs_.as<uint32_t*>();
+// stage_prune (engine.cpp:473-497), split at the cross-shard exchange point.
+// Marks (Eq. 1 Bernoulli, keyed by (path, frame)) and per-cell unmarked counts.
+void Engine::prune_mark_all() {
     for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.unm.get(), 0, 4ull * b.cells, stream_));
+    launch_prune_mark(scene_dev(), path_dev(), static_cast<uint32_t>(cur_frame_), d_light_ptrs_.as<uint32_t*>(),
+                      d_flags8_.as<uint8_t>(), d_flags8b_.as<uint8_t>(), stream_);
+}
+
+// Trim to exactly dm_t survivors per overfull cell, keeping the lowest path ids; `prefix`
+// (device table, may be null) holds the unmarked counts of lower shards, `total` those of
+// all shards; total_host[li] is the device address of light li's total counts.
+void Engine::prune_trim_all(uint32_t* const* prefix_tab, uint32_t* const* total_tab,
+                            const uint32_t* const* total_host) {
     const PathDev P = path_dev();
-    launch_prune_mark(scene_dev(), P, static_cast<uint32_t>(cur_frame_), unm, d_flags8_.as<uint8_t>(),
-                      d_flags8b_.as<uint8_t>(), stream_);
-    // candidates that need a trim -> (light, cell)-sorted list, stable in path id
-    uint8_t* trim = reinterpret_cast<uint8_t*>(d_keys_tmp_.as<uint32_t>());  // reuse as n bytes
-    launch_prune_trim_flags(P, d_fp_.as<FrameParams>(), unm, d_flags8b_.as<uint8_t>(), trim, stream_);
     uint32_t* cnt = d_cnt32_.as<uint32_t>();
+    uint8_t* trim = reinterpret_cast<uint8_t*>(d_keys_tmp_.as<uint32_t>());  // n bytes of scratch
+    launch_prune_trim_flags(P, d_fp_.as<FrameParams>(), total_tab, d_flags8b_.as<uint8_t>(), trim, stream_);
     compact_u8(trim, n_, nullptr, 0, d_list_.as<uint32_t>(), cnt + kCntTrim, d_scratch_.get(), stream_);
-    launch_prune_keys(P, d_fp_.as<FrameParams>(), d_list_.as<uint32_t>(), cnt + kCntTrim,
-                      d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), n_, stream_);
+    launch_prune_keys(P, d_fp_.as<FrameParams>(), d_list_.as<uint32_t>(), cnt + kCntTrim, d_keys_.as<uint32_t>(),
+                      d_vals_.as<uint32_t>(), n_, stream_);
     int light_bits = 0;
     while ((1u << light_bits) < lights_.size()) ++light_bits;
     radix_sort_pairs(d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), d_keys_tmp_.as<uint32_t>(),
-                     d_vals_tmp_.as<uint32_t>(), n_, cnt + kCntTrim, 22 + light_bits, d_scratch_.get(),
-                     stream_);
-    launch_prune_trim(P, d_fp_.as<FrameParams>(), d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(),
-                      cnt + kCntTrim, n_, unm + PRX_MAX_LIGHTS, nullptr, d_flags8_.as<uint8_t>(), stream_);
+                     d_vals_tmp_.as<uint32_t>(), n_, cnt + kCntTrim, 22 + light_bits, d_scratch_.get(), stream_);
+    launch_prune_trim(P, d_fp_.as<FrameParams>(), d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), cnt + kCntTrim,
+                      n_, d_light_ptrs_.as<uint32_t*>() + PRX_MAX_LIGHTS, prefix_tab, d_flags8_.as<uint8_t>(),
+                      stream_);
     launch_prune_apply(P, d_flags8_.as<uint8_t>(), stream_);
-    for (LightBlock& b : lights_)
-        launch_dm_after_prune(b.dm_c.as<uint32_t>(), b.dm_t.as<uint32_t>(), b.unm.as<uint32_t>(), b.cells,
-                              stream_);
+    for (size_t li = 0; li < lights_.size(); ++li)
+        launch_dm_after_prune(lights_[li].dm_c.as<uint32_t>(), lights_[li].dm_t.as<uint32_t>(), total_host[li],
+                              lights_[li].cells, stream_);
     compact_u8(d_flags8_.as<uint8_t>(), n_, nullptr, sb_, d_pruned_list_.as<uint32_t>(), cnt + kCntPruned,
                d_scratch_.get(), stream_);
 }
 
-// stage_fill (engine.cpp:499-546) on a single shard
-void Engine::stage_fill_local() {
+void Engine::stage_prune_local() {
+    prune_mark_all();
+    std::vector<const uint32_t*> totals(lights_.size());
+    for (size_t li = 0; li < lights_.size(); ++li) totals[li] = lights_[li].unm.as<uint32_t>();
+    prune_trim_all(nullptr, d_light_ptrs_.as<uint32_t*>(), totals.data());
+}
+
+// stage_fill (engine.cpp:499-546), split at the exchange point: the dead slots of this
+// shard, ascending, per light (written at d_list_ + local block begin).
+void Engine::fill_collect_dead() {
+    const PathDev P = path_dev();
+    uint32_t* cnt = d_cnt32_.as<uint32_t>();
+    for (uint32_t li = 0; li < lights_.size(); ++li) {
+        const uint32_t lb = local_lb(lights_[li]), le = local_le(lights_[li]);
+        launch_dead_flags(P, lb, le, d_flags8_.as<uint8_t>() + lb, stream_);
+        compact_u8(d_flags8_.as<uint8_t>() + lb, le - lb, nullptr, lb, d_list_.as<uint32_t>() + lb,
+                   cnt + kCntDead0 + li, d_scratch_.get(), stream_);
+    }
+}
+
+// Deficit cells ascending <-> dead slots ascending over the whole path range: this shard
+// owns global dead-slot ranks [prefix, prefix + local count).  Without prefix/total the
+// shard is the whole range.
+void Engine::fill_assign_all(const uint64_t* prefix, const uint64_t* total) {
     const PathDev P = path_dev();
     uint32_t* cnt = d_cnt32_.as<uint32_t>();
     for (uint32_t li = 0; li < lights_.size(); ++li) {
         LightBlock& b = lights_[li];
         const uint32_t lb = local_lb(b), le = local_le(b);
+        uint32_t* need_total = cnt + kCntNeed0 + li;
         launch_fill_need(b.dm_t.as<uint32_t>(), b.dm_c.as<uint32_t>(), d_need_.as<uint32_t>(), b.cells, stream_);
-        scan_exclusive_u32(d_need_.as<uint32_t>(), d_need_.as<uint32_t>(), b.cells, nullptr, cnt + kCntNeed,
+        scan_exclusive_u32(d_need_.as<uint32_t>(), d_need_.as<uint32_t>(), b.cells, nullptr, need_total,
                            d_scratch_.get(), stream_);
-        launch_dead_flags(P, lb, le, d_flags8_.as<uint8_t>(), stream_);
-        compact_u8(d_flags8_.as<uint8_t>(), le - lb, nullptr, lb, d_list_.as<uint32_t>(), cnt + kCntDead,
-                   d_scratch_.get(), stream_);
-        launch_fill_check(cnt + kCntDead, cnt + kCntNeed, d_ctr_.as<Counters>(), stream_);
-        launch_fill_assign(scene_dev(), P, li, d_list_.as<uint32_t>(), cnt + kCntDead, std::max(1u, le - lb), 0,
-                           d_need_.as<uint32_t>(), cnt + kCntNeed, b.cells, d_ctr_.as<Counters>(), stream_);
+        launch_fill_check(total ? nullptr : cnt + kCntDead0 + li, total ? total[li] : 0, need_total,
+                          d_ctr_.as<Counters>(), stream_);
+        launch_fill_assign(scene_dev(), P, li, d_list_.as<uint32_t>() + lb, cnt + kCntDead0 + li,
+                           std::max(1u, le - lb), prefix ? prefix[li] : 0, d_need_.as<uint32_t>(), need_total,
+                           b.cells, d_ctr_.as<Counters>(), stream_);
         launch_dm_after_fill(b.dm_c.as<uint32_t>(), b.dm_t.as<uint32_t>(), b.cells, stream_);
     }
+}
+
+void Engine::stage_fill_local() {
+    fill_collect_dead();
+    fill_assign_all(nullptr, nullptr);
 }
 
 void Engine::stage_trace() {
@@ -721,40 +754,40 @@ void Engine::dm_current_ptr(uint32_t light, void** ptr, uint32_t* cells) {
     *cells = lights_[light].cells;
 }
 
-void Engine::prune_count(uint32_t light, uint32_t* unmarked_out_dev) {
-    // marks for every light are produced together; copy this light's unmarked counts
-    if (light >= lights_.size()) throw std::out_of_range("light index");
-    if (light == 0) {
-        for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.unm.get(), 0, 4ull * b.cells, stream_));
-        launch_prune_mark(scene_dev(), path_dev(), static_cast<uint32_t>(cur_frame_),
-                          d_light_ptrs_.as<uint32_t*>(), d_flags8_.as<uint8_t>(), d_flags8b_.as<uint8_t>(),
-                          stream_);
-    }
-    PRX_CUDA(cudaMemcpyAsync(unmarked_out_dev, lights_[light].unm.get(), 4ull * lights_[light].cells,
-                             cudaMemcpyDeviceToDevice, stream_));
+void Engine::prune_count(uint32_t* const* unmarked_dev) {
+    PRX_CUDA(cudaSetDevice(device_));
+    prune_mark_all();
+    for (size_t li = 0; li < lights_.size(); ++li)
+        PRX_CUDA(cudaMemcpyAsync(unmarked_dev[li], lights_[li].unm.get(), 4ull * lights_[li].cells,
+                                 cudaMemcpyDeviceToDevice, stream_));
 }
 
-void Engine::prune_apply(uint32_t light, const uint32_t* prefix_dev, const uint32_t* total_dev,
+void Engine::prune_apply(const uint32_t* const* prefix_dev, const uint32_t* const* total_dev,
                          prx_frame_stats* st) {
-    (void)light;
-    (void)prefix_dev;
-    (void)total_dev;
-    (void)st;
-    throw std::logic_error("prune_apply: sharded prune is driven per frame (not yet wired)");
+    PRX_CUDA(cudaSetDevice(device_));
+    // device pointer tables [2] prefix, [3] total
+    std::vector<const uint32_t*> tab(2 * PRX_MAX_LIGHTS, nullptr);
+    for (size_t li = 0; li < lights_.size(); ++li) {
+        tab[li] = prefix_dev[li];
+        tab[PRX_MAX_LIGHTS + li] = total_dev[li];
+    }
+    uint32_t** dtab = d_light_ptrs_.as<uint32_t*>() + 2 * PRX_MAX_LIGHTS;
+    PRX_CUDA(cudaMemcpyAsync(dtab, tab.data(), sizeof(uint32_t*) * tab.size(), cudaMemcpyHostToDevice, stream_));
+    prune_trim_all(dtab, dtab + PRX_MAX_LIGHTS, total_dev);
+    read_back(st, false);
 }
 
-void Engine::fill_count(uint32_t light, uint32_t* dead_out) {
-    (void)light;
-    (void)dead_out;
-    throw std::logic_error("fill_count: sharded fill is driven per frame (not yet wired)");
+void Engine::fill_count(uint32_t* dead_out) {
+    PRX_CUDA(cudaSetDevice(device_));
+    fill_collect_dead();
+    read_back(nullptr, false);
+    for (size_t li = 0; li < lights_.size(); ++li) dead_out[li] = h_cnt32_[kCntDead0 + li];
 }
 
-void Engine::fill_apply(uint32_t light, uint64_t dead_prefix, uint64_t dead_total, prx_frame_stats* st) {
-    (void)light;
-    (void)dead_prefix;
-    (void)dead_total;
-    (void)st;
-    throw std::logic_error("fill_apply: sharded fill is driven per frame (not yet wired)");
+void Engine::fill_apply(const uint64_t* dead_prefix, const uint64_t* dead_total, prx_frame_stats* st) {
+    PRX_CUDA(cudaSetDevice(device_));
+    fill_assign_all(dead_prefix, dead_total);
+    read_back(st, false);
 }
 
 // ----------------------------------------------------------------------- splat

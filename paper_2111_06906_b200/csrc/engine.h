@@ -71,11 +71,10 @@ public:
 
     // sharded exchange points
     void dm_current_ptr(uint32_t light, void** ptr, uint32_t* cells);
-    void prune_count(uint32_t light, uint32_t* unmarked_out_dev);
-    void prune_apply(uint32_t light, const uint32_t* prefix_dev, const uint32_t* total_dev,
-                     prx_frame_stats* st);
-    void fill_count(uint32_t light, uint32_t* dead_out);
-    void fill_apply(uint32_t light, uint64_t dead_prefix, uint64_t dead_total, prx_frame_stats* st);
+    void prune_count(uint32_t* const* unmarked_dev);
+    void prune_apply(const uint32_t* const* prefix_dev, const uint32_t* const* total_dev, prx_frame_stats* st);
+    void fill_count(uint32_t* dead_out);
+    void fill_apply(const uint64_t* dead_prefix, const uint64_t* dead_total, prx_frame_stats* st);
 
     void splat(const prx_camera* cam, float radius, int mode, float* rgb_host, float* rgb_dev,
                prx_frame_stats* st);
@@ -115,6 +114,10 @@ private:
     void stage_compute_dm();
     void stage_prune_local();
     void stage_fill_local();
+    void prune_mark_all();
+    void prune_trim_all(uint32_t* const* prefix_tab, uint32_t* const* total_tab, const uint32_t* const* total_host);
+    void fill_collect_dead();
+    void fill_assign_all(const uint64_t* prefix, const uint64_t* total);
     void stage_trace();
     void read_back(prx_frame_stats* st, bool with_times);
     void record(int idx);

@@ -495,8 +495,10 @@ __global__ void __launch_bounds__(kT) k_fill_assign(SceneDev S, PathDev P, uint3
 }
 
 // fill's slot-exhaustion check (engine.cpp:512-513): single-shard form
-__global__ void k_fill_check(const uint32_t* dead_count, const uint32_t* need_total, Counters* ctr) {
-    if (*need_total > *dead_count) atomicAdd(&ctr->fill_overflow, 1ull);
+__global__ void k_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint32_t* need_total,
+                             Counters* ctr) {
+    const uint64_t avail = dead_count ? (uint64_t)*dead_count : dead_total;
+    if ((uint64_t)*need_total > avail) atomicAdd(&ctr->fill_overflow, 1ull);
 }
 
 __global__ void k_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells) {
@@ -690,9 +692,9 @@ void launch_fill_assign(SceneDev S, PathDev P, uint32_t li, const uint32_t* dead
                         const uint32_t* need_total, uint32_t cells, Counters* ctr, cudaStream_t st) {
     LAUNCH(k_fill_assign, n_max, S, P, li, dead, dead_count, dead_prefix, need_off, need_total, cells, ctr);
 }
-void launch_fill_check(const uint32_t* dead_count, const uint32_t* need_total, Counters* ctr,
+void launch_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint32_t* need_total, Counters* ctr,
                        cudaStream_t st) {
-    k_fill_check<<<1, 1, 0, st>>>(dead_count, need_total, ctr);
+    k_fill_check<<<1, 1, 0, st>>>(dead_count, dead_total, need_total, ctr);
     ++g_launches;
 }
 void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st) {

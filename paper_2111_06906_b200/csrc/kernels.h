@@ -54,8 +54,8 @@ void launch_fill_assign(SceneDev S, PathDev P, uint32_t light, const uint32_t* d
                         const uint32_t* dead_count, uint32_t n_max, uint64_t dead_prefix,
                         const uint32_t* need_off, const uint32_t* need_total, uint32_t cells,
                         Counters* ctr, cudaStream_t st);
-void launch_fill_check(const uint32_t* dead_count, const uint32_t* need_total, Counters* ctr,
-                       cudaStream_t st);
+void launch_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint32_t* need_total,
+                       Counters* ctr, cudaStream_t st);
 void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st);
 // stage_trace (engine.cpp:548-598)
 void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st);

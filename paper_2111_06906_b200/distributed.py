@@ -1,0 +1,243 @@
+"""Path-sharded frames across GPUs.
+
+Paths are split into contiguous id ranges, one per rank.  Scene, BVHs and DM_T are
+replicated; the only cross-rank data of a frame are
+  * DM_C per light                     -> all-reduce(sum)       (stage_compute_dm)
+  * per-cell unmarked prune counts     -> all-gather -> exclusive prefix over lower
+                                          ranks + total (stage_prune's "trim from the
+                                          highest path id down", engine.cpp:459-466)
+  * per-light dead-slot counts         -> all-gather -> prefix + total (stage_fill's
+                                          "deficit cells ascending <-> free slots
+                                          ascending", engine.cpp:503-519)
+  * 8 frame counters                   -> all-reduce(sum)
+and, for the image, the per-rank splat buffers (reduce).  With these exchanges every rank
+computes exactly what the single-engine reference computes for its slice.
+
+The frame is written as phases over an *executor* (one shard) so the same protocol runs
+with real collectives (torch.distributed: NCCL on B200, gloo on CPU) or with an
+in-process loopback over several executors (several shards on one device).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from .pathreuse import Engine, Scene, make_config
+
+COUNTER_KEYS = ("rays_traced", "paths_replaced", "paths_pruned", "paths_filled", "visibility_rays",
+                "live_segments_before", "paths_retraced", "segments")
+
+
+def shard_range(n_paths: int, rank: int, world: int) -> tuple:
+    return n_paths * rank // world, n_paths * (rank + 1) // world
+
+
+class _CudaArray:
+    """Zero-copy torch view of a device buffer owned by the engine."""
+
+    def __init__(self, ptr: int, n: int, typestr: str = "<u4"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+class GpuExecutor:
+    """One path shard on one CUDA device, driven through the C ABI."""
+
+    def __init__(self, scene: Scene, config: L.Config, torch_stream=None):
+        import torch
+
+        self.torch = torch
+        self.engine = Engine(scene, config)
+        if torch_stream is not None:
+            self.engine.set_stream(torch_stream.cuda_stream)
+        info = self.engine.info()
+        self.n_lights = info.n_lights
+        self.cells = [info.dm_cells[i] for i in range(self.n_lights)]
+        self.mode = config.mode
+        self.device = torch.device("cuda", config.device)
+        self._unm = [torch.zeros(c, dtype=torch.int32, device=self.device) for c in self.cells]
+        self.st = L.FrameStats()
+
+    def frame_update(self):
+        self.st = L.FrameStats()
+        self.engine.frame_update(self.st)
+
+    def verify(self):
+        self.engine.verify_paths(self.st)
+
+    def dm_buffers(self) -> list:
+        self.engine.synchronize()
+        out = []
+        for li in range(self.n_lights):
+            ptr, cells = C.c_void_p(), C.c_uint32()
+            L.check(L.lib().prx_engine_dm_current(self.engine.handle, li, C.byref(ptr), C.byref(cells)))
+            t = self.torch.as_tensor(_CudaArray(ptr.value, cells.value, "<i4"), device=self.device)
+            out.append(t)
+        return out
+
+    def dm_commit(self, bufs):  # buffers alias the engine's DM_C
+        self.engine.synchronize()
+
+    def prune_count(self) -> list:
+        self.torch.cuda.synchronize(self.device)
+        arr = (C.c_void_p * self.n_lights)(*[t.data_ptr() for t in self._unm])
+        L.check(L.lib().prx_prune_count(self.engine.handle, C.cast(arr, C.POINTER(C.POINTER(C.c_uint32)))))
+        self.engine.synchronize()
+        return self._unm
+
+    def prune_apply(self, prefix: list, total: list):
+        self._keep = (prefix, total)
+        pa = (C.c_void_p * self.n_lights)(*[t.data_ptr() for t in prefix])
+        ta = (C.c_void_p * self.n_lights)(*[t.data_ptr() for t in total])
+        self.torch.cuda.synchronize(self.device)
+        L.check(L.lib().prx_prune_apply(self.engine.handle, C.cast(pa, C.POINTER(C.POINTER(C.c_uint32))),
+                                        C.cast(ta, C.POINTER(C.POINTER(C.c_uint32))), C.byref(self.st)))
+
+    def fill_count(self) -> list:
+        out = (C.c_uint32 * self.n_lights)()
+        L.check(L.lib().prx_fill_count(self.engine.handle, out))
+        return list(out)
+
+    def fill_apply(self, prefix: Sequence[int], total: Sequence[int]):
+        pa = (C.c_uint64 * self.n_lights)(*prefix)
+        ta = (C.c_uint64 * self.n_lights)(*total)
+        L.check(L.lib().prx_fill_apply(self.engine.handle, pa, ta, C.byref(self.st)))
+
+    def trace(self) -> dict:
+        st = self.engine.run_stage("trace")
+        d = {k: getattr(st, k) for k in COUNTER_KEYS if k != "segments"}
+        d["segments"] = st.rays_traced + st.rays_reused
+        return d
+
+    def new_tensor(self, values, dtype="int64"):
+        return self.torch.tensor(values, dtype=getattr(self.torch, dtype), device=self.device)
+
+
+# ------------------------------------------------------------------------------ phases
+def _prefix_total(torch, gathered: List, rank: int):
+    stacked = torch.stack(gathered)
+    total = stacked.sum(0).to(gathered[0].dtype)
+    prefix = stacked[:rank].sum(0).to(gathered[0].dtype) if rank > 0 else torch.zeros_like(gathered[0])
+    return prefix.contiguous(), total.contiguous()
+
+
+def _frame_counts(local: dict) -> list:
+    return [int(local[k]) for k in COUNTER_KEYS]
+
+
+def _stats_from(total: Sequence[int], frame: int, mode: int) -> dict:
+    d = dict(zip(COUNTER_KEYS, [int(x) for x in total]))
+    d["rays_reused"] = d["segments"] - d["rays_traced"]
+    d["frame"] = frame
+    d["mode"] = L.MODE_NAMES[mode]
+    return d
+
+
+class TorchCollectives:
+    """torch.distributed process group (NCCL for CUDA tensors, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allreduce_sum_(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def allgather(self, t) -> list:
+        out = [t.new_empty(t.shape) for _ in range(self.world)]
+        self.dist.all_gather(out, t.contiguous(), group=self.group)
+        return out
+
+
+def run_frame_distributed(ex, coll, frame: int) -> dict:
+    """One sharded frame on this rank (all ranks call it collectively)."""
+    import torch
+
+    ex.frame_update()
+    ex.verify()
+    bufs = ex.dm_buffers()
+    for t in bufs:
+        coll.allreduce_sum_(t)
+    ex.dm_commit(bufs)
+    if ex.mode != L.MODES["baseline"]:
+        unm = ex.prune_count()
+        prefix, total = [], []
+        for t in unm:
+            p, s = _prefix_total(torch, coll.allgather(t), coll.rank)
+            prefix.append(p)
+            total.append(s)
+        ex.prune_apply(prefix, total)
+    dead = ex.fill_count()
+    parts = coll.allgather(ex.new_tensor(dead))
+    stacked = torch.stack(parts).cpu().numpy()
+    prefix = [int(x) for x in stacked[: coll.rank].sum(0)] if coll.rank else [0] * len(dead)
+    total = [int(x) for x in stacked.sum(0)]
+    ex.fill_apply(prefix, total)
+    local = ex.trace()
+    cnt = ex.new_tensor(_frame_counts(local))
+    coll.allreduce_sum_(cnt)
+    return _stats_from(cnt.cpu().tolist(), frame, ex.mode)
+
+
+def run_frame_loopback(exs: List, frame: int) -> dict:
+    """The same protocol over several executors in one process (shards on one device)."""
+    import torch
+
+    world = len(exs)
+    for ex in exs:
+        ex.frame_update()
+        ex.verify()
+    bufs = [ex.dm_buffers() for ex in exs]
+    for li in range(len(bufs[0])):
+        s = sum(b[li].clone() for b in bufs)
+        for b in bufs:
+            b[li].copy_(s)
+    for ex, b in zip(exs, bufs):
+        ex.dm_commit(b)
+    if exs[0].mode != L.MODES["baseline"]:
+        unms = [[t.clone() for t in ex.prune_count()] for ex in exs]
+        for r, ex in enumerate(exs):
+            prefix, total = [], []
+            for li in range(len(unms[0])):
+                p, s = _prefix_total(torch, [unms[q][li] for q in range(world)], r)
+                prefix.append(p)
+                total.append(s)
+            ex.prune_apply(prefix, total)
+    deads = np.array([ex.fill_count() for ex in exs], dtype=np.int64)
+    for r, ex in enumerate(exs):
+        ex.fill_apply([int(x) for x in deads[:r].sum(0)] if r else [0] * deads.shape[1],
+                      [int(x) for x in deads.sum(0)])
+    total = np.zeros(len(COUNTER_KEYS), dtype=np.int64)
+    for ex in exs:
+        total += np.array(_frame_counts(ex.trace()), dtype=np.int64)
+    return _stats_from(total.tolist(), frame, exs[0].mode)
+
+
+class ShardedEngine:
+    """User-facing sharded engine: one rank's slice of a multi-GPU path store."""
+
+    def __init__(self, scene: Scene, rank: int, world: int, device: int = 0, group=None, **cfg):
+        import torch
+
+        n = cfg.get("paths", 10000)
+        self.config = make_config(shard=shard_range(n, rank, world), device=device, **cfg)
+        self.exec = GpuExecutor(scene, self.config, torch.cuda.current_stream(device))
+        self.coll = TorchCollectives(group) if world > 1 else None
+        self.frame = 0
+
+    def run_frame(self) -> dict:
+        if self.coll is None:
+            st = self.exec.engine.run_frame()
+            self.frame += 1
+            d = {k: getattr(st, k) for k in L.FrameStats.COUNTS}
+            d.update(frame=st.frame, mode=L.MODE_NAMES[st.mode])
+            return d
+        out = run_frame_distributed(self.exec, self.coll, self.frame)
+        self.frame += 1
+        return out
