@@ -205,22 +205,39 @@ def main():
         shard = (n_paths * rank // world, n_paths * (rank + 1) // world)
     cfg = pr.make_config(mode=w["mode"], paths=n_paths, bounces=w["bounces"], dm=[8, 8, 64, 64],
                          threshold=w["threshold"], seed=1, device=local, shard=shard)
-    eng = pr.Engine(scene, cfg)
+    import ctypes as C
+
     stream = torch.cuda.current_stream()
-    eng.set_stream(stream.cuda_stream)
+    if world > 1:  # path-sharded frames over NCCL (paper_2111_06906_b200/distributed.py)
+        from paper_2111_06906_b200.distributed import GpuExecutor, TorchCollectives, run_frame_distributed
+
+        ex = GpuExecutor(scene, cfg, stream)
+        eng = ex.engine
+        coll = TorchCollectives()
+    else:
+        eng = pr.Engine(scene, cfg)
+        eng.set_stream(stream.cuda_stream)
     cam = scene.describe().camera
     img_dev = torch.zeros(cam.height * cam.width * 3, dtype=torch.float32, device="cuda")
+    frame_no = [0]
 
     def step(collect=None):
-        st = L.FrameStats()
-        L.check(L.lib().prx_run_frame(eng.handle, C.byref(st)))
+        if world > 1:
+            d = run_frame_distributed(ex, coll, frame_no[0])
+            st = L.FrameStats()
+            for k in L.FrameStats.COUNTS + ("live_segments_before", "paths_retraced"):
+                setattr(st, k, int(d[k]))
+        else:
+            st = L.FrameStats()
+            L.check(L.lib().prx_run_frame(eng.handle, C.byref(st)))
+        frame_no[0] += 1
         sst = L.FrameStats()
         L.check(L.lib().prx_splat(eng.handle, C.byref(cam), 0.25, args.splat_mode, None,
                                   C.c_void_p(img_dev.data_ptr()), C.byref(sst)))
+        if world > 1:  # per-rank photon splats summed into one image (NCCL all-reduce)
+            torch.distributed.all_reduce(img_dev)
         if collect is not None:
             collect.append((st, sst))
-
-    import ctypes as C
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -266,11 +283,21 @@ def main():
 
     # e2e through the public API with host buffers (stats + image read back every step)
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        eng.run_frame()
-        eng.splat(radius=0.25, mode=args.splat_mode)
+        if world > 1:  # sharded frame + reduced image read back to the host
+            step()
+            img_host = img_dev.cpu()
+        else:  # the public Python API: counters and the host image every step
+            eng.run_frame()
+            eng.splat(radius=0.25, mode=args.splat_mode)
     e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
     e2e_value = n_paths * args.steps / e2e_s
     h2d = 4 + 16 * 4 + 40 * 128 + 24 * 128 + 176 * 16 + 32 * 128  # FrameParams + transforms
     d2h = 12 * cam.width * cam.height + 96 + 32 + 8 * 21
