@@ -124,7 +124,9 @@ typedef struct prx_config {                                        /* engine.hpp
     int32_t device;             /* CUDA device ordinal                              */
     uint32_t shard_begin;       /* path range owned by this engine; [0,0) = all     */
     uint32_t shard_end;
-    int32_t exact_trig;         /* 1 (default): host-libm cosf/sinf table for bounces */
+    int32_t exact_trig;         /* >= 0 (default): host-libm cosf/sinf table for bounces */
+    int32_t dfs_traversal;      /* 1: reference-order DFS for every ray; 0 (default): near-
+                                   first traversal + exactness certificate (same results) */
 } prx_config;
 
 typedef struct prx_frame_stats {                                   /* engine.hpp:19-30 */

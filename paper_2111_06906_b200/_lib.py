@@ -88,7 +88,7 @@ class Config(C.Structure):
                 ("gather_radius", C.c_float), ("workers", C.c_uint32),
                 ("record_flags", C.c_int32), ("device", C.c_int32),
                 ("shard_begin", C.c_uint32), ("shard_end", C.c_uint32),
-                ("exact_trig", C.c_int32)]
+                ("exact_trig", C.c_int32), ("dfs_traversal", C.c_int32)]
 
 
 class FrameStats(C.Structure):

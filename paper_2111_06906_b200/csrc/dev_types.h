@@ -54,6 +54,9 @@ struct FrameParams {
 struct SceneDev {
     const float4* nodes;       // static BVH: 2 float4 per node {lo, a} {hi, b}
     uint32_t n_nodes;
+    const uint32_t* split;     // internal node: first permutation position of its right subtree
+    float cull_pad;            // fast traversal: box inflation for conservative culling
+    int32_t fast;              // 1: near-first traversal + exactness certificate
     const float4* stris;       // static tris, BVH order: {a, orig idx} {e1, obj} {e2, -}
     const float4* dtris;       // dynamic tris, world space, object-local index order
     const float4* dnodes;      // LBVH nodes: 4 float4 per internal node

@@ -443,13 +443,186 @@ __device__ __forceinline__ bool trav_hit(const SceneDev& S, const Trav& T, Hit& 
     return true;
 }
 
+// --------------------------------------------------------------------------- fast exact static traversal
+// The reference's Bvh::intersect (bvh.cpp:79-106) returns, among the triangles its left-first
+// DFS visits, the one with the smallest (t, permutation position) -- DFS order IS permutation
+// order.  If it visits the global (t, position)-minimum T*, that is its answer; it visits T*
+// iff every ancestor of T*'s leaf passes the exact box test at the t_max it has there, which
+// is > t* (a smaller t_max would need an earlier hit with t <= t*), so it suffices that each
+// ancestor passes at t_max = nextafter(t*) (the test is monotone in t_max).
+// static_fast finds T* with near-first ordering and conservative culling (boxes inflated by
+// cull_pad, t window widened); static_cert re-walks T*'s root-to-leaf path with the exact
+// test.  A ray whose certificate fails reruns the reference-order DFS (static_closest).
+__device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t_lim, float4 A, float4 B,
+                                           float pad) {
+    float t0 = t_min, t1 = t_lim;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float d = comp(r.d, a), o = comp(r.o, a);
+        const float lo = (a == 0 ? A.x : (a == 1 ? A.y : A.z)) - pad;
+        const float hi = (a == 0 ? B.x : (a == 1 ? B.y : B.z)) + pad;
+        if (d == 0.0f || !r.safe) {
+            if (d == 0.0f && (o < lo || o > hi)) return INFINITY;
+            continue;  // no culling on an axis the float slab cannot bound
+        }
+        float tn = (lo - o) * r.inv[a];
+        float tf = (hi - o) * r.inv[a];
+        if (tn > tf) {
+            const float s = tn;
+            tn = tf;
+            tf = s;
+        }
+        t0 = fmax_std(t0, tn);
+        t1 = fmin_std(t1, tf);
+    }
+    return t0 <= t1 ? t0 : INFINITY;
+}
+
+__device__ __forceinline__ float cull_limit(float best_t) { return best_t + 1e-4f * fabsf(best_t) + 1e-6f; }
+
+// global (t, position)-minimum over static triangles with t in (t_min, t_max).
+// While-while traversal (Aila & Laine 2009) with postponed leaves: a lane that reaches a
+// leaf parks it and keeps descending until every active lane of the warp holds a leaf, so
+// triangle tests run warp-wide instead of one lane at a time.  The result is the
+// order-independent lexicographic minimum, so the visit order is free.
+__device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, float t_min, float t_max,
+                                            float& best_t, uint32_t& best_pos) {
+    constexpr uint32_t kNone = 0xFFFFFFFFu;
+    const float pad = S.cull_pad;
+    best_t = t_max;
+    best_pos = kNone;
+    bool found = false;
+    uint32_t stack[64];
+    float stent[64];
+    int sp = 0;
+    const float4 R0 = __ldg(&S.nodes[0]), R1 = __ldg(&S.nodes[1]);
+    if (box_entry(r, t_min, cull_limit(t_max), R0, R1, pad) == INFINITY) return false;
+    uint32_t node = (__float_as_uint(R0.w) & kLeafBit) ? kLeafBit : 0u;  // child refs carry the leaf bit
+    uint32_t leaf = kNone;
+    auto pop = [&]() -> uint32_t {
+        while (sp > 0) {
+            --sp;
+            if (stent[sp] <= cull_limit(best_t)) return stack[sp];
+        }
+        return kNone;
+    };
+    while (node != kNone || leaf != kNone) {
+        while (node != kNone && !(node & kLeafBit)) {
+            const float4 A = __ldg(&S.nodes[2 * node]);
+            const float4 B = __ldg(&S.nodes[2 * node + 1]);
+            const uint32_t a = __float_as_uint(A.w), b = __float_as_uint(B.w);
+            const float4 LA = __ldg(&S.nodes[2 * a]), LB = __ldg(&S.nodes[2 * a + 1]);
+            const float4 RA = __ldg(&S.nodes[2 * b]), RB = __ldg(&S.nodes[2 * b + 1]);
+            const float lim = cull_limit(best_t);
+            const float tl = box_entry(r, t_min, lim, LA, LB, pad);
+            const float tr = box_entry(r, t_min, lim, RA, RB, pad);
+            const uint32_t cl = a | (__float_as_uint(LA.w) & kLeafBit);
+            const uint32_t cr = b | (__float_as_uint(RA.w) & kLeafBit);
+            if (tl == INFINITY && tr == INFINITY) {
+                node = pop();
+            } else if (tr == INFINITY) {
+                node = cl;
+            } else if (tl == INFINITY) {
+                node = cr;
+            } else if (tl <= tr) {
+                stack[sp] = cr;
+                stent[sp] = tr;
+                ++sp;
+                node = cl;
+            } else {
+                stack[sp] = cl;
+                stent[sp] = tl;
+                ++sp;
+                node = cr;
+            }
+            if (node != kNone && (node & kLeafBit) && leaf == kNone) {  // park the leaf
+                leaf = node;
+                node = pop();
+            }
+            if (!__any_sync(__activemask(), leaf == kNone)) break;
+        }
+        if (leaf == kNone && node != kNone && (node & kLeafBit)) {
+            leaf = node;
+            node = pop();
+        }
+        while (leaf != kNone) {
+            const uint32_t li = leaf & ~kLeafBit;
+            const uint32_t first = __float_as_uint(__ldg(&S.nodes[2 * li]).w) & ~kLeafBit;
+            const uint32_t count = __float_as_uint(__ldg(&S.nodes[2 * li + 1]).w);
+            for (uint32_t i = first; i < first + count; ++i) {
+                const float4 ta = __ldg(&S.stris[3 * i]);
+                const float4 t1 = __ldg(&S.stris[3 * i + 1]);
+                const float4 t2 = __ldg(&S.stris[3 * i + 2]);
+                float t;
+                // window: (t_min, t_max) before the first hit, then t <= best_t (ties by position)
+                const float lim = found ? __uint_as_float(__float_as_uint(best_t) + 1u) : t_max;
+                if (intersect_tri(r.o, r.d, t_min, lim, ld3(ta), ld3(t1), ld3(t2), t)) {
+                    if (!found || t < best_t || (t == best_t && i < best_pos)) {
+                        best_t = t;
+                        best_pos = i;
+                        found = true;
+                    }
+                }
+            }
+            leaf = kNone;
+            if (node != kNone && (node & kLeafBit)) {
+                leaf = node;
+                node = pop();
+            }
+        }
+    }
+    return found;
+}
+
+// every ancestor of permutation position `pos` passes the reference's exact box test at t_lim
+__device__ __forceinline__ bool static_cert(const SceneDev& S, const RayPre& r, float t_min, float t_lim,
+                                            uint32_t pos) {
+    uint32_t ni = 0;
+    while (true) {
+        const float4 A = __ldg(&S.nodes[2 * ni]);
+        const float4 B = __ldg(&S.nodes[2 * ni + 1]);
+        const Box box{{A.x, A.y, A.z}, {B.x, B.y, B.z}};
+        if (!ray_box(r, t_min, t_lim, box)) return false;
+        const uint32_t a = __float_as_uint(A.w);
+        if (a & kLeafBit) return true;
+        ni = pos < __ldg(&S.split[ni]) ? a : __float_as_uint(B.w);
+    }
+}
+
+// static part of intersect_scene with the reference's exact result
+__device__ __forceinline__ bool static_closest_exact(const SceneDev& S, const RayPre& r, float t_min, float& t_max,
+                                                     uint32_t& best) {
+    if (S.n_nodes == 0) return false;
+    if (!S.fast) return static_closest(S, r, t_min, t_max, best);
+    float bt;
+    uint32_t bp;
+    if (!static_fast(S, r, t_min, t_max, bt, bp)) return false;
+    if (static_cert(S, r, t_min, __uint_as_float(__float_as_uint(bt) + 1u), bp)) {
+        t_max = bt;
+        best = bp;
+        return true;
+    }
+    return static_closest(S, r, t_min, t_max, best);
+}
+
+// static part of occluded: any accepted triangle whose ancestors pass at the original t_max
+__device__ __forceinline__ bool static_any_exact(const SceneDev& S, const RayPre& r, float t_min, float t_max) {
+    if (S.n_nodes == 0) return false;
+    if (!S.fast) return static_any(S, r, t_min, t_max);
+    float bt;
+    uint32_t bp;
+    if (!static_fast(S, r, t_min, t_max, bt, bp)) return false;
+    if (static_cert(S, r, t_min, t_max, bp)) return true;
+    return static_any(S, r, t_min, t_max);
+}
+
 // intersect_scene (scene.cpp:136-168), one-shot form: tight static loop, then each dynamic
 // object behind its gate.
 __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h) {
     const RayPre r = make_ray(o, d);
     float t_max = FLT_MAX;
     uint32_t sbest = 0;
-    const bool found = static_closest(S, r, t_min, t_max, sbest);
+    const bool found = static_closest_exact(S, r, t_min, t_max, sbest);
     int kind = found ? 0 : -1;
     uint32_t dj = 0, dtri = 0;
     const FrameParams* fp = S.fp;
@@ -490,7 +663,7 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
 // occluded (scene.cpp:170-177)
 __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_min, float t_max) {
     const RayPre r = make_ray(o, d);
-    if (static_any(S, r, t_min, t_max)) return true;
+    if (static_any_exact(S, r, t_min, t_max)) return true;
     const FrameParams* fp = S.fp;
     for (uint32_t j = 0; j < fp->n_dyn; ++j) {
         const DynObj& D = fp->dyn[j];

@@ -230,6 +230,22 @@ void Engine::upload_scene() {
         }
         d_stris_.alloc(sizeof(float4) * tris.size());
         PRX_CUDA(cudaMemcpy(d_stris_.get(), tris.data(), d_stris_.size(), cudaMemcpyHostToDevice));
+        // split[n]: first permutation position of an internal node's right subtree (the
+        // fast traversal's certificate walks the reference tree by position)
+        std::vector<uint32_t> tri_count(nn, 0), begin(nn, 0), split(nn, 0);
+        for (size_t k = nn; k-- > 0;) {  // children have larger indices (pre-order build)
+            const BvhNode& n = s.bvh_nodes[k];
+            tri_count[k] = n.count ? n.count : tri_count[n.left] + tri_count[n.first];
+        }
+        for (size_t k = 0; k < nn; ++k) {
+            const BvhNode& n = s.bvh_nodes[k];
+            if (n.count) continue;
+            begin[n.left] = begin[k];
+            begin[n.first] = begin[k] + tri_count[n.left];
+            split[k] = begin[n.first];
+        }
+        d_split_.alloc(4 * nn);
+        PRX_CUDA(cudaMemcpy(d_split_.get(), split.data(), d_split_.size(), cudaMemcpyHostToDevice));
     }
     // materials / flags
     std::vector<float4> mat(s.objects.size());
@@ -364,6 +380,9 @@ SceneDev Engine::scene_dev() const {
     SceneDev S{};
     S.nodes = d_nodes_.as<float4>();
     S.n_nodes = static_cast<uint32_t>(scene_->bvh_nodes.size());
+    S.split = d_split_.as<uint32_t>();
+    S.cull_pad = 1e-5f * diag_ + 1e-6f;
+    S.fast = cfg_.dfs_traversal ? 0 : 1;
     S.stris = d_stris_.as<float4>();
     S.dtris = d_dyn_world_.as<float4>();
     S.dnodes = d_lbvh_nodes_.as<float4>();

@@ -329,6 +329,83 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
     warp_add(&ctr->vis, vis);
 }
 
+// verify_path_error_based (engine.cpp:339-403), one path per thread with one-shot
+// intersect_scene queries (fast traversal + certificate).
+__global__ void __launch_bounds__(kT) k_verify_error_walk(SceneDev S, PathDev P, float threshold,
+                                                          const uint32_t* __restrict__ list,
+                                                          const uint32_t* __restrict__ masks, const Counters* cnt,
+                                                          Counters* ctr) {
+    const FrameParams* fp = S.fp;
+    const uint32_t n_list = (uint32_t)cnt->flagged;
+    unsigned long long vis = 0;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_list; j += gridDim.x * blockDim.x) {
+        const uint32_t i = list[j];
+        const uint32_t flags = masks[j];
+        const uint32_t p = P.base + i;
+        const LightDev& L = fp->lights[light_of(fp, p)];
+        uchar4 m = P.meta[i];
+        const uint32_t k = m.x, segs = m.x + m.y;
+        const uint32_t epoch = P.epoch[i];
+        bool force = false;
+        uint32_t s = 0;
+        while (s < segs) {
+            const bool flagged = force || ((flags >> s) & 1u);
+            force = false;
+            if (!flagged) {
+                ++s;
+                continue;
+            }
+            const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, s - 1, i)]);
+            const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
+            ++vis;
+            Hit h;
+            const bool hit = intersect_scene(S, o, d, S.eps, h);
+            if (s == k) {  // escape segment: a new blocker -> retrace from here
+                if (hit) P.rstart[i] = (uint8_t)s;
+                break;
+            }
+            if (!hit) {  // destination gone: truncate and escape
+                truncate_path(P, i, s, true, m);
+                P.meta[i] = m;
+                break;
+            }
+            const size_t v = vix(P, s, i);
+            const float4 stored = P.energy[v];
+            const V3 e_prev = s == 0 ? L.flux_pp : ld3(P.energy[vix(P, s - 1, i)]);
+            const float4 am = __ldg(&S.mat[h.obj]);
+            const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
+            const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
+            if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
+                P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
+                P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+                P.energy[v] = make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius);
+                const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
+                P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
+                P.rstart[i] = (uint8_t)(s + 1);
+                break;
+            }
+            const V3 old_pos = ld3(P.pos_obj[v]);
+            const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
+            P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
+            P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+            if (s + 1 >= segs) break;
+            const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
+            if (close_pos && !hit_dyn && !((flags >> (s + 1)) & 1u)) {
+                s += 2;
+                continue;
+            }
+            if (s + 1 < k) {
+                const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
+                const V3 od = normalized(sub(next, h.pos));
+                P.out_dir[v] = make_float4(od.x, od.y, od.z, 0.f);
+            }
+            force = true;
+            ++s;
+        }
+    }
+    warp_add(&ctr->vis, vis);
+}
+
 __global__ void __launch_bounds__(kT) k_compute_dm(SceneDev S, PathDev P, Counters* ctr) {
     const FrameParams* fp = S.fp;
     unsigned long long replaced = 0;
@@ -646,9 +723,14 @@ static int persistent_grid(K kernel) {
 
 void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t* list, const uint32_t* masks,
                          const Counters* cnt, uint32_t* work, Counters* ctr, cudaStream_t st) {
-    static int grid = persistent_grid(k_verify_error);
-    cudaMemsetAsync(work, 0, 4, st);
-    k_verify_error<<<grid, kT, 0, st>>>(S, P, threshold, list, masks, cnt, work, ctr);
+    if (S.fast) {  // one-shot walks on the fast traversal
+        static int grid = persistent_grid(k_verify_error_walk);
+        k_verify_error_walk<<<grid, kT, 0, st>>>(S, P, threshold, list, masks, cnt, ctr);
+    } else {  // resumable reference-order traversal, persistent lanes
+        static int grid = persistent_grid(k_verify_error);
+        cudaMemsetAsync(work, 0, 4, st);
+        k_verify_error<<<grid, kT, 0, st>>>(S, P, threshold, list, masks, cnt, work, ctr);
+    }
     ++g_launches;
 }
 void launch_compute_dm(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st) {

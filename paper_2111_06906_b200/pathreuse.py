@@ -142,7 +142,8 @@ class Scene:
 def make_config(mode: str = "naive", paths: int = 10000, bounces: int = 7,
                 dm: Sequence[int] = (8, 8, 64, 64), threshold: float = 0.001, seed: int = 1,
                 radius: float = 0.25, workers: int = 1, record_flags: bool = False,
-                device: int = 0, shard: tuple = (0, 0), exact_trig: bool = True) -> L.Config:
+                device: int = 0, shard: tuple = (0, 0), exact_trig: bool = True,
+                dfs_traversal: bool = False) -> L.Config:
     """EngineConfig (engine.hpp:43-53) + make_config (module.cpp:15-27)."""
     if mode not in L.MODES:
         raise ValueError("unknown engine mode: " + str(mode))
@@ -163,6 +164,7 @@ def make_config(mode: str = "naive", paths: int = 10000, bounces: int = 7,
     cfg.device = int(device)
     cfg.shard_begin, cfg.shard_end = int(shard[0]), int(shard[1])
     cfg.exact_trig = 0 if exact_trig else -1
+    cfg.dfs_traversal = int(bool(dfs_traversal))
     return cfg
 
 
