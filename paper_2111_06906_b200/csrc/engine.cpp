@@ -184,6 +184,7 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
 
     upload_scene();
     alloc_state();
+    place_frame(0);
     if (cfg_.exact_trig >= 0) d_trig_ = exact_trig_table(device_);
 
     // DM_T (init_dm_target, light.cpp:230-252), keyed by the sample index within the block
@@ -470,7 +471,33 @@ void Engine::fill_frame_params() {
     PRX_CUDA(cudaMemcpyAsync(d_fp_.get(), h_fp_, sizeof(FrameParams), cudaMemcpyHostToDevice, stream_));
 }
 
-// state_at (scene.cpp:115-134) for the dynamics: host keyframes, device placement + LBVH
+// state_at (scene.cpp:115-134) on the host: every dynamic object's descriptor and current
+// bounds, and the occlusion boxes united(prev, cur).inflate(eps) (engine.cpp:211-218).
+void Engine::place_frame(int frame) {
+    FrameParams& fp = *h_fp_;
+    fp.n_boxes = 0;
+    for (size_t j = 0; j < dyn_.size(); ++j) {
+        const Object& o = scene_->objects[dyn_[j].obj];
+        const Xform now = transform_at(o.kfs, frame);
+        const Xform prev = transform_at(o.kfs, frame > 0 ? frame - 1 : 0);
+        const Box cur = transform_box(o.local_bounds, now);
+        const Box prv = transform_box(o.local_bounds, prev);
+        DynObj& D = fp.dyn[j];
+        D.obj = dyn_[j].obj;
+        D.tri_begin = dyn_[j].tri_begin;
+        D.tri_count = dyn_[j].tri_count;
+        D.node_begin = dyn_[j].node_begin;
+        D.cur = cur;
+        if (frame > 0) {
+            Box box = prv;
+            expand(box, cur);
+            inflate(box, eps_);
+            fp.boxes[fp.n_boxes++] = box;
+        }
+    }
+}
+
+// device placement of the dynamics (+ LBVH) for the transforms of cur_frame_
 void Engine::place_dynamics(bool force) {
     if (dyn_.empty()) return;
     bool changed = force;
@@ -511,28 +538,7 @@ void Engine::frame_update(prx_frame_stats* st) {
         b.pose_now = light_pose_at(*b.light, frame);
         b.moved = frame > 0 && !(b.pose_now == b.pose_prev);
     }
-    // dynamic placements and occlusion boxes (scene.cpp:115-134, engine.cpp:211-218)
-    FrameParams& fp = *h_fp_;
-    fp.n_boxes = 0;
-    for (size_t j = 0; j < dyn_.size(); ++j) {
-        const Object& o = scene_->objects[dyn_[j].obj];
-        const Xform now = transform_at(o.kfs, frame);
-        const Xform prev = transform_at(o.kfs, frame > 0 ? frame - 1 : 0);
-        const Box cur = transform_box(o.local_bounds, now);
-        const Box prv = transform_box(o.local_bounds, prev);
-        DynObj& D = fp.dyn[j];
-        D.obj = dyn_[j].obj;
-        D.tri_begin = dyn_[j].tri_begin;
-        D.tri_count = dyn_[j].tri_count;
-        D.node_begin = dyn_[j].node_begin;
-        D.cur = cur;
-        if (frame > 0) {
-            Box box = prv;
-            expand(box, cur);
-            inflate(box, eps_);
-            fp.boxes[fp.n_boxes++] = box;
-        }
-    }
+    place_frame(frame);
     fill_frame_params();
     place_dynamics(false);
     launch_frame_reset(path_dev(), cfg_.record_flags, d_ctr_.as<Counters>(), stream_);
@@ -976,6 +982,7 @@ void Engine::upload(int field, uint32_t index, const void* src, size_t bytes) {
 
 void Engine::set_frame_counter(int frames_run) {
     if (frames_run < 0) throw std::invalid_argument("frames_run must be >= 0");
+    PRX_CUDA(cudaSetDevice(device_));
     frames_run_ = frames_run;
     cur_frame_ = frames_run > 0 ? frames_run - 1 : 0;
     for (LightBlock& b : lights_) {
@@ -983,6 +990,7 @@ void Engine::set_frame_counter(int frames_run) {
         b.pose_prev = b.pose_now;
         b.moved = false;
     }
+    place_frame(cur_frame_);
     fill_frame_params();
     place_dynamics(true);
     PRX_CUDA(cudaStreamSynchronize(stream_));

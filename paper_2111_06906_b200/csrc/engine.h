@@ -108,6 +108,7 @@ private:
     void upload_scene();
     void alloc_state();
     void fill_frame_params();
+    void place_frame(int frame);
     void place_dynamics(bool force);
     void stage_update_origins();
     void stage_occlusions();
