@@ -847,6 +847,7 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
         d_gbuf_.alloc(16ull * npx);
         d_img_.alloc(12ull * npx);
         d_splat_work_.alloc(splat_work_bytes(npx));
+        if (d_splat_cand_.size() < 16 + 8ull * n_ * B_) d_splat_cand_.alloc(16 + 8ull * n_ * B_);
         img_w_ = c.width;
         img_h_ = c.height;
     }
@@ -855,7 +856,7 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
     record(kEvSplat0);
     float* out = rgb_dev ? rgb_dev : d_img_.as<float>();
     launch_splat(scene_dev(), path_dev(), C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area,
-                 d_splat_work_.get(), stream_);
+                 d_splat_work_.get(), d_splat_cand_.get(), stream_);
     record(kEvSplat1);
     if (rgb_host)
         PRX_CUDA(cudaMemcpyAsync(rgb_host, out, 12ull * npx, cudaMemcpyDeviceToHost, stream_));

@@ -70,7 +70,7 @@ void launch_unpack_photons(PathDev P, const void* photons, const void* aux, cuda
 int splat_table_bits(uint32_t npx);
 size_t splat_work_bytes(uint32_t npx);
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img,
-                  float inv_pi, float inv_area, void* work, cudaStream_t st);
+                  float inv_pi, float inv_area, void* work, void* cand_buf, cudaStream_t st);
 
 // Dynamic LBVH (lbvh.cu)
 struct LbvhBuffers {

@@ -85,32 +85,53 @@ __global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float 
     }
 }
 
-template <bool kShared>
-__global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float radius,
-                                              const float4* __restrict__ gbuf,
-                                              const unsigned long long* __restrict__ keys,
-                                              const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
-                                              const uint32_t* __restrict__ list, int bits, float* __restrict__ img) {
-    extern __shared__ float simg[];
-    if (kShared) {
-        for (uint32_t k = threadIdx.x; k < 3 * npx; k += blockDim.x) simg[k] = 0.0f;
-        __syncthreads();
-    }
-    float* acc = kShared ? simg : img;
+// K12b pass 1: stream every photon record once at full occupancy and keep only the photons
+// whose grid cell is registered by some pixel (most are not near any visible point).
+__global__ void __launch_bounds__(kT) k_splat_filter(PathDev P, float radius,
+                                                     const unsigned long long* __restrict__ keys, int bits,
+                                                     uint2* __restrict__ cand, uint32_t* __restrict__ n_cand) {
     const uint32_t mask = (1u << bits) - 1u;
-    const float r2 = radius * radius;
     const size_t total = (size_t)P.n * P.B;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
         const float4 po = __ldcs(&P.pos_obj[v]);
-        const uint32_t obj = __float_as_uint(po.w);
-        if (obj == kInvalidObj) continue;
+        if (__float_as_uint(po.w) == kInvalidObj) continue;
         const unsigned long long key =
             grid_key(cell_coord(po.x, radius), cell_coord(po.y, radius), cell_coord(po.z, radius));
         uint32_t s = slot_of(key, bits);
         unsigned long long k;
         while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
         if (k != key) continue;
-        const uint32_t n = __ldg(&cnt[s]), o = __ldg(&off[s]);
+        const unsigned m = __activemask();
+        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(n_cand, (unsigned)__popc(m));
+        base = __shfl_sync(m, base, leader);
+        cand[base + __popc(m & ((1u << lane) - 1u))] = make_uint2((uint32_t)v, s);
+    }
+}
+
+// K12b pass 2: every candidate photon against its cell's pixel list; reference filters
+// (same object, |x_ph - x_px|^2 <= r^2); energies added with shared-memory atomics into a
+// CTA-private image (global atomics when the image does not fit).
+template <bool kShared>
+__global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float radius,
+                                              const float4* __restrict__ gbuf, const uint2* __restrict__ cand,
+                                              const uint32_t* __restrict__ n_cand, const uint32_t* __restrict__ cnt,
+                                              const uint32_t* __restrict__ off, const uint32_t* __restrict__ list,
+                                              float* __restrict__ img) {
+    extern __shared__ float simg[];
+    if (kShared) {
+        for (uint32_t k = threadIdx.x; k < 3 * npx; k += blockDim.x) simg[k] = 0.0f;
+        __syncthreads();
+    }
+    float* acc = kShared ? simg : img;
+    const float r2 = radius * radius;
+    const uint32_t nc = *n_cand;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+        const uint2 vs = cand[c];
+        const float4 po = __ldg(&P.pos_obj[vs.x]);
+        const uint32_t obj = __float_as_uint(po.w);
+        const uint32_t n = __ldg(&cnt[vs.y]), o = __ldg(&off[vs.y]);
         float4 en;
         bool have_en = false;
         for (uint32_t j = 0; j < n; ++j) {
@@ -120,7 +141,7 @@ __global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float rad
             const V3 d = sub(V3{po.x, po.y, po.z}, V3{g.x, g.y, g.z});  // gather.hpp:54
             if (dot(d, d) > r2) continue;
             if (!have_en) {
-                en = __ldcs(&P.energy[v]);
+                en = __ldg(&P.energy[vs.x]);
                 have_en = true;
             }
             atomicAdd(&acc[3 * pix], en.x);
@@ -169,7 +190,7 @@ size_t splat_work_bytes(uint32_t npx) {
 }
 
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
-                  float inv_area, void* work, cudaStream_t st) {
+                  float inv_area, void* work, void* cand_buf, cudaStream_t st) {
     const uint32_t npx = C.w * C.h;
     const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
@@ -189,6 +210,10 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
     scan_exclusive_u32(cnt, off, (uint32_t)slots, nullptr, nullptr, scratch, st);
     k_pixcells<true><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, off, cursor, list,
                                                                  bits);
+    uint32_t* n_cand = static_cast<uint32_t*>(cand_buf);
+    uint2* cand = reinterpret_cast<uint2*>(static_cast<char*>(cand_buf) + 16);
+    cudaMemsetAsync(n_cand, 0, 4, st);
+    k_splat_filter<<<launch_grid((uint64_t)P.n * P.B, kT), kT, 0, st>>>(P, radius, keys, bits, cand, n_cand);
     cudaMemsetAsync(img, 0, 12ull * npx, st);
     const size_t smem = 12ull * npx;
     int dev = 0, n_sm = 148;
@@ -196,13 +221,13 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (smem <= 200u * 1024u) {
         cudaFuncSetAttribute(k_splat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_splat<true><<<n_sm, kT, smem, st>>>(P, npx, radius, gbuf, keys, cnt, off, list, bits, img);
+        k_splat<true><<<n_sm, kT, smem, st>>>(P, npx, radius, gbuf, cand, n_cand, cnt, off, list, img);
     } else {
-        k_splat<false><<<launch_grid((uint64_t)P.n * P.B, kT), kT, 0, st>>>(P, npx, radius, gbuf, keys, cnt, off,
-                                                                           list, bits, img);
+        k_splat<false><<<launch_grid((uint64_t)P.n * P.B, kT), kT, 0, st>>>(P, npx, radius, gbuf, cand, n_cand, cnt,
+                                                                           off, list, img);
     }
     k_resolve<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, S.mat, img, npx, inv_pi, inv_area);
-    g_launches += 6 + 3;
+    g_launches += 7 + 3;
 }
 
 }  // namespace prx
