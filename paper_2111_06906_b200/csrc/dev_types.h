@@ -57,6 +57,8 @@ struct SceneDev {
     const uint32_t* split;     // internal node: first permutation position of its right subtree
     float cull_pad;            // fast traversal: box inflation for conservative culling
     int32_t fast;              // 1: near-first traversal + exactness certificate
+    const float4* fnodes;      // fast SAH BVH2: 4 float4 per node {lo0,c0} {hi0,c1} {lo1,-} {hi1,-}
+    const float4* ftris;       // its triangles in leaf order: {a, ref position} {e1, obj} {e2, -}
     const float4* stris;       // static tris, BVH order: {a, orig idx} {e1, obj} {e2, -}
     const float4* dtris;       // dynamic tris, world space, object-local index order
     const float4* dnodes;      // LBVH nodes: 4 float4 per internal node

@@ -480,24 +480,21 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
 
 __device__ __forceinline__ float cull_limit(float best_t) { return best_t + 1e-4f * fabsf(best_t) + 1e-6f; }
 
-// global (t, position)-minimum over static triangles with t in (t_min, t_max).
-// While-while traversal (Aila & Laine 2009) with postponed leaves: a lane that reaches a
-// leaf parks it and keeps descending until every active lane of the warp holds a leaf, so
-// triangle tests run warp-wide instead of one lane at a time.  The result is the
-// order-independent lexicographic minimum, so the visit order is free.
+// global (t, position)-minimum over static triangles with t in (t_min, t_max), walking the
+// fast SAH tree (fast_bvh.cpp).  While-while traversal (Aila & Laine 2009) with postponed
+// leaves: a lane that reaches a leaf parks it and keeps descending until every active lane
+// of the warp holds a leaf, so triangle tests run warp-wide.  The result is the
+// order-independent lexicographic minimum, so neither tree nor visit order matters.
 __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, float t_min, float t_max,
                                             float& best_t, uint32_t& best_pos) {
     constexpr uint32_t kNone = 0xFFFFFFFFu;
-    const float pad = S.cull_pad;
     best_t = t_max;
     best_pos = kNone;
     bool found = false;
     uint32_t stack[64];
     float stent[64];
     int sp = 0;
-    const float4 R0 = __ldg(&S.nodes[0]), R1 = __ldg(&S.nodes[1]);
-    if (box_entry(r, t_min, cull_limit(t_max), R0, R1, pad) == INFINITY) return false;
-    uint32_t node = (__float_as_uint(R0.w) & kLeafBit) ? kLeafBit : 0u;  // child refs carry the leaf bit
+    uint32_t node = 0;  // the root is always an internal node
     uint32_t leaf = kNone;
     auto pop = [&]() -> uint32_t {
         while (sp > 0) {
@@ -508,32 +505,28 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
     };
     while (node != kNone || leaf != kNone) {
         while (node != kNone && !(node & kLeafBit)) {
-            const float4 A = __ldg(&S.nodes[2 * node]);
-            const float4 B = __ldg(&S.nodes[2 * node + 1]);
-            const uint32_t a = __float_as_uint(A.w), b = __float_as_uint(B.w);
-            const float4 LA = __ldg(&S.nodes[2 * a]), LB = __ldg(&S.nodes[2 * a + 1]);
-            const float4 RA = __ldg(&S.nodes[2 * b]), RB = __ldg(&S.nodes[2 * b + 1]);
+            const float4* N = S.fnodes + 4ull * node;
+            const float4 n0 = __ldg(&N[0]), n1 = __ldg(&N[1]), n2 = __ldg(&N[2]), n3 = __ldg(&N[3]);
+            const uint32_t c0 = __float_as_uint(n0.w), c1 = __float_as_uint(n1.w);
             const float lim = cull_limit(best_t);
-            const float tl = box_entry(r, t_min, lim, LA, LB, pad);
-            const float tr = box_entry(r, t_min, lim, RA, RB, pad);
-            const uint32_t cl = a | (__float_as_uint(LA.w) & kLeafBit);
-            const uint32_t cr = b | (__float_as_uint(RA.w) & kLeafBit);
+            const float tl = box_entry(r, t_min, lim, n0, n1, 0.0f);  // boxes are pre-inflated
+            const float tr = c1 != kNone ? box_entry(r, t_min, lim, n2, n3, 0.0f) : INFINITY;
             if (tl == INFINITY && tr == INFINITY) {
                 node = pop();
             } else if (tr == INFINITY) {
-                node = cl;
+                node = c0;
             } else if (tl == INFINITY) {
-                node = cr;
+                node = c1;
             } else if (tl <= tr) {
-                stack[sp] = cr;
+                stack[sp] = c1;
                 stent[sp] = tr;
                 ++sp;
-                node = cl;
+                node = c0;
             } else {
-                stack[sp] = cl;
+                stack[sp] = c0;
                 stent[sp] = tl;
                 ++sp;
-                node = cr;
+                node = c1;
             }
             if (node != kNone && (node & kLeafBit) && leaf == kNone) {  // park the leaf
                 leaf = node;
@@ -546,20 +539,19 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
             node = pop();
         }
         while (leaf != kNone) {
-            const uint32_t li = leaf & ~kLeafBit;
-            const uint32_t first = __float_as_uint(__ldg(&S.nodes[2 * li]).w) & ~kLeafBit;
-            const uint32_t count = __float_as_uint(__ldg(&S.nodes[2 * li + 1]).w);
-            for (uint32_t i = first; i < first + count; ++i) {
-                const float4 ta = __ldg(&S.stris[3 * i]);
-                const float4 t1 = __ldg(&S.stris[3 * i + 1]);
-                const float4 t2 = __ldg(&S.stris[3 * i + 2]);
+            const uint32_t first = (leaf & ~kLeafBit) >> 3, count = (leaf & 7u) + 1u;
+            for (uint32_t k = first; k < first + count; ++k) {
+                const float4 ta = __ldg(&S.ftris[3 * k]);
+                const float4 t1 = __ldg(&S.ftris[3 * k + 1]);
+                const float4 t2 = __ldg(&S.ftris[3 * k + 2]);
+                const uint32_t pos = __float_as_uint(ta.w);
                 float t;
                 // window: (t_min, t_max) before the first hit, then t <= best_t (ties by position)
                 const float lim = found ? __uint_as_float(__float_as_uint(best_t) + 1u) : t_max;
                 if (intersect_tri(r.o, r.d, t_min, lim, ld3(ta), ld3(t1), ld3(t2), t)) {
-                    if (!found || t < best_t || (t == best_t && i < best_pos)) {
+                    if (!found || t < best_t || (t == best_t && pos < best_pos)) {
                         best_t = t;
-                        best_pos = i;
+                        best_pos = pos;
                         found = true;
                     }
                 }

@@ -11,6 +11,7 @@
 #include <numbers>
 #include <thread>
 
+#include "fast_bvh.h"
 #include "prims.h"
 
 namespace prx {
@@ -247,6 +248,29 @@ void Engine::upload_scene() {
         }
         d_split_.alloc(4 * nn);
         PRX_CUDA(cudaMemcpy(d_split_.get(), split.data(), d_split_.size(), cudaMemcpyHostToDevice));
+        // the fast traversal's own SAH tree over the triangles in reference order
+        std::vector<Tri> ref_order(s.bvh_perm.size());
+        for (size_t k = 0; k < ref_order.size(); ++k) ref_order[k] = s.static_tris[s.bvh_perm[k]];
+        const FastBvh fb = build_fast_bvh(ref_order, 1e-5f * diag_ + 1e-6f);
+        std::vector<float4> fn(4 * fb.nodes.size());
+        for (size_t k = 0; k < fb.nodes.size(); ++k) {
+            const FastNode& nd = fb.nodes[k];
+            fn[4 * k] = f4(nd.box[0].lo, f_of_u(nd.child[0]));
+            fn[4 * k + 1] = f4(nd.box[0].hi, f_of_u(nd.child[1]));
+            fn[4 * k + 2] = f4(nd.box[1].lo, 0.0f);
+            fn[4 * k + 3] = f4(nd.box[1].hi, 0.0f);
+        }
+        std::vector<float4> ft(3 * fb.order.size());
+        for (size_t k = 0; k < fb.order.size(); ++k) {
+            const uint32_t pos = fb.order[k];
+            ft[3 * k] = float4{tris[3 * pos].x, tris[3 * pos].y, tris[3 * pos].z, f_of_u(pos)};
+            ft[3 * k + 1] = tris[3 * pos + 1];
+            ft[3 * k + 2] = tris[3 * pos + 2];
+        }
+        d_fnodes_.alloc(sizeof(float4) * fn.size());
+        d_ftris_.alloc(sizeof(float4) * ft.size());
+        PRX_CUDA(cudaMemcpy(d_fnodes_.get(), fn.data(), d_fnodes_.size(), cudaMemcpyHostToDevice));
+        PRX_CUDA(cudaMemcpy(d_ftris_.get(), ft.data(), d_ftris_.size(), cudaMemcpyHostToDevice));
     }
     // materials / flags
     std::vector<float4> mat(s.objects.size());
@@ -384,6 +408,8 @@ SceneDev Engine::scene_dev() const {
     S.split = d_split_.as<uint32_t>();
     S.cull_pad = 1e-5f * diag_ + 1e-6f;
     S.fast = cfg_.dfs_traversal ? 0 : 1;
+    S.fnodes = d_fnodes_.as<float4>();
+    S.ftris = d_ftris_.as<float4>();
     S.stris = d_stris_.as<float4>();
     S.dtris = d_dyn_world_.as<float4>();
     S.dnodes = d_lbvh_nodes_.as<float4>();

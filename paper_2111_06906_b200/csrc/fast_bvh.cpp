@@ -1,0 +1,186 @@
+// fast_bvh.cpp -- binned-SAH BVH2 over the static triangles for the fast traversal.
+//
+// The certified fast traversal (device_scene.cuh: static_fast) returns the (t, reference
+// permutation position)-minimum over all static triangles, which is independent of the
+// tree it walks; exactness w.r.t. the reference's own median-split tree is established
+// afterwards by the certificate.  So this tree is free to be built for speed: binned SAH
+// (Wald 2007), leaves of <= 8 triangles, child boxes stored in the parent (one 64-byte node
+// fetch per traversal step) and inflated by `pad` so that float culling stays conservative.
+#include "fast_bvh.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+namespace prx {
+
+namespace {
+
+constexpr int kBins = 16;
+constexpr uint32_t kMaxLeaf = 8;
+
+struct Prim {
+    Box box;
+    V3 c;
+};
+
+float area(const Box& b) {
+    const V3 e = sub(b.hi, b.lo);
+    if (e.x < 0.0f || e.y < 0.0f || e.z < 0.0f) return 0.0f;
+    return 2.0f * (e.x * e.y + e.y * e.z + e.z * e.x);
+}
+
+struct Builder {
+    const std::vector<Prim>& prims;
+    std::vector<uint32_t>& idx;
+    std::vector<FastNode>& nodes;
+
+    // Returns the child code for the range [b, e) (leaf code or internal node index).
+    uint32_t build(uint32_t b, uint32_t e, const Box& bounds) {
+        const uint32_t n = e - b;
+        if (n <= 2) return leaf(b, n);
+        Box cb = empty_box();
+        for (uint32_t i = b; i < e; ++i) expand(cb, prims[idx[i]].c);
+        int best_axis = -1;
+        int best_split = 0;
+        float best_cost = INFINITY;
+        for (int axis = 0; axis < 3; ++axis) {
+            const float lo = comp(cb.lo, axis), hi = comp(cb.hi, axis);
+            if (!(hi > lo)) continue;
+            Box bb[kBins];
+            uint32_t cnt[kBins] = {};
+            for (int k = 0; k < kBins; ++k) bb[k] = empty_box();
+            const float scale = kBins / (hi - lo);
+            for (uint32_t i = b; i < e; ++i) {
+                const Prim& p = prims[idx[i]];
+                int k = static_cast<int>((comp(p.c, axis) - lo) * scale);
+                k = std::min(std::max(k, 0), kBins - 1);
+                ++cnt[k];
+                expand(bb[k], p.box);
+            }
+            float right_area[kBins];
+            uint32_t right_cnt[kBins];
+            Box acc = empty_box();
+            uint32_t c = 0;
+            for (int k = kBins - 1; k > 0; --k) {
+                expand(acc, bb[k]);
+                c += cnt[k];
+                right_area[k] = area(acc);
+                right_cnt[k] = c;
+            }
+            acc = empty_box();
+            c = 0;
+            for (int k = 0; k < kBins - 1; ++k) {
+                expand(acc, bb[k]);
+                c += cnt[k];
+                if (c == 0 || right_cnt[k + 1] == 0) continue;
+                const float cost = area(acc) * c + right_area[k + 1] * right_cnt[k + 1];
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best_axis = axis;
+                    best_split = k + 1;
+                }
+            }
+        }
+        const float leaf_cost = area(bounds) * n;
+        if (n <= kMaxLeaf && (best_axis < 0 || leaf_cost <= best_cost + area(bounds) * 1.0f)) return leaf(b, n);
+        uint32_t mid;
+        if (best_axis < 0) {  // all centroids coincide: split in the middle
+            mid = b + n / 2;
+        } else {
+            const float lo = comp(cb.lo, best_axis), hi = comp(cb.hi, best_axis);
+            const float scale = kBins / (hi - lo);
+            auto it = std::partition(idx.begin() + b, idx.begin() + e, [&](uint32_t i) {
+                int k = static_cast<int>((comp(prims[i].c, best_axis) - lo) * scale);
+                k = std::min(std::max(k, 0), kBins - 1);
+                return k < best_split;
+            });
+            mid = static_cast<uint32_t>(it - idx.begin());
+            if (mid == b || mid == e) mid = b + n / 2;
+        }
+        Box lb = empty_box(), rb = empty_box();
+        for (uint32_t i = b; i < mid; ++i) expand(lb, prims[idx[i]].box);
+        for (uint32_t i = mid; i < e; ++i) expand(rb, prims[idx[i]].box);
+        const uint32_t me = static_cast<uint32_t>(nodes.size());
+        nodes.emplace_back();
+        const uint32_t l = build(b, mid, lb);
+        const uint32_t r = build(mid, e, rb);
+        FastNode& nd = nodes[me];
+        nd.box[0] = lb;
+        nd.box[1] = rb;
+        nd.child[0] = l;
+        nd.child[1] = r;
+        return me;
+    }
+
+    uint32_t leaf(uint32_t b, uint32_t n) {
+        if (n > kMaxLeaf) {  // should not happen with the SAH guard; split evenly
+            Box lb = empty_box(), rb = empty_box();
+            const uint32_t mid = b + n / 2;
+            for (uint32_t i = b; i < mid; ++i) expand(lb, prims[idx[i]].box);
+            for (uint32_t i = mid; i < b + n; ++i) expand(rb, prims[idx[i]].box);
+            const uint32_t me = static_cast<uint32_t>(nodes.size());
+            nodes.emplace_back();
+            const uint32_t l = leaf(b, mid - b), r = leaf(mid, b + n - mid);
+            nodes[me].box[0] = lb;
+            nodes[me].box[1] = rb;
+            nodes[me].child[0] = l;
+            nodes[me].child[1] = r;
+            return me;
+        }
+        return kFastLeaf | (b << 3) | (n - 1);
+    }
+};
+
+}  // namespace
+
+FastBvh build_fast_bvh(const std::vector<Tri>& tris_ref_order, float pad) {
+    FastBvh out;
+    const uint32_t n = static_cast<uint32_t>(tris_ref_order.size());
+    if (n == 0) return out;
+    std::vector<Prim> prims(n);
+    Box all = empty_box();
+    for (uint32_t i = 0; i < n; ++i) {
+        prims[i].box = tri_bounds(tris_ref_order[i]);
+        prims[i].c = mul(add(prims[i].box.lo, prims[i].box.hi), 0.5f);
+        expand(all, prims[i].box);
+    }
+    out.order.resize(n);
+    std::iota(out.order.begin(), out.order.end(), 0u);
+    out.nodes.reserve(n);
+    out.nodes.emplace_back();  // root placeholder: the root is always an internal node
+    Builder B{prims, out.order, out.nodes};
+    uint32_t root_child[2];
+    Box root_box[2];
+    if (n == 1) {
+        root_child[0] = kFastLeaf | 0u;
+        root_child[1] = kFastEmpty;
+        root_box[0] = prims[0].box;
+        root_box[1] = empty_box();
+    } else {
+        // split the top like any other internal node, then move it into slot 0
+        const uint32_t code = B.build(0, n, all);
+        if (code & kFastLeaf) {
+            root_child[0] = code;
+            root_child[1] = kFastEmpty;
+            root_box[0] = all;
+            root_box[1] = empty_box();
+        } else {
+            root_child[0] = out.nodes[code].child[0];
+            root_child[1] = out.nodes[code].child[1];
+            root_box[0] = out.nodes[code].box[0];
+            root_box[1] = out.nodes[code].box[1];
+        }
+    }
+    out.nodes[0].child[0] = root_child[0];
+    out.nodes[0].child[1] = root_child[1];
+    out.nodes[0].box[0] = root_box[0];
+    out.nodes[0].box[1] = root_box[1];
+    for (FastNode& nd : out.nodes)
+        for (int c = 0; c < 2; ++c)
+            if (nd.child[c] != kFastEmpty) inflate(nd.box[c], pad);
+    return out;
+}
+
+}  // namespace prx
