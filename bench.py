@@ -50,7 +50,7 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--paths", type=int, default=0, help="override n_paths")
-    ap.add_argument("--splat-mode", type=int, default=0)
+    ap.add_argument("--splat-mode", type=int, default=1, help="0 atomic splat, 1 ordered bit-exact gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0)
     return ap.parse_args()

@@ -499,7 +499,7 @@ inline Image gather_image(const Engine& engine, const Camera& cam, float radius,
     img.height = cam.height;
     img.pixels.assign(3ull * cam.width * cam.height, 0.0f);
     const prx_camera c{detail::v(cam.position), detail::v(cam.look_at), cam.fov_deg, cam.width, cam.height};
-    detail::check(prx_splat(engine.native(), &c, radius, 0, img.pixels.data(), nullptr, nullptr));
+    detail::check(prx_splat(engine.native(), &c, radius, 1, img.pixels.data(), nullptr, nullptr));
     return img;
 }
 

@@ -846,7 +846,7 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
                    prx_frame_stats* st) {
     PRX_CUDA(cudaSetDevice(device_));
     if (!(radius > 0.0f)) throw std::invalid_argument("gather: radius must be positive");
-    if (mode != 0) throw std::invalid_argument("splat: only mode 0 (atomic splat) is available");
+    if (mode != 0 && mode != 1) throw std::invalid_argument("splat: mode must be 0 (atomic splat) or 1 (ordered gather)");
     Camera c = scene_->camera;
     if (cam) {
         c.position = V3{cam->position.x, cam->position.y, cam->position.z};
@@ -874,15 +874,17 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
         d_img_.alloc(12ull * npx);
         d_splat_work_.alloc(splat_work_bytes(npx));
         if (d_splat_cand_.size() < 16 + 8ull * n_ * B_) d_splat_cand_.alloc(16 + 8ull * n_ * B_);
+        d_gather_.reset();
         img_w_ = c.width;
         img_h_ = c.height;
     }
     const float inv_area = 1.0f / (static_cast<float>(M_PI) * radius * radius);
     const float inv_pi = 1.0f / static_cast<float>(M_PI);
+    if (mode == 1 && d_gather_.size() == 0) d_gather_.alloc(gather_work_bytes(static_cast<uint64_t>(n_) * B_, npx));
     record(kEvSplat0);
     float* out = rgb_dev ? rgb_dev : d_img_.as<float>();
     launch_splat(scene_dev(), path_dev(), C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area,
-                 d_splat_work_.get(), d_splat_cand_.get(), stream_);
+                 d_splat_work_.get(), d_splat_cand_.get(), mode, d_gather_.get(), stream_);
     record(kEvSplat1);
     if (rgb_host)
         PRX_CUDA(cudaMemcpyAsync(rgb_host, out, 12ull * npx, cudaMemcpyDeviceToHost, stream_));

@@ -170,7 +170,7 @@ private:
     uint32_t max_cells_ = 1;
 
     // splat buffers
-    DevBuf d_gbuf_, d_img_, d_splat_work_, d_splat_cand_;
+    DevBuf d_gbuf_, d_img_, d_splat_work_, d_splat_cand_, d_gather_;
     uint32_t img_w_ = 0, img_h_ = 0;
 
     cudaEvent_t ev_[12] = {};

@@ -69,8 +69,11 @@ void launch_unpack_photons(PathDev P, const void* photons, const void* aux, cuda
 // G-buffer + splat + resolve (splat.cu), replacing gather_image (gather.cpp:35-75)
 int splat_table_bits(uint32_t npx);
 size_t splat_work_bytes(uint32_t npx);
+size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx);
+// mode 0: tiled shared-memory atomic splat; mode 1: ordered gather (bit-exact vs gather_image)
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img,
-                  float inv_pi, float inv_area, void* work, void* cand_buf, cudaStream_t st);
+                  float inv_pi, float inv_area, void* work, void* cand_buf, int mode, void* gather_buf,
+                  cudaStream_t st);
 
 // Dynamic LBVH (lbvh.cu)
 struct LbvhBuffers {

@@ -158,6 +158,115 @@ __global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float rad
     }
 }
 
+// ---------------------------------------------------------------- mode 1: ordered gather
+// Bit-exact image: photons are binned by grid cell in ascending flat record order (the
+// insertion order of the reference's GatherGrid, gather.cpp:13-20,42-52), and one warp per
+// pixel visits its 27 cells in the reference's (dz, dy, dx) order, summing contributors
+// strictly in that order -- the same fp32 additions as gather_image's per-pixel loop.
+__global__ void k_gather_flag(PathDev P, float radius, const unsigned long long* __restrict__ keys, int bits,
+                              uint8_t* __restrict__ flag, uint32_t* __restrict__ pslot, uint32_t* __restrict__ pcnt) {
+    const uint32_t mask = (1u << bits) - 1u;
+    const size_t total = (size_t)P.n * P.B;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
+        const float4 po = __ldcs(&P.pos_obj[v]);
+        uint8_t f = 0;
+        if (__float_as_uint(po.w) != kInvalidObj) {
+            const unsigned long long key =
+                grid_key(cell_coord(po.x, radius), cell_coord(po.y, radius), cell_coord(po.z, radius));
+            uint32_t s = slot_of(key, bits);
+            unsigned long long k;
+            while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
+            if (k == key) {
+                f = 1;
+                pslot[v] = s;
+                atomicAdd(&pcnt[s], 1u);
+            }
+        }
+        flag[v] = f;
+    }
+}
+
+__global__ void k_gather_keys(const uint32_t* __restrict__ cand, const uint32_t* count,
+                              const uint32_t* __restrict__ pslot, uint32_t* keys, uint32_t* vals) {
+    const uint32_t n = *count;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t v = cand[j];
+        keys[j] = pslot[v];
+        vals[j] = v;
+    }
+}
+
+__global__ void k_gather_copy(PathDev P, const uint32_t* __restrict__ vals, const uint32_t* count, float4* spo,
+                              float4* sen) {
+    const uint32_t n = *count;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t v = vals[j];
+        spo[j] = P.pos_obj[v];
+        sen[j] = P.energy[v];
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_gather_pixels(const float4* __restrict__ gbuf, uint32_t npx, float radius,
+                                                      const unsigned long long* __restrict__ keys, int bits,
+                                                      const uint32_t* __restrict__ pstart,
+                                                      const uint32_t* __restrict__ pcnt,
+                                                      const float4* __restrict__ spo, const float4* __restrict__ sen,
+                                                      const float4* __restrict__ mat, float inv_pi, float inv_area,
+                                                      float* __restrict__ img) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t mask = (1u << bits) - 1u;
+    const float r2 = radius * radius;
+    for (uint32_t pix = warp; pix < npx; pix += n_warps) {
+        const float4 g = gbuf[pix];
+        const uint32_t obj = __float_as_uint(g.w);
+        if (obj == kInvalidObj) {  // no primary hit: pixel stays 0 (gather.cpp:66)
+            if (lane < 3) img[3 * pix + lane] = 0.0f;
+            continue;
+        }
+        const V3 x{g.x, g.y, g.z};
+        const long long cx = cell_coord(g.x, radius), cy = cell_coord(g.y, radius), cz = cell_coord(g.z, radius);
+        V3 rad{0.0f, 0.0f, 0.0f};
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {  // gather.hpp:48-50 visiting order
+                    const unsigned long long key = grid_key(cx + dx, cy + dy, cz + dz);
+                    uint32_t s = slot_of(key, bits);
+                    unsigned long long k;
+                    while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
+                    if (k != key) continue;
+                    const uint32_t b0 = __ldg(&pstart[s]), n = __ldg(&pcnt[s]);
+                    for (uint32_t base = 0; base < n; base += 32) {
+                        const uint32_t j = base + lane;
+                        bool hit = false;
+                        float4 en = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (j < n) {
+                            const float4 po = __ldg(&spo[b0 + j]);
+                            const V3 d = sub(V3{po.x, po.y, po.z}, x);  // gather.hpp:54
+                            hit = dot(d, d) <= r2 && __float_as_uint(po.w) == obj;
+                            if (hit) en = __ldg(&sen[b0 + j]);
+                        }
+                        uint32_t ball = __ballot_sync(0xffffffffu, hit);
+                        while (ball) {  // in insertion order: radiance += E (gather.cpp:68)
+                            const int src = __ffs(ball) - 1;
+                            ball &= ball - 1;
+                            rad.x = rad.x + __shfl_sync(0xffffffffu, en.x, src);
+                            rad.y = rad.y + __shfl_sync(0xffffffffu, en.y, src);
+                            rad.z = rad.z + __shfl_sync(0xffffffffu, en.z, src);
+                        }
+                    }
+                }
+        if (lane == 0) {
+            const float4 a = mat[obj];
+            const V3 out = mul(mul(mulv(rad, V3{a.x, a.y, a.z}), inv_pi), inv_area);  // gather.cpp:71
+            img[3 * pix] = out.x;
+            img[3 * pix + 1] = out.y;
+            img[3 * pix + 2] = out.z;
+        }
+    }
+}
+
 __global__ void k_resolve(const float4* __restrict__ gbuf, const float4* __restrict__ mat, float* img, uint32_t n,
                           float inv_pi, float inv_area) {
     for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < n; pix += gridDim.x * blockDim.x) {
@@ -189,8 +298,14 @@ size_t splat_work_bytes(uint32_t npx) {
     return slots * (8 + 4 + 4 + 4) + 4ull * 27 * npx + prim_scratch_bytes(slots) + 64;
 }
 
+size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
+    const uint64_t slots = 1ull << splat_table_bits(npx);
+    const uint64_t nv = n_vertices;
+    return 64 + nv * (1 + 4 + 4 + 16 + 32) + slots * 8 + prim_scratch_bytes(nv > slots ? nv : slots) + 1024;
+}
+
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
-                  float inv_area, void* work, void* cand_buf, cudaStream_t st) {
+                  float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, cudaStream_t st) {
     const uint32_t npx = C.w * C.h;
     const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
@@ -207,6 +322,37 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
     cudaMemsetAsync(cursor, 0, 4 * slots, st);
     k_pixcells<false><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, nullptr, nullptr,
                                                                   nullptr, bits);
+    if (mode == 1) {  // ordered, bit-exact gather
+        const uint64_t nv = (uint64_t)P.n * P.B;
+        char* w = static_cast<char*>(gather_buf);
+        uint32_t* m_count = reinterpret_cast<uint32_t*>(w);
+        w += 64;
+        uint32_t* pslot = reinterpret_cast<uint32_t*>(w);
+        w += 4 * nv;
+        uint32_t* cand = reinterpret_cast<uint32_t*>(w);
+        w += 4 * nv;
+        uint32_t* sk = reinterpret_cast<uint32_t*>(w);
+        uint32_t* sv = sk + nv;
+        uint32_t* sk2 = sv + nv;
+        uint32_t* sv2 = sk2 + nv;
+        float4* spo = reinterpret_cast<float4*>(sv2 + nv);
+        float4* sen = spo + nv;
+        uint32_t* pcnt = reinterpret_cast<uint32_t*>(sen + nv);
+        uint32_t* pstart = pcnt + slots;
+        uint8_t* flag = reinterpret_cast<uint8_t*>(pstart + slots);
+        void* gscratch = flag + nv + 256;
+        cudaMemsetAsync(pcnt, 0, 4 * slots, st);
+        k_gather_flag<<<launch_grid(nv, kT), kT, 0, st>>>(P, radius, keys, bits, flag, pslot, pcnt);
+        compact_u8(flag, (uint32_t)nv, nullptr, 0, cand, m_count, gscratch, st);
+        k_gather_keys<<<launch_grid(nv, kT), kT, 0, st>>>(cand, m_count, pslot, sk, sv);
+        radix_sort_pairs(sk, sv, sk2, sv2, (uint32_t)nv, m_count, bits, gscratch, st);
+        scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
+        k_gather_copy<<<launch_grid(nv, kT), kT, 0, st>>>(P, sv, m_count, spo, sen);
+        k_gather_pixels<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt,
+                                                                     spo, sen, S.mat, inv_pi, inv_area, img);
+        g_launches += 8;
+        return;
+    }
     scan_exclusive_u32(cnt, off, (uint32_t)slots, nullptr, nullptr, scratch, st);
     k_pixcells<true><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, off, cursor, list,
                                                                  bits);

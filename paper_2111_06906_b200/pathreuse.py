@@ -227,7 +227,7 @@ class Engine:
         L.check(L.lib().prx_run_stage(self._h, L.STAGE[stage], C.byref(st)))
         return st
 
-    def splat(self, camera: L.Camera | None = None, radius: float | None = None, mode: int = 0,
+    def splat(self, camera: L.Camera | None = None, radius: float | None = None, mode: int = 1,
               st: L.FrameStats | None = None) -> np.ndarray:
         """gather_image (gather.cpp:35-75) as a GPU splat -> float32 [h, w, 3]."""
         info = self.info()

@@ -32,3 +32,20 @@ def test_splat_matches_gather(scene, mode, frames):
     lit = img_c > 0
     assert rel[lit].mean() <= MEAN_RTOL, f"mean rel {rel[lit].mean()}"
     assert lit.any()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene,mode,frames,synthetic", [("static-box", "naive", 1, False), ("moving-cube", "error", 3, False),
+                                                         ("villa-analog", "error", 2, False),
+                                                         ("merry-go-round-analog", "naive", 2, False),
+                                                         ("C2", "naive", 2, True), ("C3", "error", 2, True)])
+def test_ordered_gather_bit_exact(scene, mode, frames, synthetic):
+    """splat mode 1 (ordered gather) reproduces gather_image byte for byte."""
+    gpu, cpu = pair(scene, synthetic=synthetic, mode=mode, paths=20000, bounces=5, dm=[2, 2, 8, 8], seed=3)
+    for _ in range(frames):
+        gpu.run_frame()
+        cpu.run_frame()
+    img_g = gpu.splat(radius=0.25, mode=1)
+    img_c, _ = cpu.gather(radius=0.25)
+    assert img_g.tobytes() == img_c.tobytes()
+    assert (img_c > 0).any()
