@@ -63,6 +63,10 @@ struct SceneDev {
     const float4* dtris;       // dynamic tris, world space, object-local index order
     const float4* dnodes;      // LBVH nodes: 4 float4 per internal node
     const uint32_t* dleaf;     // LBVH leaf -> object-local triangle index
+    int32_t dfast;             // 1: combined LBVH over all dynamic triangles is built
+    const float4* danodes;     // combined LBVH, fast-tree layout (4 float4 per node)
+    const float4* datris;      // dynamic tris in combined-leaf order: {a, global idx} {e1, obj j} {e2, -}
+    const uint32_t* dtri_obj;  // global dynamic triangle -> dynamic object j
     const float4* mat;         // per object {albedo, glossy exponent}
     const uint32_t* oflags;    // per object: bit0 dynamic, bit1 glossy
     const FrameParams* fp;

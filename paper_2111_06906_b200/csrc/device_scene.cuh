@@ -475,18 +475,23 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
         t0 = fmax_std(t0, tn);
         t1 = fmin_std(t1, tf);
     }
-    return t0 <= t1 ? t0 : INFINITY;
+    // relative slack covers the rounding of the slab quotients far from the ray origin
+    return t0 - t1 <= 2.0e-6f * (fabsf(t0) + fabsf(t1)) ? t0 : INFINITY;
 }
 
 __device__ __forceinline__ float cull_limit(float best_t) { return best_t + 1e-4f * fabsf(best_t) + 1e-6f; }
 
-// global (t, position)-minimum over static triangles with t in (t_min, t_max), walking the
-// fast SAH tree (fast_bvh.cpp).  While-while traversal (Aila & Laine 2009) with postponed
-// leaves: a lane that reaches a leaf parks it and keeps descending until every active lane
-// of the warp holds a leaf, so triangle tests run warp-wide.  The result is the
-// order-independent lexicographic minimum, so neither tree nor visit order matters.
-__device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, float t_min, float t_max,
-                                            float& best_t, uint32_t& best_pos) {
+// global (t, position)-minimum over the triangles of a fast tree with t in (t_min, t_max).
+// Static: the SAH tree (fast_bvh.cpp), position = reference permutation position; dynamic:
+// the combined LBVH (lbvh.cu), position = global dynamic triangle index.  While-while
+// traversal (Aila & Laine 2009) with postponed leaves: a lane that reaches a leaf parks it
+// and keeps descending until every active lane of the warp holds a leaf, so triangle tests
+// run warp-wide.  The result is the order-independent lexicographic minimum, so neither
+// tree nor visit order matters.  kAny: stop at the first accepted triangle (any-hit).
+template <bool kAny>
+__device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                             const RayPre& r, float t_min, float t_max, float& best_t,
+                                             uint32_t& best_pos) {
     constexpr uint32_t kNone = 0xFFFFFFFFu;
     best_t = t_max;
     best_pos = kNone;
@@ -505,7 +510,7 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
     };
     while (node != kNone || leaf != kNone) {
         while (node != kNone && !(node & kLeafBit)) {
-            const float4* N = S.fnodes + 4ull * node;
+            const float4* N = nodes + 4ull * node;
             const float4 n0 = __ldg(&N[0]), n1 = __ldg(&N[1]), n2 = __ldg(&N[2]), n3 = __ldg(&N[3]);
             const uint32_t c0 = __float_as_uint(n0.w), c1 = __float_as_uint(n1.w);
             const float lim = cull_limit(best_t);
@@ -541,9 +546,9 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
         while (leaf != kNone) {
             const uint32_t first = (leaf & ~kLeafBit) >> 3, count = (leaf & 7u) + 1u;
             for (uint32_t k = first; k < first + count; ++k) {
-                const float4 ta = __ldg(&S.ftris[3 * k]);
-                const float4 t1 = __ldg(&S.ftris[3 * k + 1]);
-                const float4 t2 = __ldg(&S.ftris[3 * k + 2]);
+                const float4 ta = __ldg(&tris[3 * k]);
+                const float4 t1 = __ldg(&tris[3 * k + 1]);
+                const float4 t2 = __ldg(&tris[3 * k + 2]);
                 const uint32_t pos = __float_as_uint(ta.w);
                 float t;
                 // window: (t_min, t_max) before the first hit, then t <= best_t (ties by position)
@@ -553,6 +558,7 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
                         best_t = t;
                         best_pos = pos;
                         found = true;
+                        if (kAny) return true;
                     }
                 }
             }
@@ -564,6 +570,11 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
         }
     }
     return found;
+}
+
+__device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, float t_min, float t_max,
+                                            float& best_t, uint32_t& best_pos) {
+    return fast_closest<false>(S.fnodes, S.ftris, r, t_min, t_max, best_t, best_pos);
 }
 
 // every ancestor of permutation position `pos` passes the reference's exact box test at t_lim
@@ -597,29 +608,26 @@ __device__ __forceinline__ bool static_closest_exact(const SceneDev& S, const Ra
     return static_closest(S, r, t_min, t_max, best);
 }
 
-// static part of occluded: any accepted triangle whose ancestors pass at the original t_max
+// static part of occluded: the reference answers true iff some accepted triangle has all
+// ancestors passing the exact test at the (fixed) t_max, so the first accepted triangle the
+// fast walk meets certifies a hit whenever its own path does.
 __device__ __forceinline__ bool static_any_exact(const SceneDev& S, const RayPre& r, float t_min, float t_max) {
     if (S.n_nodes == 0) return false;
     if (!S.fast) return static_any(S, r, t_min, t_max);
     float bt;
     uint32_t bp;
-    if (!static_fast(S, r, t_min, t_max, bt, bp)) return false;
+    if (!fast_closest<true>(S.fnodes, S.ftris, r, t_min, t_max, bt, bp)) return false;
     if (static_cert(S, r, t_min, t_max, bp)) return true;
     return static_any(S, r, t_min, t_max);
 }
 
-// intersect_scene (scene.cpp:136-168), one-shot form: tight static loop, then each dynamic
-// object behind its gate.
-__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h) {
-    const RayPre r = make_ray(o, d);
-    float t_max = FLT_MAX;
-    uint32_t sbest = 0;
-    const bool found = static_closest_exact(S, r, t_min, t_max, sbest);
-    int kind = found ? 0 : -1;
-    uint32_t dj = 0, dtri = 0;
+// Dynamic phase of intersect_scene (scene.cpp:153-165): objects in order, each behind its
+// exact gate at the running t_max, brute-force (t, index) minimum inside.
+__device__ __forceinline__ int dyn_closest_seq(const SceneDev& S, const RayPre& r, float t_min, float& t_max,
+                                               uint32_t& dj, uint32_t& dtri) {
     const FrameParams* fp = S.fp;
-    const uint32_t n_dyn = fp->n_dyn;
-    for (uint32_t j = 0; j < n_dyn; ++j) {
+    int kind = -1;
+    for (uint32_t j = 0; j < fp->n_dyn; ++j) {
         const DynObj& D = fp->dyn[j];
         if (!ray_box(r, t_min, t_max, D.cur)) continue;
         uint32_t bt;
@@ -629,6 +637,46 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
             dtri = bt;
         }
     }
+    return kind;
+}
+
+// Certified fast form of the dynamic phase.  Without gates the sequential loop returns the
+// (t, object, index)-lexicographic minimum over all dynamic triangles with t in (t_min, t_max):
+// an object replaces the running winner only with a strictly smaller t, and triangle order
+// inside an object breaks ties.  With gates, let (t*, j*, i*) be that minimum: every object
+// before j* holds only hits with t > t*, so when j* is reached the running t_max exceeds t*,
+// and if j*'s gate passes at nextafter(t*) it passes there too (the test is monotone in
+// t_max); later objects cannot beat t* strictly.  So the minimum, found by one walk over the
+// combined LBVH (global index order == (object, index) order), is the reference's answer
+// whenever its object's gate passes at nextafter(t*); otherwise rerun the sequential loop.
+__device__ __forceinline__ int dyn_closest_exact(const SceneDev& S, const RayPre& r, float t_min, float& t_max,
+                                                 uint32_t& dj, uint32_t& dtri) {
+    const FrameParams* fp = S.fp;
+    if (fp->n_dyn == 0) return -1;
+    if (!S.fast || !S.dfast) return dyn_closest_seq(S, r, t_min, t_max, dj, dtri);
+    float bt;
+    uint32_t g;
+    if (!fast_closest<false>(S.danodes, S.datris, r, t_min, t_max, bt, g)) return -1;
+    const uint32_t j = __ldg(&S.dtri_obj[g]);
+    const DynObj& D = fp->dyn[j];
+    if (ray_box(r, t_min, __uint_as_float(__float_as_uint(bt) + 1u), D.cur)) {
+        t_max = bt;
+        dj = j;
+        dtri = g - D.tri_begin;
+        return 1;
+    }
+    return dyn_closest_seq(S, r, t_min, t_max, dj, dtri);
+}
+
+// intersect_scene (scene.cpp:136-168), one-shot form: static phase, then the dynamic phase.
+__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h) {
+    const RayPre r = make_ray(o, d);
+    float t_max = FLT_MAX;
+    uint32_t sbest = 0;
+    const bool found = static_closest_exact(S, r, t_min, t_max, sbest);
+    uint32_t dj = 0, dtri = 0;
+    int kind = dyn_closest_exact(S, r, t_min, t_max, dj, dtri);
+    if (kind < 0) kind = found ? 0 : -1;
     if (kind < 0) return false;
     V3 e1, e2;
     if (kind == 0) {
@@ -638,7 +686,7 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
         e2 = ld3(q2);
         h.obj = __float_as_uint(q1.w);
     } else {
-        const DynObj& D = fp->dyn[dj];
+        const DynObj& D = S.fp->dyn[dj];
         const float4* T = S.dtris + 3ull * (D.tri_begin + dtri);
         e1 = ld3(__ldg(&T[1]));
         e2 = ld3(__ldg(&T[2]));
@@ -652,11 +700,20 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
     return true;
 }
 
-// occluded (scene.cpp:170-177)
+// occluded (scene.cpp:170-177).  Dynamic phase: true iff some object whose gate passes at
+// t_max holds an accepted triangle; the first accepted triangle of the combined walk
+// certifies when its own object's gate passes, else the sequential loop decides.
 __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_min, float t_max) {
     const RayPre r = make_ray(o, d);
     if (static_any_exact(S, r, t_min, t_max)) return true;
     const FrameParams* fp = S.fp;
+    if (fp->n_dyn == 0) return false;
+    if (S.fast && S.dfast) {
+        float bt;
+        uint32_t g;
+        if (!fast_closest<true>(S.danodes, S.datris, r, t_min, t_max, bt, g)) return false;
+        if (ray_box(r, t_min, t_max, fp->dyn[__ldg(&S.dtri_obj[g])].cur)) return true;
+    }
     for (uint32_t j = 0; j < fp->n_dyn; ++j) {
         const DynObj& D = fp->dyn[j];
         if (!ray_box(r, t_min, t_max, D.cur)) continue;

@@ -320,8 +320,8 @@ void Engine::upload_scene() {
         PRX_CUDA(cudaMemcpy(d_dyn_local_.get(), local.data(), d_dyn_local_.size(), cudaMemcpyHostToDevice));
         PRX_CUDA(cudaMemcpy(d_dyn_tri_xf_.get(), tri_xf.data(), d_dyn_tri_xf_.size(), cudaMemcpyHostToDevice));
         d_lbvh_leaf_.alloc(4ull * tri);
-        if (nodes_total) {
-            d_lbvh_nodes_.alloc(sizeof(float4) * 4ull * nodes_total);
+        if (nodes_total) d_lbvh_nodes_.alloc(sizeof(float4) * 4ull * nodes_total);
+        if (tri >= 2) {
             const size_t n = tri;
             const size_t scratch = prim_scratch_bytes(n);
             d_lbvh_work_.alloc(4 * n * 4 + 4 * (2 * n + 2) * 2 + scratch);
@@ -333,6 +333,10 @@ void Engine::upload_scene() {
             lbvh_.parent = w + 4 * n;
             lbvh_.flags = w + 4 * n + (2 * n + 2);
             lbvh_.scratch = w + 4 * n + 2 * (2 * n + 2);
+            d_dall_nodes_.alloc(sizeof(float4) * 4 * (n - 1));
+            d_dall_tris_.alloc(sizeof(float4) * 3 * n);
+            lbvh_.all_nodes = d_dall_nodes_.as<float4>();
+            lbvh_.all_tris = d_dall_tris_.as<float4>();
         }
     }
 }
@@ -414,6 +418,10 @@ SceneDev Engine::scene_dev() const {
     S.dtris = d_dyn_world_.as<float4>();
     S.dnodes = d_lbvh_nodes_.as<float4>();
     S.dleaf = d_lbvh_leaf_.as<uint32_t>();
+    S.dfast = lbvh_.all_nodes ? 1 : 0;
+    S.danodes = d_dall_nodes_.as<float4>();
+    S.datris = d_dall_tris_.as<float4>();
+    S.dtri_obj = d_dyn_tri_xf_.as<uint32_t>();
     S.mat = d_mat_.as<float4>();
     S.oflags = d_oflags_.as<uint32_t>();
     S.fp = d_fp_.as<FrameParams>();
@@ -541,11 +549,11 @@ void Engine::place_dynamics(bool force) {
                              cudaMemcpyHostToDevice, stream_));
     launch_transform_dynamic(d_dyn_local_.as<float4>(), d_dyn_tri_xf_.as<uint32_t>(),
                              d_dyn_xf_.as<float4>(), n_dyn_tris_, d_dyn_world_.as<float4>(), stream_);
-    if (n_lbvh_nodes_)
+    if (n_dyn_tris_ >= 2)
         build_dynamic_lbvh(d_dyn_world_.as<float4>(), d_dyn_tri_xf_.as<uint32_t>(), n_dyn_tris_,
                            h_fp_->dyn, static_cast<uint32_t>(dyn_.size()),
                            reinterpret_cast<const DynObj*>(d_fp_.as<char>() + offsetof(FrameParams, dyn)),
-                           d_lbvh_nodes_.as<float4>(), d_lbvh_leaf_.as<uint32_t>(), lbvh_, stream_);
+                           n_lbvh_nodes_ ? d_lbvh_nodes_.as<float4>() : nullptr, d_lbvh_leaf_.as<uint32_t>(), lbvh_, stream_);
 }
 
 // ----------------------------------------------------------------------- stages

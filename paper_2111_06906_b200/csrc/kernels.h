@@ -84,6 +84,8 @@ struct LbvhBuffers {
     uint32_t* parent;     // per node/leaf parent index
     uint32_t* flags;      // refit arrival counters
     void* scratch;
+    float4* all_nodes;    // combined tree over all dynamic triangles (null: not built)
+    float4* all_tris;     // its leaves: dynamic triangles in sorted order
 };
 void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint32_t n_tris,
                         const DynObj* dyn_host, uint32_t n_dyn, const DynObj* dyn_dev,

@@ -51,11 +51,38 @@ __global__ void k_morton(const float4* __restrict__ tris, const uint32_t* __rest
     }
 }
 
-__device__ __forceinline__ int delta(const uint32_t* __restrict__ k, int n, int i, int j) {
+__device__ __forceinline__ int delta(const uint32_t* __restrict__ k, int n, int i, int j, uint32_t mask) {
     if (j < 0 || j >= n) return -1;
-    const uint32_t a = k[i] & 0xFFFFFFu, b = k[j] & 0xFFFFFFu;
+    const uint32_t a = k[i] & mask, b = k[j] & mask;
     if (a == b) return 32 + __clz((uint32_t)(i ^ j));
     return __clz(a ^ b);
+}
+
+// Karras 2012: range [lo, hi] of internal node i over sorted keys k[0, n) and its split g
+// (left child covers [lo, g], right child [g + 1, hi]).
+__device__ __forceinline__ void karras_node(const uint32_t* __restrict__ k, int n, int i, uint32_t mask, int& g,
+                                            int& lo, int& hi) {
+    const int d = (delta(k, n, i, i + 1, mask) - delta(k, n, i, i - 1, mask)) >= 0 ? 1 : -1;
+    const int dmin = delta(k, n, i, i - d, mask);
+    int lmax = 2;
+    while (delta(k, n, i, i + lmax * d, mask) > dmin) lmax <<= 1;
+    int l = 0;
+    for (int s = lmax >> 1; s >= 1; s >>= 1)
+        if (delta(k, n, i, i + (l + s) * d, mask) > dmin) l += s;
+    const int jj = i + l * d;
+    const int dnode = delta(k, n, i, jj, mask);
+    int s = 0;
+    int div = 2;
+    int step = (l + div - 1) / div;
+    while (true) {
+        if (delta(k, n, i, i + (s + step) * d, mask) > dnode) s += step;
+        if (step <= 1) break;
+        div <<= 1;
+        step = (l + div - 1) / div;
+    }
+    g = i + s * d + (d < 0 ? -1 : 0);
+    lo = i < jj ? i : jj;
+    hi = i < jj ? jj : i;
 }
 
 // Karras 2012, one thread per internal node of every object; `keys` sorted.
@@ -68,27 +95,8 @@ __global__ void k_karras(const uint32_t* __restrict__ keys, uint32_t n_all, cons
         const int n = (int)D.tri_count;
         const int i = (int)(t - D.tri_begin);
         if (i >= n - 1) continue;
-        const uint32_t* k = keys + D.tri_begin;
-        const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
-        const int dmin = delta(k, n, i, i - d);
-        int lmax = 2;
-        while (delta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
-        int l = 0;
-        for (int s = lmax >> 1; s >= 1; s >>= 1)
-            if (delta(k, n, i, i + (l + s) * d) > dmin) l += s;
-        const int jj = i + l * d;
-        const int dnode = delta(k, n, i, jj);
-        int s = 0;
-        int div = 2;
-        int step = (l + div - 1) / div;
-        while (true) {
-            if (delta(k, n, i, i + (s + step) * d) > dnode) s += step;
-            if (step <= 1) break;
-            div <<= 1;
-            step = (l + div - 1) / div;
-        }
-        const int g = i + s * d + (d < 0 ? -1 : 0);
-        const int lo = i < jj ? i : jj, hi = i < jj ? jj : i;
+        int g, lo, hi;
+        karras_node(keys + D.tri_begin, n, i, 0xFFFFFFu, g, lo, hi);
         const uint32_t left = (lo == g) ? (kLeafBit | (uint32_t)g) : (uint32_t)g;
         const uint32_t right = (hi == g + 1) ? (kLeafBit | (uint32_t)(g + 1)) : (uint32_t)(g + 1);
         float4* N = nodes + 4ull * (D.node_begin + i);
@@ -151,6 +159,81 @@ __global__ void k_copy_leaf(const uint32_t* __restrict__ vals, uint32_t n, uint3
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) leaf[t] = vals[t];
 }
 
+// ---------------------------------------------------------------- combined tree
+// One Karras tree over ALL dynamic triangles (full 32-bit key: object, then Morton), in the
+// fast-tree layout of fast_bvh.h ({lo0, c0} {hi0, c1} {lo1, -} {hi1, -}, leaf code
+// kLeafBit | position << 3), walked by fast_closest for the certified dynamic phase
+// (device_scene.cuh: dyn_closest_exact).  Leaves are the triangles themselves, copied in
+// sorted order with their global index (== (object, index) order) in a.w.
+__global__ void k_karras_all(const uint32_t* __restrict__ keys, uint32_t n, float4* nodes, uint32_t* parent) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t + 1 < n; t += gridDim.x * blockDim.x) {
+        int g, lo, hi;
+        karras_node(keys, (int)n, (int)t, 0xFFFFFFFFu, g, lo, hi);
+        const uint32_t left = (lo == g) ? (kLeafBit | ((uint32_t)g << 3)) : (uint32_t)g;
+        const uint32_t right = (hi == g + 1) ? (kLeafBit | ((uint32_t)(g + 1) << 3)) : (uint32_t)(g + 1);
+        float4* N = nodes + 4ull * t;
+        N[0].w = __uint_as_float(left);
+        N[1].w = __uint_as_float(right);
+        if (left & kLeafBit) parent[g] = t;
+        else parent[n + g] = t;
+        if (right & kLeafBit) parent[g + 1] = t;
+        else parent[n + g + 1] = t;
+        if (t == 0) parent[n] = 0xFFFFFFFFu;
+    }
+}
+
+__global__ void k_sorted_tris(const float4* __restrict__ tris, const uint32_t* __restrict__ keys,
+                              const uint32_t* __restrict__ vals, uint32_t n, const DynObj* __restrict__ dyn,
+                              float4* out) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const uint32_t j = keys[t] >> 24;
+        const uint32_t g = dyn[j].tri_begin + vals[t];
+        float4 a = tris[3 * g], e1 = tris[3 * g + 1], e2 = tris[3 * g + 2];
+        a.w = __uint_as_float(g);
+        e1.w = __uint_as_float(j);
+        e2.w = 0.0f;
+        out[3 * t] = a;
+        out[3 * t + 1] = e1;
+        out[3 * t + 2] = e2;
+    }
+}
+
+__global__ void k_refit_all(const float4* __restrict__ stris, uint32_t n, const DynObj* __restrict__ dyn,
+                            float4* nodes, const uint32_t* __restrict__ parent, uint32_t* flags) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const float4 a = stris[3 * t], e1 = stris[3 * t + 1], e2 = stris[3 * t + 2];
+        const DynObj D = dyn[__float_as_uint(e1.w)];
+        const float ext = fmaxf(fmaxf(D.cur.hi.x - D.cur.lo.x, D.cur.hi.y - D.cur.lo.y), D.cur.hi.z - D.cur.lo.z);
+        const float bx = a.x + e1.x, by = a.y + e1.y, bz = a.z + e1.z;
+        const float cx = a.x + e2.x, cy = a.y + e2.y, cz = a.z + e2.z;
+        float lox = fminf(a.x, fminf(bx, cx)), hix = fmaxf(a.x, fmaxf(bx, cx));
+        float loy = fminf(a.y, fminf(by, cy)), hiy = fmaxf(a.y, fmaxf(by, cy));
+        float loz = fminf(a.z, fminf(bz, cz)), hiz = fmaxf(a.z, fmaxf(bz, cz));
+        const float mag = fmaxf(fmaxf(fabsf(lox), fabsf(hix)), fmaxf(fmaxf(fabsf(loy), fabsf(hiy)),
+                                                                      fmaxf(fabsf(loz), fabsf(hiz))));
+        const float m = 1e-5f * ext + 4e-6f * mag + 1e-30f;
+        lox -= m, loy -= m, loz -= m, hix += m, hiy += m, hiz += m;
+        uint32_t child = kLeafBit | (t << 3);
+        uint32_t p = parent[t];
+        while (p != 0xFFFFFFFFu) {
+            float4* N = nodes + 4ull * p;
+            const bool is_left = __float_as_uint(__ldcg(&N[0].w)) == child;
+            const int o = is_left ? 0 : 2;
+            N[o].x = lox, N[o].y = loy, N[o].z = loz;
+            N[o + 1].x = hix, N[o + 1].y = hiy, N[o + 1].z = hiz;
+            __threadfence();
+            if (atomicAdd(&flags[p], 1u) == 0) break;  // sibling not done yet
+            __threadfence();
+            const int q = is_left ? 2 : 0;
+            const float4 smin = __ldcg(&N[q]), smax = __ldcg(&N[q + 1]);
+            lox = fminf(lox, smin.x), loy = fminf(loy, smin.y), loz = fminf(loz, smin.z);
+            hix = fmaxf(hix, smax.x), hiy = fmaxf(hiy, smax.y), hiz = fmaxf(hiz, smax.z);
+            child = p;
+            p = parent[n + p];
+        }
+    }
+}
+
 }  // namespace
 
 void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint32_t n_tris,
@@ -158,15 +241,25 @@ void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint3
                         uint32_t* leaf, const LbvhBuffers& buf, cudaStream_t st) {
     (void)dyn_host;
     (void)n_dyn;
-    if (n_tris == 0) return;
+    if (n_tris < 2) return;
     const int g = launch_grid(n_tris, kT);
     k_morton<<<g, kT, 0, st>>>(world_tris, tri_obj, n_tris, dyn_dev, buf.keys, buf.vals);
     radix_sort_pairs(buf.keys, buf.vals, buf.keys_tmp, buf.vals_tmp, n_tris, nullptr, 31, buf.scratch, st);
-    k_copy_leaf<<<g, kT, 0, st>>>(buf.vals, n_tris, leaf);
-    k_karras<<<g, kT, 0, st>>>(buf.keys, n_tris, dyn_dev, nodes, buf.parent, n_tris);
-    cudaMemsetAsync(buf.flags, 0, 4ull * n_tris, st);
-    k_refit<<<g, kT, 0, st>>>(world_tris, buf.keys, leaf, n_tris, dyn_dev, nodes, buf.parent, buf.flags, n_tris);
-    g_launches += 4 + 3 * 4;
+    g_launches += 1 + 3 * 4;
+    if (nodes) {  // per-object trees (sequential fallback and DFS mode)
+        k_copy_leaf<<<g, kT, 0, st>>>(buf.vals, n_tris, leaf);
+        k_karras<<<g, kT, 0, st>>>(buf.keys, n_tris, dyn_dev, nodes, buf.parent, n_tris);
+        cudaMemsetAsync(buf.flags, 0, 4ull * n_tris, st);
+        k_refit<<<g, kT, 0, st>>>(world_tris, buf.keys, leaf, n_tris, dyn_dev, nodes, buf.parent, buf.flags, n_tris);
+        g_launches += 3;
+    }
+    if (buf.all_nodes) {  // combined tree (fast dynamic phase)
+        k_sorted_tris<<<g, kT, 0, st>>>(world_tris, buf.keys, buf.vals, n_tris, dyn_dev, buf.all_tris);
+        k_karras_all<<<g, kT, 0, st>>>(buf.keys, n_tris, buf.all_nodes, buf.parent);
+        cudaMemsetAsync(buf.flags, 0, 4ull * n_tris, st);
+        k_refit_all<<<g, kT, 0, st>>>(buf.all_tris, n_tris, dyn_dev, buf.all_nodes, buf.parent, buf.flags);
+        g_launches += 3;
+    }
 }
 
 }  // namespace prx
