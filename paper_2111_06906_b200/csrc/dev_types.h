@@ -54,7 +54,7 @@ struct FrameParams {
 struct SceneDev {
     const float4* nodes;       // static BVH: 2 float4 per node {lo, a} {hi, b}
     uint32_t n_nodes;
-    const uint32_t* split;     // internal node: first permutation position of its right subtree
+    const uint32_t* leaf_of;   // permutation position -> reference leaf node
     float cull_pad;            // fast traversal: box inflation for conservative culling
     int32_t fast;              // 1: near-first traversal + exactness certificate
     const float4* fnodes;      // fast SAH BVH2: 4 float4 per node {lo0,c0} {hi0,c1} {lo1,-} {hi1,-}

@@ -51,6 +51,63 @@ __device__ __forceinline__ RayPre make_ray(V3 o, V3 d) {
     return r;
 }
 
+// round(N / d) <= c (le) or c <= round(N / d) (!le) for the reference's double quotient
+// (N = fl64(bound - o), d != 0) against a float c.  c * d is exact in double (24 x 24 bits),
+// so one fma gives the exact sign of N - c * d, hence of N / d - c; rounding is monotone
+// and c is representable, so that sign decides unless N / d lies within a few double ulps
+// of c, where the quotient itself is computed.
+static __device__ __noinline__ bool quot_cmp_const(double N, float d, float c, bool le) {
+    const double dd = d, cd = c;
+    const double res = fma(-cd, dd, N);  // sign(N - c d) exact
+    if (fabs(res) <= fabs(cd) * fabs(dd) * 0x1p-48 + 0x1p-1000) {
+        const double q = N / dd;
+        return le ? (q <= cd) : (cd <= q);
+    }
+    const bool q_below_c = (dd > 0.0) ? (res < 0.0) : (res > 0.0);
+    return le ? q_below_c : !q_below_c;
+}
+
+// Slow path of ray_box: decide max(lower) <= min(upper) pair by pair.  Lower candidates are
+// t_min and the entry quotients, upper ones t_max and the exit quotients; a pair the float
+// values settle is skipped, a float-vs-quotient pair is settled exactly by quot_cmp_const,
+// and a quotient-vs-quotient pair falls back to the reference's double test.
+static __device__ __noinline__ bool ray_box_refine(const RayPre& r, float t_min, float t_max, const Box& b) {
+    float fn[3], ff[3];  // the float entry / exit quotients of ray_box
+    for (int a = 0; a < 3; ++a) {
+        const float da = comp(r.d, a), oa = comp(r.o, a);
+        const float tn = (comp(b.lo, a) - oa) * r.inv[a];
+        const float tf = (comp(b.hi, a) - oa) * r.inv[a];
+        fn[a] = da == 0.0f ? 0.0f : (tn > tf ? tf : tn);
+        ff[a] = da == 0.0f ? 0.0f : (tn > tf ? tn : tf);
+    }
+    for (int i = -1; i < 3; ++i) {
+        if (i >= 0 && comp(r.d, i) == 0.0f) continue;
+        const float li = i < 0 ? t_min : fn[i];
+        for (int j = -1; j < 3; ++j) {
+            if (j >= 0 && comp(r.d, j) == 0.0f) continue;
+            const float uj = j < 0 ? t_max : ff[j];
+            const float slack = 4.0e-7f * (fabsf(li) + fabsf(uj)) + 1e-30f;
+            if (uj - li > slack) continue;  // certainly li <= uj
+            if (li - uj > slack) return false;
+            if (i < 0 && j < 0) {
+                if (!(t_min <= t_max)) return false;
+            } else if (i >= 0 && j >= 0) {
+                return ray_box_exact(r.o, r.d, t_min, t_max, b);
+            } else {
+                const int a = i >= 0 ? i : j;
+                const float da = comp(r.d, a), oa = comp(r.o, a);
+                // entry bound is lo for d > 0, hi for d < 0; exit the other one
+                const bool entry = i >= 0;
+                const float bound = (entry == (da > 0.0f)) ? comp(b.lo, a) : comp(b.hi, a);
+                const double N = (double)bound - (double)oa;
+                // entry quotient <= t_max, or t_min <= exit quotient
+                if (!quot_cmp_const(N, da, entry ? t_max : t_min, entry)) return false;
+            }
+        }
+    }
+    return true;
+}
+
 __device__ __forceinline__ bool ray_box(const RayPre& r, float t_min, float t_max, const Box& b) {
     if (!r.safe) return ray_box_exact(r.o, r.d, t_min, t_max, b);
     // Float slab: each quotient q = (bound - o) / d is approximated by f = fl(fl(bound - o)
@@ -79,7 +136,7 @@ __device__ __forceinline__ bool ray_box(const RayPre& r, float t_min, float t_ma
     const float slack = 4.0e-7f * (fabsf(t0) + fabsf(t1)) + 1e-30f;
     if (t0 - t1 > slack) return false;
     if (t1 - t0 > slack) return true;
-    return ray_box_exact(r.o, r.d, t_min, t_max, b);
+    return ray_box_refine(r, t_min, t_max, b);
 }
 
 // Static BVH closest hit (bvh.cpp:79-106) -- identical visit order, identical culling.
@@ -451,8 +508,9 @@ __device__ __forceinline__ bool trav_hit(const SceneDev& S, const Trav& T, Hit& 
 // is > t* (a smaller t_max would need an earlier hit with t <= t*), so it suffices that each
 // ancestor passes at t_max = nextafter(t*) (the test is monotone in t_max).
 // static_fast finds T* with near-first ordering and conservative culling (boxes inflated by
-// cull_pad, t window widened); static_cert re-walks T*'s root-to-leaf path with the exact
-// test.  A ray whose certificate fails reruns the reference-order DFS (static_closest).
+// cull_pad, t window widened); static_cert tests T*'s reference leaf with the exact test,
+// which implies every ancestor passes.  A ray whose certificate fails reruns the
+// reference-order DFS (static_closest).
 __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t_lim, float4 A, float4 B,
                                            float pad) {
     float t0 = t_min, t1 = t_lim;
@@ -577,19 +635,17 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
     return fast_closest<false>(S.fnodes, S.ftris, r, t_min, t_max, best_t, best_pos);
 }
 
-// every ancestor of permutation position `pos` passes the reference's exact box test at t_lim
+// Every ancestor of permutation position `pos` passes the reference's exact box test at
+// t_lim iff its leaf does: node boxes are unions of their triangles' float bounds, so an
+// ancestor box contains the leaf box, and the double slab test is monotone under box
+// inclusion (fl(lo' - o) <= fl(lo - o) for lo' <= lo, division by d keeps the order, so the
+// entry bound can only drop and the exit bound only rise).
 __device__ __forceinline__ bool static_cert(const SceneDev& S, const RayPre& r, float t_min, float t_lim,
                                             uint32_t pos) {
-    uint32_t ni = 0;
-    while (true) {
-        const float4 A = __ldg(&S.nodes[2 * ni]);
-        const float4 B = __ldg(&S.nodes[2 * ni + 1]);
-        const Box box{{A.x, A.y, A.z}, {B.x, B.y, B.z}};
-        if (!ray_box(r, t_min, t_lim, box)) return false;
-        const uint32_t a = __float_as_uint(A.w);
-        if (a & kLeafBit) return true;
-        ni = pos < __ldg(&S.split[ni]) ? a : __float_as_uint(B.w);
-    }
+    const uint32_t leaf = __ldg(&S.leaf_of[pos]);
+    const float4 A = __ldg(&S.nodes[2 * leaf]);
+    const float4 B = __ldg(&S.nodes[2 * leaf + 1]);
+    return ray_box(r, t_min, t_lim, Box{{A.x, A.y, A.z}, {B.x, B.y, B.z}});
 }
 
 // static part of intersect_scene with the reference's exact result

@@ -232,22 +232,15 @@ void Engine::upload_scene() {
         }
         d_stris_.alloc(sizeof(float4) * tris.size());
         PRX_CUDA(cudaMemcpy(d_stris_.get(), tris.data(), d_stris_.size(), cudaMemcpyHostToDevice));
-        // split[n]: first permutation position of an internal node's right subtree (the
-        // fast traversal's certificate walks the reference tree by position)
-        std::vector<uint32_t> tri_count(nn, 0), begin(nn, 0), split(nn, 0);
-        for (size_t k = nn; k-- > 0;) {  // children have larger indices (pre-order build)
-            const BvhNode& n = s.bvh_nodes[k];
-            tri_count[k] = n.count ? n.count : tri_count[n.left] + tri_count[n.first];
-        }
+        // leaf_of[k]: reference leaf holding permutation position k (the fast traversal's
+        // certificate tests that leaf's box; ancestors contain it, see device_scene.cuh)
+        std::vector<uint32_t> leaf_of(s.bvh_perm.size(), 0);
         for (size_t k = 0; k < nn; ++k) {
             const BvhNode& n = s.bvh_nodes[k];
-            if (n.count) continue;
-            begin[n.left] = begin[k];
-            begin[n.first] = begin[k] + tri_count[n.left];
-            split[k] = begin[n.first];
+            for (uint32_t i = 0; i < n.count; ++i) leaf_of[n.first + i] = static_cast<uint32_t>(k);
         }
-        d_split_.alloc(4 * nn);
-        PRX_CUDA(cudaMemcpy(d_split_.get(), split.data(), d_split_.size(), cudaMemcpyHostToDevice));
+        d_leaf_of_.alloc(4 * leaf_of.size());
+        PRX_CUDA(cudaMemcpy(d_leaf_of_.get(), leaf_of.data(), d_leaf_of_.size(), cudaMemcpyHostToDevice));
         // the fast traversal's own SAH tree over the triangles in reference order
         std::vector<Tri> ref_order(s.bvh_perm.size());
         for (size_t k = 0; k < ref_order.size(); ++k) ref_order[k] = s.static_tris[s.bvh_perm[k]];
@@ -409,7 +402,7 @@ SceneDev Engine::scene_dev() const {
     SceneDev S{};
     S.nodes = d_nodes_.as<float4>();
     S.n_nodes = static_cast<uint32_t>(scene_->bvh_nodes.size());
-    S.split = d_split_.as<uint32_t>();
+    S.leaf_of = d_leaf_of_.as<uint32_t>();
     S.cull_pad = 1e-5f * diag_ + 1e-6f;
     S.fast = cfg_.dfs_traversal ? 0 : 1;
     S.fnodes = d_fnodes_.as<float4>();

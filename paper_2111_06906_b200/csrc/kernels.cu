@@ -19,6 +19,9 @@ int launch_grid(uint64_t n, int threads) {
 namespace {
 
 constexpr int kT = 256;
+#ifndef PRX_TRACE_MINB
+#define PRX_TRACE_MINB 5  // resident CTAs per SM requested for the traversal kernels
+#endif
 
 __device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned long long v) {
 #pragma unroll
@@ -225,6 +228,29 @@ __device__ __forceinline__ uint32_t fetch_work(uint32_t* counter) {
     return base + rank;
 }
 
+// Batched refill for the persistent ray-granularity kernels: the warp stays converged at the
+// loop head; once at least PRX_REFILL lanes are idle (or nobody is working) the idle lanes
+// take consecutive queue slots with one atomic, so the state-load latency is paid once per
+// batch instead of once per lane.
+#ifndef PRX_REFILL
+#define PRX_REFILL 8
+#endif
+__device__ __forceinline__ bool refill_due(bool idle, bool working) {
+    const unsigned iw = __ballot_sync(0xffffffffu, idle);
+    const unsigned ww = __ballot_sync(0xffffffffu, working);
+    return iw != 0u && (__popc(iw) >= PRX_REFILL || ww == 0u);
+}
+// queue slot of this lane among the idle ones (>= queue length: exhausted)
+__device__ __forceinline__ uint32_t refill_slot(uint32_t* counter, bool idle) {
+    const unsigned iw = __ballot_sync(0xffffffffu, idle);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(iw) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(iw));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return base + (uint32_t)__popc(iw & ((1u << lane) - 1u));
+}
+
 // verify_path_error_based (engine.cpp:339-403): Alg. 1 walk over the flagged segments,
 // persistent: each lane walks one path at a time and advances its visibility ray one BVH
 // node per iteration, fetching the next flagged path as soon as its walk ends.
@@ -329,79 +355,97 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
     warp_add(&ctr->vis, vis);
 }
 
-// verify_path_error_based (engine.cpp:339-403), one path per thread with one-shot
-// intersect_scene queries (fast traversal + certificate).
-__global__ void __launch_bounds__(kT) k_verify_error_walk(SceneDev S, PathDev P, float threshold,
+// verify_path_error_based (engine.cpp:339-403) with one-shot intersect_scene queries (fast
+// traversal + certificate).  Persistent lanes at ray granularity: a lane skips its path's
+// unflagged segments, traces one visibility ray per iteration and fetches the next flagged
+// path as soon as its walk ends.
+__global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneDev S, PathDev P, float threshold,
                                                           const uint32_t* __restrict__ list,
                                                           const uint32_t* __restrict__ masks, const Counters* cnt,
-                                                          Counters* ctr) {
+                                                          uint32_t* work, Counters* ctr) {
     const FrameParams* fp = S.fp;
     const uint32_t n_list = (uint32_t)cnt->flagged;
     unsigned long long vis = 0;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_list; j += gridDim.x * blockDim.x) {
-        const uint32_t i = list[j];
-        const uint32_t flags = masks[j];
-        const uint32_t p = P.base + i;
-        const LightDev& L = fp->lights[light_of(fp, p)];
-        uchar4 m = P.meta[i];
-        const uint32_t k = m.x, segs = m.x + m.y;
-        const uint32_t epoch = P.epoch[i];
-        bool force = false;
-        uint32_t s = 0;
-        while (s < segs) {
-            const bool flagged = force || ((flags >> s) & 1u);
-            force = false;
-            if (!flagged) {
-                ++s;
-                continue;
+    uint32_t i = 0, flags = 0, p = 0, k = 0, segs = 0, epoch = 0, s = 0;
+    uchar4 m = make_uchar4(0, 0, 0, 0);
+    bool force = false, have = false, done = false;
+    while (true) {
+        if (refill_due(!have && !done, have)) {
+            const uint32_t j = refill_slot(work, !have && !done);
+            if (!have && !done) {
+                if (j >= n_list) {
+                    done = true;
+                } else {
+                    i = list[j];
+                    flags = masks[j];
+                    p = P.base + i;
+                    m = P.meta[i];
+                    k = m.x;
+                    segs = m.x + m.y;
+                    epoch = P.epoch[i];
+                    force = false;
+                    s = 0;
+                    have = true;
+                }
             }
-            const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, s - 1, i)]);
-            const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
-            ++vis;
-            Hit h;
-            const bool hit = intersect_scene(S, o, d, S.eps, h);
-            if (s == k) {  // escape segment: a new blocker -> retrace from here
-                if (hit) P.rstart[i] = (uint8_t)s;
-                break;
-            }
-            if (!hit) {  // destination gone: truncate and escape
-                truncate_path(P, i, s, true, m);
-                P.meta[i] = m;
-                break;
-            }
-            const size_t v = vix(P, s, i);
-            const float4 stored = P.energy[v];
-            const V3 e_prev = s == 0 ? L.flux_pp : ld3(P.energy[vix(P, s - 1, i)]);
-            const float4 am = __ldg(&S.mat[h.obj]);
-            const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
-            const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
-            if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
-                P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
-                P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
-                P.energy[v] = make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius);
-                const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
-                P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
-                P.rstart[i] = (uint8_t)(s + 1);
-                break;
-            }
-            const V3 old_pos = ld3(P.pos_obj[v]);
-            const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        if (!have) continue;
+        if (!force)
+            while (s < segs && !((flags >> s) & 1u)) ++s;
+        force = false;
+        if (s >= segs) {
+            have = false;
+            continue;
+        }
+        const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, s - 1, i)]);
+        const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
+        ++vis;
+        Hit h;
+        const bool hit = intersect_scene(S, o, d, S.eps, h);
+        have = false;  // every branch below ends the walk unless it continues explicitly
+        if (s == k) {  // escape segment: a new blocker -> retrace from here
+            if (hit) P.rstart[i] = (uint8_t)s;
+            continue;
+        }
+        if (!hit) {  // destination gone: truncate and escape
+            truncate_path(P, i, s, true, m);
+            P.meta[i] = m;
+            continue;
+        }
+        const size_t v = vix(P, s, i);
+        const float4 stored = P.energy[v];
+        const V3 e_prev = s == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[vix(P, s - 1, i)]);
+        const float4 am = __ldg(&S.mat[h.obj]);
+        const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
+        const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
+        if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
             P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
             P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
-            if (s + 1 >= segs) break;
-            const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
-            if (close_pos && !hit_dyn && !((flags >> (s + 1)) & 1u)) {
-                s += 2;
-                continue;
-            }
-            if (s + 1 < k) {
-                const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
-                const V3 od = normalized(sub(next, h.pos));
-                P.out_dir[v] = make_float4(od.x, od.y, od.z, 0.f);
-            }
-            force = true;
-            ++s;
+            P.energy[v] = make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius);
+            const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
+            P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
+            P.rstart[i] = (uint8_t)(s + 1);
+            continue;
         }
+        const V3 old_pos = ld3(P.pos_obj[v]);
+        const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
+        P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
+        P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+        if (s + 1 >= segs) continue;
+        have = true;
+        const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
+        if (close_pos && !hit_dyn && !((flags >> (s + 1)) & 1u)) {
+            s += 2;
+            continue;
+        }
+        if (s + 1 < k) {
+            const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
+            const V3 od = normalized(sub(next, h.pos));
+            P.out_dir[v] = make_float4(od.x, od.y, od.z, 0.f);
+        }
+        force = true;
+        ++s;
     }
     warp_add(&ctr->vis, vis);
 }
@@ -589,30 +633,51 @@ __global__ void k_retrace_flags(PathDev P, uint8_t* flags) {
         flags[i] = (P.meta[i].z == kLive && P.rstart[i] != kNoRetrace) ? 1 : 0;
 }
 
-// stage_trace's per-path bounce loop (engine.cpp:557-586): one path per thread.
-__global__ void __launch_bounds__(kT) k_trace(SceneDev S, PathDev P, const uint32_t* __restrict__ list,
+// stage_trace's per-path bounce loop (engine.cpp:557-586).  Persistent lanes at ray
+// granularity: each lane traces one bounce of its current path per iteration and fetches the
+// next queued path as soon as its own ends, so lanes whose paths escape early keep tracing
+// instead of idling until the warp's longest path is done.
+__global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_trace(SceneDev S, PathDev P, const uint32_t* __restrict__ list,
                                               const uint32_t* count, uint32_t* work, Counters* ctr) {
-    (void)work;
     const FrameParams* fp = S.fp;
     const uint32_t n = *count;
     unsigned long long traced = 0;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const uint32_t i = list[j];
-        const uint32_t p = P.base + i;
-        uchar4 m = P.meta[i];
-        const uint32_t epoch = P.epoch[i];
-        uint32_t b = P.rstart[i];
-        V3 pos = b == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, b - 1, i)]);
-        V3 dir = b == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, b - 1, i)]);
-        V3 energy = b == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[vix(P, b - 1, i)]);
-        bool escaped = false;
-        while (b < P.B) {
-            ++traced;
-            Hit h;
-            if (!intersect_scene(S, pos, dir, S.eps, h)) {
-                escaped = true;
-                break;
+    uint32_t i = 0, p = 0, epoch = 0, b = 0;
+    uchar4 m = make_uchar4(0, 0, 0, 0);
+    V3 pos{}, dir{}, energy{};
+    bool have = false, done = false;
+    while (true) {
+        if (refill_due(!have && !done, have)) {
+            const uint32_t j = refill_slot(work, !have && !done);
+            if (!have && !done) {
+                if (j >= n) {
+                    done = true;
+                } else {
+                    i = list[j];
+                    p = P.base + i;
+                    m = P.meta[i];
+                    epoch = P.epoch[i];
+                    b = P.rstart[i];
+                    pos = b == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, b - 1, i)]);
+                    dir = b == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, b - 1, i)]);
+                    energy = b == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[vix(P, b - 1, i)]);
+                    if (b >= P.B) {
+                        truncate_path(P, i, b, false, m);
+                        P.meta[i] = m;
+                    } else {
+                        have = true;
+                    }
+                }
             }
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        if (!have) continue;
+        ++traced;
+        Hit h;
+        bool escaped = false;
+        if (!intersect_scene(S, pos, dir, S.eps, h)) {
+            escaped = true;
+        } else {
             const float4 am = __ldg(&S.mat[h.obj]);
             energy = mulv(energy, V3{am.x, am.y, am.z});
             const size_t v = vix(P, b, i);
@@ -625,8 +690,11 @@ __global__ void __launch_bounds__(kT) k_trace(SceneDev S, PathDev P, const uint3
             dir = out;
             ++b;
         }
-        truncate_path(P, i, b, escaped, m);
-        P.meta[i] = m;
+        if (escaped || b >= P.B) {
+            truncate_path(P, i, b, escaped, m);
+            P.meta[i] = m;
+            have = false;
+        }
     }
     warp_add(&ctr->traced, traced);
 }
@@ -725,7 +793,8 @@ void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t*
                          const Counters* cnt, uint32_t* work, Counters* ctr, cudaStream_t st) {
     if (S.fast) {  // one-shot walks on the fast traversal
         static int grid = persistent_grid(k_verify_error_walk);
-        k_verify_error_walk<<<grid, kT, 0, st>>>(S, P, threshold, list, masks, cnt, ctr);
+        cudaMemsetAsync(work, 0, 4, st);
+        k_verify_error_walk<<<grid, kT, 0, st>>>(S, P, threshold, list, masks, cnt, work, ctr);
     } else {  // resumable reference-order traversal, persistent lanes
         static int grid = persistent_grid(k_verify_error);
         cudaMemsetAsync(work, 0, 4, st);
@@ -788,6 +857,7 @@ void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st) {
 void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count, uint32_t* work,
                   Counters* ctr, cudaStream_t st) {
     static int grid = persistent_grid(k_trace);
+    cudaMemsetAsync(work, 0, 4, st);
     k_trace<<<grid, kT, 0, st>>>(S, P, list, count, work, ctr);
     ++g_launches;
 }
