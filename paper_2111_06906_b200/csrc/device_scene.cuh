@@ -504,9 +504,11 @@ __device__ __forceinline__ bool trav_hit(const SceneDev& S, const Trav& T, Hit& 
 // The reference's Bvh::intersect (bvh.cpp:79-106) returns, among the triangles its left-first
 // DFS visits, the one with the smallest (t, permutation position) -- DFS order IS permutation
 // order.  If it visits the global (t, position)-minimum T*, that is its answer; it visits T*
-// iff every ancestor of T*'s leaf passes the exact box test at the t_max it has there, which
-// is > t* (a smaller t_max would need an earlier hit with t <= t*), so it suffices that each
-// ancestor passes at t_max = nextafter(t*) (the test is monotone in t_max).
+// iff every ancestor of T*'s leaf passes the exact box test at the t_max it has there.  That
+// t_max is the initial one or the t of a triangle found earlier, i.e. one with t > t* (an
+// earlier hit with t <= t* would precede T* lexicographically), so it is at least the smallest
+// accepted t above t*; the test is monotone in t_max, so it suffices that each ancestor passes
+// at any bound tc <= that value (fast_closest's t_cert; at worst nextafter(t*)).
 // static_fast finds T* with near-first ordering and conservative culling (boxes inflated by
 // cull_pad, t window widened); static_cert tests T*'s reference leaf with the exact test,
 // which implies every ancestor passes.  A ray whose certificate fails reruns the
@@ -546,13 +548,20 @@ __device__ __forceinline__ float cull_limit(float best_t) { return best_t + 1e-4
 // and keeps descending until every active lane of the warp holds a leaf, so triangle tests
 // run warp-wide.  The result is the order-independent lexicographic minimum, so neither
 // tree nor visit order matters.  kAny: stop at the first accepted triangle (any-hit).
+//
+// t_cert (closest mode) is a certificate bound: a value in (best_t, t_max] that does not exceed
+// the smallest t > best_t of any accepted triangle.  Every hit with t <= cull_limit(best_t) is
+// visited (culling only drops boxes entered beyond the limit at the time, which is larger),
+// and the leaf window tracks the smallest such t above best_t, so
+// min(that, cull_limit(best_t), t_max) is a valid bound.
 template <bool kAny>
 __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, const float4* __restrict__ tris,
                                              const RayPre& r, float t_min, float t_max, float& best_t,
-                                             uint32_t& best_pos) {
+                                             uint32_t& best_pos, float& t_cert) {
     constexpr uint32_t kNone = 0xFFFFFFFFu;
     best_t = t_max;
     best_pos = kNone;
+    float second = t_max;  // smallest accepted t strictly above best_t seen so far
     bool found = false;
     uint32_t stack[64];
     float stent[64];
@@ -609,14 +618,23 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
                 const float4 t2 = __ldg(&tris[3 * k + 2]);
                 const uint32_t pos = __float_as_uint(ta.w);
                 float t;
-                // window: (t_min, t_max) before the first hit, then t <= best_t (ties by position)
-                const float lim = found ? __uint_as_float(__float_as_uint(best_t) + 1u) : t_max;
+                // window: (t_min, t_max) before the first hit, then up to the cull limit
+                // (hits above best_t feed the certificate bound; ties go by position)
+                const float lim = found ? fminf(cull_limit(best_t), t_max) : t_max;
                 if (intersect_tri(r.o, r.d, t_min, lim, ld3(ta), ld3(t1), ld3(t2), t)) {
+                    if (kAny) {
+                        best_t = t;
+                        best_pos = pos;
+                        t_cert = t_max;
+                        return true;
+                    }
                     if (!found || t < best_t || (t == best_t && pos < best_pos)) {
+                        if (found && t < best_t) second = best_t;
                         best_t = t;
                         best_pos = pos;
                         found = true;
-                        if (kAny) return true;
+                    } else if (t > best_t && t < second) {
+                        second = t;
                     }
                 }
             }
@@ -627,12 +645,13 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
             }
         }
     }
+    t_cert = fminf(fminf(second, cull_limit(best_t)), t_max);
     return found;
 }
 
 __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, float t_min, float t_max,
-                                            float& best_t, uint32_t& best_pos) {
-    return fast_closest<false>(S.fnodes, S.ftris, r, t_min, t_max, best_t, best_pos);
+                                            float& best_t, uint32_t& best_pos, float& t_cert) {
+    return fast_closest<false>(S.fnodes, S.ftris, r, t_min, t_max, best_t, best_pos, t_cert);
 }
 
 // Every ancestor of permutation position `pos` passes the reference's exact box test at
@@ -653,10 +672,11 @@ __device__ __forceinline__ bool static_closest_exact(const SceneDev& S, const Ra
                                                      uint32_t& best) {
     if (S.n_nodes == 0) return false;
     if (!S.fast) return static_closest(S, r, t_min, t_max, best);
-    float bt;
+    float bt, tc;
     uint32_t bp;
-    if (!static_fast(S, r, t_min, t_max, bt, bp)) return false;
-    if (static_cert(S, r, t_min, __uint_as_float(__float_as_uint(bt) + 1u), bp)) {
+    if (!static_fast(S, r, t_min, t_max, bt, bp, tc)) return false;
+    // the reference visits T*'s leaf with a t_max >= tc (see fast_closest)
+    if (static_cert(S, r, t_min, tc, bp)) {
         t_max = bt;
         best = bp;
         return true;
@@ -670,9 +690,9 @@ __device__ __forceinline__ bool static_closest_exact(const SceneDev& S, const Ra
 __device__ __forceinline__ bool static_any_exact(const SceneDev& S, const RayPre& r, float t_min, float t_max) {
     if (S.n_nodes == 0) return false;
     if (!S.fast) return static_any(S, r, t_min, t_max);
-    float bt;
+    float bt, tc;
     uint32_t bp;
-    if (!fast_closest<true>(S.fnodes, S.ftris, r, t_min, t_max, bt, bp)) return false;
+    if (!fast_closest<true>(S.fnodes, S.ftris, r, t_min, t_max, bt, bp, tc)) return false;
     if (static_cert(S, r, t_min, t_max, bp)) return true;
     return static_any(S, r, t_min, t_max);
 }
@@ -700,22 +720,23 @@ __device__ __forceinline__ int dyn_closest_seq(const SceneDev& S, const RayPre& 
 // (t, object, index)-lexicographic minimum over all dynamic triangles with t in (t_min, t_max):
 // an object replaces the running winner only with a strictly smaller t, and triangle order
 // inside an object breaks ties.  With gates, let (t*, j*, i*) be that minimum: every object
-// before j* holds only hits with t > t*, so when j* is reached the running t_max exceeds t*,
-// and if j*'s gate passes at nextafter(t*) it passes there too (the test is monotone in
-// t_max); later objects cannot beat t* strictly.  So the minimum, found by one walk over the
-// combined LBVH (global index order == (object, index) order), is the reference's answer
-// whenever its object's gate passes at nextafter(t*); otherwise rerun the sequential loop.
+// before j* holds only hits with t > t*, so when j* is reached the running t_max is at least
+// min(t_max, smallest dynamic hit above t*) >= tc (fast_closest's certificate bound), and if
+// j*'s gate passes at tc it passes there too (the test is monotone in t_max); later objects
+// cannot beat t* strictly.  So the minimum, found by one walk over the combined LBVH (global
+// index order == (object, index) order), is the reference's answer whenever its object's
+// gate passes at tc; otherwise rerun the sequential loop.
 __device__ __forceinline__ int dyn_closest_exact(const SceneDev& S, const RayPre& r, float t_min, float& t_max,
                                                  uint32_t& dj, uint32_t& dtri) {
     const FrameParams* fp = S.fp;
     if (fp->n_dyn == 0) return -1;
     if (!S.fast || !S.dfast) return dyn_closest_seq(S, r, t_min, t_max, dj, dtri);
-    float bt;
+    float bt, tc;
     uint32_t g;
-    if (!fast_closest<false>(S.danodes, S.datris, r, t_min, t_max, bt, g)) return -1;
+    if (!fast_closest<false>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc)) return -1;
     const uint32_t j = __ldg(&S.dtri_obj[g]);
     const DynObj& D = fp->dyn[j];
-    if (ray_box(r, t_min, __uint_as_float(__float_as_uint(bt) + 1u), D.cur)) {
+    if (ray_box(r, t_min, tc, D.cur)) {
         t_max = bt;
         dj = j;
         dtri = g - D.tri_begin;
@@ -765,9 +786,9 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
     const FrameParams* fp = S.fp;
     if (fp->n_dyn == 0) return false;
     if (S.fast && S.dfast) {
-        float bt;
+        float bt, tc;
         uint32_t g;
-        if (!fast_closest<true>(S.danodes, S.datris, r, t_min, t_max, bt, g)) return false;
+        if (!fast_closest<true>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc)) return false;
         if (ray_box(r, t_min, t_max, fp->dyn[__ldg(&S.dtri_obj[g])].cur)) return true;
     }
     for (uint32_t j = 0; j < fp->n_dyn; ++j) {
