@@ -71,7 +71,7 @@ static __device__ __noinline__ bool quot_cmp_const(double N, float d, float c, b
 // t_min and the entry quotients, upper ones t_max and the exit quotients; a pair the float
 // values settle is skipped, a float-vs-quotient pair is settled exactly by quot_cmp_const,
 // and a quotient-vs-quotient pair falls back to the reference's double test.
-static __device__ __noinline__ bool ray_box_refine(const RayPre& r, float t_min, float t_max, const Box& b) {
+static __device__ __noinline__ bool ray_box_refine(const RayPre r, float t_min, float t_max, const Box b) {
     float fn[3], ff[3];  // the float entry / exit quotients of ray_box
     for (int a = 0; a < 3; ++a) {
         const float da = comp(r.d, a), oa = comp(r.o, a);
@@ -541,6 +541,18 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
 
 __device__ __forceinline__ float cull_limit(float best_t) { return best_t + 1e-4f * fabsf(best_t) + 1e-6f; }
 
+#ifndef PRX_SHORT_STACK
+#define PRX_SHORT_STACK 12
+#endif
+constexpr int kShortStack = PRX_SHORT_STACK;
+constexpr int kMaxBlock = 256;  // every kernel that traverses launches <= 256 threads per block
+
+// this thread's column of the block's shared short stack (entry k at [k * blockDim.x])
+__device__ __forceinline__ uint2* trav_short_stack() {
+    __shared__ uint2 s_stack[kShortStack * kMaxBlock];
+    return s_stack + threadIdx.x;
+}
+
 // global (t, position)-minimum over the triangles of a fast tree with t in (t_min, t_max).
 // Static: the SAH tree (fast_bvh.cpp), position = reference permutation position; dynamic:
 // the combined LBVH (lbvh.cu), position = global dynamic triangle index.  While-while
@@ -563,15 +575,27 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
     best_pos = kNone;
     float second = t_max;  // smallest accepted t strictly above best_t seen so far
     bool found = false;
-    uint32_t stack[64];
-    float stent[64];
+    // traversal stack {node, entry t}: the top kShortStack entries live in shared memory
+    // (per-thread column, conflict-free), deeper ones in a local overflow array that the
+    // usual traversal never touches -- a 64-deep local stack per thread would exceed L1 and
+    // L2 at full occupancy and stream to DRAM.
+    uint2* const ss = trav_short_stack();
+    const uint32_t stride = blockDim.x;
+    uint2 overflow[64 - kShortStack];
     int sp = 0;
     uint32_t node = 0;  // the root is always an internal node
     uint32_t leaf = kNone;
+    auto push = [&](uint32_t c, float ent) {
+        const uint2 e = make_uint2(c, __float_as_uint(ent));
+        if (sp < kShortStack) ss[sp * stride] = e;
+        else overflow[sp - kShortStack] = e;
+        ++sp;
+    };
     auto pop = [&]() -> uint32_t {
         while (sp > 0) {
             --sp;
-            if (stent[sp] <= cull_limit(best_t)) return stack[sp];
+            const uint2 e = sp < kShortStack ? ss[sp * stride] : overflow[sp - kShortStack];
+            if (__uint_as_float(e.y) <= cull_limit(best_t)) return e.x;
         }
         return kNone;
     };
@@ -590,14 +614,10 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
             } else if (tl == INFINITY) {
                 node = c1;
             } else if (tl <= tr) {
-                stack[sp] = c1;
-                stent[sp] = tr;
-                ++sp;
+                push(c1, tr);
                 node = c0;
             } else {
-                stack[sp] = c0;
-                stent[sp] = tl;
-                ++sp;
+                push(c0, tl);
                 node = c1;
             }
             if (node != kNone && (node & kLeafBit) && leaf == kNone) {  // park the leaf
