@@ -285,6 +285,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    xfer0 = eng.transfer_bytes()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         if world > 1:  # sharded frame + reduced image read back to the host
@@ -294,13 +295,16 @@ def main():
             eng.run_frame()
             eng.splat(radius=0.25, mode=args.splat_mode)
     e2e_s = time.perf_counter() - t0
+    xfer1 = eng.transfer_bytes()
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = n_paths * args.steps / e2e_s
-    h2d = 4 + 16 * 4 + 40 * 128 + 24 * 128 + 176 * 16 + 32 * 128  # FrameParams + transforms
-    d2h = 12 * cam.width * cam.height + 96 + 32 + 8 * 21
+    # bytes the engine itself copied per step (counted inside the library), plus the reduced
+    # image read back by torch on the sharded path
+    h2d = (xfer1[0] - xfer0[0]) // args.steps
+    d2h = (xfer1[1] - xfer0[1]) // args.steps + (12 * cam.width * cam.height if world > 1 else 0)
 
     # roofline of the dominant kernel stage (trace): algorithmic bytes per traced segment =
     # 64 B written (4 x float4 vertex streams) + 64 B per retraced path start (meta, rstart,

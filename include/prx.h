@@ -305,6 +305,10 @@ prx_status prx_engine_set_frame_counter(prx_engine* engine, int32_t frames_run);
 /* Number of kernel launches issued by this engine since creation (bench evidence). */
 uint64_t prx_engine_launch_count(const prx_engine* engine);
 
+/* Bytes this engine copied host->device and device->host since creation (every frame,
+ * splat and field transfer is counted; scene upload at creation is included). */
+prx_status prx_engine_transfer_bytes(const prx_engine* engine, uint64_t* h2d, uint64_t* d2h);
+
 const char* prx_last_error(void);
 int prx_abi_version(void);
 

@@ -167,6 +167,7 @@ SIGNATURES = [
     ("prx_engine_upload", C.c_int, [P, C.c_int, C.c_uint32, P, C.c_size_t]),
     ("prx_engine_set_frame_counter", C.c_int, [P, C.c_int32]),
     ("prx_engine_launch_count", C.c_uint64, [P]),
+    ("prx_engine_transfer_bytes", C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("prx_last_error", C.c_char_p, []),
     ("prx_abi_version", C.c_int, []),
 ]

@@ -299,4 +299,8 @@ uint64_t prx_engine_launch_count(const prx_engine* engine) {
     return engine ? engine->engine->launches() : 0;
 }
 
+prx_status prx_engine_transfer_bytes(const prx_engine* engine, uint64_t* h2d, uint64_t* d2h) {
+    return guarded([&] { eng(const_cast<prx_engine*>(engine)).transfer_bytes(h2d, d2h); });
+}
+
 }  // extern "C"

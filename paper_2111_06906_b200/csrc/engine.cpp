@@ -495,7 +495,7 @@ void Engine::fill_frame_params() {
         L.dm_c = b.dm_c.as<uint32_t>();
     }
     fp.n_dyn = static_cast<uint32_t>(dyn_.size());
-    PRX_CUDA(cudaMemcpyAsync(d_fp_.get(), h_fp_, sizeof(FrameParams), cudaMemcpyHostToDevice, stream_));
+    copy_async(d_fp_.get(), h_fp_, sizeof(FrameParams), cudaMemcpyHostToDevice);
 }
 
 // state_at (scene.cpp:115-134) on the host: every dynamic object's descriptor and current
@@ -538,8 +538,7 @@ void Engine::place_dynamics(bool force) {
         h_xf_[2 * j + 1] = float4{now.trans.x, now.trans.y, now.trans.z, now.scale};
     }
     if (!changed) return;
-    PRX_CUDA(cudaMemcpyAsync(d_dyn_xf_.get(), h_xf_, sizeof(float4) * 2 * dyn_.size(),
-                             cudaMemcpyHostToDevice, stream_));
+    copy_async(d_dyn_xf_.get(), h_xf_, sizeof(float4) * 2 * dyn_.size(), cudaMemcpyHostToDevice);
     launch_transform_dynamic(d_dyn_local_.as<float4>(), d_dyn_tri_xf_.as<uint32_t>(),
                              d_dyn_xf_.as<float4>(), n_dyn_tris_, d_dyn_world_.as<float4>(), stream_);
     if (n_dyn_tris_ >= 2)
@@ -547,6 +546,12 @@ void Engine::place_dynamics(bool force) {
                            h_fp_->dyn, static_cast<uint32_t>(dyn_.size()),
                            reinterpret_cast<const DynObj*>(d_fp_.as<char>() + offsetof(FrameParams, dyn)),
                            n_lbvh_nodes_ ? d_lbvh_nodes_.as<float4>() : nullptr, d_lbvh_leaf_.as<uint32_t>(), lbvh_, stream_);
+}
+
+void Engine::copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    PRX_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, stream_));
+    if (kind == cudaMemcpyHostToDevice) h2d_bytes_ += bytes;
+    if (kind == cudaMemcpyDeviceToHost) d2h_bytes_ += bytes;
 }
 
 // ----------------------------------------------------------------------- stages
@@ -711,8 +716,8 @@ void Engine::stage_trace() {
 }
 
 void Engine::read_back(prx_frame_stats* st, bool with_times) {
-    PRX_CUDA(cudaMemcpyAsync(h_ctr_, d_ctr_.get(), sizeof(Counters), cudaMemcpyDeviceToHost, stream_));
-    PRX_CUDA(cudaMemcpyAsync(h_cnt32_, d_cnt32_.get(), 4 * kCntN, cudaMemcpyDeviceToHost, stream_));
+    copy_async(h_ctr_, d_ctr_.get(), sizeof(Counters), cudaMemcpyDeviceToHost);
+    copy_async(h_cnt32_, d_cnt32_.get(), 4 * kCntN, cudaMemcpyDeviceToHost);
     PRX_CUDA(cudaStreamSynchronize(stream_));
     PRX_CUDA(cudaGetLastError());
     n_pruned_ = h_cnt32_[kCntPruned];
@@ -824,7 +829,7 @@ void Engine::prune_apply(const uint32_t* const* prefix_dev, const uint32_t* cons
         tab[PRX_MAX_LIGHTS + li] = total_dev[li];
     }
     uint32_t** dtab = d_light_ptrs_.as<uint32_t*>() + 2 * PRX_MAX_LIGHTS;
-    PRX_CUDA(cudaMemcpyAsync(dtab, tab.data(), sizeof(uint32_t*) * tab.size(), cudaMemcpyHostToDevice, stream_));
+    copy_async(dtab, tab.data(), sizeof(uint32_t*) * tab.size(), cudaMemcpyHostToDevice);
     prune_trim_all(dtab, dtab + PRX_MAX_LIGHTS, total_dev);
     read_back(st, false);
 }
@@ -888,7 +893,7 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
                  d_splat_work_.get(), d_splat_cand_.get(), mode, d_gather_.get(), stream_);
     record(kEvSplat1);
     if (rgb_host)
-        PRX_CUDA(cudaMemcpyAsync(rgb_host, out, 12ull * npx, cudaMemcpyDeviceToHost, stream_));
+        copy_async(rgb_host, out, 12ull * npx, cudaMemcpyDeviceToHost);
     PRX_CUDA(cudaStreamSynchronize(stream_));
     PRX_CUDA(cudaGetLastError());
     launches_ = g_launches - launch_base_;
@@ -968,7 +973,7 @@ void Engine::download(int field, uint32_t index, void* dst, size_t bytes) {
         case PRX_FIELD_PRUNED: src = d_pruned_list_.get(); break;
         default: throw std::invalid_argument("unknown field");
     }
-    PRX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_));
+    copy_async(dst, src, bytes, cudaMemcpyDeviceToHost);
     PRX_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -982,7 +987,7 @@ void Engine::upload(int field, uint32_t index, const void* src, size_t bytes) {
         case PRX_FIELD_PHOTONS:
         case PRX_FIELD_AUX: {
             tmp.alloc(bytes);
-            PRX_CUDA(cudaMemcpyAsync(tmp.get(), src, bytes, cudaMemcpyHostToDevice, stream_));
+            copy_async(tmp.get(), src, bytes, cudaMemcpyHostToDevice);
             if (field == PRX_FIELD_PHOTONS) launch_unpack_photons(path_dev(), tmp.get(), nullptr, stream_);
             else launch_unpack_photons(path_dev(), nullptr, tmp.get(), stream_);
             PRX_CUDA(cudaStreamSynchronize(stream_));
@@ -1006,7 +1011,7 @@ void Engine::upload(int field, uint32_t index, const void* src, size_t bytes) {
         case PRX_FIELD_PRUNED: throw std::invalid_argument("upload: the pruned list is read-only");
         default: throw std::invalid_argument("unknown field");
     }
-    PRX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
+    copy_async(dst, src, bytes, cudaMemcpyHostToDevice);
     PRX_CUDA(cudaStreamSynchronize(stream_));
 }
 

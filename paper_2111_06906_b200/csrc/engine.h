@@ -87,8 +87,17 @@ public:
     void synchronize();
     void info(prx_engine_info* out) const;
     uint64_t launches() const { return launches_; }
+    // bytes moved host->device / device->host by this engine since creation
+    void transfer_bytes(uint64_t* h2d, uint64_t* d2h) const {
+        if (h2d) *h2d = h2d_bytes_;
+        if (d2h) *d2h = d2h_bytes_;
+    }
 
 private:
+    // every host<->device copy of the frame/splat/field paths goes through here (counted)
+    void copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
+    uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+
     struct LightBlock {
         const Light* light = nullptr;
         uint32_t begin = 0, end = 0;  // global path range

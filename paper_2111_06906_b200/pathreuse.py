@@ -250,6 +250,12 @@ class Engine:
     def launch_count(self) -> int:
         return int(L.lib().prx_engine_launch_count(self._h))
 
+    def transfer_bytes(self) -> tuple:
+        """(host->device, device->host) bytes this engine has copied since creation."""
+        h2d, d2h = C.c_uint64(0), C.c_uint64(0)
+        L.check(L.lib().prx_engine_transfer_bytes(self._h, C.byref(h2d), C.byref(d2h)))
+        return int(h2d.value), int(d2h.value)
+
     def download(self, field: str, index: int = 0) -> np.ndarray:
         fid = L.FIELD[field]
         nbytes = L.lib().prx_field_bytes(self._h, fid, int(index))
