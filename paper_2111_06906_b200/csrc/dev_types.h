@@ -68,13 +68,14 @@ struct SceneDev {
     const float4* datris;      // dynamic tris in combined-leaf order: {a, global idx} {e1, obj j} {e2, -}
     const uint32_t* dtri_obj;  // global dynamic triangle -> dynamic object j
     const float4* mat;         // per object {albedo, glossy exponent}
-    const uint32_t* oflags;    // per object: bit0 dynamic, bit1 glossy
+    const uint32_t* oflags;    // per object: bit0 dynamic, bit1 glossy, bit2 exact pow table, bits8+ its slot
     const FrameParams* fp;
     float eps;                 // engine.cpp:74
     float two_diag;            // engine.cpp:138
     uint64_t seed_mix;         // mix64(seed) (rng.hpp:36)
     float gather_radius;
     const float2* trig;        // exact cos/sin of 2*pi*k/2^24 from the host libm (or null)
+    const float* const* pow_tabs;  // exact powf(k*2^-24, 1/(e+1)) per glossy exponent slot
 };
 
 // Per-path and per-vertex device state of one engine (one shard).  Vertex arrays are

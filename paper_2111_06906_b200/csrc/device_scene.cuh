@@ -843,9 +843,10 @@ __device__ __forceinline__ V3 cosine_sample(const SceneDev& S, V3 normal, float 
 
 // phong_lobe_sample (engine.cpp:34-42) -- glossy only (device powf: tolerance class C)
 __device__ __forceinline__ V3 phong_sample(const SceneDev& S, V3 mirror, float exponent, float u1,
-                                           uint32_t k2) {
+                                           uint32_t k1, uint32_t k2, uint32_t flags) {
     const float u2 = (float)k2 * 5.9604644775390625e-8f;
-    const float cos_theta = powf(u1, 1.0f / (exponent + 1.0f));
+    // host-libm powf by table lookup (bit-exact) when the engine built the table
+    const float cos_theta = (flags & 4u) ? __ldg(&S.pow_tabs[flags >> 8][k1]) : powf(u1, 1.0f / (exponent + 1.0f));
     const float sin_theta = sqrtf(fmax_std(0.0f, 1.0f - cos_theta * cos_theta));
     float cphi, sphi;
     if (S.trig) {
@@ -865,13 +866,14 @@ __device__ __forceinline__ V3 phong_sample(const SceneDev& S, V3 mirror, float e
 // Engine::sample_bounce (engine.cpp:159-170)
 __device__ __forceinline__ V3 sample_bounce(const SceneDev& S, uint32_t obj, V3 normal, V3 incoming,
                                             uint32_t path, uint32_t epoch, uint32_t bounce_key) {
-    const float u1 = rng_uniform_m(S.seed_mix, path, epoch, bounce_key, kBounceDir, 0);
+    const uint32_t k1 = rng_u24_m(S.seed_mix, path, epoch, bounce_key, kBounceDir, 0);
+    const float u1 = (float)k1 * 5.9604644775390625e-8f;  // rng_uniform (rng.hpp:45-49)
     const uint32_t k2 = rng_u24_m(S.seed_mix, path, epoch, bounce_key, kBounceDir, 1);
     const uint32_t flags = __ldg(&S.oflags[obj]);
     if (!(flags & 2u)) return cosine_sample(S, normal, u1, k2);
     const float4 m = __ldg(&S.mat[obj]);
     const V3 mirror = normalized(sub(incoming, mul(normal, 2.0f * dot(incoming, normal))));
-    V3 out = phong_sample(S, mirror, m.w, u1, k2);
+    V3 out = phong_sample(S, mirror, m.w, u1, k1, k2, flags);
     if (dot(out, normal) <= 0.0f) out = mirror;
     return out;
 }

@@ -60,6 +60,46 @@ float f_of_u(uint32_t u) {
 
 }  // namespace
 
+// ----------------------------------------------------------------------- exact pow tables
+// phong_lobe_sample (engine.cpp:34-42) raises the 24-bit uniform u1 = k * 2^-24 to
+// 1 / (exponent + 1) with the host libm's powf (std::pow(float, float)).  One table of all
+// 2^24 results per distinct glossy exponent (64 MB each) makes glossy bounces bit-identical
+// to the reference on the same host libm, like the trig table does for cosine_sample.
+const float* exact_pow_table(int device, float exponent) {
+    static std::mutex mu;
+    static std::map<std::pair<int, uint32_t>, float*> dev;
+    uint32_t bits;
+    std::memcpy(&bits, &exponent, 4);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = dev.find({device, bits});
+    if (it != dev.end()) return it->second;
+    constexpr uint32_t kN = 1u << 24;
+    std::vector<float> host(kN);
+    const float inv = 1.0f / (exponent + 1.0f);
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        th.emplace_back([t, nt, inv, &host] {
+            const uint32_t lo = static_cast<uint32_t>((uint64_t)kN * t / nt);
+            const uint32_t hi = static_cast<uint32_t>((uint64_t)kN * (t + 1) / nt);
+            for (uint32_t k = lo; k < hi; ++k) {
+                const float u1 = static_cast<float>(k) * 0x1.0p-24f;
+                host[k] = std::pow(u1, inv);
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    int prev = 0;
+    PRX_CUDA(cudaGetDevice(&prev));
+    PRX_CUDA(cudaSetDevice(device));
+    float* d = nullptr;
+    PRX_CUDA(cudaMalloc(&d, sizeof(float) * kN));
+    PRX_CUDA(cudaMemcpy(d, host.data(), sizeof(float) * kN, cudaMemcpyHostToDevice));
+    PRX_CUDA(cudaSetDevice(prev));
+    dev[{device, bits}] = d;
+    return d;
+}
+
 // ----------------------------------------------------------------------- exact trig table
 // cosine_sample draws phi = fl(2*pi_f) * (k * 2^-24) and evaluates cos/sin with the host
 // libm (sincosf after GCC's sin/cos CSE).  The device looks the pair up by k, so bounce
@@ -268,10 +308,26 @@ void Engine::upload_scene() {
     // materials / flags
     std::vector<float4> mat(s.objects.size());
     std::vector<uint32_t> flags(s.objects.size());
+    std::vector<const float*> pow_tabs;  // one exact pow table per distinct glossy exponent
+    std::vector<float> pow_exps;
     for (size_t i = 0; i < s.objects.size(); ++i) {
         const Object& o = s.objects[i];
         mat[i] = f4(o.material.albedo, o.material.glossy_exponent);
         flags[i] = (o.dynamic ? 1u : 0u) | (o.material.kind == PRX_MATERIAL_GLOSSY ? 2u : 0u);
+        if (o.material.kind == PRX_MATERIAL_GLOSSY && cfg_.exact_trig >= 0) {
+            const float e = o.material.glossy_exponent;
+            size_t slot = 0;
+            while (slot < pow_exps.size() && std::memcmp(&pow_exps[slot], &e, 4) != 0) ++slot;
+            if (slot == pow_exps.size()) {
+                pow_exps.push_back(e);
+                pow_tabs.push_back(exact_pow_table(device_, e));
+            }
+            flags[i] |= 4u | (static_cast<uint32_t>(slot) << 8);  // bit2: exact pow table at slot
+        }
+    }
+    if (!pow_tabs.empty()) {
+        d_pow_tabs_.alloc(sizeof(const float*) * pow_tabs.size());
+        PRX_CUDA(cudaMemcpy(d_pow_tabs_.get(), pow_tabs.data(), d_pow_tabs_.size(), cudaMemcpyHostToDevice));
     }
     d_mat_.alloc(sizeof(float4) * mat.size());
     d_oflags_.alloc(4 * flags.size());
@@ -423,6 +479,7 @@ SceneDev Engine::scene_dev() const {
     S.seed_mix = seed_mix_;
     S.gather_radius = cfg_.gather_radius;
     S.trig = d_trig_;
+    S.pow_tabs = d_pow_tabs_.as<const float*>();
     return S;
 }
 

@@ -155,7 +155,7 @@ private:
     uint32_t n_dyn_tris_ = 0, n_lbvh_nodes_ = 0;
 
     // scene device data
-    DevBuf d_nodes_, d_leaf_of_, d_fnodes_, d_ftris_, d_stris_, d_mat_, d_oflags_, d_dyn_local_, d_dyn_world_, d_dyn_xf_, d_dyn_tri_xf_,
+    DevBuf d_pow_tabs_, d_nodes_, d_leaf_of_, d_fnodes_, d_ftris_, d_stris_, d_mat_, d_oflags_, d_dyn_local_, d_dyn_world_, d_dyn_xf_, d_dyn_tri_xf_,
         d_lbvh_nodes_, d_lbvh_leaf_, d_lbvh_work_, d_dall_nodes_, d_dall_tris_;
     LbvhBuffers lbvh_{};
     const float2* d_trig_ = nullptr;
