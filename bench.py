@@ -118,6 +118,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) of one steady-state launch of `kernel` from the newest
+    committed ncu --set full summary (profiles/rNN_traffic.json, C4 workload), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        try:
+            with open(f) as fh:
+                k = json.load(fh)["kernels"].get(kernel)
+            if k:
+                return float(k["dram_bytes"]), os.path.relpath(f, os.path.dirname(os.path.abspath(__file__)))
+        except (OSError, ValueError, KeyError):
+            continue
+    return None, None
+
+
 def peaks():
     try:
         with open(PEAKS_FILE) as f:
@@ -312,9 +328,11 @@ def main():
     hbm, peak_src = peaks()
     trace_bytes = traced * 64 + retraced * 64
     achieved = trace_bytes / (trace_ms * 1e-3) / 1e9 if trace_ms > 0 else 0.0
+    traffic, traffic_src = ncu_traffic("k_trace") if name == "C4" else (None, None)
     roofline = {"bound": "hbm", "kernel": "k_trace (stage_trace: compaction + trace + finalize)",
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "peak_source": peak_src,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": trace_bytes, "peak_source": peak_src,
                 "note": "traversal is latency/issue-bound: BVH reads are implementation-defined "
                         "and not in the algorithmic bytes"}
 

@@ -418,7 +418,7 @@ public:
     const std::vector<uint32_t>& segment_flags() const { return u32(PRX_FIELD_SEGMENT_FLAGS, flags_); }
     prx_engine* native() const { return engine_.get(); }
 
-private:
+    // prx_frame_stats -> FrameStats (also used by read_stats_csv)
     static FrameStats convert(const prx_frame_stats& s) {
         FrameStats f;
         f.frame = s.frame;
@@ -435,8 +435,11 @@ private:
         f.t_prune = s.t_prune;
         f.t_fill = s.t_fill;
         f.t_trace = s.t_trace;
+        f.t_gather = s.t_gather;
         return f;
     }
+
+private:
     void refresh_info() { detail::check(prx_engine_get_info(engine_.get(), &info_)); }
     void invalidate() {
         refresh_info();
@@ -501,6 +504,100 @@ inline Image gather_image(const Engine& engine, const Camera& cam, float radius,
     const prx_camera c{detail::v(cam.position), detail::v(cam.look_at), cam.fov_deg, cam.width, cam.height};
     detail::check(prx_splat(engine.native(), &c, radius, 1, img.pixels.data(), nullptr, nullptr));
     return img;
+}
+
+// ---------------------------------------------------------------- scene documents (scene.hpp)
+namespace detail {
+inline Scene adopt(prx_scene* h) {
+    Scene s;
+    s.handle = own(h);
+    load_view(s);
+    return s;
+}
+inline prx_frame_stats to_prx(const FrameStats& f) {
+    prx_frame_stats s{};
+    s.frame = f.frame;
+    s.mode = static_cast<int32_t>(f.mode);
+    s.rays_traced = f.rays_traced;
+    s.rays_reused = f.rays_reused;
+    s.paths_replaced = f.paths_replaced;
+    s.paths_pruned = f.paths_pruned;
+    s.paths_filled = f.paths_filled;
+    s.visibility_rays = f.visibility_rays;
+    s.t_update = f.t_update;
+    s.t_occlusion = f.t_occlusion;
+    s.t_dm = f.t_dm;
+    s.t_prune = f.t_prune;
+    s.t_fill = f.t_fill;
+    s.t_trace = f.t_trace;
+    s.t_gather = f.t_gather;
+    return s;
+}
+inline std::vector<prx_frame_stats> to_prx(const std::vector<FrameStats>& rows) {
+    std::vector<prx_frame_stats> v;
+    for (const FrameStats& r : rows) v.push_back(to_prx(r));
+    return v;
+}
+}  // namespace detail
+
+// load_scene_text / load_scene / load_scene_source (scene.cpp:272-398)
+inline Scene load_scene_text(const std::string& json_text, const std::string& base_dir = "") {
+    prx_scene* h = nullptr;
+    detail::check(prx_scene_load_text(json_text.c_str(), base_dir.c_str(), &h));
+    return detail::adopt(h);
+}
+inline Scene load_scene_source(const std::string& source) {
+    prx_scene* h = nullptr;
+    detail::check(prx_scene_load(source.c_str(), &h));
+    return detail::adopt(h);
+}
+inline Scene load_scene(const std::string& path) { return load_scene_source(path); }
+
+// ---------------------------------------------------------------- offline artefacts
+// write_image / frame_image_name (gather.hpp)
+inline void write_image(const Image& image, const std::string& path) {
+    detail::check(prx_image_write_ppm(path.c_str(), image.pixels.data(), image.width, image.height));
+}
+inline std::string frame_image_name(int frame) {
+    char buf[64];
+    prx_frame_image_name(frame, buf, sizeof(buf));
+    return buf;
+}
+// write_photon_dump / read_photon_dump (photon_store.hpp)
+inline void write_photon_dump(const PhotonMap& map, const std::string& path) {
+    detail::check(prx_photon_dump_write(path.c_str(), map.n_paths(), map.max_bounces(), map.records().data(),
+                                        map.records().size() * sizeof(Photon)));
+}
+inline PhotonMap read_photon_dump(const std::string& path) {
+    uint32_t n = 0, b = 0;
+    detail::check(prx_photon_dump_read(path.c_str(), &n, &b, nullptr, 0));
+    PhotonMap map(n, b);
+    detail::check(prx_photon_dump_read(path.c_str(), &n, &b, map.records().data(),
+                                       map.records().size() * sizeof(Photon)));
+    return map;
+}
+// write_stats_csv / read_stats_csv / reuse_report (stats.hpp)
+inline void write_stats_csv(const std::vector<FrameStats>& rows, const std::string& path) {
+    const std::vector<prx_frame_stats> v = detail::to_prx(rows);
+    detail::check(prx_stats_csv_write(path.c_str(), v.data(), v.size()));
+}
+inline std::vector<FrameStats> read_stats_csv(const std::string& path) {
+    size_t n = 0;
+    detail::check(prx_stats_csv_read(path.c_str(), nullptr, 0, &n));
+    std::vector<prx_frame_stats> v(n);
+    detail::check(prx_stats_csv_read(path.c_str(), v.data(), v.size(), &n));
+    std::vector<FrameStats> out;
+    for (const prx_frame_stats& s : v) out.push_back(Engine::convert(s));
+    return out;
+}
+inline std::string reuse_report(const std::vector<FrameStats>& rows) {
+    const std::vector<prx_frame_stats> v = detail::to_prx(rows);
+    size_t n = 0;
+    detail::check(prx_reuse_report(v.data(), v.size(), nullptr, 0, &n));
+    std::string text(n + 1, '\0');
+    detail::check(prx_reuse_report(v.data(), v.size(), text.data(), text.size(), &n));
+    text.resize(n);
+    return text;
 }
 
 }  // namespace pathreuse

@@ -210,6 +210,11 @@ void prx_memory_footprint(uint64_t n_paths, uint32_t max_bounces, const uint32_t
 prx_status prx_scene_create(const prx_scene_desc* desc, prx_scene** out);
 /* make_builtin_scene (scene.cpp:603-611); names as in builtin_scenes() (module.cpp:57-61). */
 prx_status prx_scene_builtin(const char* name, prx_scene** out);
+/* Scene documents, scene.cpp:272-398 (load_scene_text / load_scene / load_scene_source):
+ * JSON with inline meshes or OBJ files (relative to the document's directory);
+ * `source` is "builtin:NAME", a builtin name, or a path.  PRX_E_SCENE on bad input. */
+prx_status prx_scene_load(const char* source, prx_scene** out);
+prx_status prx_scene_load_text(const char* json_text, const char* base_dir, prx_scene** out);
 /* Procedural BASELINE configurations: "C1".."C5" plus parameters
  * (0 = default): C5 uses n_dynamic objects; tri_scale scales static tessellation.   */
 prx_status prx_scene_synthetic(const char* name, uint32_t n_dynamic, float tri_scale,
@@ -301,6 +306,27 @@ prx_status prx_engine_upload(prx_engine* engine, int field, uint32_t index, cons
 /* Sets frames_run and the previous light poses as if frame (frames_run-1) had run --
  * used after uploading a full state captured from another implementation. */
 prx_status prx_engine_set_frame_counter(prx_engine* engine, int32_t frames_run);
+
+/* ---- offline artefacts (byte-compatible with the reference's files) ---- */
+/* PHM1 photon dump, photon_store.cpp:55-102: "PHM1", u32 n_paths, u32 max_bounces, u32 0,
+ * then n_paths*max_bounces 32-byte Photon records in b*N+p order.  PRX_E_RUNTIME on I/O
+ * errors.  _read with records == NULL only reports the sizes. */
+prx_status prx_photon_dump_write(const char* path, uint32_t n_paths, uint32_t max_bounces,
+                                 const void* records, size_t bytes);
+prx_status prx_photon_dump_read(const char* path, uint32_t* n_paths, uint32_t* max_bounces,
+                                void* records, size_t capacity);
+/* write_photon_dump(engine.photon_map(), path) of an unsharded engine */
+prx_status prx_engine_write_photon_dump(prx_engine* engine, const char* path);
+/* write_image, gather.cpp:77-92 (P6, gamma 1/2.2, lround) and frame_image_name :94-98;
+ * the latter returns the name length and writes a NUL-terminated copy into buf. */
+prx_status prx_image_write_ppm(const char* path, const float* rgb, uint32_t width, uint32_t height);
+size_t prx_frame_image_name(int32_t frame, char* buf, size_t capacity);
+/* stats.cpp:10-70 (write_stats_csv / read_stats_csv) and :72-107 (reuse_report).  Only
+ * frame, mode, the six counters and the t_* fields are written / read. */
+prx_status prx_stats_csv_write(const char* path, const prx_frame_stats* rows, size_t n);
+prx_status prx_stats_csv_read(const char* path, prx_frame_stats* rows, size_t capacity, size_t* n_out);
+prx_status prx_reuse_report(const prx_frame_stats* rows, size_t n, char* buf, size_t capacity,
+                            size_t* len_out);
 
 /* Number of kernel launches issued by this engine since creation (bench evidence). */
 uint64_t prx_engine_launch_count(const prx_engine* engine);

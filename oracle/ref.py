@@ -49,6 +49,12 @@ _SIGS = [
                                                C.POINTER(C.c_uint32), C.POINTER(C.c_size_t)]),
     ("prxref_intersect_batch", C.c_int, [_P, C.c_int, C.POINTER(C.c_float), C.c_size_t,
                                          C.POINTER(C.c_float)]),
+    ("prxref_scene_load_text", C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(_P)]),
+    ("prxref_write_photon_dump", C.c_int, [_P, C.c_char_p]),
+    ("prxref_write_image", C.c_int, [C.c_char_p, C.POINTER(C.c_float), C.c_uint32, C.c_uint32]),
+    ("prxref_write_stats_csv", C.c_int, [C.c_char_p, C.POINTER(L.FrameStats), C.c_size_t]),
+    ("prxref_reuse_report", C.c_int, [C.POINTER(L.FrameStats), C.c_size_t, C.c_char_p, C.c_size_t,
+                                      C.POINTER(C.c_size_t)]),
 ]
 
 _lib = None
@@ -90,6 +96,13 @@ class RefScene:
     def builtin(cls, name: str) -> "RefScene":
         h = C.c_void_p()
         check(lib().prxref_scene_builtin(name.encode(), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_text(cls, text: str, base_dir: str = "") -> "RefScene":
+        """load_scene_text (scene.cpp:272-379) of the reference."""
+        h = C.c_void_p()
+        check(lib().prxref_scene_load_text(text.encode(), base_dir.encode(), C.byref(h)))
         return cls(h.value)
 
     @classmethod
@@ -149,6 +162,9 @@ class RefEngine:
         if getattr(self, "_h", None) is not None and self._h.value:
             lib().prxref_engine_destroy(self._h)
             self._h = None
+
+    def write_photon_dump(self, path: str) -> None:
+        check(lib().prxref_write_photon_dump(self._h, path.encode()))
 
     def set_workers(self, n: int) -> None:
         lib().prxref_engine_set_workers(self._h, int(n))
@@ -222,3 +238,24 @@ def copy_state(src, dst, n_lights: int) -> None:
     for li in range(n_lights):
         dst.upload("dm_target", src.download("dm_target", li), li)
         dst.upload("dm_current", src.download("dm_current", li), li)
+
+
+# ---- the reference's own writers (offline artefacts) ----
+def write_image(image: np.ndarray, path: str) -> None:
+    img = np.ascontiguousarray(image, dtype=np.float32)
+    check(lib().prxref_write_image(path.encode(), img.ctypes.data_as(C.POINTER(C.c_float)),
+                                   img.shape[1], img.shape[0]))
+
+
+def write_stats_csv(rows, path: str) -> None:
+    arr = (L.FrameStats * len(rows))(*rows)
+    check(lib().prxref_write_stats_csv(path.encode(), arr, len(rows)))
+
+
+def reuse_report(rows) -> str:
+    arr = (L.FrameStats * len(rows))(*rows)
+    n = C.c_size_t(0)
+    check(lib().prxref_reuse_report(arr, len(rows), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib().prxref_reuse_report(arr, len(rows), buf, len(buf), C.byref(n)))
+    return buf.value.decode()

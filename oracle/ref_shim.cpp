@@ -35,6 +35,8 @@
 #include "pathreuse/light.hpp"
 #include "pathreuse/parallel.hpp"
 #include "pathreuse/scene.hpp"
+#include "pathreuse/stats.hpp"
+#include "pathreuse/photon_store.hpp"
 #undef private
 
 #include "prx.h"
@@ -693,6 +695,77 @@ int prxref_intersect_batch(void* sp, int frame, const float* rays, size_t n, flo
             h[6] = hit->normal.x;
             h[7] = hit->normal.y;
             h[8] = hit->normal.z;
+        }
+    });
+}
+
+// ---- offline artefacts through the reference's own writers ----
+// load_scene_text (scene.cpp:272-379)
+int prxref_scene_load_text(const char* text, const char* base_dir, void** out) {
+    return guarded([&] {
+        auto rs = std::make_unique<RefScene>();
+        rs->scene = load_scene_text(text, base_dir ? base_dir : "");
+        flatten(*rs);
+        *out = rs.release();
+    });
+}
+
+// write_photon_dump(engine.photon_map(), path) (photon_store.cpp:76-86)
+int prxref_write_photon_dump(void* ep, const char* path) {
+    return guarded([&] { write_photon_dump(static_cast<RefEngine*>(ep)->engine->photon_map(), path); });
+}
+
+// write_image (gather.cpp:77-92) of a caller-provided float RGB buffer
+int prxref_write_image(const char* path, const float* rgb, uint32_t w, uint32_t h) {
+    return guarded([&] {
+        Image img;
+        img.width = w;
+        img.height = h;
+        img.pixels.assign(rgb, rgb + static_cast<size_t>(w) * h * 3);
+        write_image(img, path);
+    });
+}
+
+static FrameStats stats_of(const prx_frame_stats& r) {
+    FrameStats s;
+    s.frame = r.frame;
+    s.mode = static_cast<EngineMode>(r.mode);
+    s.rays_traced = r.rays_traced;
+    s.rays_reused = r.rays_reused;
+    s.paths_replaced = r.paths_replaced;
+    s.paths_pruned = r.paths_pruned;
+    s.paths_filled = r.paths_filled;
+    s.visibility_rays = r.visibility_rays;
+    s.t_update = r.t_update;
+    s.t_occlusion = r.t_occlusion;
+    s.t_dm = r.t_dm;
+    s.t_prune = r.t_prune;
+    s.t_fill = r.t_fill;
+    s.t_trace = r.t_trace;
+    s.t_gather = r.t_gather;
+    return s;
+}
+
+// write_stats_csv (stats.cpp:14-33)
+int prxref_write_stats_csv(const char* path, const prx_frame_stats* rows, size_t n) {
+    return guarded([&] {
+        std::vector<FrameStats> v;
+        for (size_t i = 0; i < n; ++i) v.push_back(stats_of(rows[i]));
+        write_stats_csv(v, std::string(path));
+    });
+}
+
+// reuse_report (stats.cpp:72-107) into a caller buffer
+int prxref_reuse_report(const prx_frame_stats* rows, size_t n, char* buf, size_t cap, size_t* len) {
+    return guarded([&] {
+        std::vector<FrameStats> v;
+        for (size_t i = 0; i < n; ++i) v.push_back(stats_of(rows[i]));
+        const std::string t = reuse_report(v);
+        *len = t.size();
+        if (buf && cap) {
+            const size_t k = std::min(cap - 1, t.size());
+            std::memcpy(buf, t.data(), k);
+            buf[k] = 0;
         }
     });
 }

@@ -137,6 +137,8 @@ SIGNATURES = [
                                     C.c_int, C.POINTER(C.c_double)]),
     ("prx_scene_create", C.c_int, [C.POINTER(SceneDesc), C.POINTER(P)]),
     ("prx_scene_builtin", C.c_int, [C.c_char_p, C.POINTER(P)]),
+    ("prx_scene_load", C.c_int, [C.c_char_p, C.POINTER(P)]),
+    ("prx_scene_load_text", C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(P)]),
     ("prx_scene_synthetic", C.c_int, [C.c_char_p, C.c_uint32, C.c_float, C.POINTER(P)]),
     ("prx_scene_describe", C.c_int, [P, C.POINTER(SceneDesc)]),
     ("prx_scene_bvh_permutation", C.c_int, [P, C.POINTER(C.c_uint32), C.c_size_t,
@@ -166,6 +168,16 @@ SIGNATURES = [
     ("prx_engine_download", C.c_int, [P, C.c_int, C.c_uint32, P, C.c_size_t]),
     ("prx_engine_upload", C.c_int, [P, C.c_int, C.c_uint32, P, C.c_size_t]),
     ("prx_engine_set_frame_counter", C.c_int, [P, C.c_int32]),
+    ("prx_photon_dump_write", C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, P, C.c_size_t]),
+    ("prx_photon_dump_read", C.c_int, [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), P,
+                                       C.c_size_t]),
+    ("prx_engine_write_photon_dump", C.c_int, [P, C.c_char_p]),
+    ("prx_image_write_ppm", C.c_int, [C.c_char_p, C.POINTER(C.c_float), C.c_uint32, C.c_uint32]),
+    ("prx_frame_image_name", C.c_size_t, [C.c_int32, C.c_char_p, C.c_size_t]),
+    ("prx_stats_csv_write", C.c_int, [C.c_char_p, C.POINTER(FrameStats), C.c_size_t]),
+    ("prx_stats_csv_read", C.c_int, [C.c_char_p, C.POINTER(FrameStats), C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("prx_reuse_report", C.c_int, [C.POINTER(FrameStats), C.c_size_t, C.c_char_p, C.c_size_t,
+                                   C.POINTER(C.c_size_t)]),
     ("prx_engine_launch_count", C.c_uint64, [P]),
     ("prx_engine_transfer_bytes", C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("prx_last_error", C.c_char_p, []),

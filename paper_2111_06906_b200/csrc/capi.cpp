@@ -11,6 +11,7 @@
 #include "engine.h"
 #include "host_scene.h"
 #include "prx.h"
+#include "wire.h"
 
 struct prx_scene {
     std::shared_ptr<prx::Scene> scene;
@@ -127,6 +128,27 @@ prx_status prx_scene_builtin(const char* name, prx_scene** out) {
         need(out, "out");
         auto s = std::make_unique<prx_scene>();
         s->scene = std::make_shared<prx::Scene>(prx::make_builtin_scene(name));
+        *out = s.release();
+    });
+}
+
+// scene.cpp:272-398
+prx_status prx_scene_load(const char* source, prx_scene** out) {
+    return guarded([&] {
+        need(source, "source");
+        need(out, "out");
+        auto s = std::make_unique<prx_scene>();
+        s->scene = std::make_shared<prx::Scene>(prx::load_scene_source(source));
+        *out = s.release();
+    });
+}
+
+prx_status prx_scene_load_text(const char* json_text, const char* base_dir, prx_scene** out) {
+    return guarded([&] {
+        need(json_text, "json_text");
+        need(out, "out");
+        auto s = std::make_unique<prx_scene>();
+        s->scene = std::make_shared<prx::Scene>(prx::load_scene_text(json_text, base_dir ? base_dir : ""));
         *out = s.release();
     });
 }
@@ -293,6 +315,97 @@ prx_status prx_engine_upload(prx_engine* engine, int field, uint32_t index, cons
 
 prx_status prx_engine_set_frame_counter(prx_engine* engine, int32_t frames_run) {
     return guarded([&] { eng(engine).set_frame_counter(frames_run); });
+}
+
+// ------------------------------------------------------------------ offline artefacts
+prx_status prx_photon_dump_write(const char* path, uint32_t n_paths, uint32_t max_bounces, const void* records,
+                                 size_t bytes) {
+    return guarded([&] {
+        need(path, "path");
+        if (bytes) need(records, "records");
+        prx::write_photon_dump(path, n_paths, max_bounces, records, bytes);
+    });
+}
+
+prx_status prx_photon_dump_read(const char* path, uint32_t* n_paths, uint32_t* max_bounces, void* records,
+                                size_t capacity) {
+    return guarded([&] {
+        need(path, "path");
+        std::vector<char> buf;
+        uint32_t n = 0, b = 0;
+        prx::read_photon_dump(path, &n, &b, records ? &buf : nullptr);
+        if (records) {
+            if (capacity < buf.size()) throw std::invalid_argument("photon dump: records buffer too small");
+            std::memcpy(records, buf.data(), buf.size());
+        }
+        if (n_paths) *n_paths = n;
+        if (max_bounces) *max_bounces = b;
+    });
+}
+
+prx_status prx_engine_write_photon_dump(prx_engine* engine, const char* path) {
+    return guarded([&] {
+        need(path, "path");
+        prx_engine_info info{};
+        eng(engine).info(&info);
+        if (info.shard_begin != 0 || info.shard_end != info.n_paths)
+            throw std::invalid_argument("photon dump: engine holds a path shard, dump the gathered map");
+        const size_t bytes = eng(engine).field_bytes(PRX_FIELD_PHOTONS, 0);
+        std::vector<char> buf(bytes);
+        eng(engine).download(PRX_FIELD_PHOTONS, 0, buf.data(), bytes);
+        prx::write_photon_dump(path, info.n_paths, info.max_bounces, buf.data(), bytes);
+    });
+}
+
+prx_status prx_image_write_ppm(const char* path, const float* rgb, uint32_t width, uint32_t height) {
+    return guarded([&] {
+        need(path, "path");
+        if (width && height) need(rgb, "rgb");
+        prx::write_image_ppm(path, rgb, width, height);
+    });
+}
+
+size_t prx_frame_image_name(int32_t frame, char* buf, size_t capacity) {
+    const std::string name = prx::frame_image_name(frame);
+    if (buf && capacity) {
+        const size_t n = std::min(capacity - 1, name.size());
+        std::memcpy(buf, name.data(), n);
+        buf[n] = 0;
+    }
+    return name.size();
+}
+
+prx_status prx_stats_csv_write(const char* path, const prx_frame_stats* rows, size_t n) {
+    return guarded([&] {
+        need(path, "path");
+        if (n) need(rows, "rows");
+        prx::write_stats_csv(path, rows, n);
+    });
+}
+
+prx_status prx_stats_csv_read(const char* path, prx_frame_stats* rows, size_t capacity, size_t* n_out) {
+    return guarded([&] {
+        need(path, "path");
+        const std::vector<prx_frame_stats> r = prx::read_stats_csv(path);
+        if (n_out) *n_out = r.size();
+        if (rows) {
+            if (capacity < r.size()) throw std::invalid_argument("stats CSV: rows buffer too small");
+            std::copy(r.begin(), r.end(), rows);
+        }
+    });
+}
+
+prx_status prx_reuse_report(const prx_frame_stats* rows, size_t n, char* buf, size_t capacity, size_t* len_out) {
+    return guarded([&] {
+        if (n) need(rows, "rows");
+        const std::string text = prx::reuse_report(rows, n);
+        if (len_out) *len_out = text.size();
+        if (buf && capacity) {
+            const size_t k = std::min(capacity - 1, text.size());
+            std::memcpy(buf, text.data(), k);
+            buf[k] = 0;
+        }
+    });
 }
 
 uint64_t prx_engine_launch_count(const prx_engine* engine) {

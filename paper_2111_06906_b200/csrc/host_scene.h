@@ -139,4 +139,10 @@ Scene make_builtin_scene(const std::string& name);  // scene.cpp:603-611
 bool is_builtin_scene(const std::string& name);
 Scene make_synthetic_scene(const std::string& name, uint32_t n_dynamic, float tri_scale);
 
+// scene documents (scene_io.cpp; scene.cpp:179-398)
+std::vector<Tri> load_obj_mesh(const std::string& path);
+Scene load_scene_text(const std::string& json_text, const std::string& base_dir);
+Scene load_scene_file(const std::string& path);
+Scene load_scene_source(const std::string& source);  // "builtin:NAME", a builtin name, or a file
+
 }  // namespace prx

@@ -105,6 +105,21 @@ class Scene:
         return cls(h.value)
 
     @classmethod
+    def load(cls, source: str) -> "Scene":
+        """load_scene_source (scene.cpp:392-398): "builtin:NAME", a builtin name, or a JSON
+        scene file whose OBJ meshes are resolved relative to the file."""
+        h = C.c_void_p()
+        L.check(L.lib().prx_scene_load(str(source).encode(), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_text(cls, json_text: str, base_dir: str = "") -> "Scene":
+        """load_scene_text (scene.cpp:272-379)."""
+        h = C.c_void_p()
+        L.check(L.lib().prx_scene_load_text(json_text.encode(), str(base_dir).encode(), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
     def from_desc(cls, desc: L.SceneDesc) -> "Scene":
         h = C.c_void_p()
         L.check(L.lib().prx_scene_create(C.byref(desc), C.byref(h)))
@@ -286,6 +301,10 @@ class Engine:
     def photon_map(self) -> np.ndarray:
         return self.download("photons")
 
+    def write_photon_dump(self, path: str) -> None:
+        """write_photon_dump(engine.photon_map(), path) (photon_store.cpp:76-86)."""
+        L.check(L.lib().prx_engine_write_photon_dump(self._h, str(path).encode()))
+
     def vertex_aux(self) -> np.ndarray:
         return self.download("aux")
 
@@ -321,3 +340,77 @@ def render_builtin(scene: str, mode: str = "naive", paths: int = 10000, bounces:
     img = eng.splat(radius=radius)
     eng.close()
     return int(img.shape[1]), int(img.shape[0]), img.astype("<f4").tobytes()
+
+
+# --------------------------------------------------------------------------- offline artefacts
+def write_photon_dump(photons: np.ndarray, n_paths: int, max_bounces: int, path: str) -> None:
+    """PHM1 photon dump (photon_store.cpp:76-86) of a [max_bounces * n_paths] Photon array."""
+    rec = np.ascontiguousarray(photons, dtype=PHOTON_DTYPE)
+    L.check(L.lib().prx_photon_dump_write(str(path).encode(), int(n_paths), int(max_bounces),
+                                          rec.ctypes.data_as(C.c_void_p), rec.nbytes))
+
+
+def read_photon_dump(path: str) -> tuple:
+    """read_photon_dump (photon_store.cpp:88-102) -> (n_paths, max_bounces, photons)."""
+    n, b = C.c_uint32(0), C.c_uint32(0)
+    L.check(L.lib().prx_photon_dump_read(str(path).encode(), C.byref(n), C.byref(b), None, 0))
+    rec = np.zeros(n.value * b.value, dtype=PHOTON_DTYPE)
+    L.check(L.lib().prx_photon_dump_read(str(path).encode(), C.byref(n), C.byref(b),
+                                         rec.ctypes.data_as(C.c_void_p), rec.nbytes))
+    return int(n.value), int(b.value), rec
+
+
+def write_image(image: np.ndarray, path: str) -> None:
+    """write_image (gather.cpp:77-92): [H, W, 3] float32 -> binary PPM, gamma 1/2.2."""
+    img = np.ascontiguousarray(image, dtype=np.float32)
+    if img.ndim != 3 or img.shape[2] != 3:
+        raise ValueError("image must be [height, width, 3]")
+    L.check(L.lib().prx_image_write_ppm(str(path).encode(), img.ctypes.data_as(C.POINTER(C.c_float)),
+                                        int(img.shape[1]), int(img.shape[0])))
+
+
+def frame_image_name(frame: int) -> str:
+    """frame_image_name (gather.cpp:94-98)."""
+    buf = C.create_string_buffer(64)
+    L.lib().prx_frame_image_name(int(frame), buf, len(buf))
+    return buf.value.decode()
+
+
+def _stats_array(rows) -> C.Array:
+    arr = (L.FrameStats * len(rows))()
+    for i, r in enumerate(rows):
+        if isinstance(r, L.FrameStats):
+            C.memmove(C.byref(arr[i]), C.byref(r), C.sizeof(L.FrameStats))
+            continue
+        arr[i].frame = int(r["frame"])
+        arr[i].mode = L.MODES[r["mode"]] if isinstance(r["mode"], str) else int(r["mode"])
+        for k in L.FrameStats.COUNTS:
+            setattr(arr[i], k, int(r.get(k, 0)))
+        for k in ("t_update", "t_occlusion", "t_dm", "t_prune", "t_fill", "t_trace", "t_gather"):
+            setattr(arr[i], k, float(r.get(k, 0.0)))
+    return arr
+
+
+def write_stats_csv(rows, path: str) -> None:
+    """write_stats_csv (stats.cpp:14-33); rows are FrameStats or run_builtin-style dicts."""
+    arr = _stats_array(list(rows))
+    L.check(L.lib().prx_stats_csv_write(str(path).encode(), arr, len(arr)))
+
+
+def read_stats_csv(path: str) -> list:
+    """read_stats_csv (stats.cpp:35-70) -> list of FrameStats."""
+    n = C.c_size_t(0)
+    L.check(L.lib().prx_stats_csv_read(str(path).encode(), None, 0, C.byref(n)))
+    arr = (L.FrameStats * n.value)()
+    L.check(L.lib().prx_stats_csv_read(str(path).encode(), arr, n.value, C.byref(n)))
+    return list(arr)
+
+
+def reuse_report(rows) -> str:
+    """reuse_report (stats.cpp:72-107)."""
+    arr = _stats_array(list(rows))
+    n = C.c_size_t(0)
+    L.check(L.lib().prx_reuse_report(arr, len(arr), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    L.check(L.lib().prx_reuse_report(arr, len(arr), buf, len(buf), C.byref(n)))
+    return buf.value.decode()
