@@ -143,6 +143,18 @@ private:
         if (lit("null")) return v;
         return number();
     }
+    unsigned hex4(size_t at) const {
+        if (at + 4 > s_.size()) error("bad \\u escape");
+        unsigned v = 0;
+        for (size_t k = at; k < at + 4; ++k) {
+            const char c = s_[k];
+            const int d = (c >= '0' && c <= '9') ? c - '0' : (c >= 'a' && c <= 'f') ? c - 'a' + 10
+                        : (c >= 'A' && c <= 'F') ? c - 'A' + 10 : -1;
+            if (d < 0) error("bad \\u escape");
+            v = v * 16 + static_cast<unsigned>(d);
+        }
+        return v;
+    }
     std::string string() {
         ++p_;  // opening quote
         std::string out;
@@ -167,11 +179,10 @@ private:
                 case 'r': out.push_back('\r'); break;
                 case 't': out.push_back('\t'); break;
                 case 'u': {
-                    if (p_ + 4 > s_.size()) error("bad \\u escape");
-                    unsigned cp = std::stoul(s_.substr(p_, 4), nullptr, 16);
+                    unsigned cp = hex4(p_);
                     p_ += 4;
                     if (cp >= 0xD800 && cp < 0xDC00 && p_ + 6 <= s_.size() && s_[p_] == '\\' && s_[p_ + 1] == 'u') {
-                        const unsigned lo = std::stoul(s_.substr(p_ + 2, 4), nullptr, 16);
+                        const unsigned lo = hex4(p_ + 2);
                         p_ += 6;
                         cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
                     }
