@@ -946,8 +946,9 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
     if (mode == 1 && d_gather_.size() == 0) d_gather_.alloc(gather_work_bytes(static_cast<uint64_t>(n_) * B_, npx));
     record(kEvSplat0);
     float* out = rgb_dev ? rgb_dev : d_img_.as<float>();
-    launch_splat(scene_dev(), path_dev(), C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area,
-                 d_splat_work_.get(), d_splat_cand_.get(), mode, d_gather_.get(), stream_);
+    const SceneDev S = scene_dev();
+    launch_splat(S, path_dev(), C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, d_splat_work_.get(),
+                 d_splat_cand_.get(), mode, d_gather_.get(), stream_);
     record(kEvSplat1);
     if (rgb_host)
         copy_async(rgb_host, out, 12ull * npx, cudaMemcpyDeviceToHost);

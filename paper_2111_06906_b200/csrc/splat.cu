@@ -27,6 +27,9 @@ namespace {
 
 constexpr int kT = 256;
 constexpr unsigned long long kEmptyKey = ~0ull;
+#ifndef PRX_GATHER_UNROLL
+#define PRX_GATHER_UNROLL 8
+#endif
 
 __device__ __forceinline__ long long cell_coord(float v, float r) { return (long long)floorf(v / r); }
 
@@ -161,8 +164,9 @@ __global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float rad
 // ---------------------------------------------------------------- mode 1: ordered gather
 // Bit-exact image: photons are binned by grid cell in ascending flat record order (the
 // insertion order of the reference's GatherGrid, gather.cpp:13-20,42-52), and one warp per
-// pixel visits its 27 cells in the reference's (dz, dy, dx) order, summing contributors
-// strictly in that order -- the same fp32 additions as gather_image's per-pixel loop.
+// pixel (k_gather_staged) visits its 27 cells in the reference's (dz, dy, dx) order, summing
+// contributors strictly in that order -- the same fp32 additions as gather_image's
+// per-pixel loop.
 __global__ void k_gather_flag(PathDev P, float radius, const unsigned long long* __restrict__ keys, int bits,
                               uint8_t* __restrict__ flag, uint32_t* __restrict__ pslot, uint32_t* __restrict__ pcnt) {
     const uint32_t mask = (1u << bits) - 1u;
@@ -206,19 +210,40 @@ __global__ void k_gather_copy(PathDev P, const uint32_t* __restrict__ vals, cons
     }
 }
 
-__global__ void __launch_bounds__(kT) k_gather_pixels(const float4* __restrict__ gbuf, uint32_t npx, float radius,
+// Fused ordered gather, staged: one warp per pixel taken from a work counter (heavy pixels
+// cluster in the image, so static striding would pile them onto a few SMs); per 32-photon
+// chunk the warp tests the candidates in parallel, compacts the contributors' energies into
+// a shared-memory stage in insertion order (ballot prefix), and lanes 0..2 add them
+// sequentially, one channel each.  Cells that cannot reach the hit point are skipped.
+__device__ __forceinline__ bool cell_reaches(long long ix, long long iy, long long iz, const float4& g, float radius,
+                                             float r2) {
+    const double rd = radius;
+    auto gap = [&](long long i, float x) {  // box widened for the rounding of floor(p / r)
+        const double m = 1e-5 * rd * (double)(llabs(i) + 2);
+        const double lo = (double)i * rd - m, hi = (double)(i + 1) * rd + m;
+        return x < lo ? lo - x : (x > hi ? x - hi : 0.0);
+    };
+    const double gx = gap(ix, g.x), gy = gap(iy, g.y), gz = gap(iz, g.z);
+    return gx * gx + gy * gy + gz * gz <= (double)r2 * (1.0 + 1e-4) + 1e-30;
+}
+
+__global__ void __launch_bounds__(kT) k_gather_staged(const float4* __restrict__ gbuf, uint32_t npx, float radius,
                                                       const unsigned long long* __restrict__ keys, int bits,
                                                       const uint32_t* __restrict__ pstart,
                                                       const uint32_t* __restrict__ pcnt,
                                                       const float4* __restrict__ spo, const float4* __restrict__ sen,
                                                       const float4* __restrict__ mat, float inv_pi, float inv_area,
-                                                      float* __restrict__ img) {
+                                                      uint32_t* work, float* __restrict__ img) {
+    __shared__ float4 stage[kT];
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+    float4* const my = stage + (threadIdx.x & ~31u);
     const uint32_t mask = (1u << bits) - 1u;
     const float r2 = radius * radius;
-    for (uint32_t pix = warp; pix < npx; pix += n_warps) {
+    while (true) {
+        uint32_t pix = 0;
+        if (lane == 0) pix = atomicAdd(work, 1u);
+        pix = __shfl_sync(0xffffffffu, pix, 0);
+        if (pix >= npx) break;
         const float4 g = gbuf[pix];
         const uint32_t obj = __float_as_uint(g.w);
         if (obj == kInvalidObj) {  // no primary hit: pixel stays 0 (gather.cpp:66)
@@ -227,42 +252,54 @@ __global__ void __launch_bounds__(kT) k_gather_pixels(const float4* __restrict__
         }
         const V3 x{g.x, g.y, g.z};
         const long long cx = cell_coord(g.x, radius), cy = cell_coord(g.y, radius), cz = cell_coord(g.z, radius);
-        V3 rad{0.0f, 0.0f, 0.0f};
+        float acc = 0.0f;  // radiance += E (gather.cpp:68), channel `lane` for lanes 0..2
         for (int dz = -1; dz <= 1; ++dz)
             for (int dy = -1; dy <= 1; ++dy)
                 for (int dx = -1; dx <= 1; ++dx) {  // gather.hpp:48-50 visiting order
+                    if (!cell_reaches(cx + dx, cy + dy, cz + dz, g, radius, r2)) continue;
                     const unsigned long long key = grid_key(cx + dx, cy + dy, cz + dz);
                     uint32_t s = slot_of(key, bits);
                     unsigned long long k;
                     while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
                     if (k != key) continue;
                     const uint32_t b0 = __ldg(&pstart[s]), n = __ldg(&pcnt[s]);
-                    for (uint32_t base = 0; base < n; base += 32) {
-                        const uint32_t j = base + lane;
-                        bool hit = false;
-                        float4 en = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (j < n) {
-                            const float4 po = __ldg(&spo[b0 + j]);
-                            const V3 d = sub(V3{po.x, po.y, po.z}, x);  // gather.hpp:54
-                            hit = dot(d, d) <= r2 && __float_as_uint(po.w) == obj;
-                            if (hit) en = __ldg(&sen[b0 + j]);
+                    // kU chunks per step: all candidate loads and contributor loads of the step
+                    // are issued before the ordered adds, so L2 latency overlaps kU-fold
+                    constexpr int kU = PRX_GATHER_UNROLL;
+                    for (uint32_t base = 0; base < n; base += 32 * kU) {
+                        float4 po[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            const uint32_t j = base + 32 * u + lane;
+                            po[u] = j < n ? __ldg(&spo[b0 + j]) : make_float4(0.f, 0.f, 0.f, __uint_as_float(kInvalidObj));
                         }
-                        uint32_t ball = __ballot_sync(0xffffffffu, hit);
-                        while (ball) {  // in insertion order: radiance += E (gather.cpp:68)
-                            const int src = __ffs(ball) - 1;
-                            ball &= ball - 1;
-                            rad.x = rad.x + __shfl_sync(0xffffffffu, en.x, src);
-                            rad.y = rad.y + __shfl_sync(0xffffffffu, en.y, src);
-                            rad.z = rad.z + __shfl_sync(0xffffffffu, en.z, src);
+                        uint32_t ball[kU];
+                        float4 en[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            const V3 d = sub(V3{po[u].x, po[u].y, po[u].z}, x);  // gather.hpp:54
+                            const bool hit = dot(d, d) <= r2 && __float_as_uint(po[u].w) == obj;
+                            ball[u] = __ballot_sync(0xffffffffu, hit);
+                            en[u] = hit ? __ldg(&sen[b0 + base + 32 * u + lane]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            if (!ball[u]) continue;
+                            if ((ball[u] >> lane) & 1u) my[__popc(ball[u] & ((1u << lane) - 1u))] = en[u];
+                            __syncwarp();
+                            if (lane < 3) {
+                                const float* col = reinterpret_cast<const float*>(my) + lane;
+                                const uint32_t m = __popc(ball[u]);
+                                for (uint32_t i = 0; i < m; ++i) acc = acc + col[4 * i];
+                            }
+                            __syncwarp();
                         }
                     }
                 }
-        if (lane == 0) {
+        if (lane < 3) {
             const float4 a = mat[obj];
-            const V3 out = mul(mul(mulv(rad, V3{a.x, a.y, a.z}), inv_pi), inv_area);  // gather.cpp:71
-            img[3 * pix] = out.x;
-            img[3 * pix + 1] = out.y;
-            img[3 * pix + 2] = out.z;
+            const float alb = lane == 0 ? a.x : (lane == 1 ? a.y : a.z);
+            img[3 * pix + lane] = ((acc * alb) * inv_pi) * inv_area;  // gather.cpp:71
         }
     }
 }
@@ -348,9 +385,12 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         radix_sort_pairs(sk, sv, sk2, sv2, (uint32_t)nv, m_count, bits, gscratch, st);
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
         k_gather_copy<<<launch_grid(nv, kT), kT, 0, st>>>(P, sv, m_count, spo, sen);
-        k_gather_pixels<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt,
-                                                                     spo, sen, S.mat, inv_pi, inv_area, img);
-        g_launches += 8;
+        g_launches += 6;
+        uint32_t* wq = m_count + 4;  // pixel work counter of k_gather_staged
+        cudaMemsetAsync(wq, 0, 4, st);
+        k_gather_staged<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt, spo,
+                                                                     sen, S.mat, inv_pi, inv_area, wq, img);
+        ++g_launches;
         return;
     }
     scan_exclusive_u32(cnt, off, (uint32_t)slots, nullptr, nullptr, scratch, st);
