@@ -827,7 +827,7 @@ __device__ __forceinline__ V3 cosine_sample(const SceneDev& S, V3 normal, float 
     const float r = sqrtf(u1);
     float cphi, sphi;
     if (S.trig) {
-        const float2 cs = __ldg(&S.trig[k2]);
+        const float2 cs = __ldcs(&S.trig[k2]);  // random 1-in-2^24 lookups: evict-first
         cphi = cs.x;
         sphi = cs.y;
     } else {
@@ -846,11 +846,11 @@ __device__ __forceinline__ V3 phong_sample(const SceneDev& S, V3 mirror, float e
                                            uint32_t k1, uint32_t k2, uint32_t flags) {
     const float u2 = (float)k2 * 5.9604644775390625e-8f;
     // host-libm powf by table lookup (bit-exact) when the engine built the table
-    const float cos_theta = (flags & 4u) ? __ldg(&S.pow_tabs[flags >> 8][k1]) : powf(u1, 1.0f / (exponent + 1.0f));
+    const float cos_theta = (flags & 4u) ? __ldcs(&S.pow_tabs[flags >> 8][k1]) : powf(u1, 1.0f / (exponent + 1.0f));
     const float sin_theta = sqrtf(fmax_std(0.0f, 1.0f - cos_theta * cos_theta));
     float cphi, sphi;
     if (S.trig) {
-        const float2 cs = __ldg(&S.trig[k2]);
+        const float2 cs = __ldcs(&S.trig[k2]);  // random 1-in-2^24 lookups: evict-first
         cphi = cs.x;
         sphi = cs.y;
     } else {

@@ -39,9 +39,9 @@ __device__ __forceinline__ void truncate_path(const PathDev& P, uint32_t i, uint
                                               bool escaped, uchar4& m) {
     for (uint32_t b = new_count; b < P.B; ++b) {
         const size_t v = vix(P, b, i);
-        P.in_dir[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        P.pos_obj[v].w = __uint_as_float(kInvalidObj);
-        P.energy[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __stcs(&P.in_dir[v], make_float4(0.f, 0.f, 0.f, 0.f));
+        __stcs(&P.pos_obj[v].w, __uint_as_float(kInvalidObj));
+        __stcs(&P.energy[v], make_float4(0.f, 0.f, 0.f, 0.f));
     }
     m.x = (unsigned char)new_count;
     m.y = escaped ? 1 : 0;
@@ -322,19 +322,19 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
         const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
         const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
         if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
-            P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
-            P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
-            P.energy[v] = make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius);
+            __stcs(&P.in_dir[v], make_float4(d.x, d.y, d.z, 0.f));
+            __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[v], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
-            P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
+            __stcs(&P.out_dir[v], make_float4(out.x, out.y, out.z, 0.f));
             P.rstart[i] = (uint8_t)(s + 1);
             has = false;
             continue;
         }
         const V3 old_pos = ld3(P.pos_obj[v]);
         const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
-        P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
-        P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+        __stcs(&P.in_dir[v], make_float4(d.x, d.y, d.z, 0.f));
+        __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
         if (s + 1 >= segs) {
             has = false;
             continue;
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
         if (s + 1 < k) {
             const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
             const V3 od = normalized(sub(next, h.pos));
-            P.out_dir[v] = make_float4(od.x, od.y, od.z, 0.f);
+            __stcs(&P.out_dir[v], make_float4(od.x, od.y, od.z, 0.f));
         }
         force = true;
         ++s;
@@ -420,18 +420,18 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
         const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
         const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
         if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
-            P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
-            P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
-            P.energy[v] = make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius);
+            __stcs(&P.in_dir[v], make_float4(d.x, d.y, d.z, 0.f));
+            __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[v], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
-            P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
+            __stcs(&P.out_dir[v], make_float4(out.x, out.y, out.z, 0.f));
             P.rstart[i] = (uint8_t)(s + 1);
             continue;
         }
         const V3 old_pos = ld3(P.pos_obj[v]);
         const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
-        P.in_dir[v] = make_float4(d.x, d.y, d.z, 0.f);
-        P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
+        __stcs(&P.in_dir[v], make_float4(d.x, d.y, d.z, 0.f));
+        __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
         if (s + 1 >= segs) continue;
         have = true;
         const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
         if (s + 1 < k) {
             const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
             const V3 od = normalized(sub(next, h.pos));
-            P.out_dir[v] = make_float4(od.x, od.y, od.z, 0.f);
+            __stcs(&P.out_dir[v], make_float4(od.x, od.y, od.z, 0.f));
         }
         force = true;
         ++s;
@@ -681,11 +681,11 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_trace(SceneDev S, PathDe
             const float4 am = __ldg(&S.mat[h.obj]);
             energy = mulv(energy, V3{am.x, am.y, am.z});
             const size_t v = vix(P, b, i);
-            P.in_dir[v] = make_float4(dir.x, dir.y, dir.z, 0.f);
-            P.pos_obj[v] = make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj));
-            P.energy[v] = make_float4(energy.x, energy.y, energy.z, S.gather_radius);
+            __stcs(&P.in_dir[v], make_float4(dir.x, dir.y, dir.z, 0.f));
+            __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[v], make_float4(energy.x, energy.y, energy.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, dir, p, epoch, b + 1);
-            P.out_dir[v] = make_float4(out.x, out.y, out.z, 0.f);
+            __stcs(&P.out_dir[v], make_float4(out.x, out.y, out.z, 0.f));
             pos = h.pos;
             dir = out;
             ++b;
@@ -739,8 +739,8 @@ __global__ void k_unpack(PathDev P, const PhotonRec* ph, const AuxRec* aux) {
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
         if (ph) {
             const PhotonRec r = ph[v];
-            P.in_dir[v] = make_float4(r.dx, r.dy, r.dz, 0.f);
-            P.energy[v] = make_float4(r.ex, r.ey, r.ez, r.radius);
+            __stcs(&P.in_dir[v], make_float4(r.dx, r.dy, r.dz, 0.f));
+            __stcs(&P.energy[v], make_float4(r.ex, r.ey, r.ez, r.radius));
             P.pos_obj[v].w = __uint_as_float(r.obj);
         }
         if (aux) {
@@ -748,7 +748,7 @@ __global__ void k_unpack(PathDev P, const PhotonRec* ph, const AuxRec* aux) {
             P.pos_obj[v].x = a.px;
             P.pos_obj[v].y = a.py;
             P.pos_obj[v].z = a.pz;
-            P.out_dir[v] = make_float4(a.ox, a.oy, a.oz, 0.f);
+            __stcs(&P.out_dir[v], make_float4(a.ox, a.oy, a.oz, 0.f));
         }
     }
 }
