@@ -192,8 +192,22 @@ __global__ void __launch_bounds__(kT) k_occlusion_flags(SceneDev S, PathDev P, i
                     const V3 dir = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
                     b = add(prev, mul(dir, S.two_diag));
                 }
+                // bounding-box reject before the slab test: a segment whose box misses an
+                // occlusion box by more than 1e-6 of the extents cannot pass the double test
+                // (its quotients err by ~1e-16 relative)
+                const V3 smin{fminf(prev.x, b.x), fminf(prev.y, b.y), fminf(prev.z, b.z)};
+                const V3 smax{fmaxf(prev.x, b.x), fmaxf(prev.y, b.y), fmaxf(prev.z, b.z)};
                 for (uint32_t j = 0; j < nb; ++j) {
-                    if (segment_box(prev, b, boxes[j])) {
+                    const Box& B = boxes[j];
+                    bool apart = false;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const float tol = 1e-6f * (comp(smax, a) - comp(smin, a) + fabsf(comp(B.lo, a)) +
+                                                   fabsf(comp(B.hi, a))) + 1e-30f;
+                        apart = apart || comp(smax, a) < comp(B.lo, a) - tol || comp(smin, a) > comp(B.hi, a) + tol;
+                    }
+                    if (apart) continue;
+                    if (segment_box(prev, b, B)) {
                         flagged = true;
                         break;
                     }
