@@ -165,10 +165,12 @@ __global__ void k_copy_leaf(const uint32_t* __restrict__ vals, uint32_t n, uint3
 // kLeafBit | position << 3), walked by fast_closest for the certified dynamic phase
 // (device_scene.cuh: dyn_closest_exact).  Leaves are the triangles themselves, copied in
 // sorted order with their global index (== (object, index) order) in a.w.
-__global__ void k_karras_all(const uint32_t* __restrict__ keys, uint32_t n, float4* nodes, uint32_t* parent) {
+__global__ void k_karras_all(const uint32_t* __restrict__ keys, uint32_t n, float4* nodes, uint32_t* parent,
+                             uint2* range) {
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t + 1 < n; t += gridDim.x * blockDim.x) {
         int g, lo, hi;
         karras_node(keys, (int)n, (int)t, 0xFFFFFFFFu, g, lo, hi);
+        range[t] = make_uint2((uint32_t)lo, (uint32_t)hi);
         const uint32_t left = (lo == g) ? (kLeafBit | ((uint32_t)g << 3)) : (uint32_t)g;
         const uint32_t right = (hi == g + 1) ? (kLeafBit | ((uint32_t)(g + 1) << 3)) : (uint32_t)(g + 1);
         float4* N = nodes + 4ull * t;
@@ -179,6 +181,28 @@ __global__ void k_karras_all(const uint32_t* __restrict__ keys, uint32_t n, floa
         if (right & kLeafBit) parent[g + 1] = t;
         else parent[n + g + 1] = t;
         if (t == 0) parent[n] = 0xFFFFFFFFu;
+    }
+}
+
+// Leaf collapse: a child subtree spanning <= kCollapse sorted triangles becomes one leaf
+// (Karras ranges are contiguous in sorted order, and the triangles are stored that way), so
+// the walk tests a few triangles instead of descending the last levels one box at a time.
+// Runs after the refit, which still needs the binary child codes.
+#ifndef PRX_COLLAPSE
+#define PRX_COLLAPSE 4
+#endif
+constexpr uint32_t kCollapse = PRX_COLLAPSE;
+__global__ void k_collapse_all(uint32_t n, float4* nodes, const uint2* __restrict__ range) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t + 1 < n; t += gridDim.x * blockDim.x) {
+        float4* N = nodes + 4ull * t;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const uint32_t code = __float_as_uint(N[c].w);
+            if (code & kLeafBit) continue;
+            const uint2 r = range[code];
+            const uint32_t cnt = r.y - r.x + 1;
+            if (cnt <= kCollapse) N[c].w = __uint_as_float(kLeafBit | (r.x << 3) | (cnt - 1));
+        }
     }
 }
 
@@ -255,10 +279,12 @@ void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint3
     }
     if (buf.all_nodes) {  // combined tree (fast dynamic phase)
         k_sorted_tris<<<g, kT, 0, st>>>(world_tris, buf.keys, buf.vals, n_tris, dyn_dev, buf.all_tris);
-        k_karras_all<<<g, kT, 0, st>>>(buf.keys, n_tris, buf.all_nodes, buf.parent);
+        uint2* range = reinterpret_cast<uint2*>(buf.keys_tmp);  // free after the sort (2n words)
+        k_karras_all<<<g, kT, 0, st>>>(buf.keys, n_tris, buf.all_nodes, buf.parent, range);
         cudaMemsetAsync(buf.flags, 0, 4ull * n_tris, st);
         k_refit_all<<<g, kT, 0, st>>>(buf.all_tris, n_tris, dyn_dev, buf.all_nodes, buf.parent, buf.flags);
-        g_launches += 3;
+        k_collapse_all<<<g, kT, 0, st>>>(n_tris, buf.all_nodes, range);
+        g_launches += 4;
     }
 }
 
