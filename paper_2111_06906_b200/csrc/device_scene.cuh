@@ -35,7 +35,9 @@ __device__ __forceinline__ V3 ld3(const float4 v) { return V3{v.x, v.y, v.z}; }
 struct RayPre {
     V3 o, d;
     float inv[3];
-    bool safe;  // all |d| components either 0 or large enough for the float filter
+    float oinv[3];  // o * inv: the fast culling slabs are fma(bound, inv, -oinv)
+    float err[3];   // per-axis absolute error bound of those slabs (the rounding of oinv)
+    bool safe;      // all |d| components either 0 or large enough for the float filter
 };
 
 __device__ __forceinline__ RayPre make_ray(V3 o, V3 d) {
@@ -46,6 +48,8 @@ __device__ __forceinline__ RayPre make_ray(V3 o, V3 d) {
     for (int a = 0; a < 3; ++a) {
         const float da = comp(d, a);
         r.inv[a] = da != 0.0f ? 1.0f / da : 0.0f;
+        r.oinv[a] = comp(o, a) * r.inv[a];
+        r.err[a] = 1.2e-7f * fabsf(r.oinv[a]) + 1e-30f;
         if (da != 0.0f && fabsf(da) < 1e-18f) r.safe = false;
     }
     return r;
@@ -539,6 +543,32 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
     return t0 - t1 <= 2.0e-6f * (fabsf(t0) + fabsf(t1)) ? t0 : INFINITY;
 }
 
+// box_entry for the fast (culling-only) walks: one fma per slab bound.  fma(b, inv, -o*inv)
+// differs from (b - o) * inv by at most the rounding of o*inv (err[a]) plus a few ulps of the
+// result (covered by the relative slack), so each axis' slab is widened by its own err[a]:
+// still a conservative cull, and the entry stays a lower bound for the stack's culling.
+__device__ __forceinline__ float box_entry_fast(const RayPre& r, float t_min, float t_lim, float4 A, float4 B) {
+    float t0 = t_min, t1 = t_lim;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float d = comp(r.d, a);
+        const float lo = a == 0 ? A.x : (a == 1 ? A.y : A.z);
+        const float hi = a == 0 ? B.x : (a == 1 ? B.y : B.z);
+        if (d == 0.0f || !r.safe) {
+            if (d == 0.0f) {
+                const float o = comp(r.o, a);
+                if (o < lo || o > hi) return INFINITY;
+            }
+            continue;  // no culling on an axis the float slab cannot bound
+        }
+        const float tn = __fmaf_rn(lo, r.inv[a], -r.oinv[a]);
+        const float tf = __fmaf_rn(hi, r.inv[a], -r.oinv[a]);
+        t0 = fmaxf(t0, fminf(tn, tf) - r.err[a]);
+        t1 = fminf(t1, fmaxf(tn, tf) + r.err[a]);
+    }
+    return t0 - t1 <= 2.0e-6f * (fabsf(t0) + fabsf(t1)) ? t0 : INFINITY;
+}
+
 __device__ __forceinline__ float cull_limit(float best_t) { return best_t + 1e-4f * fabsf(best_t) + 1e-6f; }
 
 #ifndef PRX_SHORT_STACK
@@ -605,8 +635,8 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
             const float4 n0 = __ldg(&N[0]), n1 = __ldg(&N[1]), n2 = __ldg(&N[2]), n3 = __ldg(&N[3]);
             const uint32_t c0 = __float_as_uint(n0.w), c1 = __float_as_uint(n1.w);
             const float lim = cull_limit(best_t);
-            const float tl = box_entry(r, t_min, lim, n0, n1, 0.0f);  // boxes are pre-inflated
-            const float tr = c1 != kNone ? box_entry(r, t_min, lim, n2, n3, 0.0f) : INFINITY;
+            const float tl = box_entry_fast(r, t_min, lim, n0, n1);  // boxes are pre-inflated
+            const float tr = c1 != kNone ? box_entry_fast(r, t_min, lim, n2, n3) : INFINITY;
             if (tl == INFINITY && tr == INFINITY) {
                 node = pop();
             } else if (tr == INFINITY) {
