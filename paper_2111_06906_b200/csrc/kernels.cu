@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Co
 
 // compute_flag_mask (engine.cpp:172-199) with segment ends per Engine::segment_end
 // (engine.cpp:135-139); occlusion boxes staged in shared memory.
-__global__ void __launch_bounds__(kT) k_occlusion_flags(SceneDev S, PathDev P, int mode, int record,
+__global__ void __launch_bounds__(kT, 4) k_occlusion_flags(SceneDev S, PathDev P, int mode, int record,
                                                         uint32_t* list, uint32_t* masks, Counters* ctr) {
     __shared__ Box boxes[kMaxDyn];
     const FrameParams* fp = S.fp;
@@ -175,11 +175,14 @@ __global__ void __launch_bounds__(kT) k_occlusion_flags(SceneDev S, PathDev P, i
         uint32_t mask = 0;
         V3 prev = ld3(P.origin[i]);
         uint32_t prev_obj = kInvalidObj;
+        // vertex s+1 is loaded while segment s is tested (the loop is load-latency bound)
+        float4 nextv = k > 0 ? __ldcs(&P.pos_obj[vix(P, 0, i)]) : make_float4(0.f, 0.f, 0.f, 0.f);
         for (uint32_t s = 0; s < segs; ++s) {
             V3 cur{0, 0, 0};
             uint32_t cur_obj = kInvalidObj;
             if (s < k) {
-                const float4 v = P.pos_obj[vix(P, s, i)];
+                const float4 v = nextv;
+                if (s + 1 < k) nextv = __ldcs(&P.pos_obj[vix(P, s + 1, i)]);
                 cur = ld3(v);
                 cur_obj = __float_as_uint(v.w);
             }
