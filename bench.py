@@ -37,7 +37,8 @@ WORKLOADS = {
     "C4": dict(desc="Villa-scale synthetic (1.02M static tris + 8 x 20K dynamic + 2 moving lights)",
                mode="error", paths=5000000, bounces=7, threshold=0.001),
 }
-CPU_SAMPLE_PATHS = {"C1": 65536, "C2": 131072, "C3": 16384, "C4": 16384}
+# reference CPU sample sizes (~10 s of CPU work for the bench line, per-path cost scales linearly)
+CPU_SAMPLE_PATHS = {"C1": 65536, "C2": 1048576, "C3": 524288, "C4": 1048576}
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
@@ -201,9 +202,10 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": dict(config, cpu_sample_paths=sample),
                 "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "reference",
-                                 "sample": f"first {sample} of {n_paths} paths (path-prefix; per-path "
-                                           f"work is independent), {args.warmup} warm-up + "
-                                           f"{args.steps} timed frames incl. gather_image"},
+                                 "sample": f"the {name} scene and configuration with {sample} of its "
+                                           f"{n_paths} paths (per-path cost is independent of the path "
+                                           f"count), {args.warmup} warm-up + {args.steps} timed frames "
+                                           f"incl. gather_image"},
                 "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -360,8 +362,9 @@ def main():
             cpu_value, det = run_reference(args, name, sample, 2, 1)
             line["cpu_baseline"] = {"value": cpu_value, "unit": unit, "cores": os.cpu_count(),
                                     "kind": "reference",
-                                    "sample": f"first {sample} of {n_paths} paths, 1 warm-up + 2 "
-                                              f"timed frames incl. gather_image"}
+                                    "sample": f"the {name} scene and configuration with {sample} of its "
+                                              f"{n_paths} paths (per-path cost is independent of the path "
+                                              f"count), 1 warm-up + 2 timed frames incl. gather_image"}
         except Exception as exc:  # oracle not built on this box
             line["cpu_baseline"] = {"value": None, "unit": unit, "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"unavailable: {exc}"}
