@@ -307,6 +307,13 @@ prx_status prx_engine_upload(prx_engine* engine, int field, uint32_t index, cons
  * used after uploading a full state captured from another implementation. */
 prx_status prx_engine_set_frame_counter(prx_engine* engine, int32_t frames_run);
 
+/* intersect_scene / occluded (scene.cpp:136-177) on the engine's current frame state (the
+ * static BVH + the dynamic objects as placed by the last frame_update), as one GPU batch.
+ * rays: n x 8 floats {origin xyz, dir xyz (unit), t_min, t_max}.  any_hit == 0: hits n x 9
+ * floats {t, object id (u32 bits, 0xFFFFFFFF = miss), Hit::triangle (u32 bits), position
+ * xyz, normal xyz}; any_hit != 0: hits n floats, 1 = occluded.  Host buffers. */
+prx_status prx_intersect_batch(prx_engine* engine, const float* rays, size_t n, int any_hit, float* hits);
+
 /* ---- offline artefacts (byte-compatible with the reference's files) ---- */
 /* PHM1 photon dump, photon_store.cpp:55-102: "PHM1", u32 n_paths, u32 max_bounces, u32 0,
  * then n_paths*max_bounces 32-byte Photon records in b*N+p order.  PRX_E_RUNTIME on I/O

@@ -49,6 +49,7 @@ _SIGS = [
                                                C.POINTER(C.c_uint32), C.POINTER(C.c_size_t)]),
     ("prxref_intersect_batch", C.c_int, [_P, C.c_int, C.POINTER(C.c_float), C.c_size_t,
                                          C.POINTER(C.c_float)]),
+    ("prxref_occluded_batch", C.c_int, [_P, C.c_int, C.POINTER(C.c_float), C.c_size_t, C.POINTER(C.c_float)]),
     ("prxref_scene_load_text", C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(_P)]),
     ("prxref_write_photon_dump", C.c_int, [_P, C.c_char_p]),
     ("prxref_write_image", C.c_int, [C.c_char_p, C.POINTER(C.c_float), C.c_uint32, C.c_uint32]),
@@ -135,6 +136,13 @@ class RefScene:
                                            rays.ctypes.data_as(C.POINTER(C.c_float)),
                                            rays.shape[0], hits.ctypes.data_as(C.POINTER(C.c_float))))
         return hits
+
+    def occluded(self, frame: int, rays: np.ndarray) -> np.ndarray:
+        rays = np.ascontiguousarray(rays, dtype=np.float32).reshape(-1, 8)
+        out = np.zeros(rays.shape[0], dtype=np.float32)
+        check(lib().prxref_occluded_batch(self._h, int(frame), rays.ctypes.data_as(C.POINTER(C.c_float)),
+                                          rays.shape[0], out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
 
 
 _DT = {

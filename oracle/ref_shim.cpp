@@ -699,6 +699,19 @@ int prxref_intersect_batch(void* sp, int frame, const float* rays, size_t n, flo
     });
 }
 
+// occluded (scene.cpp:170-177) for a ray batch {o, d, t_min, t_max} -> 1/0 floats
+int prxref_occluded_batch(void* sp, int frame, const float* rays, size_t n, float* out) {
+    return guarded([&] {
+        const Scene& s = static_cast<RefScene*>(sp)->scene;
+        const SceneState st = state_at(s, frame);
+        for (size_t i = 0; i < n; ++i) {
+            const float* r = rays + 8 * i;
+            const Ray ray{{r[0], r[1], r[2]}, {r[3], r[4], r[5]}, r[6], r[7]};
+            out[i] = occluded(ray, st) ? 1.0f : 0.0f;
+        }
+    });
+}
+
 // ---- offline artefacts through the reference's own writers ----
 // load_scene_text (scene.cpp:272-379)
 int prxref_scene_load_text(const char* text, const char* base_dir, void** out) {

@@ -168,6 +168,7 @@ SIGNATURES = [
     ("prx_engine_download", C.c_int, [P, C.c_int, C.c_uint32, P, C.c_size_t]),
     ("prx_engine_upload", C.c_int, [P, C.c_int, C.c_uint32, P, C.c_size_t]),
     ("prx_engine_set_frame_counter", C.c_int, [P, C.c_int32]),
+    ("prx_intersect_batch", C.c_int, [P, C.POINTER(C.c_float), C.c_size_t, C.c_int, C.POINTER(C.c_float)]),
     ("prx_photon_dump_write", C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, P, C.c_size_t]),
     ("prx_photon_dump_read", C.c_int, [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), P,
                                        C.c_size_t]),

@@ -317,6 +317,16 @@ prx_status prx_engine_set_frame_counter(prx_engine* engine, int32_t frames_run) 
     return guarded([&] { eng(engine).set_frame_counter(frames_run); });
 }
 
+prx_status prx_intersect_batch(prx_engine* engine, const float* rays, size_t n, int any_hit, float* hits) {
+    return guarded([&] {
+        if (n) {
+            need(rays, "rays");
+            need(hits, "hits");
+        }
+        eng(engine).intersect_batch(rays, n, any_hit, hits);
+    });
+}
+
 // ------------------------------------------------------------------ offline artefacts
 prx_status prx_photon_dump_write(const char* path, uint32_t n_paths, uint32_t max_bounces, const void* records,
                                  size_t bytes) {

@@ -796,15 +796,18 @@ __device__ __forceinline__ int dyn_closest_exact(const SceneDev& S, const RayPre
 }
 
 // intersect_scene (scene.cpp:136-168), one-shot form: static phase, then the dynamic phase.
-__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h) {
+// `t_max` is the ray's (Ray::t_max, FLT_MAX in every engine query); `tri` (optional) receives
+// Hit::triangle: the static triangle's index in scene order, or the index inside its mesh.
+__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h,
+                                                float t_max = FLT_MAX, uint32_t* tri = nullptr) {
     const RayPre r = make_ray(o, d);
-    float t_max = FLT_MAX;
     uint32_t sbest = 0;
     const bool found = static_closest_exact(S, r, t_min, t_max, sbest);
     uint32_t dj = 0, dtri = 0;
     int kind = dyn_closest_exact(S, r, t_min, t_max, dj, dtri);
     if (kind < 0) kind = found ? 0 : -1;
     if (kind < 0) return false;
+    if (tri) *tri = kind == 0 ? __float_as_uint(__ldg(&S.stris[3 * sbest]).w) : dtri;
     V3 e1, e2;
     if (kind == 0) {
         const float4 q1 = __ldg(&S.stris[3 * sbest + 1]);

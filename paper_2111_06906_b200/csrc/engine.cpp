@@ -961,6 +961,23 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
     }
 }
 
+// ----------------------------------------------------------------------- scene queries
+void Engine::intersect_batch(const float* rays, size_t n, int any_hit, float* hits) {
+    PRX_CUDA(cudaSetDevice(device_));
+    if (n == 0) return;
+    if (n > 0xFFFFFFFFull / 9) throw std::invalid_argument("intersect_batch: too many rays");
+    const size_t out_floats = any_hit ? n : 9 * n;
+    DevBuf d_rays, d_out;
+    d_rays.alloc(sizeof(float) * 8 * n);
+    d_out.alloc(sizeof(float) * out_floats);
+    copy_async(d_rays.get(), rays, sizeof(float) * 8 * n, cudaMemcpyHostToDevice);
+    launch_intersect_batch(scene_dev(), d_rays.as<float>(), static_cast<uint32_t>(n), any_hit, d_out.as<float>(),
+                           stream_);
+    copy_async(hits, d_out.get(), sizeof(float) * out_floats, cudaMemcpyDeviceToHost);
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+    PRX_CUDA(cudaGetLastError());
+}
+
 // ----------------------------------------------------------------------- field I/O
 size_t Engine::field_bytes(int field, uint32_t index) const {
     const size_t nv = static_cast<size_t>(n_) * B_;

@@ -83,6 +83,7 @@ public:
     void download(int field, uint32_t index, void* dst, size_t bytes);
     void upload(int field, uint32_t index, const void* src, size_t bytes);
     void set_frame_counter(int frames_run);
+    void intersect_batch(const float* rays, size_t n, int any_hit, float* hits);
     void set_stream(cudaStream_t s);
     void synchronize();
     void info(prx_engine_info* out) const;

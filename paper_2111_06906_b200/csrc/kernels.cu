@@ -731,6 +731,35 @@ __global__ void k_finalize(PathDev P, Counters* ctr) {
     warp_add(&ctr->segments, segs_sum);
 }
 
+// ---------------------------------------------------------------- scene queries
+// intersect_scene / occluded (scene.cpp:136-177) for a batch of rays {o, d, t_min, t_max}:
+// closest -> 9 floats {t, object, triangle, position, normal}; any-hit -> 1 float.
+__global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_intersect_batch(SceneDev S, const float* __restrict__ rays,
+                                                                        uint32_t n, int any_hit, float* out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float* q = rays + 8ull * i;
+        const V3 o{q[0], q[1], q[2]}, d{q[3], q[4], q[5]};
+        if (any_hit) {
+            out[i] = occluded(S, o, d, q[6], q[7]) ? 1.0f : 0.0f;
+            continue;
+        }
+        Hit h;
+        uint32_t tri = 0;
+        float* w = out + 9ull * i;
+        if (intersect_scene(S, o, d, q[6], h, q[7], &tri)) {
+            w[0] = h.t;
+            w[1] = __uint_as_float(h.obj);
+            w[2] = __uint_as_float(tri);
+            w[3] = h.pos.x, w[4] = h.pos.y, w[5] = h.pos.z;
+            w[6] = h.normal.x, w[7] = h.normal.y, w[8] = h.normal.z;
+        } else {
+            w[0] = 0.0f;
+            w[1] = __uint_as_float(kInvalidObj);
+            for (int k = 2; k < 9; ++k) w[k] = 0.0f;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- layout conversion
 struct PhotonRec {  // photon_store.hpp:13-21
     float dx, dy, dz;
@@ -877,6 +906,9 @@ void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* c
     cudaMemsetAsync(work, 0, 4, st);
     k_trace<<<grid, kT, 0, st>>>(S, P, list, count, work, ctr);
     ++g_launches;
+}
+void launch_intersect_batch(SceneDev S, const float* rays, uint32_t n, int any_hit, float* out, cudaStream_t st) {
+    LAUNCH(k_intersect_batch, n, S, rays, n, any_hit, out);
 }
 void launch_finalize(PathDev P, Counters* ctr, cudaStream_t st) { LAUNCH(k_finalize, P.n, P, ctr); }
 void launch_pack_photons(PathDev P, void* photons, void* aux, cudaStream_t st) {

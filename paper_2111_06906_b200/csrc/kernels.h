@@ -62,6 +62,8 @@ void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st);
 void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count,
                   uint32_t* work, Counters* ctr, cudaStream_t st);
 void launch_finalize(PathDev P, Counters* ctr, cudaStream_t st);
+// intersect_scene / occluded for a ray batch (scene.cpp:136-177)
+void launch_intersect_batch(SceneDev S, const float* rays, uint32_t n, int any_hit, float* out, cudaStream_t st);
 // layout conversion for drop-in accessors
 void launch_pack_photons(PathDev P, void* photons, void* aux, cudaStream_t st);
 void launch_unpack_photons(PathDev P, const void* photons, const void* aux, cudaStream_t st);

@@ -301,6 +301,15 @@ class Engine:
     def photon_map(self) -> np.ndarray:
         return self.download("photons")
 
+    def intersect(self, rays: np.ndarray, any_hit: bool = False) -> np.ndarray:
+        """intersect_scene / occluded (scene.cpp:136-177) at the current frame for rays
+        [n, 8] = {origin, dir, t_min, t_max}: [n, 9] hits (see prx_intersect_batch) or [n]."""
+        r = np.ascontiguousarray(rays, dtype=np.float32).reshape(-1, 8)
+        out = np.zeros((r.shape[0],) if any_hit else (r.shape[0], 9), dtype=np.float32)
+        L.check(L.lib().prx_intersect_batch(self._h, r.ctypes.data_as(C.POINTER(C.c_float)), r.shape[0],
+                                            int(bool(any_hit)), out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
+
     def write_photon_dump(self, path: str) -> None:
         """write_photon_dump(engine.photon_map(), path) (photon_store.cpp:76-86)."""
         L.check(L.lib().prx_engine_write_photon_dump(self._h, str(path).encode()))
