@@ -699,6 +699,128 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
     return found;
 }
 
+// One walk over both fast trees (static SAH tree and combined dynamic LBVH): codes carry
+// kTreeBit for the dynamic tree, and candidates compare as (t, tree, position) -- static
+// before dynamic at equal t, which is intersect_scene's tie rule (the static hit shrinks
+// t_max first and dynamic hits must be strictly nearer).  A hit in either tree culls both,
+// so rays that hit a mover skip most of the static tree.  Returns the winner and a
+// certificate bound as fast_closest (second = smallest accepted t above the winner over both
+// trees, which bounds the reference's running t_max in either phase from below).
+constexpr uint32_t kTreeBit = 0x40000000u;
+#ifndef PRX_JOINT_STATIC_FIRST
+#define PRX_JOINT_STATIC_FIRST 0
+#endif
+template <bool kAny>
+__device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r, float t_min, float t_max,
+                                              float& best_t, uint32_t& best_tree, uint32_t& best_pos,
+                                              float& t_cert) {
+    constexpr uint32_t kNone = 0xFFFFFFFFu;
+    best_t = t_max;
+    best_pos = kNone;
+    best_tree = 0;
+    float second = t_max;
+    bool found = false;
+    uint2* const ss = trav_short_stack();
+    const uint32_t stride = blockDim.x;
+    uint2 overflow[64 - kShortStack];
+    int sp = 0;
+    auto push = [&](uint32_t c, float ent) {
+        const uint2 e = make_uint2(c, __float_as_uint(ent));
+        if (sp < kShortStack) ss[sp * stride] = e;
+        else overflow[sp - kShortStack] = e;
+        ++sp;
+    };
+    auto pop = [&]() -> uint32_t {
+        while (sp > 0) {
+            --sp;
+            const uint2 e = sp < kShortStack ? ss[sp * stride] : overflow[sp - kShortStack];
+            if (__uint_as_float(e.y) <= cull_limit(best_t)) return e.x;
+        }
+        return kNone;
+    };
+#if PRX_JOINT_STATIC_FIRST
+    push(kTreeBit, t_min);     // dynamic root, after the static tree
+    uint32_t node = 0u;        // static root
+#else
+    push(0u, t_min);           // static root, after the (small) dynamic tree
+    uint32_t node = kTreeBit;  // dynamic root
+#endif
+    uint32_t leaf = kNone;
+    while (node != kNone || leaf != kNone) {
+        while (node != kNone && !(node & kLeafBit)) {
+            const uint32_t tree = node & kTreeBit;
+            const float4* N = (tree ? S.danodes : S.fnodes) + 4ull * (node & ~kTreeBit);
+            const float4 n0 = __ldg(&N[0]), n1 = __ldg(&N[1]), n2 = __ldg(&N[2]), n3 = __ldg(&N[3]);
+            const uint32_t c0 = __float_as_uint(n0.w) | tree, c1r = __float_as_uint(n1.w);
+            const uint32_t c1 = c1r | tree;
+            const float lim = cull_limit(best_t);
+            const float tl = box_entry_fast(r, t_min, lim, n0, n1);  // boxes are pre-inflated
+            const float tr = c1r != kNone ? box_entry_fast(r, t_min, lim, n2, n3) : INFINITY;
+            if (tl == INFINITY && tr == INFINITY) {
+                node = pop();
+            } else if (tr == INFINITY) {
+                node = c0;
+            } else if (tl == INFINITY) {
+                node = c1;
+            } else if (tl <= tr) {
+                push(c1, tr);
+                node = c0;
+            } else {
+                push(c0, tl);
+                node = c1;
+            }
+            if (node != kNone && (node & kLeafBit) && leaf == kNone) {  // park the leaf
+                leaf = node;
+                node = pop();
+            }
+            if (!__any_sync(__activemask(), leaf == kNone)) break;
+        }
+        if (leaf == kNone && node != kNone && (node & kLeafBit)) {
+            leaf = node;
+            node = pop();
+        }
+        while (leaf != kNone) {
+            const uint32_t tree = (leaf & kTreeBit) ? 1u : 0u;
+            const float4* tris = tree ? S.datris : S.ftris;
+            const uint32_t first = (leaf & ~(kLeafBit | kTreeBit)) >> 3, count = (leaf & 7u) + 1u;
+            for (uint32_t k = first; k < first + count; ++k) {
+                const float4 ta = __ldg(&tris[3 * k]);
+                const float4 t1 = __ldg(&tris[3 * k + 1]);
+                const float4 t2 = __ldg(&tris[3 * k + 2]);
+                const uint32_t pos = __float_as_uint(ta.w);
+                float t;
+                const float lim = found ? fminf(cull_limit(best_t), t_max) : t_max;
+                if (intersect_tri(r.o, r.d, t_min, lim, ld3(ta), ld3(t1), ld3(t2), t)) {
+                    if (kAny) {
+                        best_t = t;
+                        best_tree = tree;
+                        best_pos = pos;
+                        t_cert = t_max;
+                        return true;
+                    }
+                    if (!found || t < best_t ||
+                        (t == best_t && (tree < best_tree || (tree == best_tree && pos < best_pos)))) {
+                        if (found && t < best_t) second = best_t;
+                        best_t = t;
+                        best_tree = tree;
+                        best_pos = pos;
+                        found = true;
+                    } else if (t > best_t && t < second) {
+                        second = t;
+                    }
+                }
+            }
+            leaf = kNone;
+            if (node != kNone && (node & kLeafBit)) {
+                leaf = node;
+                node = pop();
+            }
+        }
+    }
+    t_cert = fminf(fminf(second, cull_limit(best_t)), t_max);
+    return found;
+}
+
 __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, float t_min, float t_max,
                                             float& best_t, uint32_t& best_pos, float& t_cert) {
     return fast_closest<false>(S.fnodes, S.ftris, r, t_min, t_max, best_t, best_pos, t_cert);
@@ -795,19 +917,10 @@ __device__ __forceinline__ int dyn_closest_exact(const SceneDev& S, const RayPre
     return dyn_closest_seq(S, r, t_min, t_max, dj, dtri);
 }
 
-// intersect_scene (scene.cpp:136-168), one-shot form: static phase, then the dynamic phase.
-// `t_max` is the ray's (Ray::t_max, FLT_MAX in every engine query); `tri` (optional) receives
-// Hit::triangle: the static triangle's index in scene order, or the index inside its mesh.
-__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h,
-                                                float t_max = FLT_MAX, uint32_t* tri = nullptr) {
-    const RayPre r = make_ray(o, d);
-    uint32_t sbest = 0;
-    const bool found = static_closest_exact(S, r, t_min, t_max, sbest);
-    uint32_t dj = 0, dtri = 0;
-    int kind = dyn_closest_exact(S, r, t_min, t_max, dj, dtri);
-    if (kind < 0) kind = found ? 0 : -1;
-    if (kind < 0) return false;
-    if (tri) *tri = kind == 0 ? __float_as_uint(__ldg(&S.stris[3 * sbest]).w) : dtri;
+// Hit of intersect_scene for the winner: kind 0 static triangle at BVH position sbest,
+// kind 1 dynamic object dj, triangle dtri of its mesh; t is the hit distance.
+__device__ __forceinline__ void make_hit(const SceneDev& S, V3 o, V3 d, int kind, uint32_t sbest, uint32_t dj,
+                                         uint32_t dtri, float t, Hit& h) {
     V3 e1, e2;
     if (kind == 0) {
         const float4 q1 = __ldg(&S.stris[3 * sbest + 1]);
@@ -822,11 +935,50 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
         e2 = ld3(__ldg(&T[2]));
         h.obj = D.obj;
     }
-    h.t = t_max;
-    h.pos = add(o, mul(d, t_max));
+    h.t = t;
+    h.pos = add(o, mul(d, t));
     V3 n = normalized(cross(e1, e2));  // Triangle::geometric_normal (geometry.hpp:64)
     if (dot(n, d) > 0.0f) n = neg(n);
     h.normal = n;
+}
+
+// intersect_scene (scene.cpp:136-168), one-shot form: static phase, then the dynamic phase.
+// `t_max` is the ray's (Ray::t_max, FLT_MAX in every engine query); `tri` (optional) receives
+// Hit::triangle: the static triangle's index in scene order, or the index inside its mesh.
+__device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h,
+                                                float t_max = FLT_MAX, uint32_t* tri = nullptr) {
+    const RayPre r = make_ray(o, d);
+    if (S.fast && S.dfast && S.n_nodes > 0 && S.fp->n_dyn > 0) {
+        // one walk over both trees; the winner's certificate makes it the two-phase answer:
+        // a static winner beats every dynamic hit, so the dynamic phase adds nothing; a
+        // dynamic winner is strictly nearer than every static hit, and its gate is certified
+        // at the bound (which the reference's running t_max at that object exceeds)
+        float bt, tc;
+        uint32_t tree, pos;
+        if (!joint_closest<false>(S, r, t_min, t_max, bt, tree, pos, tc)) return false;
+        bool ok;
+        uint32_t dj = 0, dtri = 0;
+        if (tree == 0) {
+            ok = static_cert(S, r, t_min, tc, pos);
+        } else {
+            dj = __ldg(&S.dtri_obj[pos]);
+            dtri = pos - S.fp->dyn[dj].tri_begin;
+            ok = ray_box(r, t_min, tc, S.fp->dyn[dj].cur);
+        }
+        if (ok) {
+            if (tri) *tri = tree == 0 ? __float_as_uint(__ldg(&S.stris[3 * pos]).w) : dtri;
+            make_hit(S, o, d, tree == 0 ? 0 : 1, pos, dj, dtri, bt, h);
+            return true;
+        }
+    }
+    uint32_t sbest = 0;
+    const bool found = static_closest_exact(S, r, t_min, t_max, sbest);
+    uint32_t dj = 0, dtri = 0;
+    int kind = dyn_closest_exact(S, r, t_min, t_max, dj, dtri);
+    if (kind < 0) kind = found ? 0 : -1;
+    if (kind < 0) return false;
+    if (tri) *tri = kind == 0 ? __float_as_uint(__ldg(&S.stris[3 * sbest]).w) : dtri;
+    make_hit(S, o, d, kind, sbest, dj, dtri, t_max, h);
     return true;
 }
 
@@ -835,6 +987,16 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
 // certifies when its own object's gate passes, else the sequential loop decides.
 __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_min, float t_max) {
     const RayPre r = make_ray(o, d);
+    if (S.fast && S.dfast && S.n_nodes > 0 && S.fp->n_dyn > 0) {
+        // one walk over both trees to the first accepted triangle; it decides when its own
+        // reference path (static leaf, or its object's gate) passes at the fixed t_max
+        float bt, tc;
+        uint32_t tree, pos;
+        if (!joint_closest<true>(S, r, t_min, t_max, bt, tree, pos, tc)) return false;
+        if (tree == 0 ? static_cert(S, r, t_min, t_max, pos)
+                      : ray_box(r, t_min, t_max, S.fp->dyn[__ldg(&S.dtri_obj[pos])].cur))
+            return true;
+    }
     if (static_any_exact(S, r, t_min, t_max)) return true;
     const FrameParams* fp = S.fp;
     if (fp->n_dyn == 0) return false;
