@@ -706,7 +706,7 @@ void Engine::prune_trim_all(uint32_t* const* prefix_tab, uint32_t* const* total_
     launch_prune_trim(P, d_fp_.as<FrameParams>(), d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), cnt + kCntTrim,
                       n_, d_light_ptrs_.as<uint32_t*>() + PRX_MAX_LIGHTS, prefix_tab, d_flags8_.as<uint8_t>(),
                       stream_);
-    launch_prune_apply(P, d_flags8_.as<uint8_t>(), stream_);
+    launch_prune_apply(P, d_flags8_.as<uint8_t>(), in_full_frame_ ? 0 : 1, stream_);
     for (size_t li = 0; li < lights_.size(); ++li)
         launch_dm_after_prune(lights_[li].dm_c.as<uint32_t>(), lights_[li].dm_t.as<uint32_t>(), total_host[li],
                               lights_[li].cells, stream_);
@@ -807,7 +807,9 @@ void Engine::read_back(prx_frame_stats* st, bool with_times) {
 void Engine::retrace_invalid(prx_frame_stats* st) {
     PRX_CUDA(cudaSetDevice(device_));
     record(kEvPrune0);
+    in_full_frame_ = true;  // prune -> fill -> trace run back to back: skip the prune clears
     if (cfg_.mode != PRX_MODE_BASELINE) stage_prune_local();
+    in_full_frame_ = false;
     record(kEvFill0);
     stage_fill_local();
     record(kEvTrace0);

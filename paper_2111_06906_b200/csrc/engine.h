@@ -98,6 +98,7 @@ private:
     // every host<->device copy of the frame/splat/field paths goes through here (counted)
     void copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
     uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+    bool in_full_frame_ = false;  // retrace_invalid: prune/fill/trace back to back
 
     struct LightBlock {
         const Light* light = nullptr;

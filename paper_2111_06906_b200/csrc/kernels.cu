@@ -566,11 +566,20 @@ __global__ void k_prune_trim(const FrameParams* fp, const uint32_t* keys, const 
     }
 }
 
-__global__ void k_prune_apply(PathDev P, const uint8_t* pruned) {
+// clear_records == 0 inside a full frame: every dead slot is refilled and retraced by the same
+// frame (sum of fill deficits == dead slots, engine.cpp:499-546), and the retrace rewrites all
+// of the path's records, so the scattered record clears (sector read-modify-writes) are skipped;
+// only the stage-by-stage entry points need the intermediate state materialised.
+__global__ void k_prune_apply(PathDev P, const uint8_t* pruned, int clear_records) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
         if (!pruned[i]) continue;
         uchar4 m = P.meta[i];
-        truncate_path(P, i, 0, false, m);
+        if (clear_records) {
+            truncate_path(P, i, 0, false, m);
+        } else {
+            m.x = 0;
+            m.y = 0;
+        }
         m.z = kDead;
         P.meta[i] = m;
     }
@@ -870,8 +879,8 @@ void launch_prune_trim(PathDev P, const FrameParams* fp, const uint32_t* keys, c
     LAUNCH(k_prune_heads, n_max, keys, count, seg_start);
     LAUNCH(k_prune_trim, n_max, fp, keys, vals, count, seg_start, prefix, pruned);
 }
-void launch_prune_apply(PathDev P, const uint8_t* pruned, cudaStream_t st) {
-    LAUNCH(k_prune_apply, P.n, P, pruned);
+void launch_prune_apply(PathDev P, const uint8_t* pruned, int clear_records, cudaStream_t st) {
+    LAUNCH(k_prune_apply, P.n, P, pruned, clear_records);
 }
 void launch_dm_after_prune(uint32_t* dm_c, const uint32_t* dm_t, const uint32_t* unm, uint32_t cells,
                            cudaStream_t st) {

@@ -43,7 +43,7 @@ void launch_prune_keys(PathDev P, const FrameParams* fp, const uint32_t* list, c
 void launch_prune_trim(PathDev P, const FrameParams* fp, const uint32_t* keys, const uint32_t* vals,
                        const uint32_t* count, uint32_t n_max, uint32_t* const* seg_start,
                        uint32_t* const* prefix, uint8_t* pruned, cudaStream_t st);
-void launch_prune_apply(PathDev P, const uint8_t* pruned, cudaStream_t st);
+void launch_prune_apply(PathDev P, const uint8_t* pruned, int clear_records, cudaStream_t st);
 void launch_dm_after_prune(uint32_t* dm_c, const uint32_t* dm_t, const uint32_t* unm_total,
                            uint32_t cells, cudaStream_t st);
 // stage_fill (engine.cpp:499-546)
