@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -17,8 +18,11 @@ namespace prx {
 
 namespace {
 
-constexpr int kBins = 16;
-constexpr uint32_t kMaxLeaf = 8;
+constexpr int kMaxBins = 64;
+// build knobs (PRX_SAH_BINS / PRX_SAH_TRAV / PRX_SAH_MAXLEAF override, for tuning runs)
+int g_bins = 16;
+float g_trav = 1.0f;
+uint32_t g_max_leaf = 8;
 
 struct Prim {
     Box box;
@@ -48,8 +52,9 @@ struct Builder {
         for (int axis = 0; axis < 3; ++axis) {
             const float lo = comp(cb.lo, axis), hi = comp(cb.hi, axis);
             if (!(hi > lo)) continue;
-            Box bb[kBins];
-            uint32_t cnt[kBins] = {};
+            const int kBins = g_bins;
+            Box bb[kMaxBins];
+            uint32_t cnt[kMaxBins] = {};
             for (int k = 0; k < kBins; ++k) bb[k] = empty_box();
             const float scale = kBins / (hi - lo);
             for (uint32_t i = b; i < e; ++i) {
@@ -59,8 +64,8 @@ struct Builder {
                 ++cnt[k];
                 expand(bb[k], p.box);
             }
-            float right_area[kBins];
-            uint32_t right_cnt[kBins];
+            float right_area[kMaxBins];
+            uint32_t right_cnt[kMaxBins];
             Box acc = empty_box();
             uint32_t c = 0;
             for (int k = kBins - 1; k > 0; --k) {
@@ -84,12 +89,13 @@ struct Builder {
             }
         }
         const float leaf_cost = area(bounds) * n;
-        if (n <= kMaxLeaf && (best_axis < 0 || leaf_cost <= best_cost + area(bounds) * 1.0f)) return leaf(b, n);
+        if (n <= g_max_leaf && (best_axis < 0 || leaf_cost <= best_cost + area(bounds) * g_trav)) return leaf(b, n);
         uint32_t mid;
         if (best_axis < 0) {  // all centroids coincide: split in the middle
             mid = b + n / 2;
         } else {
             const float lo = comp(cb.lo, best_axis), hi = comp(cb.hi, best_axis);
+            const int kBins = g_bins;
             const float scale = kBins / (hi - lo);
             auto it = std::partition(idx.begin() + b, idx.begin() + e, [&](uint32_t i) {
                 int k = static_cast<int>((comp(prims[i].c, best_axis) - lo) * scale);
@@ -115,7 +121,7 @@ struct Builder {
     }
 
     uint32_t leaf(uint32_t b, uint32_t n) {
-        if (n > kMaxLeaf) {  // should not happen with the SAH guard; split evenly
+        if (n > 8) {  // leaf codes hold <= 8 triangles: split evenly
             Box lb = empty_box(), rb = empty_box();
             const uint32_t mid = b + n / 2;
             for (uint32_t i = b; i < mid; ++i) expand(lb, prims[idx[i]].box);
@@ -136,6 +142,10 @@ struct Builder {
 }  // namespace
 
 FastBvh build_fast_bvh(const std::vector<Tri>& tris_ref_order, float pad) {
+    if (const char* e = std::getenv("PRX_SAH_BINS")) g_bins = std::min(std::max(std::atoi(e), 4), kMaxBins);
+    if (const char* e = std::getenv("PRX_SAH_TRAV")) g_trav = static_cast<float>(std::atof(e));
+    if (const char* e = std::getenv("PRX_SAH_MAXLEAF"))
+        g_max_leaf = static_cast<uint32_t>(std::min(std::max(std::atoi(e), 1), 8));
     FastBvh out;
     const uint32_t n = static_cast<uint32_t>(tris_ref_order.size());
     if (n == 0) return out;
