@@ -392,10 +392,11 @@ void Engine::upload_scene() {
 
 void Engine::alloc_state() {
     const size_t nv = static_cast<size_t>(n_) * B_;
-    d_pos_obj_.alloc(16 * nv);
-    d_energy_.alloc(16 * nv);
-    d_in_dir_.alloc(16 * nv);
-    d_out_dir_.alloc(16 * nv);
+    // vertex streams, interleaved per vertex so that every vertex write of the trace is a
+    // whole 32-byte sector (no read-modify-write): [B][n] x {pos_obj, energy} and
+    // [B][n] x {in_dir, out_dir}
+    d_pos_obj_.alloc(32 * nv);
+    d_in_dir_.alloc(32 * nv);
     d_origin_.alloc(16ull * n_);
     d_emis_.alloc(16ull * n_);
     d_canon_.alloc(16ull * n_);
@@ -408,9 +409,7 @@ void Engine::alloc_state() {
     // reference initial state (engine.cpp:104-116): empty photons, emission dir (0,0,1),
     // everything else zero, status dead, retrace 0xFF
     PRX_CUDA(cudaMemsetAsync(d_pos_obj_.get(), 0, d_pos_obj_.size(), stream_));
-    PRX_CUDA(cudaMemsetAsync(d_energy_.get(), 0, d_energy_.size(), stream_));
     PRX_CUDA(cudaMemsetAsync(d_in_dir_.get(), 0, d_in_dir_.size(), stream_));
-    PRX_CUDA(cudaMemsetAsync(d_out_dir_.get(), 0, d_out_dir_.size(), stream_));
     PRX_CUDA(cudaMemsetAsync(d_origin_.get(), 0, d_origin_.size(), stream_));
     PRX_CUDA(cudaMemsetAsync(d_canon_.get(), 0, d_canon_.size(), stream_));
     PRX_CUDA(cudaMemsetAsync(d_cell_.get(), 0, d_cell_.size(), stream_));
@@ -426,8 +425,8 @@ void Engine::alloc_state() {
         std::vector<float4> po(std::min<size_t>(nv, 1 << 20), float4{0, 0, 0, f_of_u(kInvalidObj)});
         for (size_t off = 0; off < nv; off += po.size()) {
             const size_t cnt = std::min(po.size(), nv - off);
-            PRX_CUDA(cudaMemcpyAsync(d_pos_obj_.as<float4>() + off, po.data(), 16 * cnt,
-                                     cudaMemcpyHostToDevice, stream_));
+            PRX_CUDA(cudaMemcpy2DAsync(d_pos_obj_.as<float4>() + 2 * off, 32, po.data(), 16, 16, cnt,
+                                       cudaMemcpyHostToDevice, stream_));
             PRX_CUDA(cudaStreamSynchronize(stream_));
         }
     }
@@ -488,10 +487,10 @@ PathDev Engine::path_dev() const {
     P.n = n_;
     P.base = sb_;
     P.B = B_;
-    P.pos_obj = d_pos_obj_.as<float4>();
-    P.energy = d_energy_.as<float4>();
+    P.pos_obj = d_pos_obj_.as<float4>();  // element v at [2 v] (kernels index 2 * v)
+    P.energy = d_pos_obj_.as<float4>() + 1;
     P.in_dir = d_in_dir_.as<float4>();
-    P.out_dir = d_out_dir_.as<float4>();
+    P.out_dir = d_in_dir_.as<float4>() + 1;
     P.origin = d_origin_.as<float4>();
     P.emis = d_emis_.as<float4>();
     P.canon = d_canon_.as<float4>();
@@ -1032,10 +1031,18 @@ void Engine::download(int field, uint32_t index, void* dst, size_t bytes) {
             launch_pack_photons(path_dev(), nullptr, tmp.get(), stream_);
             src = tmp.get();
             break;
-        case PRX_FIELD_POS_OBJ: src = d_pos_obj_.get(); break;
-        case PRX_FIELD_ENERGY: src = d_energy_.get(); break;
-        case PRX_FIELD_IN_DIR: src = d_in_dir_.get(); break;
-        case PRX_FIELD_OUT_DIR: src = d_out_dir_.get(); break;
+        case PRX_FIELD_POS_OBJ:
+        case PRX_FIELD_ENERGY:
+        case PRX_FIELD_IN_DIR:
+        case PRX_FIELD_OUT_DIR: {  // one float4 of each interleaved 32-byte vertex record
+            const float4* base = field == PRX_FIELD_POS_OBJ || field == PRX_FIELD_ENERGY ? d_pos_obj_.as<float4>()
+                                                                                         : d_in_dir_.as<float4>();
+            const int off = field == PRX_FIELD_ENERGY || field == PRX_FIELD_OUT_DIR ? 1 : 0;
+            PRX_CUDA(cudaMemcpy2DAsync(dst, 16, base + off, 32, 16, bytes / 16, cudaMemcpyDeviceToHost, stream_));
+            d2h_bytes_ += bytes;
+            PRX_CUDA(cudaStreamSynchronize(stream_));
+            return;
+        }
         case PRX_FIELD_ORIGIN: src = d_origin_.get(); break;
         case PRX_FIELD_EMISSION_DIR: src = d_emis_.get(); break;
         case PRX_FIELD_CANONICAL: src = d_canon_.get(); break;
@@ -1070,10 +1077,18 @@ void Engine::upload(int field, uint32_t index, const void* src, size_t bytes) {
             PRX_CUDA(cudaStreamSynchronize(stream_));
             return;
         }
-        case PRX_FIELD_POS_OBJ: dst = d_pos_obj_.get(); break;
-        case PRX_FIELD_ENERGY: dst = d_energy_.get(); break;
-        case PRX_FIELD_IN_DIR: dst = d_in_dir_.get(); break;
-        case PRX_FIELD_OUT_DIR: dst = d_out_dir_.get(); break;
+        case PRX_FIELD_POS_OBJ:
+        case PRX_FIELD_ENERGY:
+        case PRX_FIELD_IN_DIR:
+        case PRX_FIELD_OUT_DIR: {
+            float4* base = field == PRX_FIELD_POS_OBJ || field == PRX_FIELD_ENERGY ? d_pos_obj_.as<float4>()
+                                                                                   : d_in_dir_.as<float4>();
+            const int off = field == PRX_FIELD_ENERGY || field == PRX_FIELD_OUT_DIR ? 1 : 0;
+            PRX_CUDA(cudaMemcpy2DAsync(base + off, 32, src, 16, 16, bytes / 16, cudaMemcpyHostToDevice, stream_));
+            h2d_bytes_ += bytes;
+            PRX_CUDA(cudaStreamSynchronize(stream_));
+            return;
+        }
         case PRX_FIELD_ORIGIN: dst = d_origin_.get(); break;
         case PRX_FIELD_EMISSION_DIR: dst = d_emis_.get(); break;
         case PRX_FIELD_CANONICAL: dst = d_canon_.get(); break;
@@ -1146,7 +1161,7 @@ void Engine::info(prx_engine_info* out) const {
     }
     uint64_t bytes = 0;
     for (const DevBuf* b : {&d_nodes_, &d_stris_, &d_dyn_local_, &d_dyn_world_, &d_lbvh_nodes_, &d_pos_obj_,
-                            &d_energy_, &d_in_dir_, &d_out_dir_, &d_origin_, &d_emis_, &d_canon_, &d_cell_,
+                            &d_in_dir_, &d_origin_, &d_emis_, &d_canon_, &d_cell_,
                             &d_epoch_, &d_path_info_, &d_seg_flags_, &d_meta_, &d_rstart_, &d_list_, &d_masks_,
                             &d_keys_, &d_vals_, &d_keys_tmp_, &d_vals_tmp_, &d_pruned_list_})
         bytes += b->size();

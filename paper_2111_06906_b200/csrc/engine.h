@@ -169,7 +169,7 @@ private:
     DevBuf d_light_ptrs_;  // uint32_t*[3][PRX_MAX_LIGHTS]: unm, seg_start, prefix
 
     // path state
-    DevBuf d_pos_obj_, d_energy_, d_in_dir_, d_out_dir_, d_origin_, d_emis_, d_canon_, d_cell_,
+    DevBuf d_pos_obj_, d_in_dir_, d_origin_, d_emis_, d_canon_, d_cell_,
         d_epoch_, d_path_info_, d_seg_flags_, d_meta_, d_rstart_;
     // work arrays
     DevBuf d_list_, d_masks_, d_flags8_, d_flags8b_, d_keys_, d_vals_, d_keys_tmp_, d_vals_tmp_,

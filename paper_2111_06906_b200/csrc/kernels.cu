@@ -39,9 +39,9 @@ __device__ __forceinline__ void truncate_path(const PathDev& P, uint32_t i, uint
                                               bool escaped, uchar4& m) {
     for (uint32_t b = new_count; b < P.B; ++b) {
         const size_t v = vix(P, b, i);
-        __stcs(&P.in_dir[v], make_float4(0.f, 0.f, 0.f, 0.f));
-        __stcs(&P.pos_obj[v].w, __uint_as_float(kInvalidObj));
-        __stcs(&P.energy[v], make_float4(0.f, 0.f, 0.f, 0.f));
+        __stcs(&P.in_dir[2 * (v)], make_float4(0.f, 0.f, 0.f, 0.f));
+        __stcs(&P.pos_obj[2 * (v)].w, __uint_as_float(kInvalidObj));
+        __stcs(&P.energy[2 * (v)], make_float4(0.f, 0.f, 0.f, 0.f));
     }
     m.x = (unsigned char)new_count;
     m.y = escaped ? 1 : 0;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Co
         if (L.kind == PRX_LIGHT_POINT || L.kind == PRX_LIGHT_SPOT) {
             P.origin[i] = make_float4(L.position.x, L.position.y, L.position.z, 0.f);
             if (m.x > 0) {
-                const V3 primary = ld3(P.pos_obj[i]);
+                const V3 primary = ld3(P.pos_obj[2 * (i)]);
                 const V3 to = sub(primary, L.position);
                 const float dist = length(to);
                 if (dist <= S.eps) {
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Co
         } else {
             if (m.x > 0) {
                 const V3 d = ld3(P.emis[i]);
-                const V3 primary = ld3(P.pos_obj[i]);
+                const V3 primary = ld3(P.pos_obj[2 * (i)]);
                 const float denom = dot(d, L.normal);
                 if (denom <= 1e-6f) {
                     m.z = kReplace;
@@ -176,13 +176,13 @@ __global__ void __launch_bounds__(kT, 4) k_occlusion_flags(SceneDev S, PathDev P
         V3 prev = ld3(P.origin[i]);
         uint32_t prev_obj = kInvalidObj;
         // vertex s+1 is loaded while segment s is tested (the loop is load-latency bound)
-        float4 nextv = k > 0 ? __ldcs(&P.pos_obj[vix(P, 0, i)]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 nextv = k > 0 ? __ldcs(&P.pos_obj[2 * (vix(P, 0, i))]) : make_float4(0.f, 0.f, 0.f, 0.f);
         for (uint32_t s = 0; s < segs; ++s) {
             V3 cur{0, 0, 0};
             uint32_t cur_obj = kInvalidObj;
             if (s < k) {
                 const float4 v = nextv;
-                if (s + 1 < k) nextv = __ldcs(&P.pos_obj[vix(P, s + 1, i)]);
+                if (s + 1 < k) nextv = __ldcs(&P.pos_obj[2 * (vix(P, s + 1, i))]);
                 cur = ld3(v);
                 cur_obj = __float_as_uint(v.w);
             }
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kT, 4) k_occlusion_flags(SceneDev S, PathDev P
             if (!flagged) {
                 V3 b = cur;
                 if (s >= k) {  // escape segment, clipped to twice the diagonal
-                    const V3 dir = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
+                    const V3 dir = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, s - 1, i))]);
                     b = add(prev, mul(dir, S.two_diag));
                 }
                 // bounding-box reject before the slab test: a segment whose box misses an
@@ -310,8 +310,8 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
                 has = false;
                 continue;
             }
-            const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, s - 1, i)]);
-            const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
+            const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[2 * (vix(P, s - 1, i))]);
+            const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, s - 1, i))]);
             ++vis;
             trav_init(S, T, o, d, S.eps, FLT_MAX, false);
             ray = true;
@@ -333,25 +333,25 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
             continue;
         }
         const size_t v = vix(P, s, i);
-        const float4 stored = P.energy[v];
-        const V3 e_prev = s == 0 ? fp->lights[li].flux_pp : ld3(P.energy[vix(P, s - 1, i)]);
+        const float4 stored = P.energy[2 * (v)];
+        const V3 e_prev = s == 0 ? fp->lights[li].flux_pp : ld3(P.energy[2 * (vix(P, s - 1, i))]);
         const float4 am = __ldg(&S.mat[h.obj]);
         const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
         const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
         if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
-            __stcs(&P.in_dir[v], make_float4(d.x, d.y, d.z, 0.f));
-            __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
-            __stcs(&P.energy[v], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
+            __stcs(&P.in_dir[2 * (v)], make_float4(d.x, d.y, d.z, 0.f));
+            __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[2 * (v)], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
-            __stcs(&P.out_dir[v], make_float4(out.x, out.y, out.z, 0.f));
+            __stcs(&P.out_dir[2 * (v)], make_float4(out.x, out.y, out.z, 0.f));
             P.rstart[i] = (uint8_t)(s + 1);
             has = false;
             continue;
         }
-        const V3 old_pos = ld3(P.pos_obj[v]);
+        const V3 old_pos = ld3(P.pos_obj[2 * (v)]);
         const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
-        __stcs(&P.in_dir[v], make_float4(d.x, d.y, d.z, 0.f));
-        __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+        __stcs(&P.in_dir[2 * (v)], make_float4(d.x, d.y, d.z, 0.f));
+        __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
         if (s + 1 >= segs) {
             has = false;
             continue;
@@ -362,9 +362,9 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
             continue;
         }
         if (s + 1 < k) {
-            const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
+            const V3 next = ld3(P.pos_obj[2 * (vix(P, s + 1, i))]);
             const V3 od = normalized(sub(next, h.pos));
-            __stcs(&P.out_dir[v], make_float4(od.x, od.y, od.z, 0.f));
+            __stcs(&P.out_dir[2 * (v)], make_float4(od.x, od.y, od.z, 0.f));
         }
         force = true;
         ++s;
@@ -415,8 +415,8 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
             have = false;
             continue;
         }
-        const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, s - 1, i)]);
-        const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, s - 1, i)]);
+        const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[2 * (vix(P, s - 1, i))]);
+        const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, s - 1, i))]);
         ++vis;
         Hit h;
         const bool hit = intersect_scene(S, o, d, S.eps, h);
@@ -431,24 +431,24 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
             continue;
         }
         const size_t v = vix(P, s, i);
-        const float4 stored = P.energy[v];
-        const V3 e_prev = s == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[vix(P, s - 1, i)]);
+        const float4 stored = P.energy[2 * (v)];
+        const V3 e_prev = s == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[2 * (vix(P, s - 1, i))]);
         const float4 am = __ldg(&S.mat[h.obj]);
         const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
         const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
         if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
-            __stcs(&P.in_dir[v], make_float4(d.x, d.y, d.z, 0.f));
-            __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
-            __stcs(&P.energy[v], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
+            __stcs(&P.in_dir[2 * (v)], make_float4(d.x, d.y, d.z, 0.f));
+            __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[2 * (v)], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
-            __stcs(&P.out_dir[v], make_float4(out.x, out.y, out.z, 0.f));
+            __stcs(&P.out_dir[2 * (v)], make_float4(out.x, out.y, out.z, 0.f));
             P.rstart[i] = (uint8_t)(s + 1);
             continue;
         }
-        const V3 old_pos = ld3(P.pos_obj[v]);
+        const V3 old_pos = ld3(P.pos_obj[2 * (v)]);
         const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
-        __stcs(&P.in_dir[v], make_float4(d.x, d.y, d.z, 0.f));
-        __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+        __stcs(&P.in_dir[2 * (v)], make_float4(d.x, d.y, d.z, 0.f));
+        __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
         if (s + 1 >= segs) continue;
         have = true;
         const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
@@ -457,9 +457,9 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
             continue;
         }
         if (s + 1 < k) {
-            const V3 next = ld3(P.pos_obj[vix(P, s + 1, i)]);
+            const V3 next = ld3(P.pos_obj[2 * (vix(P, s + 1, i))]);
             const V3 od = normalized(sub(next, h.pos));
-            __stcs(&P.out_dir[v], make_float4(od.x, od.y, od.z, 0.f));
+            __stcs(&P.out_dir[2 * (v)], make_float4(od.x, od.y, od.z, 0.f));
         }
         force = true;
         ++s;
@@ -684,9 +684,9 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_trace(SceneDev S, PathDe
                     m = P.meta[i];
                     epoch = P.epoch[i];
                     b = P.rstart[i];
-                    pos = b == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[vix(P, b - 1, i)]);
-                    dir = b == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[vix(P, b - 1, i)]);
-                    energy = b == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[vix(P, b - 1, i)]);
+                    pos = b == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[2 * (vix(P, b - 1, i))]);
+                    dir = b == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, b - 1, i))]);
+                    energy = b == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[2 * (vix(P, b - 1, i))]);
                     if (b >= P.B) {
                         truncate_path(P, i, b, false, m);
                         P.meta[i] = m;
@@ -707,11 +707,11 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_trace(SceneDev S, PathDe
             const float4 am = __ldg(&S.mat[h.obj]);
             energy = mulv(energy, V3{am.x, am.y, am.z});
             const size_t v = vix(P, b, i);
-            __stcs(&P.in_dir[v], make_float4(dir.x, dir.y, dir.z, 0.f));
-            __stcs(&P.pos_obj[v], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
-            __stcs(&P.energy[v], make_float4(energy.x, energy.y, energy.z, S.gather_radius));
+            __stcs(&P.in_dir[2 * (v)], make_float4(dir.x, dir.y, dir.z, 0.f));
+            __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[2 * (v)], make_float4(energy.x, energy.y, energy.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, dir, p, epoch, b + 1);
-            __stcs(&P.out_dir[v], make_float4(out.x, out.y, out.z, 0.f));
+            __stcs(&P.out_dir[2 * (v)], make_float4(out.x, out.y, out.z, 0.f));
             pos = h.pos;
             dir = out;
             ++b;
@@ -783,7 +783,7 @@ struct AuxRec {  // photon_store.hpp:75-78
 __global__ void k_pack(PathDev P, PhotonRec* ph, AuxRec* aux) {
     const size_t total = (size_t)P.n * P.B;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const float4 po = P.pos_obj[v], en = P.energy[v], in = P.in_dir[v], od = P.out_dir[v];
+        const float4 po = P.pos_obj[2 * (v)], en = P.energy[2 * (v)], in = P.in_dir[2 * (v)], od = P.out_dir[2 * (v)];
         if (ph) ph[v] = PhotonRec{in.x, in.y, in.z, __float_as_uint(po.w), en.x, en.y, en.z, en.w};
         if (aux) aux[v] = AuxRec{po.x, po.y, po.z, od.x, od.y, od.z};
     }
@@ -794,16 +794,16 @@ __global__ void k_unpack(PathDev P, const PhotonRec* ph, const AuxRec* aux) {
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
         if (ph) {
             const PhotonRec r = ph[v];
-            __stcs(&P.in_dir[v], make_float4(r.dx, r.dy, r.dz, 0.f));
-            __stcs(&P.energy[v], make_float4(r.ex, r.ey, r.ez, r.radius));
-            P.pos_obj[v].w = __uint_as_float(r.obj);
+            __stcs(&P.in_dir[2 * (v)], make_float4(r.dx, r.dy, r.dz, 0.f));
+            __stcs(&P.energy[2 * (v)], make_float4(r.ex, r.ey, r.ez, r.radius));
+            P.pos_obj[2 * (v)].w = __uint_as_float(r.obj);
         }
         if (aux) {
             const AuxRec a = aux[v];
-            P.pos_obj[v].x = a.px;
-            P.pos_obj[v].y = a.py;
-            P.pos_obj[v].z = a.pz;
-            __stcs(&P.out_dir[v], make_float4(a.ox, a.oy, a.oz, 0.f));
+            P.pos_obj[2 * (v)].x = a.px;
+            P.pos_obj[2 * (v)].y = a.py;
+            P.pos_obj[2 * (v)].z = a.pz;
+            __stcs(&P.out_dir[2 * (v)], make_float4(a.ox, a.oy, a.oz, 0.f));
         }
     }
 }
