@@ -212,11 +212,18 @@ def main():
 
     import torch
 
+    # one process per GPU; PRX_DIST_BACKEND=gloo with fewer GPUs than ranks is a functional
+    # check of the sharded path only (ranks share a device), never a measurement
+    backend = os.environ.get("PRX_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2111_06906_b200 import pathreuse as pr
     from paper_2111_06906_b200 import _lib as L
 
@@ -250,6 +257,11 @@ def main():
             st = L.FrameStats()
             for k in L.FrameStats.COUNTS + ("live_segments_before", "paths_retraced"):
                 setattr(st, k, int(d[k]))
+            lm = d.get("local_ms", {})  # this rank's device stage times
+            st.ms_frame_update = lm.get("frame_update", 0.0)
+            st.ms_verify = lm.get("verify", 0.0)
+            st.t_trace = lm.get("trace", 0.0) * 1e-3  # compaction + trace + finalize
+            st.ms_retrace = lm.get("trace", 0.0)      # prune/fill exchanges not included
         else:
             st = L.FrameStats()
             L.check(L.lib().prx_run_frame(eng.handle, C.byref(st)))

@@ -50,8 +50,10 @@ class GpuExecutor:
 
         self.torch = torch
         self.engine = Engine(scene, config)
+        self.stream = torch_stream
         if torch_stream is not None:
             self.engine.set_stream(torch_stream.cuda_stream)
+        self._ev = {}
         info = self.engine.info()
         self.n_lights = info.n_lights
         self.cells = [info.dm_cells[i] for i in range(self.n_lights)]
@@ -60,12 +62,25 @@ class GpuExecutor:
         self._unm = [torch.zeros(c, dtype=torch.int32, device=self.device) for c in self.cells]
         self.st = L.FrameStats()
 
+    def _mark(self, name: str, end: bool):
+        """CUDA event on the engine's stream (stage times of this shard, for reporting)."""
+        if self.stream is None:
+            return
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        self._ev.setdefault(name, [None, None])[1 if end else 0] = ev
+
     def frame_update(self):
         self.st = L.FrameStats()
+        self._ev = {}
+        self._mark("frame_update", False)
         self.engine.frame_update(self.st)
+        self._mark("frame_update", True)
 
     def verify(self):
+        self._mark("verify", False)
         self.engine.verify_paths(self.st)
+        self._mark("verify", True)
 
     def dm_buffers(self) -> list:
         self.engine.synchronize()
@@ -106,9 +121,16 @@ class GpuExecutor:
         L.check(L.lib().prx_fill_apply(self.engine.handle, pa, ta, C.byref(self.st)))
 
     def trace(self) -> dict:
+        self._mark("trace", False)
         st = self.engine.run_stage("trace")
+        self._mark("trace", True)
         d = {k: getattr(st, k) for k in COUNTER_KEYS if k != "segments"}
         d["segments"] = st.rays_traced + st.rays_reused
+        # this shard's device stage times (CUDA events on its stream), for reporting
+        self.local_ms = {}
+        if self.stream is not None:
+            self.stream.synchronize()
+            self.local_ms = {k: a.elapsed_time(b) for k, (a, b) in self._ev.items() if a is not None and b is not None}
         return d
 
     def new_tensor(self, values, dtype="int64"):
@@ -182,7 +204,9 @@ def run_frame_distributed(ex, coll, frame: int) -> dict:
     local = ex.trace()
     cnt = ex.new_tensor(_frame_counts(local))
     coll.allreduce_sum_(cnt)
-    return _stats_from(cnt.cpu().tolist(), frame, ex.mode)
+    out = _stats_from(cnt.cpu().tolist(), frame, ex.mode)
+    out["local_ms"] = dict(getattr(ex, "local_ms", {}))
+    return out
 
 
 def run_frame_loopback(exs: List, frame: int) -> dict:
