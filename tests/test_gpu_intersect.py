@@ -105,3 +105,52 @@ def test_intersect_and_occluded_bit_exact(scene, synthetic, frames):
     assert hits.mean() > 0.3
     occ = eng.intersect(rays, any_hit=True)
     assert np.array_equal(occ, rs.occluded(frame, rays))
+
+
+def _offset_doc(offset):
+    """test_io's document with every object and light moved far from the origin."""
+    import json
+
+    from tests.test_io import DOC
+
+    d = json.loads(DOC)
+    ox, oy, oz = offset
+    for node in d["objects"] + d["lights"]:
+        kfs = node.get("keyframes") or [{"frame": 0}]
+        for kf in kfs:
+            t = kf.get("translation", [0, 0, 0])
+            kf["translation"] = [t[0] + ox, t[1] + oy, t[2] + oz]
+        node["keyframes"] = kfs
+    c = d["camera"]
+    c["position"] = [c["position"][0] + ox, c["position"][1] + oy, c["position"][2] + oz]
+    c["look_at"] = [c["look_at"][0] + ox, c["look_at"][1] + oy, c["look_at"][2] + oz]
+    return json.dumps(d)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("offset", [(12345.0, -6789.0, 4321.5), (-3.0e5, 2.5e5, 1.0e5)])
+def test_far_from_origin_bit_exact(tmp_path, offset):
+    """Coordinates far from the origin stress the float filters' margins (slab quotients,
+    box inflation relative to the scene diagonal, fma culling error bounds)."""
+    from oracle import ref
+    from tests.helpers import compare_state, counts
+    from tests.test_io import OBJ_TEXT
+
+    (tmp_path / "part.obj").write_text(OBJ_TEXT)
+    doc = _offset_doc(offset)
+    sc = pr.Scene.from_text(doc, str(tmp_path))
+    rs = ref.RefScene.from_text(doc, str(tmp_path))
+    cfg = dict(mode="error", paths=4000, bounces=5, dm=[2, 2, 8, 8], threshold=0.001, seed=3)
+    eng = pr.Engine(sc, pr.make_config(**cfg))
+    cpu = ref.RefEngine(rs, pr.make_config(**cfg))
+    cpu.set_workers(0)
+    for f in range(3):
+        sg, scs = eng.run_frame(), cpu.run_frame()
+        assert counts(sg) == counts(scs), f"frame {f}"
+        bad = compare_state(eng, cpu, eng.info().n_lights)
+        assert all(v == 0 for v in bad.values()), f"frame {f}: {bad}"
+    rays = make_rays(sc.describe(), 30000, np.random.default_rng(5), sc.diagonal)
+    frame = eng.info().frames_run - 1
+    got, want = eng.intersect(rays), rs.intersect(frame, rays)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert np.array_equal(eng.intersect(rays, any_hit=True), rs.occluded(frame, rays))
