@@ -35,9 +35,8 @@ __device__ __forceinline__ V3 ld3(const float4 v) { return V3{v.x, v.y, v.z}; }
 struct RayPre {
     V3 o, d;
     float inv[3];
-    float oinv[3];  // o * inv: the fast culling slabs are fma(bound, inv, -oinv)
-    float err[3];   // per-axis absolute error bound of those slabs (the rounding of oinv)
-    bool safe;      // all |d| components either 0 or large enough for the float filter
+    bool safe;  // all |d| components either 0 or large enough for the float filter
+    bool regular;  // safe and no zero component: the fast culling slabs need no branches
 };
 
 __device__ __forceinline__ RayPre make_ray(V3 o, V3 d) {
@@ -45,13 +44,14 @@ __device__ __forceinline__ RayPre make_ray(V3 o, V3 d) {
     r.o = o;
     r.d = d;
     r.safe = true;
+    r.regular = true;
     for (int a = 0; a < 3; ++a) {
         const float da = comp(d, a);
         r.inv[a] = da != 0.0f ? 1.0f / da : 0.0f;
-        r.oinv[a] = comp(o, a) * r.inv[a];
-        r.err[a] = 1.2e-7f * fabsf(r.oinv[a]) + 1e-30f;
         if (da != 0.0f && fabsf(da) < 1e-18f) r.safe = false;
+        if (da == 0.0f) r.regular = false;
     }
+    r.regular = r.regular && r.safe;
     return r;
 }
 
@@ -543,29 +543,16 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
     return t0 - t1 <= 2.0e-6f * (fabsf(t0) + fabsf(t1)) ? t0 : INFINITY;
 }
 
-// box_entry for the fast (culling-only) walks: one fma per slab bound.  fma(b, inv, -o*inv)
-// differs from (b - o) * inv by at most the rounding of o*inv (err[a]) plus a few ulps of the
-// result (covered by the relative slack), so each axis' slab is widened by its own err[a]:
-// still a conservative cull, and the entry stays a lower bound for the stack's culling.
+// box_entry for the fast (culling-only) walks.  Regular rays (no zero or tiny direction
+// component) take a branch-free slab with single-instruction min/max; the others fall back
+// to box_entry.  Same values and the same relative slack as box_entry.
 __device__ __forceinline__ float box_entry_fast(const RayPre& r, float t_min, float t_lim, float4 A, float4 B) {
-    float t0 = t_min, t1 = t_lim;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const float d = comp(r.d, a);
-        const float lo = a == 0 ? A.x : (a == 1 ? A.y : A.z);
-        const float hi = a == 0 ? B.x : (a == 1 ? B.y : B.z);
-        if (d == 0.0f || !r.safe) {
-            if (d == 0.0f) {
-                const float o = comp(r.o, a);
-                if (o < lo || o > hi) return INFINITY;
-            }
-            continue;  // no culling on an axis the float slab cannot bound
-        }
-        const float tn = __fmaf_rn(lo, r.inv[a], -r.oinv[a]);
-        const float tf = __fmaf_rn(hi, r.inv[a], -r.oinv[a]);
-        t0 = fmaxf(t0, fminf(tn, tf) - r.err[a]);
-        t1 = fminf(t1, fmaxf(tn, tf) + r.err[a]);
-    }
+    if (!r.regular) return box_entry(r, t_min, t_lim, A, B, 0.0f);
+    const float tnx = (A.x - r.o.x) * r.inv[0], tfx = (B.x - r.o.x) * r.inv[0];
+    const float tny = (A.y - r.o.y) * r.inv[1], tfy = (B.y - r.o.y) * r.inv[1];
+    const float tnz = (A.z - r.o.z) * r.inv[2], tfz = (B.z - r.o.z) * r.inv[2];
+    const float t0 = fmaxf(fmaxf(t_min, fminf(tnx, tfx)), fmaxf(fminf(tny, tfy), fminf(tnz, tfz)));
+    const float t1 = fminf(fminf(t_lim, fmaxf(tnx, tfx)), fminf(fmaxf(tny, tfy), fmaxf(tnz, tfz)));
     return t0 - t1 <= 2.0e-6f * (fabsf(t0) + fabsf(t1)) ? t0 : INFINITY;
 }
 
