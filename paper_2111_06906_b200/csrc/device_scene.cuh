@@ -609,10 +609,13 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
         ++sp;
     };
     auto pop = [&]() -> uint32_t {
+        const float lim = cull_limit(best_t);
         while (sp > 0) {
             --sp;
-            const uint2 e = sp < kShortStack ? ss[sp * stride] : overflow[sp - kShortStack];
-            if (__uint_as_float(e.y) <= cull_limit(best_t)) return e.x;
+            uint2 e;
+            if (sp < kShortStack) e = ss[sp * stride];
+            else e = overflow[sp - kShortStack];
+            if (__uint_as_float(e.y) <= lim) return e.x;
         }
         return kNone;
     };
@@ -718,10 +721,13 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
         ++sp;
     };
     auto pop = [&]() -> uint32_t {
+        const float lim = cull_limit(best_t);
         while (sp > 0) {
             --sp;
-            const uint2 e = sp < kShortStack ? ss[sp * stride] : overflow[sp - kShortStack];
-            if (__uint_as_float(e.y) <= cull_limit(best_t)) return e.x;
+            uint2 e;
+            if (sp < kShortStack) e = ss[sp * stride];
+            else e = overflow[sp - kShortStack];
+            if (__uint_as_float(e.y) <= lim) return e.x;
         }
         return kNone;
     };
