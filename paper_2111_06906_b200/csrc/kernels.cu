@@ -23,10 +23,23 @@ constexpr int kT = 256;
 #define PRX_TRACE_MINB 5  // resident CTAs per SM requested for the traversal kernels
 #endif
 
+// Block-wide sum of a per-thread counter, one atomic per CTA (a per-warp atomic on one
+// address serialises ~20K warps in the path-wide kernels).  Every thread of the block must
+// call it (the kernels call it once, after their grid-stride loop).
 __device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned long long v) {
+    __shared__ unsigned long long s_part[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+    if (lane == 0) s_part[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long x = lane < (int)(blockDim.x >> 5) ? s_part[lane] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0 && x) atomicAdd(dst, x);
+    }
+    __syncthreads();
 }
 
 __device__ __forceinline__ size_t vix(const PathDev& P, uint32_t b, uint32_t i) {
