@@ -332,13 +332,13 @@ int splat_table_bits(uint32_t npx) {
 
 size_t splat_work_bytes(uint32_t npx) {
     const uint64_t slots = 1ull << splat_table_bits(npx);
-    return slots * (8 + 4 + 4 + 4) + 4ull * 27 * npx + prim_scratch_bytes(slots) + 64;
+    return slots * (8 + 4 + 4 + 4) + 4ull * 27 * npx + prim_scratch_bytes(slots) + 64 + 256;
 }
 
 size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
     const uint64_t slots = 1ull << splat_table_bits(npx);
     const uint64_t nv = n_vertices;
-    return 64 + nv * (1 + 4 + 4 + 16 + 32) + slots * 8 + prim_scratch_bytes(nv > slots ? nv : slots) + 1024;
+    return 64 + nv * (1 + 4 + 4 + 16 + 32) + slots * 8 + prim_scratch_bytes(nv > slots ? nv : slots) + 16 * 256;
 }
 
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
@@ -351,7 +351,7 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
     uint32_t* off = cnt + slots;
     uint32_t* cursor = off + slots;
     uint32_t* list = cursor + slots;
-    void* scratch = list + 27ull * npx;
+    void* scratch = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(list + 27ull * npx) + 255) & ~uintptr_t(255));
 
     k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
     cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
@@ -361,23 +361,26 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
                                                                   nullptr, bits);
     if (mode == 1) {  // ordered, bit-exact gather
         const uint64_t nv = (uint64_t)P.n * P.B;
+        // carve the work buffer in 256-byte aligned pieces (float4 / u32 views of any n)
         char* w = static_cast<char*>(gather_buf);
-        uint32_t* m_count = reinterpret_cast<uint32_t*>(w);
-        w += 64;
-        uint32_t* pslot = reinterpret_cast<uint32_t*>(w);
-        w += 4 * nv;
-        uint32_t* cand = reinterpret_cast<uint32_t*>(w);
-        w += 4 * nv;
-        uint32_t* sk = reinterpret_cast<uint32_t*>(w);
-        uint32_t* sv = sk + nv;
-        uint32_t* sk2 = sv + nv;
-        uint32_t* sv2 = sk2 + nv;
-        float4* spo = reinterpret_cast<float4*>(sv2 + nv);
-        float4* sen = spo + nv;
-        uint32_t* pcnt = reinterpret_cast<uint32_t*>(sen + nv);
-        uint32_t* pstart = pcnt + slots;
-        uint8_t* flag = reinterpret_cast<uint8_t*>(pstart + slots);
-        void* gscratch = flag + nv + 256;
+        auto take = [&](size_t bytes) {
+            char* p = w;
+            w += (bytes + 255) & ~size_t(255);
+            return p;
+        };
+        uint32_t* m_count = reinterpret_cast<uint32_t*>(take(64));
+        uint32_t* pslot = reinterpret_cast<uint32_t*>(take(4 * nv));
+        uint32_t* cand = reinterpret_cast<uint32_t*>(take(4 * nv));
+        uint32_t* sk = reinterpret_cast<uint32_t*>(take(4 * nv));
+        uint32_t* sv = reinterpret_cast<uint32_t*>(take(4 * nv));
+        uint32_t* sk2 = reinterpret_cast<uint32_t*>(take(4 * nv));
+        uint32_t* sv2 = reinterpret_cast<uint32_t*>(take(4 * nv));
+        float4* spo = reinterpret_cast<float4*>(take(16 * nv));
+        float4* sen = reinterpret_cast<float4*>(take(16 * nv));
+        uint32_t* pcnt = reinterpret_cast<uint32_t*>(take(4 * slots));
+        uint32_t* pstart = reinterpret_cast<uint32_t*>(take(4 * slots));
+        uint8_t* flag = reinterpret_cast<uint8_t*>(take(nv));
+        void* gscratch = take(0);
         cudaMemsetAsync(pcnt, 0, 4 * slots, st);
         k_gather_flag<<<launch_grid(nv, kT), kT, 0, st>>>(P, radius, keys, bits, flag, pslot, pcnt);
         compact_u8(flag, (uint32_t)nv, nullptr, 0, cand, m_count, gscratch, st);

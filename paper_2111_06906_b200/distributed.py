@@ -218,8 +218,9 @@ def run_frame_loopback(exs: List, frame: int) -> dict:
         ex.frame_update()
         ex.verify()
     bufs = [ex.dm_buffers() for ex in exs]
+    dev0 = bufs[0][0].device if bufs[0] else None
     for li in range(len(bufs[0])):
-        s = sum(b[li].clone() for b in bufs)
+        s = sum(b[li].to(dev0) for b in bufs)  # shards may live on different devices
         for b in bufs:
             b[li].copy_(s)
     for ex, b in zip(exs, bufs):
@@ -229,7 +230,7 @@ def run_frame_loopback(exs: List, frame: int) -> dict:
         for r, ex in enumerate(exs):
             prefix, total = [], []
             for li in range(len(unms[0])):
-                p, s = _prefix_total(torch, [unms[q][li] for q in range(world)], r)
+                p, s = _prefix_total(torch, [unms[q][li].to(ex.device) for q in range(world)], r)
                 prefix.append(p)
                 total.append(s)
             ex.prune_apply(prefix, total)
@@ -265,3 +266,36 @@ class ShardedEngine:
         out = run_frame_distributed(self.exec, self.coll, self.frame)
         self.frame += 1
         return out
+
+
+class MultiGpuEngine:
+    """One process driving path shards on several GPUs (the reference's single Engine object
+    over N devices): the exchange protocol of run_frame_distributed run in-process
+    (run_frame_loopback), the image summed over the shards.  Frames and images are
+    bit-identical to one engine except the fp32 image sum order across shards."""
+
+    def __init__(self, scene: Scene, devices: Sequence[int] | None = None, **cfg):
+        import torch
+
+        self.torch = torch
+        devs = list(devices) if devices is not None else list(range(torch.cuda.device_count()))
+        n = cfg.get("paths", 10000)
+        self.execs = []
+        for r, dev in enumerate(devs):
+            c = make_config(shard=shard_range(n, r, len(devs)), device=dev, **cfg)
+            with torch.cuda.device(dev):
+                self.execs.append(GpuExecutor(scene, c, torch.cuda.current_stream(dev)))
+        self.frame = 0
+
+    def run_frame(self) -> dict:
+        out = run_frame_loopback(self.execs, self.frame)
+        self.frame += 1
+        return out
+
+    def splat(self, camera=None, radius: float = 0.25, mode: int = 1):
+        """Per-shard photons splatted on each device, summed on the host (float64 then fp32)."""
+        imgs = [ex.engine.splat(camera=camera, radius=radius, mode=mode) for ex in self.execs]
+        total = imgs[0].astype(np.float64)
+        for im in imgs[1:]:
+            total += im
+        return total.astype(np.float32)

@@ -37,3 +37,28 @@ def test_shards_match_single_engine(world, scene, mode):
         for li in range(exs[0].n_lights):
             for ex in exs:
                 assert np.array_equal(ex.engine.download("dm_current", li), single.download("dm_current", li))
+
+
+@pytest.mark.gpu
+def test_multi_gpu_engine_matches_single_engine():
+    """MultiGpuEngine over all visible devices (shards share the device when there is one)."""
+    import torch
+
+    from paper_2111_06906_b200.distributed import MultiGpuEngine
+
+    devices = list(range(torch.cuda.device_count()))
+    if len(devices) < 2:
+        devices = [0, 0]
+    cfg = dict(mode="error", paths=5003, bounces=5, dm=[2, 2, 8, 8], seed=9)
+    sc = pr.Scene.builtin("moving-cube")
+    single = pr.Engine(sc, pr.make_config(**cfg))
+    multi = MultiGpuEngine(sc, devices=devices, **cfg)
+    for f in range(4):
+        st = single.run_frame()
+        got = multi.run_frame()
+        for k in ("rays_traced", "rays_reused", "paths_replaced", "paths_pruned", "paths_filled", "visibility_rays"):
+            assert got[k] == getattr(st, k), (f, k)
+    img_single = single.splat(radius=0.25)
+    img_multi = multi.splat(radius=0.25)
+    assert np.allclose(img_multi, img_single, rtol=1e-4, atol=0)  # shard sums reorder the fp32 adds
+    assert np.array_equal(img_multi == 0, img_single == 0)

@@ -65,3 +65,14 @@ def test_ordered_gather_cameras():
         img_g = gpu.splat(camera=c, radius=radius, mode=1)
         img_c, _ = cpu.gather(camera=c, radius=radius)
         assert img_g.tobytes() == img_c.tobytes(), (w, h, radius)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("paths,bounces", [(20001, 5), (4097, 3), (999, 7)])
+def test_ordered_gather_odd_sizes(paths, bounces):
+    """Odd vertex counts (n x B) -- the work-buffer carving must keep every view aligned."""
+    gpu, cpu = pair("moving-cube", mode="error", paths=paths, bounces=bounces, dm=[2, 2, 8, 8], seed=21)
+    for _ in range(2):
+        gpu.run_frame()
+        cpu.run_frame()
+    assert gpu.splat(radius=0.25, mode=1).tobytes() == cpu.gather(radius=0.25)[0].tobytes()
