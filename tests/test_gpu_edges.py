@@ -66,3 +66,21 @@ def test_bounce_limits_rejected(bounces):
         pr.Engine(pr.Scene.builtin("static-box"), pr.make_config(paths=100, bounces=bounces))
     with pytest.raises(ValueError):
         ref.RefEngine(ref.RefScene.builtin("static-box"), pr.make_config(paths=100, bounces=bounces))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["naive", "error", "baseline"])
+def test_odd_sizes_bit_exact(mode):
+    """Odd path and vertex counts through every stage and the image."""
+    from oracle import ref
+
+    cfg = dict(mode=mode, paths=7777, bounces=5, dm=[3, 5, 7, 9], threshold=0.001, seed=29)
+    gpu = pr.Engine(pr.Scene.builtin("merry-go-round-analog"), pr.make_config(**cfg))
+    cpu = ref.RefEngine(ref.RefScene.builtin("merry-go-round-analog"), pr.make_config(**cfg))
+    cpu.set_workers(0)
+    for f in range(3):
+        sg, sc = gpu.run_frame(), cpu.run_frame()
+        assert counts(sg) == counts(sc), f
+        bad = compare_state(gpu, cpu, gpu.info().n_lights)
+        assert all(v == 0 for v in bad.values()), (f, bad)
+    assert gpu.splat(radius=0.25).tobytes() == cpu.gather(radius=0.25)[0].tobytes()
