@@ -17,6 +17,8 @@
 //   resolve         L = sum(E) * albedo / pi / (pi r^2) (gather.cpp:71).
 // The contributing (photon, pixel) set is identical to the reference's; only the fp32
 // summation order differs (tolerance class C).
+#include <cstdlib>
+
 #include "device_scene.cuh"
 #include "kernels.h"
 #include "prims.h"
@@ -233,17 +235,20 @@ __global__ void __launch_bounds__(kT) k_gather_staged(const float4* __restrict__
                                                       const uint32_t* __restrict__ pcnt,
                                                       const float4* __restrict__ spo, const float4* __restrict__ sen,
                                                       const float4* __restrict__ mat, float inv_pi, float inv_area,
-                                                      uint32_t* work, float* __restrict__ img) {
+                                                      uint32_t* work, float* __restrict__ img,
+                                                      const uint32_t* __restrict__ pix_list, const uint32_t* pix_count) {
     __shared__ float4 stage[kT];
+    const uint32_t n_items = pix_list ? *pix_count : npx;
     const uint32_t lane = threadIdx.x & 31;
     float4* const my = stage + (threadIdx.x & ~31u);
     const uint32_t mask = (1u << bits) - 1u;
     const float r2 = radius * radius;
     while (true) {
-        uint32_t pix = 0;
-        if (lane == 0) pix = atomicAdd(work, 1u);
-        pix = __shfl_sync(0xffffffffu, pix, 0);
-        if (pix >= npx) break;
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(work, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items) break;
+        const uint32_t pix = pix_list ? pix_list[item] : item;
         const float4 g = gbuf[pix];
         const uint32_t obj = __float_as_uint(g.w);
         if (obj == kInvalidObj) {  // no primary hit: pixel stays 0 (gather.cpp:66)
@@ -304,6 +309,128 @@ __global__ void __launch_bounds__(kT) k_gather_staged(const float4* __restrict__
     }
 }
 
+// ---- pixel groups: pixels whose hit points share a grid cell share the 27 neighbour cells
+// and their visiting order, so one warp can serve up to 32 of them: the warp stages each
+// chunk of 32 candidate photons in shared memory and every lane walks the chunk in order for
+// its own pixel (same tests, same per-pixel addition order as gather_image).  Pays off when
+// many pixels fall in one cell (high resolutions); small groups keep the per-pixel path.
+constexpr uint32_t kGroupMin = 12;
+
+__global__ void k_pixel_home(const float4* __restrict__ gbuf, uint32_t npx, float radius,
+                             const unsigned long long* __restrict__ keys, int bits, uint32_t* hk, uint32_t* pv) {
+    const uint32_t mask = (1u << bits) - 1u;
+    for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < npx; pix += gridDim.x * blockDim.x) {
+        const float4 g = gbuf[pix];
+        uint32_t slot = 1u << bits;  // no hit: sorts last
+        if (__float_as_uint(g.w) != kInvalidObj) {
+            const unsigned long long key =
+                grid_key(cell_coord(g.x, radius), cell_coord(g.y, radius), cell_coord(g.z, radius));
+            uint32_t s = slot_of(key, bits);
+            while (__ldg(&keys[s]) != key) s = (s + 1) & mask;  // inserted by k_pixcells
+            slot = s;
+        }
+        hk[pix] = slot;
+        pv[pix] = pix;
+    }
+}
+
+__global__ void k_group_heads(const uint32_t* __restrict__ hk, uint32_t npx, uint8_t* head) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < npx; j += gridDim.x * blockDim.x)
+        head[j] = (j == 0 || hk[j] != hk[j - 1]) ? 1 : 0;
+}
+
+// groups of >= kGroupMin hit pixels -> 32-pixel chunks; the rest -> the per-pixel list
+__global__ void k_group_split(const uint32_t* __restrict__ starts, const uint32_t* n_groups, uint32_t npx,
+                              const uint32_t* __restrict__ hk, const uint32_t* __restrict__ pv, int bits,
+                              uint2* chunks, uint32_t* n_chunks, uint32_t* small, uint32_t* n_small) {
+    const uint32_t G = *n_groups;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        const uint32_t b = starts[g], e = g + 1 < G ? starts[g + 1] : npx;
+        const uint32_t len = e - b;
+        if (hk[b] != (1u << bits) && len >= kGroupMin) {
+            const uint32_t nc = (len + 31) / 32;
+            const uint32_t c0 = atomicAdd(n_chunks, nc);
+            for (uint32_t c = 0; c < nc; ++c) chunks[c0 + c] = make_uint2(b + 32 * c, min(32u, len - 32 * c));
+        } else {
+            const uint32_t s0 = atomicAdd(n_small, len);
+            for (uint32_t k = 0; k < len; ++k) small[s0 + k] = pv[b + k];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_gather_groups(const float4* __restrict__ gbuf, float radius,
+                                                      const unsigned long long* __restrict__ keys, int bits,
+                                                      const uint32_t* __restrict__ pstart,
+                                                      const uint32_t* __restrict__ pcnt,
+                                                      const float4* __restrict__ spo, const float4* __restrict__ sen,
+                                                      const float4* __restrict__ mat, float inv_pi, float inv_area,
+                                                      const uint2* __restrict__ chunks, const uint32_t* n_chunks,
+                                                      const uint32_t* __restrict__ pv, uint32_t* work,
+                                                      float* __restrict__ img) {
+    __shared__ float4 s_pos[kT];
+    __shared__ float4 s_en[kT];
+    const uint32_t lane = threadIdx.x & 31;
+    float4* const wpos = s_pos + (threadIdx.x & ~31u);
+    float4* const wen = s_en + (threadIdx.x & ~31u);
+    const uint32_t mask = (1u << bits) - 1u;
+    const float r2 = radius * radius;
+    const uint32_t nch = *n_chunks;
+    while (true) {
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(work, 1u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= nch) break;
+        const uint2 ch = chunks[c];
+        const bool mine = lane < ch.y;
+        const uint32_t pix = mine ? pv[ch.x + lane] : pv[ch.x];
+        const float4 g = gbuf[pix];
+        const uint32_t obj = __float_as_uint(g.w);
+        const V3 x{g.x, g.y, g.z};
+        // every pixel of the chunk has this home cell (grouped by it)
+        const float4 g0 = gbuf[pv[ch.x]];
+        const long long cx = cell_coord(g0.x, radius), cy = cell_coord(g0.y, radius), cz = cell_coord(g0.z, radius);
+        float ax = 0.0f, ay = 0.0f, az = 0.0f;  // radiance += E (gather.cpp:68), per lane
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {  // gather.hpp:48-50 visiting order
+                    const unsigned long long key = grid_key(cx + dx, cy + dy, cz + dz);
+                    uint32_t s = slot_of(key, bits);
+                    unsigned long long k;
+                    while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
+                    if (k != key) continue;
+                    const uint32_t b0 = __ldg(&pstart[s]), n = __ldg(&pcnt[s]);
+                    for (uint32_t base = 0; base < n; base += 32) {
+                        const uint32_t j = base + lane;
+                        __syncwarp();
+                        if (j < n) {
+                            wpos[lane] = __ldg(&spo[b0 + j]);
+                            wen[lane] = __ldg(&sen[b0 + j]);
+                        }
+                        __syncwarp();
+                        const uint32_t m = n - base < 32 ? n - base : 32;
+                        if (mine) {
+                            for (uint32_t q = 0; q < m; ++q) {
+                                const float4 po = wpos[q];
+                                const V3 d = sub(V3{po.x, po.y, po.z}, x);  // gather.hpp:54
+                                if (dot(d, d) <= r2 && __float_as_uint(po.w) == obj) {
+                                    const float4 e = wen[q];
+                                    ax = ax + e.x;
+                                    ay = ay + e.y;
+                                    az = az + e.z;
+                                }
+                            }
+                        }
+                    }
+                }
+        if (mine) {
+            const float4 a = mat[obj];
+            img[3 * pix] = ((ax * a.x) * inv_pi) * inv_area;  // gather.cpp:71
+            img[3 * pix + 1] = ((ay * a.y) * inv_pi) * inv_area;
+            img[3 * pix + 2] = ((az * a.z) * inv_pi) * inv_area;
+        }
+    }
+}
+
 __global__ void k_resolve(const float4* __restrict__ gbuf, const float4* __restrict__ mat, float* img, uint32_t n,
                           float inv_pi, float inv_area) {
     for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < n; pix += gridDim.x * blockDim.x) {
@@ -338,7 +465,9 @@ size_t splat_work_bytes(uint32_t npx) {
 size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
     const uint64_t slots = 1ull << splat_table_bits(npx);
     const uint64_t nv = n_vertices;
-    return 64 + nv * (1 + 4 + 4 + 16 + 32) + slots * 8 + prim_scratch_bytes(nv > slots ? nv : slots) + 16 * 256;
+    uint64_t scan_n = nv > slots ? nv : slots;
+    if (npx > scan_n) scan_n = npx;
+    return 64 + nv * (1 + 4 + 4 + 16 + 32) + slots * 8 + 41ull * npx + 2 * prim_scratch_bytes(scan_n) + 32 * 256;
 }
 
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
@@ -389,11 +518,43 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
         k_gather_copy<<<launch_grid(nv, kT), kT, 0, st>>>(P, sv, m_count, spo, sen);
         g_launches += 6;
-        uint32_t* wq = m_count + 4;  // pixel work counter of k_gather_staged
-        cudaMemsetAsync(wq, 0, 4, st);
+        // Large images: pixel groups by home cell (sorted), big groups in 32-pixel chunks, the
+        // rest per pixel.  Small images (few pixels per cell) go straight to the per-pixel walk.
+        const char* genv = std::getenv("PRX_GATHER_GROUPS");
+        const bool groups = genv ? genv[0] == '1' : npx >= (1u << 18);
+        if (!groups) {
+            uint32_t* wq = m_count + 4;
+            cudaMemsetAsync(wq, 0, 4, st);
+            k_gather_staged<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt,
+                                                                         spo, sen, S.mat, inv_pi, inv_area, wq, img,
+                                                                         nullptr, nullptr);
+            ++g_launches;
+            return;
+        }
+        uint32_t* hk = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        uint32_t* pv = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        uint32_t* hk2 = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        uint32_t* pv2 = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        uint8_t* head = reinterpret_cast<uint8_t*>(take(npx));
+        uint32_t* starts = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        uint2* chunks = reinterpret_cast<uint2*>(take(8ull * npx));
+        uint32_t* small = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        void* gscratch2 = take(0);
+        uint32_t* ctl = m_count + 4;  // [0] group count, [1] chunks, [2] small, [3] / [4] work counters
+        cudaMemsetAsync(ctl, 0, 5 * 4, st);
+        k_pixel_home<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, hk, pv);
+        radix_sort_pairs(hk, pv, hk2, pv2, npx, nullptr, bits + 1, gscratch2, st);
+        k_group_heads<<<launch_grid(npx, kT), kT, 0, st>>>(hk, npx, head);
+        compact_u8(head, npx, nullptr, 0, starts, ctl + 0, gscratch2, st);
+        k_group_split<<<launch_grid(npx, kT), kT, 0, st>>>(starts, ctl + 0, npx, hk, pv, bits, chunks, ctl + 1, small,
+                                                         ctl + 2);
+        k_gather_groups<<<launch_grid(32ull * npx / 8 + 32, kT), kT, 0, st>>>(
+            gbuf, radius, keys, bits, pstart, pcnt, spo, sen, S.mat, inv_pi, inv_area, chunks, ctl + 1, pv, ctl + 3,
+            img);
         k_gather_staged<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt, spo,
-                                                                     sen, S.mat, inv_pi, inv_area, wq, img);
-        ++g_launches;
+                                                                     sen, S.mat, inv_pi, inv_area, ctl + 4, img, small,
+                                                                     ctl + 2);
+        g_launches += 6 + 3 * 4;
         return;
     }
     scan_exclusive_u32(cnt, off, (uint32_t)slots, nullptr, nullptr, scratch, st);

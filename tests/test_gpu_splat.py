@@ -76,3 +76,20 @@ def test_ordered_gather_odd_sizes(paths, bounces):
         gpu.run_frame()
         cpu.run_frame()
     assert gpu.splat(radius=0.25, mode=1).tobytes() == cpu.gather(radius=0.25)[0].tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("groups", ["0", "1"])
+@pytest.mark.parametrize("w,h", [(120, 90), (640, 480)])
+def test_ordered_gather_pixel_groups(monkeypatch, groups, w, h):
+    """The per-pixel walk and the pixel-group walk (one warp per 32 pixels sharing a home
+    cell, the default for large images) both reproduce gather_image byte for byte."""
+    from paper_2111_06906_b200 import _lib as L
+
+    monkeypatch.setenv("PRX_GATHER_GROUPS", groups)
+    gpu, cpu = pair("C2", synthetic=True, mode="naive", paths=40000, bounces=4, dm=[2, 2, 8, 8], seed=19)
+    gpu.run_frame()
+    cpu.run_frame()
+    cam = gpu.scene.describe().camera
+    c = L.Camera(cam.position, cam.look_at, cam.fov_deg, w, h)
+    assert gpu.splat(camera=c, radius=0.25, mode=1).tobytes() == cpu.gather(camera=c, radius=0.25)[0].tobytes()
