@@ -1,22 +1,21 @@
-// splat.cu -- photon splatting into an fp32 image (north_star subsystem 6), replacing the
-// reference's per-pixel gather_image (gather.cpp:35-75).
+// splat.cu -- gather_image (gather.cpp:35-75) on the GPU (north_star subsystem 6).
 //
 // The reference, per pixel: primary hit x (camera_ray + intersect_scene), then every live
 // photon in the 27 grid cells around cell(x) (cell edge = r, 21-bit wrapped keys,
-// gather.hpp:38-74) with the same object and |x_ph - x|^2 <= r^2 adds its energy.
-// Inverting that relation, photon ph contributes to pixel p iff key(cell(ph)) is one of
-// the 27 keys key(cell(x_p) + o).  So:
-//   K11 gbuffer     primary hits (same float ops as camera_ray / intersect_scene);
-//   K12a pixcells   each hit pixel inserts its 27 neighbour-cell keys into an
-//                   open-addressing hash table -> per-key pixel lists (count, scan, fill);
-//   K12b splat      every photon streams once through HBM (16 B {pos, obj}), probes the
-//                   table with its own cell key (an L2-resident table), and for each listed
-//                   pixel applies the reference filters and adds its energy with shared-memory
-//                   atomics into a CTA-private image (global atomics when the image does not
-//                   fit in shared memory);
-//   resolve         L = sum(E) * albedo / pi / (pi r^2) (gather.cpp:71).
-// The contributing (photon, pixel) set is identical to the reference's; only the fp32
-// summation order differs (tolerance class C).
+// gather.hpp:38-74) with the same object and |x_ph - x|^2 <= r^2 adds its energy, in cell
+// order (dz, dy, dx) and photon insertion order.
+//   k_gbuffer   primary hits (same float ops as camera_ray / intersect_scene);
+//   k_pixcells  each hit pixel inserts its 27 neighbour-cell keys into an open-addressing
+//               table (the cells any pixel can read);
+//   mode 1 (default, bit-exact): photons of those cells are compacted and stably sorted by
+//               cell slot (= the reference's insertion order per cell), copied contiguous, and
+//               summed per pixel in the reference's order -- one warp per pixel with staged
+//               in-order accumulation (k_gather_staged), or, for large images, one warp per 32
+//               pixels that share a home cell walking the shared candidates (k_gather_groups);
+//   mode 0 (fast, fp32 atomics): every photon probes the table with its own cell and adds its
+//               energy to the listed pixels with shared-memory atomics (k_splat_filter,
+//               k_splat); same contributing set, different summation order;
+//   resolve     L = sum(E) * albedo / pi / (pi r^2) (gather.cpp:71).
 #include <cstdlib>
 
 #include "device_scene.cuh"
