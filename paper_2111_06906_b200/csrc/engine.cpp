@@ -4,7 +4,9 @@
 // box arithmetic done here matches the reference's host arithmetic bit for bit.
 #include "engine.h"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -224,6 +226,7 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     PRX_CUDA(cudaMemsetAsync(d_cnt32_.get(), 0, 4 * kCntN, stream_));
 
     upload_scene();
+    apply_l2_policy();
     alloc_state();
     place_frame(0);
     if (cfg_.exact_trig >= 0) d_trig_ = exact_trig_table(device_);
@@ -247,6 +250,33 @@ Engine::~Engine() {
     if (stream_ && own_stream_) cudaStreamDestroy(stream_);
 }
 
+// Keep the traversal's static working set (C4: ~85 MB of nodes and triangles, read at random
+// by every ray) resident in L2 against the path store's streaming traffic: one persisting
+// access-policy window on the engine stream over the hot arena's prefix, sized to the
+// device's persisting-L2 limit. Opt-in (PRX_L2_PERSIST=1, or =N for an N MB cap): measured on
+// C4 it does not pay -- 8-16 MB windows are neutral, 32-85 MB slow every stage by 1-18% by
+// shrinking the normal L2 (profiles/r01_sweeps.md); traversal is issue-bound, not DRAM-bound.
+void Engine::apply_l2_policy() {
+    const char* env = std::getenv("PRX_L2_PERSIST");
+    if (!d_hot_.get() || !env || std::atoi(env) <= 0) return;
+    int max_persist = 0, max_window = 0;
+    PRX_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device_));
+    PRX_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device_));
+    if (max_persist <= 0 || max_window <= 0) return;
+    size_t limit = static_cast<size_t>(max_persist);
+    if (env && std::atoi(env) > 1) limit = std::min(limit, static_cast<size_t>(std::atoi(env)) << 20);
+    const size_t window = std::min({d_hot_.size(), static_cast<size_t>(max_window), limit});
+    PRX_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit));
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = d_hot_.get();
+    attr.accessPolicyWindow.num_bytes = window;
+    attr.accessPolicyWindow.hitRatio = 1.0f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    PRX_CUDA(cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &attr));
+    l2_window_ = window;
+}
+
 void Engine::upload_scene() {
     const Scene& s = *scene_;
     // static BVH nodes: {lo, a} {hi, b}; leaf: a = first | leaf bit, b = count
@@ -260,8 +290,6 @@ void Engine::upload_scene() {
             nodes[2 * i] = f4(n.bounds.lo, f_of_u(a));
             nodes[2 * i + 1] = f4(n.bounds.hi, f_of_u(b));
         }
-        d_nodes_.alloc(sizeof(float4) * nodes.size());
-        PRX_CUDA(cudaMemcpy(d_nodes_.get(), nodes.data(), d_nodes_.size(), cudaMemcpyHostToDevice));
         std::vector<float4> tris(3 * s.bvh_perm.size());
         for (size_t k = 0; k < s.bvh_perm.size(); ++k) {
             const uint32_t orig = s.bvh_perm[k];
@@ -279,8 +307,6 @@ void Engine::upload_scene() {
             const BvhNode& n = s.bvh_nodes[k];
             for (uint32_t i = 0; i < n.count; ++i) leaf_of[n.first + i] = static_cast<uint32_t>(k);
         }
-        d_leaf_of_.alloc(4 * leaf_of.size());
-        PRX_CUDA(cudaMemcpy(d_leaf_of_.get(), leaf_of.data(), d_leaf_of_.size(), cudaMemcpyHostToDevice));
         // the fast traversal's own SAH tree over the triangles in reference order
         std::vector<Tri> ref_order(s.bvh_perm.size());
         for (size_t k = 0; k < ref_order.size(); ++k) ref_order[k] = s.static_tris[s.bvh_perm[k]];
@@ -300,10 +326,20 @@ void Engine::upload_scene() {
             ft[3 * k + 1] = tris[3 * pos + 1];
             ft[3 * k + 2] = tris[3 * pos + 2];
         }
-        d_fnodes_.alloc(sizeof(float4) * fn.size());
-        d_ftris_.alloc(sizeof(float4) * ft.size());
-        PRX_CUDA(cudaMemcpy(d_fnodes_.get(), fn.data(), d_fnodes_.size(), cudaMemcpyHostToDevice));
-        PRX_CUDA(cudaMemcpy(d_ftris_.get(), ft.data(), d_ftris_.size(), cudaMemcpyHostToDevice));
+        // hot arena, hottest first: a window over its prefix keeps what fits persisting in L2
+        const auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+        const size_t b_fn = sizeof(float4) * fn.size(), b_ft = sizeof(float4) * ft.size();
+        const size_t b_lo = 4 * leaf_of.size(), b_nd = sizeof(float4) * nodes.size();
+        d_hot_.alloc(up(b_fn) + up(b_ft) + up(b_lo) + up(b_nd));
+        char* base = static_cast<char*>(d_hot_.get());
+        p_fnodes_ = reinterpret_cast<float4*>(base);
+        p_ftris_ = reinterpret_cast<float4*>(base + up(b_fn));
+        p_leaf_of_ = reinterpret_cast<uint32_t*>(base + up(b_fn) + up(b_ft));
+        p_nodes_ = reinterpret_cast<float4*>(base + up(b_fn) + up(b_ft) + up(b_lo));
+        PRX_CUDA(cudaMemcpy(p_fnodes_, fn.data(), b_fn, cudaMemcpyHostToDevice));
+        PRX_CUDA(cudaMemcpy(p_ftris_, ft.data(), b_ft, cudaMemcpyHostToDevice));
+        PRX_CUDA(cudaMemcpy(p_leaf_of_, leaf_of.data(), b_lo, cudaMemcpyHostToDevice));
+        PRX_CUDA(cudaMemcpy(p_nodes_, nodes.data(), b_nd, cudaMemcpyHostToDevice));
     }
     // materials / flags
     std::vector<float4> mat(s.objects.size());
@@ -455,13 +491,13 @@ void Engine::alloc_state() {
 
 SceneDev Engine::scene_dev() const {
     SceneDev S{};
-    S.nodes = d_nodes_.as<float4>();
+    S.nodes = p_nodes_;
     S.n_nodes = static_cast<uint32_t>(scene_->bvh_nodes.size());
-    S.leaf_of = d_leaf_of_.as<uint32_t>();
+    S.leaf_of = p_leaf_of_;
     S.cull_pad = 1e-5f * diag_ + 1e-6f;
     S.fast = cfg_.dfs_traversal ? 0 : 1;
-    S.fnodes = d_fnodes_.as<float4>();
-    S.ftris = d_ftris_.as<float4>();
+    S.fnodes = p_fnodes_;
+    S.ftris = p_ftris_;
     S.stris = d_stris_.as<float4>();
     S.dtris = d_dyn_world_.as<float4>();
     S.dnodes = d_lbvh_nodes_.as<float4>();
@@ -1160,7 +1196,7 @@ void Engine::info(prx_engine_info* out) const {
         out->flux_per_path[li][2] = b.flux_pp.z;
     }
     uint64_t bytes = 0;
-    for (const DevBuf* b : {&d_nodes_, &d_stris_, &d_dyn_local_, &d_dyn_world_, &d_lbvh_nodes_, &d_pos_obj_,
+    for (const DevBuf* b : {&d_hot_, &d_stris_, &d_dyn_local_, &d_dyn_world_, &d_lbvh_nodes_, &d_pos_obj_,
                             &d_in_dir_, &d_origin_, &d_emis_, &d_canon_, &d_cell_,
                             &d_epoch_, &d_path_info_, &d_seg_flags_, &d_meta_, &d_rstart_, &d_list_, &d_masks_,
                             &d_keys_, &d_vals_, &d_keys_tmp_, &d_vals_tmp_, &d_pruned_list_})

@@ -117,6 +117,7 @@ private:
     };
 
     void upload_scene();
+    void apply_l2_policy();
     void alloc_state();
     void fill_frame_params();
     void place_frame(int frame);
@@ -157,9 +158,15 @@ private:
     uint32_t n_dyn_tris_ = 0, n_lbvh_nodes_ = 0;
 
     // scene device data
-    DevBuf d_pow_tabs_, d_nodes_, d_leaf_of_, d_fnodes_, d_ftris_, d_stris_, d_mat_, d_oflags_, d_dyn_local_, d_dyn_world_, d_dyn_xf_, d_dyn_tri_xf_,
+    DevBuf d_pow_tabs_, d_stris_, d_mat_, d_oflags_, d_dyn_local_, d_dyn_world_, d_dyn_xf_, d_dyn_tri_xf_,
         d_lbvh_nodes_, d_lbvh_leaf_, d_lbvh_work_, d_dall_nodes_, d_dall_tris_;
     LbvhBuffers lbvh_{};
+    // the traversal's hot static data in one arena (fast SAH nodes | their triangles |
+    // leaf_of | reference nodes) so one L2 access-policy window can cover it (apply_l2_policy)
+    DevBuf d_hot_;
+    float4 *p_fnodes_ = nullptr, *p_ftris_ = nullptr, *p_nodes_ = nullptr;
+    uint32_t* p_leaf_of_ = nullptr;
+    size_t l2_window_ = 0;
     const float2* d_trig_ = nullptr;
 
     // frame params (pinned host + device)
