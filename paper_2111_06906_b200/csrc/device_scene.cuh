@@ -583,6 +583,16 @@ __device__ __forceinline__ uint2* trav_short_stack() {
 // visited (culling only drops boxes entered beyond the limit at the time, which is larger),
 // and the leaf window tracks the smallest such t above best_t, so
 // min(that, cull_limit(best_t), t_max) is a valid bound.
+#ifdef PRX_CERT_STATS  // diagnostic build only: [0] joint walks, [1] their certificate failures,
+// [2]/[3] any-hit walks / failures, [4]/[5] static/dynamic inner nodes, [6]/[7] static/dynamic triangles
+static __device__ unsigned long long g_cert_stats[8];
+#define PRX_CERT_COUNT(k) atomicAdd(&g_cert_stats[k], 1ull)
+#define PRX_CERT_ADD(k, v) atomicAdd(&g_cert_stats[k], (unsigned long long)(v))
+#else
+#define PRX_CERT_COUNT(k) ((void)0)
+#define PRX_CERT_ADD(k, v) ((void)0)
+#endif
+
 template <bool kAny>
 __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, const float4* __restrict__ tris,
                                              const RayPre& r, float t_min, float t_max, float& best_t,
@@ -739,9 +749,15 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
     uint32_t node = kTreeBit;  // dynamic root
 #endif
     uint32_t leaf = kNone;
+#ifdef PRX_CERT_STATS
+    uint32_t st_n[2] = {0, 0}, st_t[2] = {0, 0};
+#endif
     while (node != kNone || leaf != kNone) {
         while (node != kNone && !(node & kLeafBit)) {
             const uint32_t tree = node & kTreeBit;
+#ifdef PRX_CERT_STATS
+            ++st_n[tree ? 1 : 0];
+#endif
             const float4* N = (tree ? S.danodes : S.fnodes) + 4ull * (node & ~kTreeBit);
             const float4 n0 = __ldg(&N[0]), n1 = __ldg(&N[1]), n2 = __ldg(&N[2]), n3 = __ldg(&N[3]);
             const uint32_t c0 = __float_as_uint(n0.w) | tree, c1r = __float_as_uint(n1.w);
@@ -776,6 +792,9 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
             const uint32_t tree = (leaf & kTreeBit) ? 1u : 0u;
             const float4* tris = tree ? S.datris : S.ftris;
             const uint32_t first = (leaf & ~(kLeafBit | kTreeBit)) >> 3, count = (leaf & 7u) + 1u;
+#ifdef PRX_CERT_STATS
+            st_t[tree] += count;
+#endif
             for (uint32_t k = first; k < first + count; ++k) {
                 const float4 ta = __ldg(&tris[3 * k]);
                 const float4 t1 = __ldg(&tris[3 * k + 1]);
@@ -811,6 +830,12 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
         }
     }
     t_cert = fminf(fminf(second, cull_limit(best_t)), t_max);
+#ifdef PRX_CERT_STATS
+    PRX_CERT_ADD(4, st_n[0]);
+    PRX_CERT_ADD(5, st_n[1]);
+    PRX_CERT_ADD(6, st_t[0]);
+    PRX_CERT_ADD(7, st_t[1]);
+#endif
     return found;
 }
 
@@ -948,6 +973,7 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
         // at the bound (which the reference's running t_max at that object exceeds)
         float bt, tc;
         uint32_t tree, pos;
+        PRX_CERT_COUNT(0);
         if (!joint_closest<false>(S, r, t_min, t_max, bt, tree, pos, tc)) return false;
         bool ok;
         uint32_t dj = 0, dtri = 0;
@@ -963,6 +989,7 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
             make_hit(S, o, d, tree == 0 ? 0 : 1, pos, dj, dtri, bt, h);
             return true;
         }
+        PRX_CERT_COUNT(1);
     }
     uint32_t sbest = 0;
     const bool found = static_closest_exact(S, r, t_min, t_max, sbest);
@@ -985,10 +1012,12 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
         // reference path (static leaf, or its object's gate) passes at the fixed t_max
         float bt, tc;
         uint32_t tree, pos;
+        PRX_CERT_COUNT(2);
         if (!joint_closest<true>(S, r, t_min, t_max, bt, tree, pos, tc)) return false;
         if (tree == 0 ? static_cert(S, r, t_min, t_max, pos)
                       : ray_box(r, t_min, t_max, S.fp->dyn[__ldg(&S.dtri_obj[pos])].cur))
             return true;
+        PRX_CERT_COUNT(3);
     }
     if (static_any_exact(S, r, t_min, t_max)) return true;
     const FrameParams* fp = S.fp;

@@ -418,10 +418,39 @@ void Engine::upload_scene() {
             lbvh_.parent = w + 4 * n;
             lbvh_.flags = w + 4 * n + (2 * n + 2);
             lbvh_.scratch = w + 4 * n + 2 * (2 * n + 2);
-            d_dall_nodes_.alloc(sizeof(float4) * 4 * (n - 1));
             d_dall_tris_.alloc(sizeof(float4) * 3 * n);
-            lbvh_.all_nodes = d_dall_nodes_.as<float4>();
             lbvh_.all_tris = d_dall_tris_.as<float4>();
+            const char* kind = std::getenv("PRX_DYN_TREE");
+            if (kind && std::strcmp(kind, "karras") == 0) {  // per-frame Karras rebuild (A/B runs)
+                d_dall_nodes_.alloc(sizeof(float4) * 4 * (n - 1));
+            } else {  // per-object SAH topologies, built once, refit per frame
+                std::vector<std::vector<Tri>> objs;
+                std::vector<uint32_t> begins;
+                std::vector<Box> boxes;
+                for (const DynInfo& d : dyn_) {
+                    const Object& o = s.objects[d.obj];
+                    objs.push_back(o.mesh);
+                    begins.push_back(d.tri_begin);
+                    boxes.push_back(transform_box(o.local_bounds, transform_at(o.kfs, 0)));
+                }
+                const DynSahTopology topo = build_dyn_sah(objs, begins, boxes);
+                d_dall_nodes_.alloc(sizeof(float4) * topo.nodes.size());
+                PRX_CUDA(cudaMemcpy(d_dall_nodes_.get(), topo.nodes.data(), d_dall_nodes_.size(),
+                                    cudaMemcpyHostToDevice));
+                const size_t b_perm = 4 * topo.perm.size(), b_leaf = 4 * topo.leaves.size();
+                d_dsah_.alloc(b_perm + b_leaf + 4 * topo.parent.size());
+                char* base = d_dsah_.as<char>();
+                PRX_CUDA(cudaMemcpy(base, topo.perm.data(), b_perm, cudaMemcpyHostToDevice));
+                PRX_CUDA(cudaMemcpy(base + b_perm, topo.leaves.data(), b_leaf, cudaMemcpyHostToDevice));
+                PRX_CUDA(cudaMemcpy(base + b_perm + b_leaf, topo.parent.data(), 4 * topo.parent.size(),
+                                    cudaMemcpyHostToDevice));
+                lbvh_.sah_perm = reinterpret_cast<const uint32_t*>(base);
+                lbvh_.sah_leaf = reinterpret_cast<const uint4*>(base + b_perm);
+                lbvh_.sah_parent = reinterpret_cast<const uint32_t*>(base + b_perm + b_leaf);
+                lbvh_.n_sah_leaves = static_cast<uint32_t>(topo.leaves.size() / 4);
+                lbvh_.n_sah_nodes = static_cast<uint32_t>(topo.parent.size());
+            }
+            lbvh_.all_nodes = d_dall_nodes_.as<float4>();
         }
     }
 }

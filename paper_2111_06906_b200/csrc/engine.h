@@ -159,7 +159,7 @@ private:
 
     // scene device data
     DevBuf d_pow_tabs_, d_stris_, d_mat_, d_oflags_, d_dyn_local_, d_dyn_world_, d_dyn_xf_, d_dyn_tri_xf_,
-        d_lbvh_nodes_, d_lbvh_leaf_, d_lbvh_work_, d_dall_nodes_, d_dall_tris_;
+        d_lbvh_nodes_, d_lbvh_leaf_, d_lbvh_work_, d_dall_nodes_, d_dall_tris_, d_dsah_;
     LbvhBuffers lbvh_{};
     // the traversal's hot static data in one arena (fast SAH nodes | their triangles |
     // leaf_of | reference nodes) so one L2 access-policy window can cover it (apply_l2_policy)

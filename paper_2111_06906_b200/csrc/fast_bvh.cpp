@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <stdexcept>
 
 namespace prx {
 
@@ -190,6 +191,119 @@ FastBvh build_fast_bvh(const std::vector<Tri>& tris_ref_order, float pad) {
     for (FastNode& nd : out.nodes)
         for (int c = 0; c < 2; ++c)
             if (nd.child[c] != kFastEmpty) inflate(nd.box[c], pad);
+    return out;
+}
+
+namespace {
+
+float f_of(uint32_t u) {
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+// top tree over objects: median split on the widest centroid axis; returns the child code
+// (object root / internal top node) of the subtree over objs[lo, hi)
+uint32_t build_top(std::vector<uint32_t>& objs, uint32_t lo, uint32_t hi, const std::vector<Box>& boxes,
+                   const std::vector<uint32_t>& obj_root, std::vector<FastNode>& top) {
+    if (hi - lo == 1) return obj_root[objs[lo]];
+    Box cb = empty_box();
+    for (uint32_t i = lo; i < hi; ++i) {
+        const V3 c = mul(add(boxes[objs[i]].lo, boxes[objs[i]].hi), 0.5f);
+        expand(cb, Box{c, c});
+    }
+    const V3 e = sub(cb.hi, cb.lo);
+    const int axis = e.x >= e.y && e.x >= e.z ? 0 : (e.y >= e.z ? 1 : 2);
+    auto key = [&](uint32_t j) {
+        const V3 c = add(boxes[j].lo, boxes[j].hi);
+        return axis == 0 ? c.x : (axis == 1 ? c.y : c.z);
+    };
+    const uint32_t mid = lo + (hi - lo) / 2;
+    std::nth_element(objs.begin() + lo, objs.begin() + mid, objs.begin() + hi,
+                     [&](uint32_t a, uint32_t b) { return key(a) < key(b) || (key(a) == key(b) && a < b); });
+    const uint32_t me = static_cast<uint32_t>(top.size());
+    top.emplace_back();
+    const uint32_t l = build_top(objs, lo, mid, boxes, obj_root, top);
+    const uint32_t r = build_top(objs, mid, hi, boxes, obj_root, top);
+    top[me].child[0] = l;
+    top[me].child[1] = r;
+    return me;
+}
+
+}  // namespace
+
+DynSahTopology build_dyn_sah(const std::vector<std::vector<Tri>>& objects, const std::vector<uint32_t>& tri_begin,
+                             const std::vector<Box>& boxes) {
+    DynSahTopology out;
+    const uint32_t n_obj = static_cast<uint32_t>(objects.size());
+    if (n_obj == 0) return out;
+    std::vector<FastBvh> trees(n_obj);
+    for (uint32_t j = 0; j < n_obj; ++j) trees[j] = build_fast_bvh(objects[j], 0.0f);
+    // node numbering: top nodes [0, n_top), then each object's nodes at obj_off[j]
+    const uint32_t n_top = std::max<uint32_t>(1, n_obj - 1);
+    std::vector<uint32_t> obj_off(n_obj), obj_root(n_obj);
+    uint32_t total = n_top;
+    for (uint32_t j = 0; j < n_obj; ++j) {
+        obj_off[j] = total;
+        obj_root[j] = total;  // build_fast_bvh's root (node 0) is always internal
+        total += static_cast<uint32_t>(trees[j].nodes.size());
+    }
+    std::vector<FastNode> top;
+    top.reserve(n_top);
+    std::vector<uint32_t> objs;  // objects with triangles (an empty mesh has no tree)
+    for (uint32_t j = 0; j < n_obj; ++j)
+        if (!objects[j].empty()) objs.push_back(j);
+    if (objs.size() <= 1) {
+        top.emplace_back();
+        if (!objs.empty()) top[0].child[0] = obj_root[objs[0]];
+    } else {  // the first node made (0) is the root
+        build_top(objs, 0, static_cast<uint32_t>(objs.size()), boxes, obj_root, top);
+    }
+    if (top.size() > n_top) throw std::logic_error("build_dyn_sah: top tree overflow");
+    uint32_t n_tris = 0;
+    for (uint32_t j = 0; j < n_obj; ++j) n_tris += static_cast<uint32_t>(objects[j].size());
+    out.nodes.assign(4ull * total, float4{0.f, 0.f, 0.f, 0.f});
+    out.parent.assign(total, ~0u);
+    out.perm.resize(n_tris);
+    auto emit = [&](uint32_t node, const FastNode& nd, uint32_t code_off_node, int32_t obj) {
+        for (int c = 0; c < 2; ++c) {
+            uint32_t code = nd.child[c];
+            if (code == kFastEmpty) {
+                out.nodes[4ull * node + c].w = f_of(kFastEmpty);
+                continue;
+            }
+            if (code & kFastLeaf) {
+                const uint32_t first = ((code & ~kFastLeaf) >> 3) + tri_begin[obj];
+                const uint32_t count = (code & 7u) + 1u;
+                code = kFastLeaf | (first << 3) | (count - 1u);
+                out.leaves.insert(out.leaves.end(), {first, count, node, static_cast<uint32_t>(c)});
+            } else {
+                code += code_off_node;
+                out.parent[code] = node << 1 | static_cast<uint32_t>(c);
+            }
+            out.nodes[4ull * node + c].w = f_of(code);
+        }
+    };
+    for (uint32_t k = 0; k < top.size(); ++k) emit(k, top[k], 0, -1);
+    for (uint32_t j = 0; j < n_obj; ++j) {
+        const FastBvh& t = trees[j];
+        // only the nodes reachable from the root (build_fast_bvh leaves the node it moved into
+        // slot 0 orphaned); unreachable slots keep empty codes and are never refit
+        for (uint32_t k = 0; k < t.nodes.size(); ++k) {
+            out.nodes[4ull * (obj_off[j] + k)].w = f_of(kFastEmpty);
+            out.nodes[4ull * (obj_off[j] + k) + 1].w = f_of(kFastEmpty);
+        }
+        std::vector<uint32_t> stack{0u};
+        while (!stack.empty()) {
+            const uint32_t k = stack.back();
+            stack.pop_back();
+            emit(obj_off[j] + k, t.nodes[k], obj_off[j], static_cast<int32_t>(j));
+            for (int c = 0; c < 2; ++c)
+                if (t.nodes[k].child[c] != kFastEmpty && !(t.nodes[k].child[c] & kFastLeaf))
+                    stack.push_back(t.nodes[k].child[c]);
+        }
+        for (uint32_t s = 0; s < t.order.size(); ++s) out.perm[tri_begin[j] + s] = tri_begin[j] + t.order[s];
+    }
     return out;
 }
 

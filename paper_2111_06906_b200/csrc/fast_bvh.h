@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <vector>
 
+#include <vector_types.h>
+
 #include "host_scene.h"
 
 namespace prx {
@@ -23,5 +25,20 @@ struct FastBvh {
 
 // `tris_ref_order[k]` is the static triangle at reference permutation position k.
 FastBvh build_fast_bvh(const std::vector<Tri>& tris_ref_order, float pad);
+
+// The combined dynamic tree's fixed topology (lbvh.cu: refit every frame the movers move):
+// one SAH tree per rigid dynamic object, built once over its object-local triangles, under
+// a top tree over the objects.  Nodes are in the fast layout with child codes in .w and
+// boxes left for the refit; internal node 0 is the root.
+struct DynSahTopology {
+    std::vector<float4> nodes;      // 4 per internal node: {lo0, c0} {hi0, c1} {lo1, -} {hi1, -}
+    std::vector<uint32_t> perm;     // leaf slot -> global dynamic triangle index
+    std::vector<uint32_t> leaves;   // 4 per leaf: first slot, count, parent node, side
+    std::vector<uint32_t> parent;   // per internal node: parent << 1 | side (root: ~0u)
+};
+// `objects[j]` holds object j's local triangles (global indices tri_begin[j] + i);
+// `boxes[j]` is a representative world box (frame 0) that orders the top tree.
+DynSahTopology build_dyn_sah(const std::vector<std::vector<Tri>>& objects, const std::vector<uint32_t>& tri_begin,
+                             const std::vector<Box>& boxes);
 
 }  // namespace prx

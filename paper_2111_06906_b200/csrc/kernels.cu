@@ -3,6 +3,7 @@
 // One thread per path (grid-stride), bounce-major vertex streams so that every warp
 // access to bounce b of 32 consecutive paths is one coalesced 512-byte float4 load.
 // Citations: reference function each kernel restates (paths under /root/reference/proj).
+#include <cstdio>
 #include "device_scene.cuh"
 #include "kernels.h"
 
@@ -857,12 +858,29 @@ static int persistent_grid(K kernel) {
     return sms * (per_sm > 0 ? per_sm : 1);
 }
 
+#ifdef PRX_CERT_STATS
+static void cert_report(const char* stage, cudaStream_t st) {
+    unsigned long long c[8] = {};
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(c, g_cert_stats, sizeof(c));
+    std::fprintf(stderr, "[cert] %s: closest %llu fail %llu | any %llu fail %llu | nodes s %llu d %llu | tris s %llu d %llu\n",
+                 stage, c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]);
+    const unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_cert_stats, z, sizeof(z));
+}
+#define CERT_REPORT(stage) cert_report(stage, st)
+#else
+#define CERT_REPORT(stage) ((void)0)
+#endif
+
 void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t* list, const uint32_t* masks,
                          const Counters* cnt, uint32_t* work, Counters* ctr, cudaStream_t st) {
     if (S.fast) {  // one-shot walks on the fast traversal
         static int grid = persistent_grid(k_verify_error_walk);
         cudaMemsetAsync(work, 0, 4, st);
+        CERT_REPORT("before verify");
         k_verify_error_walk<<<grid, kT, 0, st>>>(S, P, threshold, list, masks, cnt, work, ctr);
+        CERT_REPORT("verify walk");
     } else {  // resumable reference-order traversal, persistent lanes
         static int grid = persistent_grid(k_verify_error);
         cudaMemsetAsync(work, 0, 4, st);
@@ -926,7 +944,9 @@ void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* c
                   Counters* ctr, cudaStream_t st) {
     static int grid = persistent_grid(k_trace);
     cudaMemsetAsync(work, 0, 4, st);
+    CERT_REPORT("before trace");
     k_trace<<<grid, kT, 0, st>>>(S, P, list, count, work, ctr);
+    CERT_REPORT("trace");
     ++g_launches;
 }
 void launch_intersect_batch(SceneDev S, const float* rays, uint32_t n, int any_hit, float* out, cudaStream_t st) {

@@ -88,6 +88,12 @@ struct LbvhBuffers {
     void* scratch;
     float4* all_nodes;    // combined tree over all dynamic triangles (null: not built)
     float4* all_tris;     // its leaves: dynamic triangles in sorted order
+    // fixed-topology variant of the combined tree (fast_bvh.h: DynSahTopology), refit only;
+    // null sah_perm: rebuild it as a Karras tree every frame
+    const uint32_t* sah_perm;    // leaf slot -> global dynamic triangle
+    const uint4* sah_leaf;       // {first slot, count, parent, side}
+    const uint32_t* sah_parent;  // per internal node: parent << 1 | side
+    uint32_t n_sah_leaves, n_sah_nodes;
 };
 void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint32_t n_tris,
                         const DynObj* dyn_host, uint32_t n_dyn, const DynObj* dyn_dev,

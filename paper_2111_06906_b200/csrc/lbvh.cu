@@ -258,6 +258,71 @@ __global__ void k_refit_all(const float4* __restrict__ stris, uint32_t n, const 
     }
 }
 
+// ---------------------------------------------------------------- fixed SAH topology
+// The movers are rigid, so a per-object SAH tree built once over the local triangles stays
+// a good tree under the frame's transform: each frame only the leaves (triangles copied into
+// slot order) and the boxes (bottom-up refit) change.
+__global__ void k_dsah_tris(const float4* __restrict__ tris, const uint32_t* __restrict__ tri_obj,
+                            const uint32_t* __restrict__ perm, uint32_t n, float4* out) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const uint32_t g = perm[t];
+        float4 a = tris[3 * g], e1 = tris[3 * g + 1], e2 = tris[3 * g + 2];
+        a.w = __uint_as_float(g);
+        e1.w = __uint_as_float(tri_obj[g]);
+        e2.w = 0.0f;
+        out[3 * t] = a;
+        out[3 * t + 1] = e1;
+        out[3 * t + 2] = e2;
+    }
+}
+
+// one thread per leaf: the union of its (padded, as k_refit_all) triangle boxes goes into
+// the parent's child slot; the second arrival at a node carries the union upwards.
+__global__ void k_dsah_refit(const float4* __restrict__ stris, const uint4* __restrict__ leaves, uint32_t n_leaves,
+                             const DynObj* __restrict__ dyn, float4* nodes, const uint32_t* __restrict__ parent,
+                             uint32_t* flags) {
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_leaves; l += gridDim.x * blockDim.x) {
+        const uint4 L = leaves[l];
+        float lox = INFINITY, loy = INFINITY, loz = INFINITY, hix = -INFINITY, hiy = -INFINITY, hiz = -INFINITY;
+        for (uint32_t t = L.x; t < L.x + L.y; ++t) {
+            const float4 a = stris[3 * t], e1 = stris[3 * t + 1], e2 = stris[3 * t + 2];
+            const DynObj D = dyn[__float_as_uint(e1.w)];
+            const float ext = fmaxf(fmaxf(D.cur.hi.x - D.cur.lo.x, D.cur.hi.y - D.cur.lo.y), D.cur.hi.z - D.cur.lo.z);
+            const float bx = a.x + e1.x, by = a.y + e1.y, bz = a.z + e1.z;
+            const float cx = a.x + e2.x, cy = a.y + e2.y, cz = a.z + e2.z;
+            float tlx = fminf(a.x, fminf(bx, cx)), thx = fmaxf(a.x, fmaxf(bx, cx));
+            float tly = fminf(a.y, fminf(by, cy)), thy = fmaxf(a.y, fmaxf(by, cy));
+            float tlz = fminf(a.z, fminf(bz, cz)), thz = fmaxf(a.z, fmaxf(bz, cz));
+            const float mag = fmaxf(fmaxf(fmaxf(fabsf(tlx), fabsf(thx)), fmaxf(fabsf(tly), fabsf(thy))),
+                                    fmaxf(fabsf(tlz), fabsf(thz)));
+            const float m = 1e-5f * ext + 4e-6f * mag + 1e-30f;
+            lox = fminf(lox, tlx - m), loy = fminf(loy, tly - m), loz = fminf(loz, tlz - m);
+            hix = fmaxf(hix, thx + m), hiy = fmaxf(hiy, thy + m), hiz = fmaxf(hiz, thz + m);
+        }
+        uint32_t p = L.z, side = L.w;
+        while (true) {
+            float4* N = nodes + 4ull * p;
+            const int o = side ? 2 : 0;
+            N[o].x = lox, N[o].y = loy, N[o].z = loz;
+            N[o + 1].x = hix, N[o + 1].y = hiy, N[o + 1].z = hiz;
+            const uint32_t sib = __float_as_uint(__ldcg(&N[side ? 0 : 1].w));
+            if (sib != 0xFFFFFFFFu) {  // two children: the second arrival continues
+                __threadfence();
+                if (atomicAdd(&flags[p], 1u) == 0) break;
+                __threadfence();
+                const int q = side ? 0 : 2;
+                const float4 smin = __ldcg(&N[q]), smax = __ldcg(&N[q + 1]);
+                lox = fminf(lox, smin.x), loy = fminf(loy, smin.y), loz = fminf(loz, smin.z);
+                hix = fmaxf(hix, smax.x), hiy = fmaxf(hiy, smax.y), hiz = fmaxf(hiz, smax.z);
+            }
+            const uint32_t pp = parent[p];
+            if (pp == 0xFFFFFFFFu) break;
+            p = pp >> 1;
+            side = pp & 1u;
+        }
+    }
+}
+
 }  // namespace
 
 void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint32_t n_tris,
@@ -267,6 +332,16 @@ void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint3
     (void)n_dyn;
     if (n_tris < 2) return;
     const int g = launch_grid(n_tris, kT);
+    const bool sah = buf.all_nodes && buf.sah_perm;
+    if (sah) {  // combined tree: fixed SAH topology, refit
+        k_dsah_tris<<<g, kT, 0, st>>>(world_tris, tri_obj, buf.sah_perm, n_tris, buf.all_tris);
+        cudaMemsetAsync(buf.flags, 0, 4ull * buf.n_sah_nodes, st);
+        k_dsah_refit<<<launch_grid(buf.n_sah_leaves, kT), kT, 0, st>>>(buf.all_tris, buf.sah_leaf, buf.n_sah_leaves,
+                                                                      dyn_dev, buf.all_nodes, buf.sah_parent,
+                                                                      buf.flags);
+        g_launches += 2;
+        if (!nodes) return;
+    }
     k_morton<<<g, kT, 0, st>>>(world_tris, tri_obj, n_tris, dyn_dev, buf.keys, buf.vals);
     radix_sort_pairs(buf.keys, buf.vals, buf.keys_tmp, buf.vals_tmp, n_tris, nullptr, 31, buf.scratch, st);
     g_launches += 1 + 3 * 4;
@@ -277,7 +352,7 @@ void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint3
         k_refit<<<g, kT, 0, st>>>(world_tris, buf.keys, leaf, n_tris, dyn_dev, nodes, buf.parent, buf.flags, n_tris);
         g_launches += 3;
     }
-    if (buf.all_nodes) {  // combined tree (fast dynamic phase)
+    if (buf.all_nodes && !sah) {  // combined tree (fast dynamic phase), Karras
         k_sorted_tris<<<g, kT, 0, st>>>(world_tris, buf.keys, buf.vals, n_tris, dyn_dev, buf.all_tris);
         uint2* range = reinterpret_cast<uint2*>(buf.keys_tmp);  // free after the sort (2n words)
         k_karras_all<<<g, kT, 0, st>>>(buf.keys, n_tris, buf.all_nodes, buf.parent, range);

@@ -107,6 +107,28 @@ def test_intersect_and_occluded_bit_exact(scene, synthetic, frames):
     assert np.array_equal(occ, rs.occluded(frame, rays))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("tree", ["sah", "karras"])
+@pytest.mark.parametrize("scene", ["merry-go-round-analog", "C4"])
+def test_dynamic_tree_variants_bit_exact(monkeypatch, tree, scene):
+    """The combined dynamic tree is either per-object SAH topologies refit every frame (the
+    default) or a per-frame Karras rebuild (PRX_DYN_TREE=karras); the query result must not
+    depend on it."""
+    from oracle import ref
+
+    monkeypatch.setenv("PRX_DYN_TREE", tree)
+    synthetic = scene.startswith("C")
+    sc = pr.Scene.synthetic(scene) if synthetic else pr.Scene.builtin(scene)
+    rs = ref.RefScene.from_desc(sc.describe()) if synthetic else ref.RefScene.builtin(scene)
+    eng = pr.Engine(sc, pr.make_config("naive", paths=1000, bounces=2, dm=[2, 2, 4, 4]))
+    for _ in range(3):
+        eng.run_frame()
+    frame = eng.info().frames_run - 1
+    rays = make_rays(sc.describe(), 40000, np.random.default_rng(23), sc.diagonal)
+    assert np.array_equal(eng.intersect(rays).view(np.uint32), rs.intersect(frame, rays).view(np.uint32))
+    assert np.array_equal(eng.intersect(rays, any_hit=True), rs.occluded(frame, rays))
+
+
 def _offset_doc(offset):
     """test_io's document with every object and light moved far from the origin."""
     import json
