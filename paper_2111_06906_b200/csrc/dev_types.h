@@ -24,6 +24,7 @@ struct DynObj {
     uint32_t tri_count;
     uint32_t node_begin;  // first LBVH node, kLbvhBrute = linear scan
     Box cur;              // bounds_current (scene.cpp:129)
+    uint32_t sah_root;    // its subtree in the combined SAH tree (kLbvhBrute: none)
 };
 
 struct LightDev {
@@ -57,6 +58,7 @@ struct SceneDev {
     const uint32_t* leaf_of;   // permutation position -> reference leaf node
     float cull_pad;            // fast traversal: box inflation for conservative culling
     int32_t fast;              // 1: near-first traversal + exactness certificate
+    int32_t cert_off;          // 1: every certificate fails (tests: exercises the exact fallbacks)
     const float4* fnodes;      // fast SAH BVH2: 4 float4 per node {lo0,c0} {hi0,c1} {lo1,-} {hi1,-}
     const float4* ftris;       // its triangles in leaf order: {a, ref position} {e1, obj} {e2, -}
     const float4* stris;       // static tris, BVH order: {a, orig idx} {e1, obj} {e2, -}

@@ -241,8 +241,23 @@ __device__ __forceinline__ bool ray_box_conservative(const RayPre& r, float t_mi
 
 // Closest hit inside one dynamic object: the (t, index)-lexicographic minimum over its
 // triangles with t in (t_min, t_max) -- brute_force_intersect's result (bvh.cpp:108-117).
+template <bool kAny>
+__device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                             const RayPre& r, float t_min, float t_max, float& best_t,
+                                             uint32_t& best_pos, float& t_cert, uint32_t root = 0);
+
 __device__ __forceinline__ bool dyn_closest(const SceneDev& S, const DynObj& D, const RayPre& r,
                                             float t_min, float& t_max, uint32_t& best_tri) {
+    if (S.fast && S.dfast && D.sah_root != kLbvhBrute) {
+        // the (t, index) minimum over the object's triangles in the window: its subtree of the
+        // combined SAH tree (fast_closest is exact over the triangles it is given)
+        float bt, tc;
+        uint32_t g;
+        if (!fast_closest<false>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc, D.sah_root)) return false;
+        best_tri = g - D.tri_begin;
+        t_max = bt;
+        return true;
+    }
     bool found = false;
     const float4* T = S.dtris + 3ull * D.tri_begin;
     if (D.node_begin == kLbvhBrute) {
@@ -303,6 +318,11 @@ __device__ __forceinline__ bool dyn_closest(const SceneDev& S, const DynObj& D, 
 
 __device__ __forceinline__ bool dyn_any(const SceneDev& S, const DynObj& D, const RayPre& r,
                                         float t_min, float t_max) {
+    if (S.fast && S.dfast && D.sah_root != kLbvhBrute) {
+        float bt, tc;
+        uint32_t g;
+        return fast_closest<true>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc, D.sah_root);
+    }
     const float4* T = S.dtris + 3ull * D.tri_begin;
     if (D.node_begin == kLbvhBrute) {
         for (uint32_t i = 0; i < D.tri_count; ++i) {
@@ -596,7 +616,7 @@ static __device__ unsigned long long g_cert_stats[8];
 template <bool kAny>
 __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, const float4* __restrict__ tris,
                                              const RayPre& r, float t_min, float t_max, float& best_t,
-                                             uint32_t& best_pos, float& t_cert) {
+                                             uint32_t& best_pos, float& t_cert, uint32_t root) {
     constexpr uint32_t kNone = 0xFFFFFFFFu;
     best_t = t_max;
     best_pos = kNone;
@@ -610,7 +630,7 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
     const uint32_t stride = blockDim.x;
     uint2 overflow[64 - kShortStack];
     int sp = 0;
-    uint32_t node = 0;  // the root is always an internal node
+    uint32_t node = root;  // always an internal node
     uint32_t leaf = kNone;
     auto push = [&](uint32_t c, float ent) {
         const uint2 e = make_uint2(c, __float_as_uint(ent));
@@ -851,6 +871,7 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
 // entry bound can only drop and the exit bound only rise).
 __device__ __forceinline__ bool static_cert(const SceneDev& S, const RayPre& r, float t_min, float t_lim,
                                             uint32_t pos) {
+    if (S.cert_off) return false;
     const uint32_t leaf = __ldg(&S.leaf_of[pos]);
     const float4 A = __ldg(&S.nodes[2 * leaf]);
     const float4 B = __ldg(&S.nodes[2 * leaf + 1]);
@@ -926,7 +947,7 @@ __device__ __forceinline__ int dyn_closest_exact(const SceneDev& S, const RayPre
     if (!fast_closest<false>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc)) return -1;
     const uint32_t j = __ldg(&S.dtri_obj[g]);
     const DynObj& D = fp->dyn[j];
-    if (ray_box(r, t_min, tc, D.cur)) {
+    if (!S.cert_off && ray_box(r, t_min, tc, D.cur)) {
         t_max = bt;
         dj = j;
         dtri = g - D.tri_begin;
@@ -982,7 +1003,7 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
         } else {
             dj = __ldg(&S.dtri_obj[pos]);
             dtri = pos - S.fp->dyn[dj].tri_begin;
-            ok = ray_box(r, t_min, tc, S.fp->dyn[dj].cur);
+            ok = !S.cert_off && ray_box(r, t_min, tc, S.fp->dyn[dj].cur);
         }
         if (ok) {
             if (tri) *tri = tree == 0 ? __float_as_uint(__ldg(&S.stris[3 * pos]).w) : dtri;
@@ -1015,7 +1036,7 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
         PRX_CERT_COUNT(2);
         if (!joint_closest<true>(S, r, t_min, t_max, bt, tree, pos, tc)) return false;
         if (tree == 0 ? static_cert(S, r, t_min, t_max, pos)
-                      : ray_box(r, t_min, t_max, S.fp->dyn[__ldg(&S.dtri_obj[pos])].cur))
+                      : !S.cert_off && ray_box(r, t_min, t_max, S.fp->dyn[__ldg(&S.dtri_obj[pos])].cur))
             return true;
         PRX_CERT_COUNT(3);
     }
@@ -1026,7 +1047,7 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
         float bt, tc;
         uint32_t g;
         if (!fast_closest<true>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc)) return false;
-        if (ray_box(r, t_min, t_max, fp->dyn[__ldg(&S.dtri_obj[g])].cur)) return true;
+        if (!S.cert_off && ray_box(r, t_min, t_max, fp->dyn[__ldg(&S.dtri_obj[g])].cur)) return true;
     }
     for (uint32_t j = 0; j < fp->n_dyn; ++j) {
         const DynObj& D = fp->dyn[j];

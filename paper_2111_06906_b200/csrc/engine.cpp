@@ -225,6 +225,7 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     PRX_CUDA(cudaMemsetAsync(d_ctr_.get(), 0, sizeof(Counters), stream_));
     PRX_CUDA(cudaMemsetAsync(d_cnt32_.get(), 0, 4 * kCntN, stream_));
 
+    if (const char* e = std::getenv("PRX_CERT_OFF")) cert_off_ = std::atoi(e) != 0 ? 1 : 0;
     upload_scene();
     apply_l2_policy();
     alloc_state();
@@ -373,6 +374,13 @@ void Engine::upload_scene() {
     std::vector<float4> local;
     std::vector<uint32_t> tri_xf;
     uint32_t tri = 0, nodes_total = 0;
+    // the combined dynamic tree: per-object SAH topologies refit per frame (default), or a
+    // per-frame Karras rebuild (PRX_DYN_TREE=karras, A/B runs).  With the SAH topology the
+    // fast mode answers per-object queries from the object's subtree, so the per-object
+    // Karras trees are only built for the DFS traversal mode or the Karras variant.
+    const char* tree_kind = std::getenv("PRX_DYN_TREE");
+    const bool karras_all = tree_kind && std::strcmp(tree_kind, "karras") == 0;
+    const bool per_object = cfg_.dfs_traversal || karras_all;
     for (const Object& o : s.objects) {
         if (!o.dynamic) continue;
         if (dyn_.size() >= static_cast<size_t>(kMaxDyn))
@@ -381,7 +389,7 @@ void Engine::upload_scene() {
         d.obj = o.id;
         d.tri_begin = tri;
         d.tri_count = static_cast<uint32_t>(o.mesh.size());
-        if (d.tri_count > 32) {  // LBVH for anything beyond a few boxes
+        if (per_object && d.tri_count > 32) {  // LBVH for anything beyond a few boxes
             d.node_begin = nodes_total;
             nodes_total += d.tri_count - 1;
         }
@@ -420,8 +428,7 @@ void Engine::upload_scene() {
             lbvh_.scratch = w + 4 * n + 2 * (2 * n + 2);
             d_dall_tris_.alloc(sizeof(float4) * 3 * n);
             lbvh_.all_tris = d_dall_tris_.as<float4>();
-            const char* kind = std::getenv("PRX_DYN_TREE");
-            if (kind && std::strcmp(kind, "karras") == 0) {  // per-frame Karras rebuild (A/B runs)
+            if (karras_all) {
                 d_dall_nodes_.alloc(sizeof(float4) * 4 * (n - 1));
             } else {  // per-object SAH topologies, built once, refit per frame
                 std::vector<std::vector<Tri>> objs;
@@ -449,6 +456,8 @@ void Engine::upload_scene() {
                 lbvh_.sah_parent = reinterpret_cast<const uint32_t*>(base + b_perm + b_leaf);
                 lbvh_.n_sah_leaves = static_cast<uint32_t>(topo.leaves.size() / 4);
                 lbvh_.n_sah_nodes = static_cast<uint32_t>(topo.parent.size());
+                if (!cfg_.dfs_traversal)
+                    for (size_t j = 0; j < dyn_.size(); ++j) dyn_[j].sah_root = topo.obj_root[j];
             }
             lbvh_.all_nodes = d_dall_nodes_.as<float4>();
         }
@@ -525,6 +534,7 @@ SceneDev Engine::scene_dev() const {
     S.leaf_of = p_leaf_of_;
     S.cull_pad = 1e-5f * diag_ + 1e-6f;
     S.fast = cfg_.dfs_traversal ? 0 : 1;
+    S.cert_off = cert_off_;
     S.fnodes = p_fnodes_;
     S.ftris = p_ftris_;
     S.stris = d_stris_.as<float4>();
@@ -635,6 +645,7 @@ void Engine::place_frame(int frame) {
         D.tri_begin = dyn_[j].tri_begin;
         D.tri_count = dyn_[j].tri_count;
         D.node_begin = dyn_[j].node_begin;
+        D.sah_root = dyn_[j].sah_root;
         D.cur = cur;
         if (frame > 0) {
             Box box = prv;

@@ -111,7 +111,7 @@ private:
         DevBuf dm_t, dm_c, unm, seg_start;
     };
     struct DynInfo {
-        uint32_t obj = 0, tri_begin = 0, tri_count = 0, node_begin = kLbvhBrute;
+        uint32_t obj = 0, tri_begin = 0, tri_count = 0, node_begin = kLbvhBrute, sah_root = kLbvhBrute;
         Xform last_xf;
         bool placed = false;
     };
@@ -167,6 +167,7 @@ private:
     float4 *p_fnodes_ = nullptr, *p_ftris_ = nullptr, *p_nodes_ = nullptr;
     uint32_t* p_leaf_of_ = nullptr;
     size_t l2_window_ = 0;
+    int32_t cert_off_ = 0;  // PRX_CERT_OFF=1: every query takes its exact fallback (tests)
     const float2* d_trig_ = nullptr;
 
     // frame params (pinned host + device)

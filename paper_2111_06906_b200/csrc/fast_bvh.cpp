@@ -260,6 +260,8 @@ DynSahTopology build_dyn_sah(const std::vector<std::vector<Tri>>& objects, const
         build_top(objs, 0, static_cast<uint32_t>(objs.size()), boxes, obj_root, top);
     }
     if (top.size() > n_top) throw std::logic_error("build_dyn_sah: top tree overflow");
+    out.obj_root.assign(n_obj, ~0u);
+    for (uint32_t j : objs) out.obj_root[j] = obj_root[j];
     uint32_t n_tris = 0;
     for (uint32_t j = 0; j < n_obj; ++j) n_tris += static_cast<uint32_t>(objects[j].size());
     out.nodes.assign(4ull * total, float4{0.f, 0.f, 0.f, 0.f});

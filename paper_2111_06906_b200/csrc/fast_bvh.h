@@ -35,6 +35,7 @@ struct DynSahTopology {
     std::vector<uint32_t> perm;     // leaf slot -> global dynamic triangle index
     std::vector<uint32_t> leaves;   // 4 per leaf: first slot, count, parent node, side
     std::vector<uint32_t> parent;   // per internal node: parent << 1 | side (root: ~0u)
+    std::vector<uint32_t> obj_root; // per object: its root node (~0u: no triangles)
 };
 // `objects[j]` holds object j's local triangles (global indices tri_begin[j] + i);
 // `boxes[j]` is a representative world box (frame 0) that orders the top tree.

@@ -129,6 +129,35 @@ def test_dynamic_tree_variants_bit_exact(monkeypatch, tree, scene):
     assert np.array_equal(eng.intersect(rays, any_hit=True), rs.occluded(frame, rays))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene", ["merry-go-round-analog", "C3"])
+def test_exact_fallbacks_bit_exact(monkeypatch, scene):
+    """PRX_CERT_OFF=1 fails every certificate, so each query takes the exact fallback the
+    fast path relies on in its rare certificate failures (reference-order static DFS, the
+    sequential gated dynamic phase over per-object subtrees); engine state and queries must
+    still match the reference."""
+    from oracle import ref
+    from tests.helpers import compare_state, counts
+
+    monkeypatch.setenv("PRX_CERT_OFF", "1")
+    synthetic = scene.startswith("C")
+    sc = pr.Scene.synthetic(scene) if synthetic else pr.Scene.builtin(scene)
+    rs = ref.RefScene.from_desc(sc.describe()) if synthetic else ref.RefScene.builtin(scene)
+    cfg = dict(mode="error", paths=3000, bounces=4, dm=[2, 2, 8, 8], threshold=0.001, seed=41)
+    eng = pr.Engine(sc, pr.make_config(**cfg))
+    cpu = ref.RefEngine(rs, pr.make_config(**cfg))
+    cpu.set_workers(0)
+    for f in range(3):
+        sg, scs = eng.run_frame(), cpu.run_frame()
+        assert counts(sg) == counts(scs), f
+        bad = compare_state(eng, cpu, eng.info().n_lights)
+        assert all(v == 0 for v in bad.values()), (f, bad)
+    frame = eng.info().frames_run - 1
+    rays = make_rays(sc.describe(), 12000, np.random.default_rng(29), sc.diagonal)
+    assert np.array_equal(eng.intersect(rays).view(np.uint32), rs.intersect(frame, rays).view(np.uint32))
+    assert np.array_equal(eng.intersect(rays, any_hit=True), rs.occluded(frame, rays))
+
+
 def _offset_doc(offset):
     """test_io's document with every object and light moved far from the origin."""
     import json
