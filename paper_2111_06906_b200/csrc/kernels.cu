@@ -92,13 +92,30 @@ __global__ void k_transform_dynamic(const float4* __restrict__ local, const uint
     }
 }
 
+// Four paths per thread with whole-word accesses: clearing only meta.w per path compiles to
+// stride-4 byte stores (partial sectors, ~85 GB/s); 16-byte meta and 4-byte rstart words
+// write whole sectors.  Buffers are cudaMalloc-aligned, so the word views are aligned.
+__device__ __forceinline__ uint32_t reset_meta_word(uint32_t m, unsigned long long& segs) {
+    if (((m >> 16) & 0xFFu) == kLive) segs += (m & 0xFFu) + ((m >> 8) & 0xFFu);  // {count, escaped, status, filled}
+    return m & 0x00FFFFFFu;
+}
 __global__ void k_frame_reset(PathDev P, int record, Counters* ctr) {
     unsigned long long segs = 0;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
-        uchar4 m = P.meta[i];
-        if (m.z == kLive) segs += m.x + m.y;
-        m.w = 0;
-        P.meta[i] = m;
+    const uint32_t n4 = P.n / 4;
+    uint4* meta4 = reinterpret_cast<uint4*>(P.meta);
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += gridDim.x * blockDim.x) {
+        uint4 m = __ldcs(&meta4[q]);
+        m.x = reset_meta_word(m.x, segs);
+        m.y = reset_meta_word(m.y, segs);
+        m.z = reset_meta_word(m.z, segs);
+        m.w = reset_meta_word(m.w, segs);
+        __stcs(&meta4[q], m);
+        __stcs(reinterpret_cast<uint32_t*>(P.rstart) + q, 0x01010101u * kNoRetrace);
+        if (record) __stcs(reinterpret_cast<uint4*>(P.seg_flags) + q, make_uint4(0u, 0u, 0u, 0u));
+    }
+    for (uint32_t i = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        uint32_t* mw = reinterpret_cast<uint32_t*>(P.meta) + i;
+        __stcs(mw, reset_meta_word(*mw, segs));
         P.rstart[i] = kNoRetrace;
         if (record) P.seg_flags[i] = 0;
     }
@@ -178,9 +195,28 @@ __global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Co
 __global__ void __launch_bounds__(kT, 4) k_occlusion_flags(SceneDev S, PathDev P, int mode, int record,
                                                         uint32_t* list, uint32_t* masks, Counters* ctr) {
     __shared__ Box boxes[kMaxDyn];
+    __shared__ float4 wide[2 * kMaxDyn];  // boxes pre-widened by the reject tolerance at ext_bound
     const FrameParams* fp = S.fp;
     const uint32_t nb = fp->n_boxes;
-    for (uint32_t k = threadIdx.x; k < nb; k += blockDim.x) boxes[k] = fp->boxes[k];
+    // Bounding-box reject before the slab test: a segment whose box misses an occlusion box by
+    // more than tol = 1e-6 (segment extent + |lo| + |hi|) per axis cannot pass the double test
+    // (its quotients err by ~1e-16 relative).  The tolerance is evaluated once per box at an
+    // extent bound (every step is monotone, so it only grows and the reject stays sound);
+    // segments longer than the bound skip the reject.
+    const float ext_bound = 2.0f * S.two_diag;
+    for (uint32_t k = threadIdx.x; k < nb; k += blockDim.x) {
+        const Box B = fp->boxes[k];
+        boxes[k] = B;
+        float lo[3], hi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float tol = 1e-6f * (ext_bound + fabsf(comp(B.lo, a)) + fabsf(comp(B.hi, a))) + 1e-30f;
+            lo[a] = comp(B.lo, a) - tol;
+            hi[a] = comp(B.hi, a) + tol;
+        }
+        wide[2 * k] = make_float4(lo[0], lo[1], lo[2], 0.f);
+        wide[2 * k + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+    }
     __syncthreads();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
         const uchar4 m = P.meta[i];
@@ -209,22 +245,18 @@ __global__ void __launch_bounds__(kT, 4) k_occlusion_flags(SceneDev S, PathDev P
                     const V3 dir = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, s - 1, i))]);
                     b = add(prev, mul(dir, S.two_diag));
                 }
-                // bounding-box reject before the slab test: a segment whose box misses an
-                // occlusion box by more than 1e-6 of the extents cannot pass the double test
-                // (its quotients err by ~1e-16 relative)
                 const V3 smin{fminf(prev.x, b.x), fminf(prev.y, b.y), fminf(prev.z, b.z)};
                 const V3 smax{fmaxf(prev.x, b.x), fmaxf(prev.y, b.y), fmaxf(prev.z, b.z)};
+                const bool bounded = smax.x - smin.x <= ext_bound && smax.y - smin.y <= ext_bound &&
+                                     smax.z - smin.z <= ext_bound;
                 for (uint32_t j = 0; j < nb; ++j) {
-                    const Box& B = boxes[j];
-                    bool apart = false;
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        const float tol = 1e-6f * (comp(smax, a) - comp(smin, a) + fabsf(comp(B.lo, a)) +
-                                                   fabsf(comp(B.hi, a))) + 1e-30f;
-                        apart = apart || comp(smax, a) < comp(B.lo, a) - tol || comp(smin, a) > comp(B.hi, a) + tol;
+                    if (bounded) {  // (an unbounded segment goes straight to the exact test)
+                        const float4 lo = wide[2 * j], hi = wide[2 * j + 1];
+                        if (smax.x < lo.x || smax.y < lo.y || smax.z < lo.z || smin.x > hi.x || smin.y > hi.y ||
+                            smin.z > hi.z)
+                            continue;
                     }
-                    if (apart) continue;
-                    if (segment_box(prev, b, B)) {
+                    if (segment_box(prev, b, boxes[j])) {
                         flagged = true;
                         break;
                     }
@@ -839,7 +871,7 @@ void launch_transform_dynamic(const float4* local, const uint32_t* tri_xf, const
     if (n) LAUNCH(k_transform_dynamic, n, local, tri_xf, xf, n, world);
 }
 void launch_frame_reset(PathDev P, int record, Counters* ctr, cudaStream_t st) {
-    LAUNCH(k_frame_reset, P.n, P, record, ctr);
+    LAUNCH(k_frame_reset, (P.n + 3) / 4, P, record, ctr);
 }
 void launch_release_all(PathDev P, cudaStream_t st) { LAUNCH(k_release_all, P.n, P); }
 void launch_update_origins(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st) {
