@@ -1298,7 +1298,7 @@ __device__ __forceinline__ bool segment_box(V3 a, V3 b, const Box& box) {
         }
         const float d = e - o;
         if (fabsf(d) < 1e-30f) return segment_box_exact(a, b, box);
-        const float inv = 1.0f / d;
+        const float inv = __frcp_rn(d);  // == 1.0f / d (both correctly rounded), cheaper
         float tn = (lo - o) * inv;
         float tf = (hi - o) * inv;
         if (tn > tf) {

@@ -192,7 +192,10 @@ __global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Co
 
 // compute_flag_mask (engine.cpp:172-199) with segment ends per Engine::segment_end
 // (engine.cpp:135-139); occlusion boxes staged in shared memory.
-__global__ void __launch_bounds__(kT, 4) k_occlusion_flags(SceneDev S, PathDev P, int mode, int record,
+#ifndef PRX_OCC_MINB
+#define PRX_OCC_MINB 4
+#endif
+__global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S, PathDev P, int mode, int record,
                                                         uint32_t* list, uint32_t* masks, Counters* ctr) {
     __shared__ Box boxes[kMaxDyn];
     __shared__ float4 wide[2 * kMaxDyn];  // boxes pre-widened by the reject tolerance at ext_bound
