@@ -86,7 +86,7 @@ class Scene:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and L is not None:  # (module globals may be gone at exit)
             L.lib().prx_scene_destroy(h)
             self._h = None
 
@@ -207,7 +207,7 @@ class Engine:
 
     def close(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and L is not None:  # (module globals may be gone at exit)
             L.lib().prx_engine_destroy(h)
         self._h = None
 
