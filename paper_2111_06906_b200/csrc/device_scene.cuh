@@ -657,23 +657,15 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
             const float lim = cull_limit(best_t);
             const float tl = box_entry_fast(r, t_min, lim, n0, n1);  // boxes are pre-inflated
             const float tr = c1 != kNone ? box_entry_fast(r, t_min, lim, n2, n3) : INFINITY;
-            if (tl == INFINITY && tr == INFINITY) {
-                node = pop();
-            } else if (tr == INFINITY) {
-                node = c0;
-            } else if (tl == INFINITY) {
-                node = c1;
-            } else if (tl <= tr) {
-                push(c1, tr);
-                node = c0;
-            } else {
-                push(c0, tl);
-                node = c1;
+            const bool hl = tl != INFINITY, hr = tr != INFINITY, left_first = tl <= tr;
+            uint32_t next = kNone;
+            if (hl || hr) next = (hl && (left_first || !hr)) ? c0 : c1;
+            if (hl && hr) push(left_first ? c1 : c0, left_first ? tr : tl);
+            if (next != kNone && (next & kLeafBit) && leaf == kNone) {  // park the leaf
+                leaf = next;
+                next = kNone;
             }
-            if (node != kNone && (node & kLeafBit) && leaf == kNone) {  // park the leaf
-                leaf = node;
-                node = pop();
-            }
+            node = next != kNone ? next : pop();
             if (!__any_sync(__activemask(), leaf == kNone)) break;
         }
         if (leaf == kNone && node != kNone && (node & kLeafBit)) {
@@ -785,23 +777,16 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
             const float lim = cull_limit(best_t);
             const float tl = box_entry_fast(r, t_min, lim, n0, n1);  // boxes are pre-inflated
             const float tr = c1r != kNone ? box_entry_fast(r, t_min, lim, n2, n3) : INFINITY;
-            if (tl == INFINITY && tr == INFINITY) {
-                node = pop();
-            } else if (tr == INFINITY) {
-                node = c0;
-            } else if (tl == INFINITY) {
-                node = c1;
-            } else if (tl <= tr) {
-                push(c1, tr);
-                node = c0;
-            } else {
-                push(c0, tl);
-                node = c1;
+            // near child next, far child pushed; one pop site for "both missed" and "parked"
+            const bool hl = tl != INFINITY, hr = tr != INFINITY, left_first = tl <= tr;
+            uint32_t next = kNone;
+            if (hl || hr) next = (hl && (left_first || !hr)) ? c0 : c1;
+            if (hl && hr) push(left_first ? c1 : c0, left_first ? tr : tl);
+            if (next != kNone && (next & kLeafBit) && leaf == kNone) {  // park the leaf
+                leaf = next;
+                next = kNone;
             }
-            if (node != kNone && (node & kLeafBit) && leaf == kNone) {  // park the leaf
-                leaf = node;
-                node = pop();
-            }
+            node = next != kNone ? next : pop();
             if (!__any_sync(__activemask(), leaf == kNone)) break;
         }
         if (leaf == kNone && node != kNone && (node & kLeafBit)) {
