@@ -344,7 +344,7 @@ void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint3
     }
     k_morton<<<g, kT, 0, st>>>(world_tris, tri_obj, n_tris, dyn_dev, buf.keys, buf.vals);
     radix_sort_pairs(buf.keys, buf.vals, buf.keys_tmp, buf.vals_tmp, n_tris, nullptr, 31, buf.scratch, st);
-    g_launches += 1 + 3 * 4;
+    ++g_launches;  // (the sort counts its own)
     if (nodes) {  // per-object trees (sequential fallback and DFS mode)
         k_copy_leaf<<<g, kT, 0, st>>>(buf.vals, n_tris, leaf);
         k_karras<<<g, kT, 0, st>>>(buf.keys, n_tris, dyn_dev, nodes, buf.parent, n_tris);

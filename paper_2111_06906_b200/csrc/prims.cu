@@ -9,6 +9,8 @@
 
 namespace prx {
 
+extern uint64_t g_launches;  // kernels.cu: launches by this library (bench evidence)
+
 namespace {
 
 __device__ __forceinline__ uint32_t n_of(uint32_t n_max, const uint32_t* n_dev) {
@@ -240,12 +242,14 @@ Scratch carve(void* p, uint64_t n_max) {
 void scan_inplace(uint32_t* v, uint32_t m, uint32_t* total_dev, uint32_t* tmp, cudaStream_t st) {
     if (m <= 64u * 1024u) {
         k_scan_small<<<1, kPrimThreads, 0, st>>>(v, m, total_dev);
+        ++g_launches;
         return;
     }
     const uint32_t tiles = prim_tiles(m);
     k_tile_sum<<<tiles, kPrimThreads, 0, st>>>(v, m, nullptr, tmp);
     k_scan_small<<<1, kPrimThreads, 0, st>>>(tmp, tiles, total_dev);
     k_tile_scan<<<tiles, kPrimThreads, 0, st>>>(v, v, m, nullptr, tmp);
+    g_launches += 3;
 }
 
 }  // namespace
@@ -263,6 +267,7 @@ void scan_exclusive_u32(const uint32_t* in, uint32_t* out, uint32_t n_max, const
     k_tile_sum<<<tiles, kPrimThreads, 0, st>>>(in, n_max, n_dev, s.tile);
     scan_inplace(s.tile, tiles, total_dev, s.tile2, st);
     k_tile_scan<<<tiles, kPrimThreads, 0, st>>>(in, out, n_max, n_dev, s.tile);
+    g_launches += 2;
 }
 
 void compact_u8(const uint8_t* flags, uint32_t n_max, const uint32_t* n_dev, uint32_t base,
@@ -276,6 +281,7 @@ void compact_u8(const uint8_t* flags, uint32_t n_max, const uint32_t* n_dev, uin
     k_flag_count<uint8_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, n_dev, s.tile);
     scan_inplace(s.tile, tiles, count_dev, s.tile2, st);
     k_flag_scatter<uint8_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, n_dev, base, s.tile, out);
+    g_launches += 2;
 }
 
 void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, uint32_t base,
@@ -289,6 +295,7 @@ void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, u
     k_flag_count<uint32_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, n_dev, s.tile);
     scan_inplace(s.tile, tiles, count_dev, s.tile2, st);
     k_flag_scatter<uint32_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, n_dev, base, s.tile, out);
+    g_launches += 2;
 }
 
 void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
@@ -306,6 +313,7 @@ void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32
         scan_inplace(s.hist, tiles * kRadix, nullptr, s.tile2, st);
         k_rs_scatter<<<tiles, kPrimThreads, 0, st>>>(ki, vi, ko, vo, n_max, n_dev, shift, mask, tiles,
                                                      s.hist);
+        g_launches += 2;
         uint32_t* t = ki;
         ki = ko;
         ko = t;

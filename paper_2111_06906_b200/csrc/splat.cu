@@ -487,6 +487,7 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
     cudaMemsetAsync(cursor, 0, 4 * slots, st);
     k_pixcells<false><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, nullptr, nullptr,
                                                                   nullptr, bits);
+    g_launches += 2;  // gbuffer, pixcells
     if (mode == 1) {  // ordered, bit-exact gather
         const uint64_t nv = (uint64_t)P.n * P.B;
         // carve the work buffer in 256-byte aligned pieces (float4 / u32 views of any n)
@@ -516,7 +517,7 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         radix_sort_pairs(sk, sv, sk2, sv2, (uint32_t)nv, m_count, bits, gscratch, st);
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
         k_gather_copy<<<launch_grid(nv, kT), kT, 0, st>>>(P, sv, m_count, spo, sen);
-        g_launches += 6;
+        g_launches += 3;  // flag, keys, copy (the prims count their own)
         // Large images: pixel groups by home cell (sorted), big groups in 32-pixel chunks, the
         // rest per pixel.  Small images (few pixels per cell) go straight to the per-pixel walk.
         const char* genv = std::getenv("PRX_GATHER_GROUPS");
@@ -553,7 +554,7 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         k_gather_staged<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt, spo,
                                                                      sen, S.mat, inv_pi, inv_area, ctl + 4, img, small,
                                                                      ctl + 2);
-        g_launches += 6 + 3 * 4;
+        g_launches += 5;  // home, heads, split, groups, staged
         return;
     }
     scan_exclusive_u32(cnt, off, (uint32_t)slots, nullptr, nullptr, scratch, st);
@@ -576,7 +577,7 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
                                                                            off, list, img);
     }
     k_resolve<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, S.mat, img, npx, inv_pi, inv_area);
-    g_launches += 7 + 3;
+    g_launches += 4;  // pixcells, filter, splat, resolve
 }
 
 }  // namespace prx
