@@ -252,16 +252,25 @@ __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S
                 const V3 smax{fmaxf(prev.x, b.x), fmaxf(prev.y, b.y), fmaxf(prev.z, b.z)};
                 const bool bounded = smax.x - smin.x <= ext_bound && smax.y - smin.y <= ext_bound &&
                                      smax.z - smin.z <= ext_bound;
-                for (uint32_t j = 0; j < nb; ++j) {
-                    if (bounded) {  // (an unbounded segment goes straight to the exact test)
-                        const float4 lo = wide[2 * j], hi = wide[2 * j + 1];
-                        if (smax.x < lo.x || smax.y < lo.y || smax.z < lo.z || smin.x > hi.x || smin.y > hi.y ||
-                            smin.z > hi.z)
-                            continue;
+                // the boxes passing the reject, 32 at a time, then their exact tests: lanes
+                // test their k-th candidates together (the flag is an OR over boxes, so the
+                // order does not matter), instead of each lane's candidates at its own j
+                for (uint32_t base = 0; base < nb && !flagged; base += 32) {
+                    const uint32_t cnt = nb - base < 32 ? nb - base : 32;
+                    uint32_t cand = 0;
+                    for (uint32_t q = 0; q < cnt; ++q) {
+                        const float4 lo = wide[2 * (base + q)], hi = wide[2 * (base + q) + 1];
+                        const bool apart = bounded && (smax.x < lo.x || smax.y < lo.y || smax.z < lo.z ||
+                                                       smin.x > hi.x || smin.y > hi.y || smin.z > hi.z);
+                        cand |= apart ? 0u : 1u << q;
                     }
-                    if (segment_box(prev, b, boxes[j])) {
-                        flagged = true;
-                        break;
+                    while (cand) {
+                        const uint32_t q = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        if (segment_box(prev, b, boxes[base + q])) {
+                            flagged = true;
+                            break;
+                        }
                     }
                 }
             }
