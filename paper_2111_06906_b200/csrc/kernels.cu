@@ -199,6 +199,12 @@ __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S
                                                         uint32_t* list, uint32_t* masks, Counters* ctr) {
     __shared__ Box boxes[kMaxDyn];
     __shared__ float4 wide[2 * kMaxDyn];  // boxes pre-widened by the reject tolerance at ext_bound
+    // per warp: a queue of (segment, box) pairs that passed the reject; the exact tests run 32
+    // at a time, one pair per lane, whichever lane's path they belong to (the segment flag is
+    // an OR over boxes, so order and early exit do not matter)
+    constexpr uint32_t kQ = 64;
+    __shared__ float4 q_a[kT / 32][kQ], q_b[kT / 32][kQ];  // {a, owner << 16 | s << 8 | box} {b, -}
+    __shared__ uint32_t q_mask[kT];
     const FrameParams* fp = S.fp;
     const uint32_t nb = fp->n_boxes;
     // Bounding-box reject before the slab test: a segment whose box misses an occlusion box by
@@ -221,63 +227,108 @@ __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S
         wide[2 * k + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
     }
     __syncthreads();
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
-        const uchar4 m = P.meta[i];
-        if (m.z != kLive) continue;
-        const uint32_t k = m.x, segs = m.x + m.y;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float4* const QA = q_a[warp];
+    float4* const QB = q_b[warp];
+    uint32_t* const QM = q_mask + 32 * warp;
+    uint32_t qn = 0;  // warp-uniform queue length
+    auto test_front = [&](uint32_t cnt) {  // exact tests of queue entries [0, cnt), cnt <= 32
+        if (lane < cnt) {
+            const float4 a = QA[lane], b = QB[lane];
+            const uint32_t code = __float_as_uint(a.w);
+            if (segment_box(V3{a.x, a.y, a.z}, V3{b.x, b.y, b.z}, boxes[code & 0xFFu]))
+                atomicOr(&QM[code >> 16], 1u << ((code >> 8) & 0xFFu));
+        }
+        __syncwarp();
+    };
+    for (uint32_t i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < P.n; i0 += gridDim.x * blockDim.x) {
+        const uint32_t i = i0 + lane;
+        const uchar4 m = i < P.n ? P.meta[i] : make_uchar4(0, 0, kDead, 0);
+        const bool live = m.z == kLive;
+        const uint32_t k = live ? m.x : 0u, segs = live ? m.x + m.y : 0u;
+        QM[lane] = 0u;
         uint32_t mask = 0;
-        V3 prev = ld3(P.origin[i]);
+        V3 prev = live ? ld3(P.origin[i]) : V3{0.f, 0.f, 0.f};
         uint32_t prev_obj = kInvalidObj;
         // vertex s+1 is loaded while segment s is tested (the loop is load-latency bound)
         float4 nextv = k > 0 ? __ldcs(&P.pos_obj[2 * (vix(P, 0, i))]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (uint32_t s = 0; s < segs; ++s) {
+        const uint32_t s_end = __reduce_max_sync(0xffffffffu, segs);
+        for (uint32_t s = 0; s < s_end; ++s) {
+            const bool act = s < segs;
             V3 cur{0, 0, 0};
             uint32_t cur_obj = kInvalidObj;
-            if (s < k) {
+            if (act && s < k) {
                 const float4 v = nextv;
                 if (s + 1 < k) nextv = __ldcs(&P.pos_obj[2 * (vix(P, s + 1, i))]);
                 cur = ld3(v);
                 cur_obj = __float_as_uint(v.w);
             }
             bool flagged = false;
-            if (s > 0 && prev_obj != kInvalidObj && (__ldg(&S.oflags[prev_obj]) & 1u)) flagged = true;
-            if (!flagged && s < k && cur_obj != kInvalidObj && (__ldg(&S.oflags[cur_obj]) & 1u)) flagged = true;
-            if (!flagged) {
-                V3 b = cur;
+            if (act && s > 0 && prev_obj != kInvalidObj && (__ldg(&S.oflags[prev_obj]) & 1u)) flagged = true;
+            if (act && !flagged && s < k && cur_obj != kInvalidObj && (__ldg(&S.oflags[cur_obj]) & 1u)) flagged = true;
+            if (flagged) mask |= 1u << s;
+            const bool probe = act && !flagged;
+            V3 b = cur, smin{}, smax{};
+            bool bounded = false;
+            if (probe) {
                 if (s >= k) {  // escape segment, clipped to twice the diagonal
                     const V3 dir = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, s - 1, i))]);
                     b = add(prev, mul(dir, S.two_diag));
                 }
-                const V3 smin{fminf(prev.x, b.x), fminf(prev.y, b.y), fminf(prev.z, b.z)};
-                const V3 smax{fmaxf(prev.x, b.x), fmaxf(prev.y, b.y), fmaxf(prev.z, b.z)};
-                const bool bounded = smax.x - smin.x <= ext_bound && smax.y - smin.y <= ext_bound &&
-                                     smax.z - smin.z <= ext_bound;
-                // the boxes passing the reject, 32 at a time, then their exact tests: lanes
-                // test their k-th candidates together (the flag is an OR over boxes, so the
-                // order does not matter), instead of each lane's candidates at its own j
-                for (uint32_t base = 0; base < nb && !flagged; base += 32) {
-                    const uint32_t cnt = nb - base < 32 ? nb - base : 32;
-                    uint32_t cand = 0;
+                smin = V3{fminf(prev.x, b.x), fminf(prev.y, b.y), fminf(prev.z, b.z)};
+                smax = V3{fmaxf(prev.x, b.x), fmaxf(prev.y, b.y), fmaxf(prev.z, b.z)};
+                bounded = smax.x - smin.x <= ext_bound && smax.y - smin.y <= ext_bound && smax.z - smin.z <= ext_bound;
+            }
+            for (uint32_t base = 0; base < nb; base += 32) {
+                const uint32_t cnt = nb - base < 32 ? nb - base : 32;
+                uint32_t cand = 0;
+                if (probe) {
                     for (uint32_t q = 0; q < cnt; ++q) {
                         const float4 lo = wide[2 * (base + q)], hi = wide[2 * (base + q) + 1];
                         const bool apart = bounded && (smax.x < lo.x || smax.y < lo.y || smax.z < lo.z ||
                                                        smin.x > hi.x || smin.y > hi.y || smin.z > hi.z);
                         cand |= apart ? 0u : 1u << q;
                     }
-                    while (cand) {
+                }
+                while (__any_sync(0xffffffffu, cand != 0u)) {  // append one candidate per lane
+                    const bool has = cand != 0u;
+                    const unsigned who = __ballot_sync(0xffffffffu, has);
+                    if (has) {
                         const uint32_t q = __ffs(cand) - 1;
                         cand &= cand - 1;
-                        if (segment_box(prev, b, boxes[base + q])) {
-                            flagged = true;
-                            break;
+                        const uint32_t at = qn + __popc(who & ((1u << lane) - 1u));
+                        QA[at] = make_float4(prev.x, prev.y, prev.z, __uint_as_float(lane << 16 | s << 8 | (base + q)));
+                        QB[at] = make_float4(b.x, b.y, b.z, 0.f);
+                    }
+                    qn += __popc(who);
+                    __syncwarp();
+                    if (qn >= 32) {
+                        test_front(32);
+                        qn -= 32;
+                        float4 ta, tb;
+                        if (lane < qn) {
+                            ta = QA[32 + lane];
+                            tb = QB[32 + lane];
                         }
+                        __syncwarp();
+                        if (lane < qn) {
+                            QA[lane] = ta;
+                            QB[lane] = tb;
+                        }
+                        __syncwarp();
                     }
                 }
             }
-            if (flagged) mask |= 1u << s;
             prev = cur;
             prev_obj = cur_obj;
         }
+        if (qn > 0) {
+            test_front(qn);
+            qn = 0;
+        }
+        mask |= QM[lane];
+        __syncwarp();
+        if (!live) continue;
         if (record) P.seg_flags[i] = mask;
         if (mask == 0) continue;
         if (mode == PRX_MODE_NAIVE) {
