@@ -316,21 +316,44 @@ def main():
     traced = med(lambda a, b: a.rays_traced)
     vis = med(lambda a, b: a.visibility_rays)
 
-    # e2e through the public API with host buffers (stats + image read back every step)
+    # e2e through the public API with host buffers (stats + image read back every step), on a
+    # fresh engine replaying the same frames as the timed loop (the workload drifts with the
+    # animation, so later frames would not be comparable)
+    if world > 1:
+        ex2 = GpuExecutor(scene, cfg, stream)
+        eng2 = ex2.engine
+    else:
+        eng2 = pr.Engine(scene, cfg)
+        eng2.set_stream(stream.cuda_stream)
+    frame2 = [0]
+    e2e_dev = []  # device stage times of the e2e frames (diagnostic: host overhead = wall - this)
+
+    def step_e2e(collect):
+        if world > 1:  # sharded frame + reduced image read back to the host
+            run_frame_distributed(ex2, coll, frame2[0])
+            L.check(L.lib().prx_splat(eng2.handle, C.byref(cam), 0.25, args.splat_mode, None,
+                                      C.c_void_p(img_dev.data_ptr()), None))
+            torch.distributed.all_reduce(img_dev)
+            img_dev.cpu()
+        else:  # the public Python API: counters and the host image every step
+            st = eng2.run_frame()
+            sst = L.FrameStats()
+            eng2.splat(radius=0.25, mode=args.splat_mode, st=sst)
+            if collect:
+                e2e_dev.append(st.ms_frame_update + st.ms_verify + st.ms_retrace + sst.ms_splat)
+        frame2[0] += 1
+
+    for _ in range(max(3, args.warmup)):
+        step_e2e(False)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    xfer0 = eng.transfer_bytes()
+    xfer0 = eng2.transfer_bytes()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        if world > 1:  # sharded frame + reduced image read back to the host
-            step()
-            img_host = img_dev.cpu()
-        else:  # the public Python API: counters and the host image every step
-            eng.run_frame()
-            eng.splat(radius=0.25, mode=args.splat_mode)
+        step_e2e(True)
     e2e_s = time.perf_counter() - t0
-    xfer1 = eng.transfer_bytes()
+    xfer1 = eng2.transfer_bytes()
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -365,7 +388,8 @@ def main():
             "retraced_paths_per_frame": retraced, "rays_traced_per_frame": traced,
             "visibility_rays_per_frame": vis,
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / args.steps,
+                    "device_ms_per_step": (statistics.mean(e2e_dev) if e2e_dev else None)},
             "gpu_launches": launches, "clocks": clk, "roofline": roofline}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
