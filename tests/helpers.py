@@ -22,11 +22,6 @@ def counts(st):
                                           "paths_pruned", "paths_filled", "visibility_rays"))
 
 
-def live_mask(meta, bounces):
-    """[B*N] mask of live photon records."""
-    return None
-
-
 def compare_state(gpu, cpu, n_lights, fields=("photons", "path_info", "meta", "cell", "epoch",
                                               "origin", "emission_dir", "canonical", "retrace_start")):
     """Return {field: number of mismatching entries} (0 everywhere = bit-exact)."""

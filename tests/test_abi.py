@@ -2,7 +2,6 @@
 symbol include/prx.h declares, its host-side functions reproduce the reference's
 known answers, scenes/BVHs equal the reference's, and errors map to the reference's
 exception types.  No kernel runs here (no GPU in this container)."""
-import ctypes as C
 import json
 import os
 import re

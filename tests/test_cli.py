@@ -3,7 +3,6 @@
 import os
 import subprocess
 
-import numpy as np
 import pytest
 
 from paper_2111_06906_b200 import _lib as L

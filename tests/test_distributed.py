@@ -11,13 +11,12 @@ import tempfile
 
 import numpy as np
 import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import port
 from paper_2111_06906_b200 import pathreuse as pr
-from paper_2111_06906_b200.distributed import COUNTER_KEYS, TorchCollectives, run_frame_distributed, shard_range
+from paper_2111_06906_b200.distributed import TorchCollectives, run_frame_distributed, shard_range
 
 FIELDS = ("photons", "path_info", "meta", "cell", "epoch", "origin", "emission_dir", "canonical")
 SLICED = {"photons": True}

@@ -4,8 +4,6 @@ own loader and writers (oracle/_ref): same scenes bit for bit, byte-identical fi
 CPU only: the loader and writers are host code behind the C ABI (csrc/scene_io.cpp,
 csrc/wire.cpp); the engine-level photon dump is covered in test_gpu_io.py.
 """
-import ctypes as C
-import os
 import struct
 
 import numpy as np
