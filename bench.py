@@ -53,6 +53,7 @@ def parse_args():
     ap.add_argument("--paths", type=int, default=0, help="override n_paths")
     ap.add_argument("--splat-mode", type=int, default=1, help="0 atomic splat, 1 ordered bit-exact gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e replay (profiling passes)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     return ap.parse_args()
 
@@ -319,7 +320,9 @@ def main():
     # e2e through the public API with host buffers (stats + image read back every step), on a
     # fresh engine replaying the same frames as the timed loop (the workload drifts with the
     # animation, so later frames would not be comparable)
-    if world > 1:
+    if args.no_e2e:
+        eng2 = eng
+    elif world > 1:
         ex2 = GpuExecutor(scene, cfg, stream)
         eng2 = ex2.engine
     else:
@@ -343,26 +346,27 @@ def main():
                 e2e_dev.append(st.ms_frame_update + st.ms_verify + st.ms_retrace + sst.ms_splat)
         frame2[0] += 1
 
-    for _ in range(max(3, args.warmup)):
+    e2e_steps = 0 if args.no_e2e else args.steps
+    for _ in range(max(3, args.warmup) if e2e_steps else 0):
         step_e2e(False)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     xfer0 = eng2.transfer_bytes()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         step_e2e(True)
-    e2e_s = time.perf_counter() - t0
+    e2e_s = max(time.perf_counter() - t0, 1e-9)
     xfer1 = eng2.transfer_bytes()
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = n_paths * args.steps / e2e_s
+    e2e_value = n_paths * e2e_steps / e2e_s if e2e_steps else None
     # bytes the engine itself copied per step (counted inside the library), plus the reduced
     # image read back by torch on the sharded path
-    h2d = (xfer1[0] - xfer0[0]) // args.steps
-    d2h = (xfer1[1] - xfer0[1]) // args.steps + (12 * cam.width * cam.height if world > 1 else 0)
+    h2d = (xfer1[0] - xfer0[0]) // max(e2e_steps, 1)
+    d2h = (xfer1[1] - xfer0[1]) // max(e2e_steps, 1) + (12 * cam.width * cam.height if world > 1 else 0)
 
     # roofline of the dominant kernel stage (trace): algorithmic bytes per traced segment =
     # 64 B written (4 x float4 vertex streams) + 64 B per retraced path start (meta, rstart,
@@ -388,7 +392,7 @@ def main():
             "retraced_paths_per_frame": retraced, "rays_traced_per_frame": traced,
             "visibility_rays_per_frame": vis,
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / args.steps,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / e2e_steps if e2e_steps else None,
                     "device_ms_per_step": (statistics.mean(e2e_dev) if e2e_dev else None)},
             "gpu_launches": launches, "clocks": clk, "roofline": roofline}
 

@@ -10,7 +10,7 @@ out=gpurun_out
 mkdir -p "$out"
 python bench.py --steps 5 --warmup 3 > "$out/${tag}_bench.json" 2> "$out/${tag}_bench.err"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/${tag}_launches.csv" \
-    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$out/${tag}_ncu_launches.log" 2>&1
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > "$out/${tag}_ncu_launches.log" 2>&1
 ncu --set full --import-source on --clock-control none \
-    -k regex:"k_trace|k_verify_error_walk|k_gather_pixels|k_occlusion_flags" --launch-skip 8 -c 4 \
-    -o "$out/${tag}_full" python bench.py --steps 1 --warmup 3 --no-cpu-baseline > "$out/${tag}_ncu_full.log" 2>&1
+    -k regex:"k_trace|k_verify_error_walk|k_gather_pixels|k_occlusion_flags" --launch-skip 7 -c 3 \
+    -o "$out/${tag}_full" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > "$out/${tag}_ncu_full.log" 2>&1
