@@ -219,6 +219,10 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     d_fp_.alloc(sizeof(FrameParams));
     PRX_CUDA(cudaMallocHost(&h_ctr_, sizeof(Counters)));
     PRX_CUDA(cudaMallocHost(&h_cnt32_, 4 * kCntN));
+    PRX_CUDA(cudaMallocHost(&h_prune_frame_, 4));
+    *h_prune_frame_ = 0;
+    d_prune_frame_.alloc(4);
+    if (const char* e = std::getenv("PRX_GRAPHS")) graphs_on_ = std::atoi(e) != 0;
     d_ctr_.alloc(sizeof(Counters));
     d_cnt32_.alloc(4 * kCntN);
     d_work_.alloc(64);
@@ -248,6 +252,10 @@ Engine::~Engine() {
     if (h_ctr_) cudaFreeHost(h_ctr_);
     if (h_cnt32_) cudaFreeHost(h_cnt32_);
     if (h_xf_) cudaFreeHost(h_xf_);
+    if (h_prune_frame_) cudaFreeHost(h_prune_frame_);
+    for (auto& kv : graphs_)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (capture_stream_) cudaStreamDestroy(capture_stream_);
     if (stream_ && own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -586,7 +594,10 @@ uint32_t Engine::local_le(const LightBlock& b) const {
 }
 
 void Engine::record(int idx) {
-    PRX_CUDA(cudaEventRecord(ev_[idx], stream_));
+    if (capturing_)  // an event-record node of the frame graph (timed like a stream event)
+        PRX_CUDA(cudaEventRecordWithFlags(ev_[idx], stream_, cudaEventRecordExternal));
+    else
+        PRX_CUDA(cudaEventRecord(ev_[idx], stream_));
     ev_recorded_[idx] = true;
 }
 
@@ -598,7 +609,7 @@ double Engine::elapsed_ms(int a, int b) {
 }
 
 // ----------------------------------------------------------------------- frame params
-void Engine::fill_frame_params() {
+void Engine::fill_frame_params_host() {
     FrameParams& fp = *h_fp_;
     fp.frame = cur_frame_;
     fp.n_lights = static_cast<uint32_t>(lights_.size());
@@ -626,6 +637,10 @@ void Engine::fill_frame_params() {
         L.dm_c = b.dm_c.as<uint32_t>();
     }
     fp.n_dyn = static_cast<uint32_t>(dyn_.size());
+}
+
+void Engine::fill_frame_params() {
+    fill_frame_params_host();
     copy_async(d_fp_.get(), h_fp_, sizeof(FrameParams), cudaMemcpyHostToDevice);
 }
 
@@ -658,7 +673,12 @@ void Engine::place_frame(int frame) {
 
 // device placement of the dynamics (+ LBVH) for the transforms of cur_frame_
 void Engine::place_dynamics(bool force) {
-    if (dyn_.empty()) return;
+    if (place_dynamics_host(force)) place_dynamics_enqueue();
+}
+
+// transforms of cur_frame_ into pinned host memory; true when the device copy must change
+bool Engine::place_dynamics_host(bool force) {
+    if (dyn_.empty()) return false;
     bool changed = force;
     for (size_t j = 0; j < dyn_.size(); ++j) {
         const Object& o = scene_->objects[dyn_[j].obj];
@@ -669,7 +689,10 @@ void Engine::place_dynamics(bool force) {
         h_xf_[2 * j] = float4{now.rot.x, now.rot.y, now.rot.z, now.rot.w};
         h_xf_[2 * j + 1] = float4{now.trans.x, now.trans.y, now.trans.z, now.scale};
     }
-    if (!changed) return;
+    return changed;
+}
+
+void Engine::place_dynamics_enqueue() {
     copy_async(d_dyn_xf_.get(), h_xf_, sizeof(float4) * 2 * dyn_.size(), cudaMemcpyHostToDevice);
     launch_transform_dynamic(d_dyn_local_.as<float4>(), d_dyn_tri_xf_.as<uint32_t>(),
                              d_dyn_xf_.as<float4>(), n_dyn_tris_, d_dyn_world_.as<float4>(), stream_);
@@ -687,14 +710,23 @@ void Engine::copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind
 }
 
 // ----------------------------------------------------------------------- stages
+// frame_update = its host part (frame counter, light poses, frame parameters and transforms in
+// pinned host memory) + its device part (uploads and kernels), split so that run_frame can
+// replay the device parts of a whole frame as one CUDA graph.
 void Engine::frame_update(prx_frame_stats* st) {
+    frame_update_host();
+    frame_update_enqueue();
+    if (st) {
+        st->frame = cur_frame_;
+        st->mode = cfg_.mode;
+    }
+}
+
+void Engine::frame_update_host() {
     PRX_CUDA(cudaSetDevice(device_));
     for (bool& r : ev_recorded_) r = false;
-    record(kEvFrame0);
     const int frame = frames_run_++;
     cur_frame_ = frame;
-    PRX_CUDA(cudaMemsetAsync(d_ctr_.get(), 0, sizeof(Counters), stream_));
-    PRX_CUDA(cudaMemsetAsync(d_cnt32_.get(), 0, 4 * kCntN, stream_));
     n_pruned_ = 0;
     // light poses (engine.cpp:205-209)
     for (LightBlock& b : lights_) {
@@ -703,18 +735,24 @@ void Engine::frame_update(prx_frame_stats* st) {
         b.moved = frame > 0 && !(b.pose_now == b.pose_prev);
     }
     place_frame(frame);
-    fill_frame_params();
-    place_dynamics(false);
+    fill_frame_params_host();
+    dyn_changed_ = place_dynamics_host(false);
+    *h_prune_frame_ = static_cast<uint32_t>(cur_frame_);
+}
+
+void Engine::frame_update_enqueue() {
+    record(kEvFrame0);
+    PRX_CUDA(cudaMemsetAsync(d_ctr_.get(), 0, sizeof(Counters), stream_));
+    PRX_CUDA(cudaMemsetAsync(d_cnt32_.get(), 0, 4 * kCntN, stream_));
+    copy_async(d_fp_.get(), h_fp_, sizeof(FrameParams), cudaMemcpyHostToDevice);
+    copy_async(d_prune_frame_.get(), h_prune_frame_, 4, cudaMemcpyHostToDevice);
+    if (dyn_changed_) place_dynamics_enqueue();
     launch_frame_reset(path_dev(), cfg_.record_flags, d_ctr_.as<Counters>(), stream_);
     if (cfg_.mode == PRX_MODE_BASELINE) {  // engine.cpp:228-232
         launch_release_all(path_dev(), stream_);
         for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.dm_c.get(), 0, 4ull * b.cells, stream_));
     }
     record(kEvVerify0);
-    if (st) {
-        st->frame = frame;
-        st->mode = cfg_.mode;
-    }
 }
 
 void Engine::stage_update_origins() {
@@ -757,8 +795,12 @@ void Engine::verify_paths(prx_frame_stats* st) {
 // stage_prune (engine.cpp:473-497), split at the cross-shard exchange point.
 // Marks (Eq. 1 Bernoulli, keyed by (path, frame)) and per-cell unmarked counts.
 void Engine::prune_mark_all() {
+    if (!capturing_) {  // (a frame graph uploads the frame number itself, from frame_update_host)
+        *h_prune_frame_ = static_cast<uint32_t>(cur_frame_);
+        copy_async(d_prune_frame_.get(), h_prune_frame_, 4, cudaMemcpyHostToDevice);
+    }
     for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.unm.get(), 0, 4ull * b.cells, stream_));
-    launch_prune_mark(scene_dev(), path_dev(), static_cast<uint32_t>(cur_frame_), d_light_ptrs_.as<uint32_t*>(),
+    launch_prune_mark(scene_dev(), path_dev(), d_prune_frame_.as<uint32_t>(), d_light_ptrs_.as<uint32_t*>(),
                       d_flags8_.as<uint8_t>(), d_flags8b_.as<uint8_t>(), stream_);
 }
 
@@ -880,6 +922,11 @@ void Engine::read_back(prx_frame_stats* st, bool with_times) {
 }
 
 void Engine::retrace_invalid(prx_frame_stats* st) {
+    retrace_enqueue();
+    read_back(st, true);
+}
+
+void Engine::retrace_enqueue() {
     PRX_CUDA(cudaSetDevice(device_));
     record(kEvPrune0);
     in_full_frame_ = true;  // prune -> fill -> trace run back to back: skip the prune clears
@@ -890,14 +937,86 @@ void Engine::retrace_invalid(prx_frame_stats* st) {
     record(kEvTrace0);
     stage_trace();
     record(kEvEnd);
+}
+
+// One frame. The device work of a frame depends on the host only through a few decisions
+// (first frame, lights moved, occlusion boxes present, dynamics moved, mode); a frame whose
+// decisions repeat the previous frame's is captured once as a CUDA graph and replayed
+// (its uploads read the pinned frame parameters at execution time), removing the per-launch
+// gaps of ~120 small launches. PRX_GRAPHS=0 keeps plain stream launches.
+void Engine::run_frame(prx_frame_stats* st) {
+    if (st) std::memset(st, 0, sizeof(*st));
+    frame_update_host();
+    bool any_moved = false;
+    for (const LightBlock& b : lights_) any_moved = any_moved || b.moved;
+    const uint32_t sig = (cur_frame_ > 0 ? 1u : 0u) | (any_moved ? 2u : 0u) | (h_fp_->n_boxes > 0 ? 4u : 0u) |
+                         (dyn_changed_ ? 8u : 0u) | (static_cast<uint32_t>(cfg_.mode) << 4);
+    auto plain = [&] {
+        frame_update_enqueue();
+        verify_paths(nullptr);
+        retrace_enqueue();
+    };
+    auto it = graphs_on_ ? graphs_.find(sig) : graphs_.end();
+    if (it != graphs_.end()) {
+        const FrameGraph& g = it->second;
+        PRX_CUDA(cudaGraphLaunch(g.exec, stream_));
+        h2d_bytes_ += g.h2d;
+        d2h_bytes_ += g.d2h;
+        g_launches += g.launches;
+        for (int k = 0; k < 12; ++k) ev_recorded_[k] = g.ev[k];
+    } else if (graphs_on_ && sig == last_sig_) {
+        capture_frame(sig, plain);
+    } else {
+        plain();
+    }
+    last_sig_ = sig;
+    if (st) {
+        st->frame = cur_frame_;
+        st->mode = cfg_.mode;
+    }
     read_back(st, true);
 }
 
-void Engine::run_frame(prx_frame_stats* st) {
-    if (st) std::memset(st, 0, sizeof(*st));
-    frame_update(st);
-    verify_paths(st);
-    retrace_invalid(st);
+template <typename F>
+void Engine::capture_frame(uint32_t sig, F&& enqueue) {
+    if (!capture_stream_) PRX_CUDA(cudaStreamCreateWithFlags(&capture_stream_, cudaStreamNonBlocking));
+    const cudaStream_t saved = stream_;
+    const uint64_t h2d0 = h2d_bytes_, d2h0 = d2h_bytes_, l0 = g_launches;
+    cudaGraph_t graph = nullptr;
+    stream_ = capture_stream_;
+    capturing_ = true;
+    cudaError_t err = cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal);
+    if (err == cudaSuccess) {
+        try {
+            enqueue();
+        } catch (...) {
+            err = cudaErrorStreamCaptureInvalidated;
+        }
+        const cudaError_t end = cudaStreamEndCapture(stream_, &graph);
+        if (err == cudaSuccess) err = end;
+    }
+    capturing_ = false;
+    stream_ = saved;
+    cudaGraphExec_t exec = nullptr;
+    if (err == cudaSuccess && graph) err = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (err != cudaSuccess || !exec) {  // stay on plain launches; the frame was not executed
+        cudaGetLastError();
+        graphs_on_ = false;
+        h2d_bytes_ = h2d0;
+        d2h_bytes_ = d2h0;
+        g_launches = l0;
+        enqueue();
+        return;
+    }
+    FrameGraph g;
+    g.exec = exec;
+    g.h2d = h2d_bytes_ - h2d0;
+    g.d2h = d2h_bytes_ - d2h0;
+    g.launches = g_launches - l0;
+    for (int k = 0; k < 12; ++k) g.ev[k] = ev_recorded_[k];
+    graphs_[sig] = g;
+    PRX_CUDA(cudaGraphLaunch(exec, stream_));
 }
 
 void Engine::run_stage(int stage, prx_frame_stats* st) {

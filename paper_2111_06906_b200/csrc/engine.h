@@ -11,6 +11,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "dev_types.h"
@@ -120,6 +121,14 @@ private:
     void apply_l2_policy();
     void alloc_state();
     void fill_frame_params();
+    void fill_frame_params_host();
+    void frame_update_host();
+    void frame_update_enqueue();
+    void retrace_enqueue();
+    bool place_dynamics_host(bool force);
+    void place_dynamics_enqueue();
+    template <typename F>
+    void capture_frame(uint32_t sig, F&& enqueue);
     void place_frame(int frame);
     void place_dynamics(bool force);
     void stage_update_origins();
@@ -194,6 +203,19 @@ private:
 
     cudaEvent_t ev_[12] = {};
     bool ev_recorded_[12] = {};
+
+    // whole-frame CUDA graphs (run_frame), keyed by the frame's host decisions
+    struct FrameGraph {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t h2d = 0, d2h = 0, launches = 0;
+        bool ev[12] = {};
+    };
+    std::map<uint32_t, FrameGraph> graphs_;
+    uint32_t last_sig_ = ~0u;
+    bool graphs_on_ = true, capturing_ = false, dyn_changed_ = false;
+    cudaStream_t capture_stream_ = nullptr;
+    uint32_t* h_prune_frame_ = nullptr;  // pinned: the frame number the prune marks are keyed by
+    DevBuf d_prune_frame_;
 };
 
 // host-libm cos/sin table for cosine_sample's 2^24 possible angles (device copy, cached)

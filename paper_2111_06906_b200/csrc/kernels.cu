@@ -605,9 +605,10 @@ __global__ void __launch_bounds__(kT) k_compute_dm(SceneDev S, PathDev P, Counte
 }
 
 // ---------------------------------------------------------------- prune (engine.cpp:443-497)
-__global__ void k_prune_mark(SceneDev S, PathDev P, uint32_t frame, uint32_t* const* unmarked,
+__global__ void k_prune_mark(SceneDev S, PathDev P, const uint32_t* frame_dev, uint32_t* const* unmarked,
                              uint8_t* pruned, uint8_t* cand) {
     const FrameParams* fp = S.fp;
+    const uint32_t frame = *frame_dev;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
         pruned[i] = 0;
         cand[i] = 0;
@@ -986,7 +987,7 @@ void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t*
 void launch_compute_dm(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st) {
     LAUNCH(k_compute_dm, P.n, S, P, ctr);
 }
-void launch_prune_mark(SceneDev S, PathDev P, uint32_t frame, uint32_t* const* unmarked, uint8_t* pruned,
+void launch_prune_mark(SceneDev S, PathDev P, const uint32_t* frame, uint32_t* const* unmarked, uint8_t* pruned,
                        uint8_t* cand, cudaStream_t st) {
     LAUNCH(k_prune_mark, P.n, S, P, frame, unmarked, pruned, cand);
 }

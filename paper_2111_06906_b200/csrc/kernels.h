@@ -34,7 +34,7 @@ void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t*
 // stage_compute_dm (engine.cpp:405-441)
 void launch_compute_dm(SceneDev S, PathDev P, Counters* ctr, cudaStream_t st);
 // stage_prune (engine.cpp:443-497): marks + per-cell unmarked counts
-void launch_prune_mark(SceneDev S, PathDev P, uint32_t frame, uint32_t* const* unmarked,
+void launch_prune_mark(SceneDev S, PathDev P, const uint32_t* frame, uint32_t* const* unmarked,
                        uint8_t* pruned, uint8_t* cand, cudaStream_t st);
 void launch_prune_trim_flags(PathDev P, const FrameParams* fp, uint32_t* const* unm_total,
                              const uint8_t* cand, uint8_t* trim, cudaStream_t st);
