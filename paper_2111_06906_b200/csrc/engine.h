@@ -127,8 +127,10 @@ private:
     void retrace_enqueue();
     bool place_dynamics_host(bool force);
     void place_dynamics_enqueue();
+    struct FrameGraph;
     template <typename F>
-    void capture_frame(uint32_t sig, F&& enqueue);
+    bool capture_graph(F&& enqueue, FrameGraph& out);
+    void launch_graph(const FrameGraph& g);
     void place_frame(int frame);
     void place_dynamics(bool force);
     void stage_update_origins();
