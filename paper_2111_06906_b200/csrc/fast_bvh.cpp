@@ -20,6 +20,18 @@ namespace prx {
 namespace {
 
 constexpr int kMaxBins = 64;
+// The traversal kernels keep a 64-entry stack (device_scene.cuh: fast_closest /
+// joint_closest push at most one entry per level).  The binned SAH has no depth bound on
+// adversarial inputs (clustered or log-spaced centroids peel off a few triangles per
+// level), so a subtree that could not finish within g_max_depth levels is split at its
+// centroid median instead, which needs at most ceil(log2(n / 2)) more levels.
+int g_max_depth = 48;  // PRX_SAH_MAXDEPTH overrides (tests: measure the uncapped depth)
+
+int ceil_log2(uint32_t n) {
+    int d = 0;
+    while ((1ull << d) < n) ++d;
+    return d;
+}
 // build knobs (PRX_SAH_BINS / PRX_SAH_TRAV / PRX_SAH_MAXLEAF override, for tuning runs)
 int g_bins = 16;
 float g_trav = 1.0f;
@@ -42,11 +54,14 @@ struct Builder {
     std::vector<FastNode>& nodes;
 
     // Returns the child code for the range [b, e) (leaf code or internal node index).
-    uint32_t build(uint32_t b, uint32_t e, const Box& bounds) {
+    int max_depth = 0;  // internal-node levels of the finished tree (root = 1)
+
+    uint32_t build(uint32_t b, uint32_t e, const Box& bounds, int depth = 1) {
         const uint32_t n = e - b;
         if (n <= 2) return leaf(b, n);
         Box cb = empty_box();
         for (uint32_t i = b; i < e; ++i) expand(cb, prims[idx[i]].c);
+        if (depth + ceil_log2(n) >= g_max_depth) return median(b, e, cb, depth);
         int best_axis = -1;
         int best_split = 0;
         float best_cost = INFINITY;
@@ -106,13 +121,30 @@ struct Builder {
             mid = static_cast<uint32_t>(it - idx.begin());
             if (mid == b || mid == e) mid = b + n / 2;
         }
+        return internal(b, mid, e, depth);
+    }
+
+    // centroid-median split on the widest centroid axis (the depth-bounded fallback)
+    uint32_t median(uint32_t b, uint32_t e, const Box& cb, int depth) {
+        const V3 ext = sub(cb.hi, cb.lo);
+        const int axis = ext.x >= ext.y && ext.x >= ext.z ? 0 : (ext.y >= ext.z ? 1 : 2);
+        const uint32_t mid = b + (e - b) / 2;
+        std::nth_element(idx.begin() + b, idx.begin() + mid, idx.begin() + e, [&](uint32_t i, uint32_t j) {
+            const float ci = comp(prims[i].c, axis), cj = comp(prims[j].c, axis);
+            return ci < cj || (ci == cj && i < j);
+        });
+        return internal(b, mid, e, depth);
+    }
+
+    uint32_t internal(uint32_t b, uint32_t mid, uint32_t e, int depth) {
+        max_depth = std::max(max_depth, depth);
         Box lb = empty_box(), rb = empty_box();
         for (uint32_t i = b; i < mid; ++i) expand(lb, prims[idx[i]].box);
         for (uint32_t i = mid; i < e; ++i) expand(rb, prims[idx[i]].box);
         const uint32_t me = static_cast<uint32_t>(nodes.size());
         nodes.emplace_back();
-        const uint32_t l = build(b, mid, lb);
-        const uint32_t r = build(mid, e, rb);
+        const uint32_t l = build(b, mid, lb, depth + 1);
+        const uint32_t r = build(mid, e, rb, depth + 1);
         FastNode& nd = nodes[me];
         nd.box[0] = lb;
         nd.box[1] = rb;
@@ -147,7 +179,10 @@ FastBvh build_fast_bvh(const std::vector<Tri>& tris_ref_order, float pad) {
     if (const char* e = std::getenv("PRX_SAH_TRAV")) g_trav = static_cast<float>(std::atof(e));
     if (const char* e = std::getenv("PRX_SAH_MAXLEAF"))
         g_max_leaf = static_cast<uint32_t>(std::min(std::max(std::atoi(e), 1), 8));
+    if (const char* e = std::getenv("PRX_SAH_MAXDEPTH")) g_max_depth = std::max(std::atoi(e), 8);
     FastBvh out;
+    if (tris_ref_order.size() >= kMaxTreeTris)  // leaf codes hold first << 3 below kTreeBit
+        throw std::length_error("fast BVH: more than 2^27 - 1 triangles in one tree");
     const uint32_t n = static_cast<uint32_t>(tris_ref_order.size());
     if (n == 0) return out;
     std::vector<Prim> prims(n);
@@ -172,6 +207,9 @@ FastBvh build_fast_bvh(const std::vector<Tri>& tris_ref_order, float pad) {
     } else {
         // split the top like any other internal node, then move it into slot 0
         const uint32_t code = B.build(0, n, all);
+        out.depth = std::max(1, B.max_depth);
+        if (out.depth + 1 > kMaxTraversalDepth)  // only reachable with a PRX_SAH_MAXDEPTH override
+            throw std::length_error("fast BVH deeper than the traversal stack");
         if (code & kFastLeaf) {
             root_child[0] = code;
             root_child[1] = kFastEmpty;
@@ -260,10 +298,19 @@ DynSahTopology build_dyn_sah(const std::vector<std::vector<Tri>>& objects, const
         build_top(objs, 0, static_cast<uint32_t>(objs.size()), boxes, obj_root, top);
     }
     if (top.size() > n_top) throw std::logic_error("build_dyn_sah: top tree overflow");
+    // stack bound of the joint walk: the static root is parked while the dynamic tree is
+    // walked, so the combined depth (top median tree + deepest object tree) must stay < 63
+    int obj_depth = 0;
+    for (uint32_t j = 0; j < n_obj; ++j) obj_depth = std::max(obj_depth, trees[j].depth);
+    out.depth = (objs.size() > 1 ? ceil_log2(static_cast<uint32_t>(objs.size())) : 0) + obj_depth;
+    if (out.depth + 1 > kMaxTraversalDepth)
+        throw std::length_error("dynamic BVH deeper than the traversal stack (too many dynamic objects)");
     out.obj_root.assign(n_obj, ~0u);
     for (uint32_t j : objs) out.obj_root[j] = obj_root[j];
-    uint32_t n_tris = 0;
-    for (uint32_t j = 0; j < n_obj; ++j) n_tris += static_cast<uint32_t>(objects[j].size());
+    size_t n_tris_all = 0;
+    for (uint32_t j = 0; j < n_obj; ++j) n_tris_all += objects[j].size();
+    if (n_tris_all >= kMaxTreeTris) throw std::length_error("dynamic BVH: more than 2^27 - 1 triangles");
+    const uint32_t n_tris = static_cast<uint32_t>(n_tris_all);
     out.nodes.assign(4ull * total, float4{0.f, 0.f, 0.f, 0.f});
     out.parent.assign(total, ~0u);
     out.perm.resize(n_tris);

@@ -12,6 +12,8 @@ namespace prx {
 
 constexpr uint32_t kFastLeaf = 0x80000000u;   // child code: leaf | first << 3 | (count - 1)
 constexpr uint32_t kFastEmpty = 0xFFFFFFFFu;  // absent child
+constexpr size_t kMaxTreeTris = size_t(1) << 27;  // leaf code `first << 3` stays below bit 30
+constexpr int kMaxTraversalDepth = 63;            // device traversal stacks hold 64 entries
 
 struct FastNode {
     Box box[2];
@@ -21,6 +23,7 @@ struct FastNode {
 struct FastBvh {
     std::vector<FastNode> nodes;   // nodes[0] is the root (always internal)
     std::vector<uint32_t> order;   // leaf slot -> reference permutation position
+    int depth = 1;                 // internal-node levels (<= 48 by construction)
 };
 
 // `tris_ref_order[k]` is the static triangle at reference permutation position k.
@@ -36,6 +39,7 @@ struct DynSahTopology {
     std::vector<uint32_t> leaves;   // 4 per leaf: first slot, count, parent node, side
     std::vector<uint32_t> parent;   // per internal node: parent << 1 | side (root: ~0u)
     std::vector<uint32_t> obj_root; // per object: its root node (~0u: no triangles)
+    int depth = 0;                  // internal-node levels of the combined tree
 };
 // `objects[j]` holds object j's local triangles (global indices tri_begin[j] + i);
 // `boxes[j]` is a representative world box (frame 0) that orders the top tree.

@@ -29,3 +29,20 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+_PARITY_RECORDS = []
+
+
+def report_parity(tag: str, record: dict) -> None:
+    """Collect a per-frame mismatch record; printed in the terminal summary so the counts
+    are visible in a -q run (tests/test_gpu_scale_parity.py)."""
+    _PARITY_RECORDS.append((tag, record))
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    if not _PARITY_RECORDS:
+        return
+    terminalreporter.section("scale parity (mismatching entries per field; 0 = bit-exact)")
+    for tag, rec in _PARITY_RECORDS:
+        terminalreporter.write_line(f"{tag}: " + ", ".join(f"{k}={v}" for k, v in rec.items()))
