@@ -320,6 +320,8 @@ void Engine::upload_scene() {
         std::vector<Tri> ref_order(s.bvh_perm.size());
         for (size_t k = 0; k < ref_order.size(); ++k) ref_order[k] = s.static_tris[s.bvh_perm[k]];
         const FastBvh fb = build_fast_bvh(ref_order, 1e-5f * diag_ + 1e-6f);
+        if (fb.depth + 1 > kMaxTraversalDepth)  // only with a PRX_SAH_MAXDEPTH override
+            throw std::length_error("static fast BVH deeper than the traversal stack");
         std::vector<float4> fn(4 * fb.nodes.size());
         for (size_t k = 0; k < fb.nodes.size(); ++k) {
             const FastNode& nd = fb.nodes[k];

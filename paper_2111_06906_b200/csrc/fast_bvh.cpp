@@ -208,8 +208,6 @@ FastBvh build_fast_bvh(const std::vector<Tri>& tris_ref_order, float pad) {
         // split the top like any other internal node, then move it into slot 0
         const uint32_t code = B.build(0, n, all);
         out.depth = std::max(1, B.max_depth);
-        if (out.depth + 1 > kMaxTraversalDepth)  // only reachable with a PRX_SAH_MAXDEPTH override
-            throw std::length_error("fast BVH deeper than the traversal stack");
         if (code & kFastLeaf) {
             root_child[0] = code;
             root_child[1] = kFastEmpty;
