@@ -150,15 +150,17 @@ def scene_for(pr, name):
 
 
 def run_reference(args, name, n_paths, steps, warmup):
-    """The reference CPU engine on a path-prefix sample; returns (paths/s, detail)."""
+    """The reference CPU engine on a path-prefix sample; returns (paths/s, detail).
+
+    Only oracle/_ref is loaded: the scene comes from the generators compiled into the oracle
+    library (oracle/scene_gen.cpp), the config from pure-Python make_config (no _prx.so)."""
     from oracle import ref
-    from paper_2111_06906_b200 import pathreuse as pr
+    from paper_2111_06906_b200.pathreuse import make_config
 
     w = WORKLOADS[name]
-    scene = scene_for(pr, name)
-    rscene = ref.RefScene.from_desc(scene.describe())
-    cfg = pr.make_config(mode=w["mode"], paths=n_paths, bounces=w["bounces"],
-                         dm=[8, 8, 64, 64], threshold=w["threshold"], seed=1, workers=0)
+    rscene = ref.RefScene.synthetic(name)
+    cfg = make_config(mode=w["mode"], paths=n_paths, bounces=w["bounces"],
+                      dm=[8, 8, 64, 64], threshold=w["threshold"], seed=1, workers=0)
     eng = ref.RefEngine(rscene, cfg)
     eng.set_workers(0)
     for _ in range(warmup):
@@ -199,9 +201,12 @@ def main():
         cores = os.cpu_count()
         line = {"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": 0,
                 "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": det["frame_s_mean"] * 1e3 * (n_paths / sample),
+                # measured: one step = one frame (+ gather_image) of the `sample`-path prefix
+                "ms_per_step": det["frame_s_mean"] * 1e3, "sample_paths": sample,
+                # linear extrapolation to the full path count (per-path work is independent)
+                "ms_per_full_frame_extrapolated": det["frame_s_mean"] * 1e3 * (n_paths / sample),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic", "config": dict(config, cpu_sample_paths=sample),
+                "data": "synthetic (procedural scene, seed 1)", "config": config,
                 "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "reference",
                                  "sample": f"the {name} scene and configuration with {sample} of its "
                                            f"{n_paths} paths (per-path cost is independent of the path "
@@ -229,8 +234,7 @@ def main():
     from paper_2111_06906_b200 import _lib as L
 
     scene = scene_for(pr, name)
-    counts = scene.counts()
-    config.update(static_tris=counts["static_triangles"], dynamic_tris=counts["dynamic_triangles"])
+    scene_counts = scene.counts()
     shard = (0, 0)
     if world > 1:
         shard = (n_paths * rank // world, n_paths * (rank + 1) // world)
@@ -394,7 +398,9 @@ def main():
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / e2e_steps if e2e_steps else None,
                     "device_ms_per_step": (statistics.mean(e2e_dev) if e2e_dev else None)},
-            "gpu_launches": launches, "clocks": clk, "roofline": roofline}
+            "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+            "scene_counts": {"static_tris": scene_counts["static_triangles"],
+                             "dynamic_tris": scene_counts["dynamic_triangles"]}}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sample = args.cpu_sample or CPU_SAMPLE_PATHS[name]

@@ -50,6 +50,10 @@ _SIGS = [
     ("prxref_intersect_batch", C.c_int, [_P, C.c_int, C.POINTER(C.c_float), C.c_size_t,
                                          C.POINTER(C.c_float)]),
     ("prxref_occluded_batch", C.c_int, [_P, C.c_int, C.POINTER(C.c_float), C.c_size_t, C.POINTER(C.c_float)]),
+    ("prxref_gen_last_error", C.c_char_p, []),
+    ("prxref_synthetic_desc", C.c_int, [C.c_char_p, C.c_uint32, C.c_float, C.POINTER(_P),
+                                        C.POINTER(L.SceneDesc)]),
+    ("prxref_synthetic_free", None, [_P]),
     ("prxref_scene_load_text", C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(_P)]),
     ("prxref_write_photon_dump", C.c_int, [_P, C.c_char_p]),
     ("prxref_write_image", C.c_int, [C.c_char_p, C.POINTER(C.c_float), C.c_uint32, C.c_uint32]),
@@ -105,6 +109,20 @@ class RefScene:
         h = C.c_void_p()
         check(lib().prxref_scene_load_text(text.encode(), base_dir.encode(), C.byref(h)))
         return cls(h.value)
+
+    @classmethod
+    def synthetic(cls, name: str, n_dynamic: int = 0, tri_scale: float = 0.0) -> "RefScene":
+        """The BASELINE workload scenes C1-C5 from the generators compiled into the oracle
+        library (oracle/scene_gen.cpp) -- same description as pathreuse.Scene.synthetic,
+        without loading the product library."""
+        holder, desc = C.c_void_p(), L.SceneDesc()
+        if lib().prxref_synthetic_desc(name.encode(), int(n_dynamic), float(tri_scale), C.byref(holder),
+                                       C.byref(desc)) != 0:
+            raise L.SceneError(lib().prxref_gen_last_error().decode(errors="replace"))
+        try:
+            return cls.from_desc(desc)
+        finally:
+            lib().prxref_synthetic_free(holder)
 
     @classmethod
     def from_desc(cls, desc: L.SceneDesc) -> "RefScene":

@@ -196,3 +196,30 @@ def test_photon_dump_byte_identical(tmp_path):
     (tmp_path / "magic.phm").write_bytes(b"XXXX" + bytes(12))
     with pytest.raises(L.PrxError):
         pr.read_photon_dump(str(tmp_path / "magic.phm"))
+
+
+def test_oracle_synthetic_scenes_identical():
+    """The reference arm builds C1-C4 from the generators compiled into the oracle library
+    (oracle/scene_gen.cpp): the same description bit for bit as the product's."""
+    for name in ("C1", "C2", "C3", "C4"):
+        a, b = ref.RefScene.synthetic(name), pr.Scene.synthetic(name)
+        assert digest(a.describe()) == digest(b.describe()), name
+        assert np.array_equal(a.bvh_permutation(), b.bvh_permutation()), name
+
+
+def test_reference_arm_loads_only_the_oracle():
+    """bench.py --impl reference runs without loading the product library."""
+    import subprocess
+    import sys
+
+    code = ("import sys, json; sys.argv=['bench.py']; import bench; "
+            "v, d = bench.run_reference(None, 'C1', 2000, 1, 0); "
+            "maps = open('/proc/self/maps').read(); "
+            "print(json.dumps({'prx': '_prx.so' in maps, 'ref': 'libpathreuse_ref.so' in maps, 'v': v}))")
+    import json
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, check=True)
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["ref"] and not res["prx"] and res["v"] > 0
