@@ -55,6 +55,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e replay (profiling passes)")
     ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--no-splat-sweep", action="store_true", help="skip the per-mode splat timings")
     return ap.parse_args()
 
 
@@ -321,6 +322,26 @@ def main():
     traced = med(lambda a, b: a.rays_traced)
     vis = med(lambda a, b: a.visibility_rays)
 
+    # splat stage alone, both modes, at the scene camera and at the paper's 1920x1080, on the
+    # final photon map (device time from the engine's own events, median of 5)
+    def time_splat(mode, w_px, h_px, reps=5):
+        c = L.Camera(cam.position, cam.look_at, cam.fov_deg, w_px, h_px)
+        buf = img_dev if w_px * h_px == cam.width * cam.height else \
+            torch.zeros(w_px * h_px * 3, dtype=torch.float32, device="cuda")
+        ts = []
+        for _ in range(reps + 1):
+            sst = L.FrameStats()
+            L.check(L.lib().prx_splat(eng.handle, C.byref(c), 0.25, mode, None, C.c_void_p(buf.data_ptr()),
+                                      C.byref(sst)))
+            ts.append(sst.ms_splat)
+        return statistics.median(ts[1:])
+
+    splat_modes = {}
+    if not args.no_splat_sweep:
+        for mode, tag in ((1, "ordered"), (0, "atomic")):
+            for w_px, h_px in ((cam.width, cam.height), (1920, 1080)):
+                splat_modes[f"{tag}_{w_px}x{h_px}"] = time_splat(mode, w_px, h_px)
+
     # e2e through the public API with host buffers (stats + image read back every step), on a
     # fresh engine replaying the same frames as the timed loop (the workload drifts with the
     # animation, so later frames would not be comparable)
@@ -392,6 +413,7 @@ def main():
             "data": "synthetic (procedural scene, seed 1)", "config": config,
             "stages_ms": {"frame_update": update_ms, "verify": verify_ms, "occlusions": occl_ms,
                           "retrace": retrace_ms, "trace": trace_ms, "splat": splat_ms},
+            "splat_ms": splat_modes,
             "verified_segments_per_s": seg_before / (verify_ms * 1e-3) if verify_ms else None,
             "retraced_paths_per_frame": retraced, "rays_traced_per_frame": traced,
             "visibility_rays_per_frame": vis,

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <memory>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -56,6 +57,11 @@ struct Vec3 {
 inline constexpr uint32_t kInvalidObjectId = 0xFFFFFFFFu;
 struct Triangle {
     Vec3 a, b, c;
+};
+struct Aabb {  // geometry.hpp:20-39
+    Vec3 lo{3.402823466e+38f, 3.402823466e+38f, 3.402823466e+38f};
+    Vec3 hi{-3.402823466e+38f, -3.402823466e+38f, -3.402823466e+38f};
+    bool valid() const { return lo.x <= hi.x && lo.y <= hi.y && lo.z <= hi.z; }
 };
 struct Quat {
     float x = 0.0f, y = 0.0f, z = 0.0f, w = 1.0f;
@@ -220,6 +226,48 @@ inline Scene make_builtin_scene(const std::string& name) {
     return s;
 }
 
+// state_at (scene.hpp:62-74): the dynamic objects placed at one frame.  The static BVH lives
+// on the device (the reference's `static_bvh` member has no host counterpart here); `engine`
+// (B200 extension) names the engine whose device scene this state describes, which is what
+// gather_image(state, ...) splats against.
+struct PlacedDynamic {
+    uint32_t object_id = 0;
+    std::vector<Triangle> triangles;  // world space at the current frame
+    Aabb bounds_current;
+    Aabb bounds_previous;  // equals bounds_current of frame-1 (frame 0: identical)
+};
+class Engine;
+struct SceneState {
+    int frame = 0;
+    const Scene* scene = nullptr;
+    std::vector<PlacedDynamic> placed_dynamics;
+    const Engine* engine = nullptr;
+};
+
+// state_at (scene.cpp:115-134), evaluated on the host in the reference's float order
+inline SceneState state_at(const Scene& scene, int frame) {
+    SceneState st;
+    st.frame = frame;
+    st.scene = &scene;
+    size_t nd = 0, nt = 0;
+    detail::check(prx_scene_state_at(scene.handle.get(), frame, nullptr, 0, &nd, nullptr, 0, &nt));
+    std::vector<prx_placed_dynamic> dyn(nd);
+    std::vector<prx_triangle> tris(nt);
+    detail::check(prx_scene_state_at(scene.handle.get(), frame, dyn.data(), nd, &nd, tris.data(), nt, &nt));
+    for (const prx_placed_dynamic& d : dyn) {
+        PlacedDynamic pd;
+        pd.object_id = d.object_id;
+        for (uint32_t t = 0; t < d.tri_count; ++t) {
+            const prx_triangle& x = tris[d.tri_begin + t];
+            pd.triangles.push_back({detail::v(x.a), detail::v(x.b), detail::v(x.c)});
+        }
+        pd.bounds_current = {detail::v(d.cur_lo), detail::v(d.cur_hi)};
+        pd.bounds_previous = {detail::v(d.prev_lo), detail::v(d.prev_hi)};
+        st.placed_dynamics.push_back(std::move(pd));
+    }
+    return st;
+}
+
 // ---------------------------------------------------------------- photon store (photon_store.hpp)
 struct Photon {
     Vec3 incoming_dir;
@@ -317,15 +365,36 @@ struct EngineConfig {
     int device = 0;  // B200 extension
 };
 constexpr uint8_t kNoRetrace = 0xFF;
-struct DistributionMap {
+struct DmLayout {  // light.hpp:62-70
     std::vector<uint32_t> dims;
+    uint32_t total_cells() const {
+        uint32_t n = 1;
+        for (uint32_t d : dims) n *= d;
+        return n;
+    }
+};
+struct DistributionMap {  // light.hpp:72-84
+    DmLayout layout;
     std::vector<uint32_t> counts;
+    explicit DistributionMap(DmLayout l = {})
+        : layout(std::move(l)), counts(layout.dims.empty() ? 0 : layout.total_cells(), 0u) {}
     uint64_t total() const {
         uint64_t s = 0;
         for (uint32_t c : counts) s += c;
         return s;
     }
 };
+
+// select_paths_to_prune (engine.hpp:62-63, engine.cpp:443-471)
+inline std::vector<uint32_t> select_paths_to_prune(std::span<const uint32_t> cell_paths, uint32_t dm_c,
+                                                   uint32_t dm_t, uint64_t seed, uint32_t frame) {
+    std::vector<uint32_t> out(cell_paths.size());
+    size_t n = 0;
+    detail::check(prx_select_paths_to_prune(cell_paths.data(), cell_paths.size(), dm_c, dm_t, seed, frame,
+                                            out.data(), &n));
+    out.resize(n);
+    return out;
+}
 struct Image {
     uint32_t width = 0, height = 0;
     std::vector<float> pixels;  // RGB rows, top-left origin
@@ -412,8 +481,30 @@ public:
     uint32_t path_cell(uint32_t p) const { return u32(PRX_FIELD_CELL, cell_)[p]; }
     uint32_t path_epoch(uint32_t p) const { return u32(PRX_FIELD_EPOCH, epoch_)[p]; }
     uint32_t segment_count(uint32_t p) const { return photon_count(p) + (path_escaped(p) ? 1u : 0u); }
-    DistributionMap dm_target(size_t li) const { return dm(PRX_FIELD_DM_TARGET, li); }
-    DistributionMap dm_current(size_t li) const { return dm(PRX_FIELD_DM_CURRENT, li); }
+    const SceneState& scene_state() const {  // engine.hpp:79 (state_at of the last frame run)
+        if (!state_) {
+            state_ = std::make_unique<SceneState>();
+            if (info_.frames_run > 0) *state_ = state_at(scene_, info_.frames_run - 1);
+            state_->engine = this;
+        }
+        return *state_;
+    }
+    const DmLayout& dm_layout(size_t li) const { return layouts().at(li); }  // engine.hpp:102
+    const DistributionMap& dm_target(size_t li) const { return dm(PRX_FIELD_DM_TARGET, li, dm_t_); }
+    const DistributionMap& dm_current(size_t li) const { return dm(PRX_FIELD_DM_CURRENT, li, dm_c_); }
+    // engine.cpp:125-139: segment i runs from vertex i-1 (or the light) toward vertex i
+    Vec3 segment_origin(uint32_t p, uint32_t i) const {
+        if (i == 0) return path_origin(p);
+        return aux_at(i - 1, p).position;
+    }
+    Vec3 segment_dir(uint32_t p, uint32_t i) const {
+        if (i == 0) return path_emission_dir(p);
+        return aux_at(i - 1, p).outgoing;
+    }
+    Vec3 segment_end(uint32_t p, uint32_t i) const {  // escape segments clipped at 2 x diagonal
+        if (i < photon_count(p)) return aux_at(i, p).position;
+        return segment_origin(p, i) + segment_dir(p, i) * (2.0f * scene_.diagonal());
+    }
     const std::vector<uint32_t>& pruned_paths() const { return u32(PRX_FIELD_PRUNED, pruned_); }
     const std::vector<uint32_t>& segment_flags() const { return u32(PRX_FIELD_SEGMENT_FLAGS, flags_); }
     prx_engine* native() const { return engine_.get(); }
@@ -443,6 +534,9 @@ private:
     void refresh_info() { detail::check(prx_engine_get_info(engine_.get(), &info_)); }
     void invalidate() {
         refresh_info();
+        state_.reset();
+        dm_t_.clear();
+        dm_c_.clear();
         photons_.reset();
         aux_.reset();
         meta_.reset();
@@ -476,12 +570,23 @@ private:
         }
         return {(*cache)[4 * p], (*cache)[4 * p + 1], (*cache)[4 * p + 2]};
     }
-    DistributionMap dm(int field, size_t li) const {
-        DistributionMap m;
-        for (uint32_t a = 0; a < info_.dm_ndims[li]; ++a) m.dims.push_back(info_.dm_dims[li][a]);
-        m.counts.resize(info_.dm_cells[li]);
-        fetch(field, static_cast<uint32_t>(li), m.counts.data());
-        return m;
+    const std::vector<DmLayout>& layouts() const {
+        if (layouts_.empty())
+            for (uint32_t li = 0; li < info_.n_lights; ++li) {
+                DmLayout l;
+                for (uint32_t a = 0; a < info_.dm_ndims[li]; ++a) l.dims.push_back(info_.dm_dims[li][a]);
+                layouts_.push_back(std::move(l));
+            }
+        return layouts_;
+    }
+    const DistributionMap& dm(int field, size_t li, std::vector<std::unique_ptr<DistributionMap>>& cache) const {
+        if (li >= info_.n_lights) throw std::out_of_range("light index out of range");
+        if (cache.size() < info_.n_lights) cache.resize(info_.n_lights);
+        if (!cache[li]) {
+            cache[li] = std::make_unique<DistributionMap>(layouts()[li]);
+            fetch(field, static_cast<uint32_t>(li), cache[li]->counts.data());
+        }
+        return *cache[li];
     }
 
     Scene scene_;
@@ -493,9 +598,19 @@ private:
     mutable std::unique_ptr<std::vector<uint8_t>> meta_, rstart_;
     mutable std::unique_ptr<std::vector<uint32_t>> path_info_, cell_, epoch_, pruned_, flags_;
     mutable std::unique_ptr<std::vector<float>> origin_, emis_;
+    mutable std::unique_ptr<SceneState> state_;
+    mutable std::vector<DmLayout> layouts_;
+    mutable std::vector<std::unique_ptr<DistributionMap>> dm_t_, dm_c_;
 };
 
-// gather_image (gather.hpp:81-83) over the engine's current photons, as the GPU splat.
+// gather_image (gather.hpp:81-83) with the reference's signature.  The state must come from
+// engine.scene_state() (it names the engine whose device scene the splat runs against).  When
+// `photons`/`aux` are that engine's own mirrors the splat reads the device path store directly;
+// any other host photon map is uploaded and splatted (prx_gather_photons).  The image is the
+// ordered GPU gather: byte-identical to the reference's.  `workers` is ignored.
+inline Image gather_image(const SceneState& state, const PhotonMap& photons, std::span<const PathVertexAux> aux,
+                          const Camera& cam, float radius, unsigned workers);
+// B200 convenience: the engine's current photons
 inline Image gather_image(const Engine& engine, const Camera& cam, float radius, unsigned /*workers*/ = 1) {
     Image img;
     img.width = cam.width;
@@ -503,6 +618,25 @@ inline Image gather_image(const Engine& engine, const Camera& cam, float radius,
     img.pixels.assign(3ull * cam.width * cam.height, 0.0f);
     const prx_camera c{detail::v(cam.position), detail::v(cam.look_at), cam.fov_deg, cam.width, cam.height};
     detail::check(prx_splat(engine.native(), &c, radius, 1, img.pixels.data(), nullptr, nullptr));
+    return img;
+}
+
+inline Image gather_image(const SceneState& state, const PhotonMap& photons, std::span<const PathVertexAux> aux,
+                          const Camera& cam, float radius, unsigned workers) {
+    if (!state.engine)
+        throw std::invalid_argument("gather_image: the SceneState does not come from an Engine (scene_state())");
+    const Engine& engine = *state.engine;
+    if (&photons == &engine.photon_map() && aux.data() == engine.vertex_aux().data())
+        return gather_image(engine, cam, radius, workers);
+    if (aux.size() != photons.records().size())
+        throw std::invalid_argument("gather_image: photon map and aux sizes differ");
+    Image img;
+    img.width = cam.width;
+    img.height = cam.height;
+    img.pixels.assign(3ull * cam.width * cam.height, 0.0f);
+    const prx_camera c{detail::v(cam.position), detail::v(cam.look_at), cam.fov_deg, cam.width, cam.height};
+    detail::check(prx_gather_photons(engine.native(), photons.records().data(), aux.data(), photons.n_paths(),
+                                     photons.max_bounces(), state.frame, &c, radius, 1, img.pixels.data()));
     return img;
 }
 

@@ -189,6 +189,13 @@ typedef enum prx_field {
 
 /* ---- pure functions (pybind module.cpp:47-82) ------------------------------------ */
 
+/* select_paths_to_prune (engine.hpp:62-63, engine.cpp:443-471): the prune selection of one
+ * DM cell (Eq. 1 Bernoulli marks keyed (path, frame, PruneMark), then the trim from the
+ * highest path id down to exactly dm_t); `out` (capacity n) receives the pruned ids in
+ * ascending order.  The engine itself selects on the GPU (k_prune_mark / k_prune_trim). */
+prx_status prx_select_paths_to_prune(const uint32_t* cell_paths, size_t n, uint32_t dm_c, uint32_t dm_t,
+                                     uint64_t seed, uint32_t frame, uint32_t* out, size_t* n_out);
+
 /* light.hpp:132-135 */
 double prx_prune_probability(uint32_t dm_current, uint32_t dm_target);
 /* engine.hpp:34-41 */
@@ -227,6 +234,19 @@ prx_status prx_scene_bvh_permutation(const prx_scene* scene, uint32_t* out, size
 /* counts: {static triangles, dynamic triangles, bvh nodes, objects} */
 prx_status prx_scene_counts(const prx_scene* scene, uint64_t counts[4]);
 float prx_scene_diagonal(const prx_scene* scene);
+/* state_at (scene.cpp:115-134) on the host: every dynamic object placed at `frame` --
+ * world-space triangles (transform_triangle) and bounds_current / bounds_previous -- for
+ * Engine::scene_state() of the C++ drop-in.  Pass NULL buffers to query the counts. */
+typedef struct prx_placed_dynamic {
+    uint32_t object_id;
+    uint32_t tri_begin;   /* first triangle of this object in the `tris` array */
+    uint32_t tri_count;
+    uint32_t reserved;
+    prx_vec3 cur_lo, cur_hi, prev_lo, prev_hi;
+} prx_placed_dynamic;
+prx_status prx_scene_state_at(const prx_scene* scene, int32_t frame, prx_placed_dynamic* dyn,
+                              size_t dyn_capacity, size_t* n_dyn, prx_triangle* tris,
+                              size_t tri_capacity, size_t* n_tris);
 void prx_scene_destroy(prx_scene* scene);
 
 /* ---- engine (engine.hpp:69-179) --------------------------------------------------- */
@@ -294,6 +314,13 @@ prx_status prx_engine_synchronize(prx_engine* engine);
  * reference's 27-cell insertion order). */
 prx_status prx_splat(prx_engine* engine, const prx_camera* camera, float radius, int mode,
                      float* rgb_out, float* rgb_dev, prx_frame_stats* stats);
+/* gather_image(state, photons, aux, camera, radius, workers) (gather.hpp:81-83) over a HOST
+ * photon map that need not be the engine's own: the records (32-byte Photon + 24-byte
+ * PathVertexAux, [max_bounces][n_paths]) are uploaded to engine scratch and splatted against
+ * the scene placed at frame `frame` (the engine's state is not modified).  mode as prx_splat. */
+prx_status prx_gather_photons(prx_engine* engine, const void* photons, const void* aux, uint32_t n_paths,
+                              uint32_t max_bounces, int32_t frame, const prx_camera* camera, float radius,
+                              int mode, float* rgb_out);
 
 /* Lazy host mirrors for the introspection accessors (engine.hpp:76-122) and the
  * state-injection parity harness.  `index` selects the light for DM fields.

@@ -135,6 +135,9 @@ SIGNATURES = [
                                     C.POINTER(C.c_uint32), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("prx_memory_footprint", None, [C.c_uint64, C.c_uint32, C.POINTER(C.c_uint32), C.c_uint32,
                                     C.c_int, C.POINTER(C.c_double)]),
+    ("prx_select_paths_to_prune", C.c_int, [C.POINTER(C.c_uint32), C.c_size_t, C.c_uint32, C.c_uint32,
+                                            C.c_uint64, C.c_uint32, C.POINTER(C.c_uint32),
+                                            C.POINTER(C.c_size_t)]),
     ("prx_scene_create", C.c_int, [C.POINTER(SceneDesc), C.POINTER(P)]),
     ("prx_scene_builtin", C.c_int, [C.c_char_p, C.POINTER(P)]),
     ("prx_scene_load", C.c_int, [C.c_char_p, C.POINTER(P)]),
@@ -145,6 +148,8 @@ SIGNATURES = [
                                             C.POINTER(C.c_size_t)]),
     ("prx_scene_counts", C.c_int, [P, C.POINTER(C.c_uint64)]),
     ("prx_scene_diagonal", C.c_float, [P]),
+    ("prx_scene_state_at", C.c_int, [P, C.c_int32, P, C.c_size_t, C.POINTER(C.c_size_t), P, C.c_size_t,
+                                     C.POINTER(C.c_size_t)]),
     ("prx_scene_destroy", None, [P]),
     ("prx_engine_create", C.c_int, [P, C.POINTER(Config), C.POINTER(P)]),
     ("prx_engine_destroy", None, [P]),
@@ -164,6 +169,8 @@ SIGNATURES = [
     ("prx_engine_synchronize", C.c_int, [P]),
     ("prx_splat", C.c_int, [P, C.POINTER(Camera), C.c_float, C.c_int, P, P,
                             C.POINTER(FrameStats)]),
+    ("prx_gather_photons", C.c_int, [P, P, P, C.c_uint32, C.c_uint32, C.c_int32, C.POINTER(Camera),
+                                     C.c_float, C.c_int, P]),
     ("prx_field_bytes", C.c_size_t, [P, C.c_int, C.c_uint32]),
     ("prx_engine_download", C.c_int, [P, C.c_int, C.c_uint32, P, C.c_size_t]),
     ("prx_engine_upload", C.c_int, [P, C.c_int, C.c_uint32, P, C.c_size_t]),

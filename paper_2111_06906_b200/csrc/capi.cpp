@@ -64,6 +64,75 @@ extern "C" {
 const char* prx_last_error(void) { return g_error.c_str(); }
 int prx_abi_version(void) { return PRX_ABI_VERSION; }
 
+// select_paths_to_prune (engine.cpp:443-471), host restatement for the C++ drop-in
+prx_status prx_select_paths_to_prune(const uint32_t* cell_paths, size_t n, uint32_t dm_c, uint32_t dm_t,
+                                     uint64_t seed, uint32_t frame, uint32_t* out, size_t* n_out) {
+    return guarded([&] {
+        if (n && (!cell_paths || !out)) throw std::invalid_argument("select_paths_to_prune: NULL buffer");
+        need(n_out, "n_out");
+        std::vector<uint32_t> sorted(cell_paths, cell_paths + n);
+        std::sort(sorted.begin(), sorted.end());
+        const double prob = prx::prune_probability(dm_c, dm_t);
+        const uint64_t mix = prx::mix64(seed);
+        std::vector<uint8_t> marks(n, 0);
+        uint32_t survivors = 0;
+        for (size_t i = 0; i < n; ++i) {
+            const float u = prx::rng_uniform_m(mix, sorted[i], frame, 0, prx::kPruneMark, 0);
+            if (prob > 0.0 && u < prob) marks[i] = 1;
+            else ++survivors;
+        }
+        for (size_t i = n; survivors > dm_t && i-- > 0;)  // trim from the top path id down
+            if (!marks[i]) {
+                marks[i] = 1;
+                --survivors;
+            }
+        size_t k = 0;
+        for (size_t i = 0; i < n; ++i)
+            if (marks[i]) out[k++] = sorted[i];
+        *n_out = k;
+    });
+}
+
+// state_at (scene.cpp:115-134): dynamic objects placed at `frame`, on the host
+prx_status prx_scene_state_at(const prx_scene* scene, int32_t frame, prx_placed_dynamic* dyn,
+                              size_t dyn_capacity, size_t* n_dyn, prx_triangle* tris, size_t tri_capacity,
+                              size_t* n_tris) {
+    return guarded([&] {
+        need(scene, "scene");
+        const prx::Scene& s = *scene->scene;
+        size_t nd = 0, nt = 0;
+        for (const prx::Object& o : s.objects) {
+            if (!o.dynamic) continue;
+            if (dyn && nd < dyn_capacity) {
+                const prx::Xform now = prx::transform_at(o.kfs, frame);
+                const prx::Xform prev = prx::transform_at(o.kfs, frame > 0 ? frame - 1 : 0);
+                const prx::Box cur = prx::transform_box(o.local_bounds, now);
+                const prx::Box prv = prx::transform_box(o.local_bounds, prev);
+                prx_placed_dynamic& d = dyn[nd];
+                d.object_id = o.id;
+                d.tri_begin = static_cast<uint32_t>(nt);
+                d.tri_count = static_cast<uint32_t>(o.mesh.size());
+                d.reserved = 0;
+                d.cur_lo = {cur.lo.x, cur.lo.y, cur.lo.z};
+                d.cur_hi = {cur.hi.x, cur.hi.y, cur.hi.z};
+                d.prev_lo = {prv.lo.x, prv.lo.y, prv.lo.z};
+                d.prev_hi = {prv.hi.x, prv.hi.y, prv.hi.z};
+                if (tris && nt + o.mesh.size() <= tri_capacity)
+                    for (size_t t = 0; t < o.mesh.size(); ++t) {
+                        const prx::Tri& m = o.mesh[t];
+                        const prx::V3 a = prx::apply_point(now, m.a), b = prx::apply_point(now, m.b),
+                                      c = prx::apply_point(now, m.c);
+                        tris[nt + t] = {{a.x, a.y, a.z}, {b.x, b.y, b.z}, {c.x, c.y, c.z}};
+                    }
+            }
+            ++nd;
+            nt += o.mesh.size();
+        }
+        if (n_dyn) *n_dyn = nd;
+        if (n_tris) *n_tris = nt;
+    });
+}
+
 double prx_prune_probability(uint32_t dm_current, uint32_t dm_target) {
     return prx::prune_probability(dm_current, dm_target);
 }
@@ -287,6 +356,14 @@ prx_status prx_engine_synchronize(prx_engine* engine) {
 prx_status prx_splat(prx_engine* engine, const prx_camera* camera, float radius, int mode, float* rgb_out,
                      float* rgb_dev, prx_frame_stats* stats) {
     return guarded([&] { eng(engine).splat(camera, radius, mode, rgb_out, rgb_dev, stats); });
+}
+
+prx_status prx_gather_photons(prx_engine* engine, const void* photons, const void* aux, uint32_t n_paths,
+                              uint32_t max_bounces, int32_t frame, const prx_camera* camera, float radius,
+                              int mode, float* rgb_out) {
+    return guarded([&] {
+        eng(engine).gather_photons(photons, aux, n_paths, max_bounces, frame, camera, radius, mode, rgb_out);
+    });
 }
 
 size_t prx_field_bytes(const prx_engine* engine, int field, uint32_t index) {

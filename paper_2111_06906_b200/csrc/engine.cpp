@@ -1111,6 +1111,47 @@ void Engine::fill_apply(const uint64_t* dead_prefix, const uint64_t* dead_total,
 // ----------------------------------------------------------------------- splat
 void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_host, float* rgb_dev,
                    prx_frame_stats* st) {
+    splat_store(path_dev(), cam, radius, mode, rgb_host, rgb_dev, st);
+}
+
+// gather_image(state, photons, aux, ...) over a host photon map (gather.hpp:81-83): the
+// records are converted to the engine's 32-byte {pos_obj, energy} vertex layout, uploaded
+// to scratch and splatted against the scene as placed for the engine's current frame.
+void Engine::gather_photons(const void* photons, const void* aux, uint32_t n_paths, uint32_t max_bounces,
+                            int frame, const prx_camera* cam, float radius, int mode, float* rgb_host) {
+    PRX_CUDA(cudaSetDevice(device_));
+    if (frame != cur_frame_)
+        throw std::invalid_argument("gather_image: the scene state is not the engine's current frame");
+    if ((n_paths && max_bounces && (!photons || !aux)) || !rgb_host)
+        throw std::invalid_argument("gather_image: NULL photon, aux or image buffer");
+    const size_t nv = static_cast<size_t>(n_paths) * max_bounces;
+    struct RefPhoton { float dir[3]; uint32_t obj; float e[3]; float radius; };
+    struct RefAux { float pos[3]; float out[3]; };
+    static_assert(sizeof(RefPhoton) == 32 && sizeof(RefAux) == 24, "reference record sizes");
+    std::vector<float4> rec(2 * std::max<size_t>(nv, 1));
+    const auto* ph = static_cast<const RefPhoton*>(photons);
+    const auto* ax = static_cast<const RefAux*>(aux);
+    for (size_t v = 0; v < nv; ++v) {
+        float w;
+        std::memcpy(&w, &ph[v].obj, 4);
+        rec[2 * v] = float4{ax[v].pos[0], ax[v].pos[1], ax[v].pos[2], w};
+        rec[2 * v + 1] = float4{ph[v].e[0], ph[v].e[1], ph[v].e[2], ph[v].radius};
+    }
+    DevBuf store(sizeof(float4) * rec.size());
+    copy_async(store.get(), rec.data(), sizeof(float4) * 2 * nv, cudaMemcpyHostToDevice);
+    PathDev P{};
+    P.n = n_paths;
+    P.B = max_bounces;
+    P.pos_obj = store.as<float4>();
+    P.energy = store.as<float4>() + 1;
+    d_gather_.reset();  // sized for this store
+    splat_store(P, cam, radius, mode, rgb_host, nullptr, nullptr);
+    d_gather_.reset();
+    if (d_splat_cand_.size() > 16 + 8ull * n_ * B_) d_splat_cand_.reset();
+}
+
+void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, int mode, float* rgb_host,
+                         float* rgb_dev, prx_frame_stats* st) {
     PRX_CUDA(cudaSetDevice(device_));
     if (!(radius > 0.0f)) throw std::invalid_argument("gather: radius must be positive");
     if (mode != 0 && mode != 1) throw std::invalid_argument("splat: mode must be 0 (atomic splat) or 1 (ordered gather)");
@@ -1140,19 +1181,20 @@ void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_hos
         d_gbuf_.alloc(16ull * npx);
         d_img_.alloc(12ull * npx);
         d_splat_work_.alloc(splat_work_bytes(npx));
-        if (d_splat_cand_.size() < 16 + 8ull * n_ * B_) d_splat_cand_.alloc(16 + 8ull * n_ * B_);
         d_gather_.reset();
         img_w_ = c.width;
         img_h_ = c.height;
     }
+    const uint64_t nv = static_cast<uint64_t>(P.n) * P.B;
+    if (d_splat_cand_.size() < 16 + 8 * nv) d_splat_cand_.alloc(16 + 8 * nv);
     const float inv_area = 1.0f / (static_cast<float>(M_PI) * radius * radius);
     const float inv_pi = 1.0f / static_cast<float>(M_PI);
-    if (mode == 1 && d_gather_.size() == 0) d_gather_.alloc(gather_work_bytes(static_cast<uint64_t>(n_) * B_, npx));
+    if (mode == 1 && d_gather_.size() == 0) d_gather_.alloc(gather_work_bytes(nv, npx));
     float* out = rgb_dev ? rgb_dev : d_img_.as<float>();
     const SceneDev S = scene_dev();
     // (plain launches: a captured graph of these ~25 launches measured slower, 1.93 vs 1.89 ms)
     record(kEvSplat0);
-    launch_splat(S, path_dev(), C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, d_splat_work_.get(),
+    launch_splat(S, P, C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, d_splat_work_.get(),
                  d_splat_cand_.get(), mode, d_gather_.get(), stream_);
     record(kEvSplat1);
     if (rgb_host)

@@ -79,6 +79,8 @@ public:
 
     void splat(const prx_camera* cam, float radius, int mode, float* rgb_host, float* rgb_dev,
                prx_frame_stats* st);
+    void gather_photons(const void* photons, const void* aux, uint32_t n_paths, uint32_t max_bounces, int frame,
+                        const prx_camera* cam, float radius, int mode, float* rgb_host);
 
     size_t field_bytes(int field, uint32_t index) const;
     void download(int field, uint32_t index, void* dst, size_t bytes);
@@ -144,6 +146,8 @@ private:
     void fill_assign_all(const uint64_t* prefix, const uint64_t* total);
     void stage_trace();
     void read_back(prx_frame_stats* st, bool with_times);
+    void splat_store(const PathDev& P, const prx_camera* cam, float radius, int mode, float* rgb_host,
+                     float* rgb_dev, prx_frame_stats* st);
     void record(int idx);
     double elapsed_ms(int a, int b);
     SceneDev scene_dev() const;

@@ -127,3 +127,27 @@ def test_engine_fails_loudly_without_gpu():
         pass
     with pytest.raises((L.CudaError, L.PrxError)):
         pr.Engine(pr.Scene.builtin("static-box"), pr.make_config(paths=100))
+
+
+def test_select_paths_to_prune_matches_reference():
+    """select_paths_to_prune (engine.cpp:443-471) behind the C ABI == the reference's."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import ref
+
+    if not ref.available():
+        import pytest
+
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(3)
+    for n, dm_c, dm_t, seed, frame in ((1000, 1000, 600, 5, 3), (600, 600, 600, 5, 3), (37, 80, 12, 9, 0),
+                                       (500, 300, 0, 1, 7), (0, 0, 5, 1, 1), (2000, 5000, 4999, 11, 2)):
+        paths = rng.permutation(np.arange(100, 100 + 3 * n, 3, dtype=np.uint32))[:n]
+        out = np.zeros(max(n, 1), dtype=np.uint32)
+        k = C.c_size_t()
+        L.check(L.lib().prx_select_paths_to_prune(paths.ctypes.data_as(C.POINTER(C.c_uint32)), n, dm_c, dm_t,
+                                                   seed, frame, out.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                   C.byref(k)))
+        assert np.array_equal(out[: k.value], ref.select_paths_to_prune(paths, dm_c, dm_t, seed, frame))
