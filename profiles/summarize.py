@@ -59,7 +59,12 @@ def full_metrics(rep):
             "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
             "sm__warps_active.avg.pct_of_peak_sustained_active",
             "smsp__thread_inst_executed_per_inst_executed.ratio",
-            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread"]
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+            "l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum",
+            "l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum",
+            "smsp__inst_executed_op_shared_atom.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rd = list(csv.reader(txt.splitlines()))
     header, units = rd[0], rd[1]
@@ -100,23 +105,32 @@ def main(tag, src="gpurun_out"):
     md += t + [""]
     t, _, _ = table(recs, "Whole command (cold frame 0 + warm-up + timed frames)")
     md += t + [""]
-    rep = os.path.join(src, f"{tag}_full.ncu-rep")
+    import glob
+    reps = sorted(glob.glob(os.path.join(src, f"{tag}_full*.ncu-rep")))
     traffic = {}
-    if os.path.exists(rep):
-        fm = full_metrics(rep)
+    if reps:
+        fm = [row for rep in reps for row in full_metrics(rep)]
         md += ["### `ncu --set full` (one steady-state launch each)", "",
-               "| kernel | ms | DRAM read GB | DRAM write GB | L2 hit % | L1 hit % | warps active % | thr/inst | regs |",
-               "|---|---:|---:|---:|---:|---:|---:|---:|---:|"]
+               "| kernel | ms | DRAM read GB | DRAM write GB | DRAM % peak | L2 hit % | L1 hit % | warps active % | issue active % | thr/inst | inst (M) | regs | global atom/red | shared atom |",
+               "|---|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|"]
         for r in fm:
-            md.append("| `{}` | {:.3f} | {:.3f} | {:.3f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} |".format(
+            md.append("| `{}` | {:.3f} | {:.3f} | {:.3f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.0f} | {:.0f} |".format(
                 r["kernel"], r.get("gpu__time_duration.sum", 0), r.get("dram__bytes_read.sum", 0) / 1e9,
-                r.get("dram__bytes_write.sum", 0) / 1e9, r.get("lts__t_sector_hit_rate.pct", 0),
+                r.get("dram__bytes_write.sum", 0) / 1e9,
+                r.get("dram__throughput.avg.pct_of_peak_sustained_elapsed", 0),
+                r.get("lts__t_sector_hit_rate.pct", 0),
                 r.get("l1tex__t_sector_hit_rate.pct", 0),
                 r.get("sm__warps_active.avg.pct_of_peak_sustained_active", 0),
+                r.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0),
                 r.get("smsp__thread_inst_executed_per_inst_executed.ratio", 0),
-                r.get("launch__registers_per_thread", 0)))
+                r.get("smsp__inst_executed.sum", 0) / 1e6,
+                r.get("launch__registers_per_thread", 0),
+                r.get("l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum", 0)
+                + r.get("l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum", 0),
+                r.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", 0)))
             traffic[r["kernel"]] = {"dram_bytes": r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0),
-                                    "ms": r.get("gpu__time_duration.sum", 0)}
+                                    "ms": r.get("gpu__time_duration.sum", 0),
+                                    "inst": r.get("smsp__inst_executed.sum", 0)}
         md.append("")
     bj = os.path.join(src, f"{tag}_bench.json")
     if os.path.exists(bj):
