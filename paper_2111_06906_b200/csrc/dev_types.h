@@ -40,6 +40,7 @@ struct LightDev {
     uint32_t dims[4];
     uint32_t* dm_t;
     uint32_t* dm_c;
+    int32_t xt_force;     // PRX_XT_FORCE=1: every light transcendental takes the exact path (tests)
 };
 
 struct FrameParams {

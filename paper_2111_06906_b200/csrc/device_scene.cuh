@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include "dev_types.h"
+#include "exact_trig.h"
 
 namespace prx {
 
@@ -1126,15 +1127,27 @@ __device__ __forceinline__ double dclamp(double v, double lo, double hi) {
     return (v < lo) ? lo : ((hi < v) ? hi : v);
 }
 
-// dir_from_angles (light.cpp:40-47)
+// dir_from_angles (light.cpp:40-47).  cos/sin(phi) come from CUDA's libm unless the
+// narrowing (float)(cos(phi) * sin_theta) is not decided by it (exact_trig.h); then from the
+// correctly rounded double-double evaluation.
 __device__ __forceinline__ V3 dir_from_angles(const LightDev& L, double cos_theta, double phi) {
     const double sin_theta = sqrt(dmax_std(0.0, 1.0 - cos_theta * cos_theta));
     double sp, cp;
     sincos(phi, &sp, &cp);
+    if (L.xt_force || !xt::product_narrows_stably(cp, sin_theta) || !xt::product_narrows_stably(sp, sin_theta))
+        xt::sincos_rn(phi, sp, cp);
     const double cx = cp * sin_theta;
     const double cy = sp * sin_theta;
     return normalized(add(add(mul(L.tangent, (float)cx), mul(L.bitangent, (float)cy)),
                           mul(L.normal, (float)cos_theta)));
+}
+
+// wrap_unit(atan2(y, x) / 2pi) narrowed to float, with the same checked narrowing
+__device__ __forceinline__ float wrapped_angle(const LightDev& L, double y, double x) {
+    double a = atan2(y, x);
+    if (L.xt_force || (float)wrap_unit(xt::win_lo(a) / kTwoPiD) != (float)wrap_unit(xt::win_hi(a) / kTwoPiD))
+        a = xt::atan2_rn(y, x, a);
+    return (float)wrap_unit(a / kTwoPiD);
 }
 
 // warp_canonical (light.cpp:70-117): canonical coords -> (origin, dir)
@@ -1159,6 +1172,8 @@ __device__ __forceinline__ void warp_canonical(const LightDev& L, const float c[
             const double phi_s = kTwoPiD * (double)c[1];
             double sp, cp;
             sincos(phi_s, &sp, &cp);
+            if (L.xt_force || !xt::product_narrows_stably(cp, r) || !xt::product_narrows_stably(sp, r))
+                xt::sincos_rn(phi_s, sp, cp);
             origin = add(add(L.position, mul(L.tangent, (float)(r * cp))), mul(L.bitangent, (float)(r * sp)));
             const double cos_theta = sqrt(dmax_std(0.0, 1.0 - (double)c[2]));
             dir = dir_from_angles(L, cos_theta, kTwoPiD * (double)c[3]);
@@ -1183,18 +1198,18 @@ __device__ __forceinline__ bool canonical_of(const LightDev& L, V3 origin, V3 di
     const double dn = dot(dir, L.normal);
     const double dt = dot(dir, L.tangent);
     const double db = dot(dir, L.bitangent);
-    const double phi = wrap_unit(atan2(db, dt) / kTwoPiD);
+    const float phi = wrapped_angle(L, db, dt);  // wrap_unit(atan2(db, dt) / 2pi), narrowed
     const double kTol = 1e-4;
     switch (L.kind) {
         case PRX_LIGHT_POINT:
             c[0] = (float)dclamp((1.0 - dn) / 2.0, 0.0, 1.0);
-            c[1] = (float)phi;
+            c[1] = phi;
             return true;
         case PRX_LIGHT_SPOT: {
             const double q = (1.0 - dn) / (1.0 - L.cos_half);
             if (q < 0.0 || q > 1.0) return false;
             c[0] = (float)dmin_std(q, 1.0);
-            c[1] = (float)phi;
+            c[1] = phi;
             return true;
         }
         default: {
@@ -1208,7 +1223,7 @@ __device__ __forceinline__ bool canonical_of(const LightDev& L, V3 origin, V3 di
                 const double q = (lx * lx + ly * ly) / (r_max * r_max);
                 if (q > 1.0 + kTol) return false;
                 c[0] = (float)dmin_std(q, 1.0);
-                c[1] = (float)wrap_unit(atan2(ly, lx) / kTwoPiD);
+                c[1] = wrapped_angle(L, ly, lx);
             } else {
                 const double hx = (double)L.half_x * (double)L.scale;
                 const double hy = (double)L.half_y * (double)L.scale;
@@ -1221,7 +1236,7 @@ __device__ __forceinline__ bool canonical_of(const LightDev& L, V3 origin, V3 di
             }
             if (dn <= 0.0) return false;
             c[2] = (float)dclamp(1.0 - dn * dn, 0.0, 1.0);
-            c[3] = (float)phi;
+            c[3] = phi;
             return true;
         }
     }

@@ -165,6 +165,7 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     eps_ = 1e-4f * scene_->diagonal();
     diag_ = scene_->diagonal();
     seed_mix_ = mix64(cfg_.seed);
+    if (const char* e = std::getenv("PRX_XT_FORCE")) xt_force_ = e[0] == '1' ? 1 : 0;
 
     PRX_CUDA(cudaSetDevice(device_));
     PRX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -637,6 +638,7 @@ void Engine::fill_frame_params_host() {
         for (int a = 0; a < 4; ++a) L.dims[a] = b.dims[a];
         L.dm_t = b.dm_t.as<uint32_t>();
         L.dm_c = b.dm_c.as<uint32_t>();
+        L.xt_force = xt_force_;
     }
     fp.n_dyn = static_cast<uint32_t>(dyn_.size());
 }

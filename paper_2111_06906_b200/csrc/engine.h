@@ -182,7 +182,8 @@ private:
     float4 *p_fnodes_ = nullptr, *p_ftris_ = nullptr, *p_nodes_ = nullptr;
     uint32_t* p_leaf_of_ = nullptr;
     size_t l2_window_ = 0;
-    int32_t cert_off_ = 0;  // PRX_CERT_OFF=1: every query takes its exact fallback (tests)
+    int32_t cert_off_ = 0;
+    int32_t xt_force_ = 0;  // PRX_XT_FORCE=1: exact light transcendentals everywhere (tests)  // PRX_CERT_OFF=1: every query takes its exact fallback (tests)
     const float2* d_trig_ = nullptr;
 
     // frame params (pinned host + device)
