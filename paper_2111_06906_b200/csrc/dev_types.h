@@ -84,6 +84,17 @@ struct SceneDev {
 // Per-path and per-vertex device state of one engine (one shard).  Vertex arrays are
 // bounce-major [B][n] like the reference PhotonMap (photon_store.cpp:32-36), split into
 // 16-byte streams so the verify kernels read exactly {position, object} per vertex.
+// Vertex streams (PRX_VERTEX_SOA, build knob): 0 (default) = two interleaved 32-byte record
+// streams {pos_obj, energy} {in_dir, out_dir}, each [B][n]; 1 = four 16-byte streams pos_obj |
+// energy | in_dir | out_dir.  Measured end to end on C4 (profiles/r02_sweeps.md): the SoA
+// streams speed up the sequential pos_obj readers but slow the verify walk and the splat's
+// candidate copy (one vertex then touches 4 sectors instead of 2): 10.92 vs 10.63 ms/frame.
+// Kernels index vertex v of a stream as stream[kVS * v].
+#ifndef PRX_VERTEX_SOA
+#define PRX_VERTEX_SOA 0
+#endif
+constexpr uint32_t kVS = PRX_VERTEX_SOA ? 1u : 2u;
+
 struct PathDev {
     uint32_t n;      // paths held by this engine
     uint32_t base;   // global id of local path 0

@@ -510,7 +510,7 @@ void Engine::alloc_state() {
         std::vector<float4> po(std::min<size_t>(nv, 1 << 20), float4{0, 0, 0, f_of_u(kInvalidObj)});
         for (size_t off = 0; off < nv; off += po.size()) {
             const size_t cnt = std::min(po.size(), nv - off);
-            PRX_CUDA(cudaMemcpy2DAsync(d_pos_obj_.as<float4>() + 2 * off, 32, po.data(), 16, 16, cnt,
+            PRX_CUDA(cudaMemcpy2DAsync(path_dev().pos_obj + kVS * off, 16 * kVS, po.data(), 16, 16, cnt,
                                        cudaMemcpyHostToDevice, stream_));
             PRX_CUDA(cudaStreamSynchronize(stream_));
         }
@@ -573,10 +573,12 @@ PathDev Engine::path_dev() const {
     P.n = n_;
     P.base = sb_;
     P.B = B_;
-    P.pos_obj = d_pos_obj_.as<float4>();  // element v at [2 v] (kernels index 2 * v)
-    P.energy = d_pos_obj_.as<float4>() + 1;
+    // vertex v of a stream at [kVS * v] (dev_types.h): four SoA streams or two interleaved
+    const size_t second = PRX_VERTEX_SOA ? static_cast<size_t>(n_) * B_ : 1;
+    P.pos_obj = d_pos_obj_.as<float4>();
+    P.energy = d_pos_obj_.as<float4>() + second;
     P.in_dir = d_in_dir_.as<float4>();
-    P.out_dir = d_in_dir_.as<float4>() + 1;
+    P.out_dir = d_in_dir_.as<float4>() + second;
     P.origin = d_origin_.as<float4>();
     P.emis = d_emis_.as<float4>();
     P.canon = d_canon_.as<float4>();
@@ -1130,14 +1132,16 @@ void Engine::gather_photons(const void* photons, const void* aux, uint32_t n_pat
     struct RefPhoton { float dir[3]; uint32_t obj; float e[3]; float radius; };
     struct RefAux { float pos[3]; float out[3]; };
     static_assert(sizeof(RefPhoton) == 32 && sizeof(RefAux) == 24, "reference record sizes");
+    // the engine's vertex layout (kVS, dev_types.h): {pos_obj, energy} streams
+    const size_t second = PRX_VERTEX_SOA ? nv : 1;
     std::vector<float4> rec(2 * std::max<size_t>(nv, 1));
     const auto* ph = static_cast<const RefPhoton*>(photons);
     const auto* ax = static_cast<const RefAux*>(aux);
     for (size_t v = 0; v < nv; ++v) {
         float w;
         std::memcpy(&w, &ph[v].obj, 4);
-        rec[2 * v] = float4{ax[v].pos[0], ax[v].pos[1], ax[v].pos[2], w};
-        rec[2 * v + 1] = float4{ph[v].e[0], ph[v].e[1], ph[v].e[2], ph[v].radius};
+        rec[kVS * v] = float4{ax[v].pos[0], ax[v].pos[1], ax[v].pos[2], w};
+        rec[kVS * v + second] = float4{ph[v].e[0], ph[v].e[1], ph[v].e[2], ph[v].radius};
     }
     DevBuf store(sizeof(float4) * rec.size());
     copy_async(store.get(), rec.data(), sizeof(float4) * 2 * nv, cudaMemcpyHostToDevice);
@@ -1145,7 +1149,7 @@ void Engine::gather_photons(const void* photons, const void* aux, uint32_t n_pat
     P.n = n_paths;
     P.B = max_bounces;
     P.pos_obj = store.as<float4>();
-    P.energy = store.as<float4>() + 1;
+    P.energy = store.as<float4>() + second;
     d_gather_.reset();  // sized for this store
     splat_store(P, cam, radius, mode, rgb_host, nullptr, nullptr);
     d_gather_.reset();
@@ -1282,11 +1286,12 @@ void Engine::download(int field, uint32_t index, void* dst, size_t bytes) {
         case PRX_FIELD_POS_OBJ:
         case PRX_FIELD_ENERGY:
         case PRX_FIELD_IN_DIR:
-        case PRX_FIELD_OUT_DIR: {  // one float4 of each interleaved 32-byte vertex record
-            const float4* base = field == PRX_FIELD_POS_OBJ || field == PRX_FIELD_ENERGY ? d_pos_obj_.as<float4>()
-                                                                                         : d_in_dir_.as<float4>();
-            const int off = field == PRX_FIELD_ENERGY || field == PRX_FIELD_OUT_DIR ? 1 : 0;
-            PRX_CUDA(cudaMemcpy2DAsync(dst, 16, base + off, 32, 16, bytes / 16, cudaMemcpyDeviceToHost, stream_));
+        case PRX_FIELD_OUT_DIR: {  // one float4 per vertex of that stream (stride kVS)
+            const PathDev P = path_dev();
+            const float4* base = field == PRX_FIELD_POS_OBJ ? P.pos_obj
+                                 : field == PRX_FIELD_ENERGY ? P.energy
+                                 : field == PRX_FIELD_IN_DIR ? P.in_dir : P.out_dir;
+            PRX_CUDA(cudaMemcpy2DAsync(dst, 16, base, 16 * kVS, 16, bytes / 16, cudaMemcpyDeviceToHost, stream_));
             d2h_bytes_ += bytes;
             PRX_CUDA(cudaStreamSynchronize(stream_));
             return;
@@ -1329,10 +1334,11 @@ void Engine::upload(int field, uint32_t index, const void* src, size_t bytes) {
         case PRX_FIELD_ENERGY:
         case PRX_FIELD_IN_DIR:
         case PRX_FIELD_OUT_DIR: {
-            float4* base = field == PRX_FIELD_POS_OBJ || field == PRX_FIELD_ENERGY ? d_pos_obj_.as<float4>()
-                                                                                   : d_in_dir_.as<float4>();
-            const int off = field == PRX_FIELD_ENERGY || field == PRX_FIELD_OUT_DIR ? 1 : 0;
-            PRX_CUDA(cudaMemcpy2DAsync(base + off, 32, src, 16, 16, bytes / 16, cudaMemcpyHostToDevice, stream_));
+            const PathDev P = path_dev();
+            float4* base = field == PRX_FIELD_POS_OBJ ? P.pos_obj
+                           : field == PRX_FIELD_ENERGY ? P.energy
+                           : field == PRX_FIELD_IN_DIR ? P.in_dir : P.out_dir;
+            PRX_CUDA(cudaMemcpy2DAsync(base, 16 * kVS, src, 16, 16, bytes / 16, cudaMemcpyHostToDevice, stream_));
             h2d_bytes_ += bytes;
             PRX_CUDA(cudaStreamSynchronize(stream_));
             return;

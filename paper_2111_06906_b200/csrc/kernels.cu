@@ -53,9 +53,9 @@ __device__ __forceinline__ void truncate_path(const PathDev& P, uint32_t i, uint
                                               bool escaped, uchar4& m) {
     for (uint32_t b = new_count; b < P.B; ++b) {
         const size_t v = vix(P, b, i);
-        __stcs(&P.in_dir[2 * (v)], make_float4(0.f, 0.f, 0.f, 0.f));
-        __stcs(&P.pos_obj[2 * (v)].w, __uint_as_float(kInvalidObj));
-        __stcs(&P.energy[2 * (v)], make_float4(0.f, 0.f, 0.f, 0.f));
+        __stcs(&P.in_dir[kVS * (v)], make_float4(0.f, 0.f, 0.f, 0.f));
+        __stcs(&P.pos_obj[kVS * (v)].w, __uint_as_float(kInvalidObj));
+        __stcs(&P.energy[kVS * (v)], make_float4(0.f, 0.f, 0.f, 0.f));
     }
     m.x = (unsigned char)new_count;
     m.y = escaped ? 1 : 0;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Co
         if (L.kind == PRX_LIGHT_POINT || L.kind == PRX_LIGHT_SPOT) {
             P.origin[i] = make_float4(L.position.x, L.position.y, L.position.z, 0.f);
             if (m.x > 0) {
-                const V3 primary = ld3(P.pos_obj[2 * (i)]);
+                const V3 primary = ld3(P.pos_obj[kVS * (i)]);
                 const V3 to = sub(primary, L.position);
                 const float dist = length(to);
                 if (dist <= S.eps) {
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Co
         } else {
             if (m.x > 0) {
                 const V3 d = ld3(P.emis[i]);
-                const V3 primary = ld3(P.pos_obj[2 * (i)]);
+                const V3 primary = ld3(P.pos_obj[kVS * (i)]);
                 const float denom = dot(d, L.normal);
                 if (denom <= 1e-6f) {
                     m.z = kReplace;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S
         V3 prev = live ? ld3(P.origin[i]) : V3{0.f, 0.f, 0.f};
         uint32_t prev_obj = kInvalidObj;
         // vertex s+1 is loaded while segment s is tested (the loop is load-latency bound)
-        float4 nextv = k > 0 ? __ldcs(&P.pos_obj[2 * (vix(P, 0, i))]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 nextv = k > 0 ? __ldcs(&P.pos_obj[kVS * (vix(P, 0, i))]) : make_float4(0.f, 0.f, 0.f, 0.f);
         const uint32_t s_end = __reduce_max_sync(0xffffffffu, segs);
         for (uint32_t s = 0; s < s_end; ++s) {
             const bool act = s < segs;
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S
             uint32_t cur_obj = kInvalidObj;
             if (act && s < k) {
                 const float4 v = nextv;
-                if (s + 1 < k) nextv = __ldcs(&P.pos_obj[2 * (vix(P, s + 1, i))]);
+                if (s + 1 < k) nextv = __ldcs(&P.pos_obj[kVS * (vix(P, s + 1, i))]);
                 cur = ld3(v);
                 cur_obj = __float_as_uint(v.w);
             }
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S
             bool bounded = false;
             if (probe) {
                 if (s >= k) {  // escape segment, clipped to twice the diagonal
-                    const V3 dir = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, s - 1, i))]);
+                    const V3 dir = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[kVS * (vix(P, s - 1, i))]);
                     b = add(prev, mul(dir, S.two_diag));
                 }
                 smin = V3{fminf(prev.x, b.x), fminf(prev.y, b.y), fminf(prev.z, b.z)};
@@ -419,8 +419,8 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
                 has = false;
                 continue;
             }
-            const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[2 * (vix(P, s - 1, i))]);
-            const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, s - 1, i))]);
+            const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[kVS * (vix(P, s - 1, i))]);
+            const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[kVS * (vix(P, s - 1, i))]);
             ++vis;
             trav_init(S, T, o, d, S.eps, FLT_MAX, false);
             ray = true;
@@ -442,25 +442,25 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
             continue;
         }
         const size_t v = vix(P, s, i);
-        const float4 stored = P.energy[2 * (v)];
-        const V3 e_prev = s == 0 ? fp->lights[li].flux_pp : ld3(P.energy[2 * (vix(P, s - 1, i))]);
+        const float4 stored = P.energy[kVS * (v)];
+        const V3 e_prev = s == 0 ? fp->lights[li].flux_pp : ld3(P.energy[kVS * (vix(P, s - 1, i))]);
         const float4 am = __ldg(&S.mat[h.obj]);
         const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
         const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
         if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
-            __stcs(&P.in_dir[2 * (v)], make_float4(d.x, d.y, d.z, 0.f));
-            __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
-            __stcs(&P.energy[2 * (v)], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
+            __stcs(&P.in_dir[kVS * (v)], make_float4(d.x, d.y, d.z, 0.f));
+            __stcs(&P.pos_obj[kVS * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[kVS * (v)], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
-            __stcs(&P.out_dir[2 * (v)], make_float4(out.x, out.y, out.z, 0.f));
+            __stcs(&P.out_dir[kVS * (v)], make_float4(out.x, out.y, out.z, 0.f));
             P.rstart[i] = (uint8_t)(s + 1);
             has = false;
             continue;
         }
-        const V3 old_pos = ld3(P.pos_obj[2 * (v)]);
+        const V3 old_pos = ld3(P.pos_obj[kVS * (v)]);
         const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
-        __stcs(&P.in_dir[2 * (v)], make_float4(d.x, d.y, d.z, 0.f));
-        __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+        __stcs(&P.in_dir[kVS * (v)], make_float4(d.x, d.y, d.z, 0.f));
+        __stcs(&P.pos_obj[kVS * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
         if (s + 1 >= segs) {
             has = false;
             continue;
@@ -471,9 +471,9 @@ __global__ void __launch_bounds__(kT) k_verify_error(SceneDev S, PathDev P, floa
             continue;
         }
         if (s + 1 < k) {
-            const V3 next = ld3(P.pos_obj[2 * (vix(P, s + 1, i))]);
+            const V3 next = ld3(P.pos_obj[kVS * (vix(P, s + 1, i))]);
             const V3 od = normalized(sub(next, h.pos));
-            __stcs(&P.out_dir[2 * (v)], make_float4(od.x, od.y, od.z, 0.f));
+            __stcs(&P.out_dir[kVS * (v)], make_float4(od.x, od.y, od.z, 0.f));
         }
         force = true;
         ++s;
@@ -524,8 +524,8 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
             have = false;
             continue;
         }
-        const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[2 * (vix(P, s - 1, i))]);
-        const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, s - 1, i))]);
+        const V3 o = s == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[kVS * (vix(P, s - 1, i))]);
+        const V3 d = s == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[kVS * (vix(P, s - 1, i))]);
         ++vis;
         Hit h;
         const bool hit = intersect_scene(S, o, d, S.eps, h);
@@ -540,24 +540,24 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
             continue;
         }
         const size_t v = vix(P, s, i);
-        const float4 stored = P.energy[2 * (v)];
-        const V3 e_prev = s == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[2 * (vix(P, s - 1, i))]);
+        const float4 stored = P.energy[kVS * (v)];
+        const V3 e_prev = s == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[kVS * (vix(P, s - 1, i))]);
         const float4 am = __ldg(&S.mat[h.obj]);
         const V3 e_new = mulv(e_prev, V3{am.x, am.y, am.z});
         const bool glossy = (__ldg(&S.oflags[h.obj]) & 2u) != 0;
         if (glossy || !energies_close(ld3(stored), e_new, threshold)) {
-            __stcs(&P.in_dir[2 * (v)], make_float4(d.x, d.y, d.z, 0.f));
-            __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
-            __stcs(&P.energy[2 * (v)], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
+            __stcs(&P.in_dir[kVS * (v)], make_float4(d.x, d.y, d.z, 0.f));
+            __stcs(&P.pos_obj[kVS * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[kVS * (v)], make_float4(e_new.x, e_new.y, e_new.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, d, p, epoch, s + 1);
-            __stcs(&P.out_dir[2 * (v)], make_float4(out.x, out.y, out.z, 0.f));
+            __stcs(&P.out_dir[kVS * (v)], make_float4(out.x, out.y, out.z, 0.f));
             P.rstart[i] = (uint8_t)(s + 1);
             continue;
         }
-        const V3 old_pos = ld3(P.pos_obj[2 * (v)]);
+        const V3 old_pos = ld3(P.pos_obj[kVS * (v)]);
         const bool close_pos = length(sub(h.pos, old_pos)) <= S.eps;
-        __stcs(&P.in_dir[2 * (v)], make_float4(d.x, d.y, d.z, 0.f));
-        __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+        __stcs(&P.in_dir[kVS * (v)], make_float4(d.x, d.y, d.z, 0.f));
+        __stcs(&P.pos_obj[kVS * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
         if (s + 1 >= segs) continue;
         have = true;
         const bool hit_dyn = (__ldg(&S.oflags[h.obj]) & 1u) != 0;
@@ -566,9 +566,9 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
             continue;
         }
         if (s + 1 < k) {
-            const V3 next = ld3(P.pos_obj[2 * (vix(P, s + 1, i))]);
+            const V3 next = ld3(P.pos_obj[kVS * (vix(P, s + 1, i))]);
             const V3 od = normalized(sub(next, h.pos));
-            __stcs(&P.out_dir[2 * (v)], make_float4(od.x, od.y, od.z, 0.f));
+            __stcs(&P.out_dir[kVS * (v)], make_float4(od.x, od.y, od.z, 0.f));
         }
         force = true;
         ++s;
@@ -715,7 +715,8 @@ __global__ void k_dead_flags(PathDev P, uint32_t lb, uint32_t le, uint8_t* flags
 
 __global__ void __launch_bounds__(kT) k_fill_assign(SceneDev S, PathDev P, uint32_t li,
                                                     const uint32_t* dead, const uint32_t* dead_count,
-                                                    uint64_t dead_prefix, const uint32_t* need_off,
+                                                    uint64_t dead_prefix, const uint64_t* dead_prefix_dev,
+                                                    const uint32_t* need_off,
                                                     const uint32_t* need_total, uint32_t cells,
                                                     Counters* ctr) {
     const LightDev& L = S.fp->lights[li];
@@ -723,7 +724,7 @@ __global__ void __launch_bounds__(kT) k_fill_assign(SceneDev S, PathDev P, uint3
     const uint64_t total = *need_total;
     unsigned long long filled = 0;
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nd; j += gridDim.x * blockDim.x) {
-        const uint64_t u = dead_prefix + j;
+        const uint64_t u = (dead_prefix_dev ? dead_prefix_dev[li] : dead_prefix) + j;
         if (u >= total) continue;
         // cell c with need_off[c] <= u < need_off[c] + need[c]: last c with need_off[c] <= u
         uint32_t lo = 0, hi = cells;  // invariant: need_off[lo] <= u, answer in [lo, hi)
@@ -751,11 +752,41 @@ __global__ void __launch_bounds__(kT) k_fill_assign(SceneDev S, PathDev P, uint3
     warp_add(&ctr->filled, filled);
 }
 
-// fill's slot-exhaustion check (engine.cpp:512-513): single-shard form
-__global__ void k_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint32_t* need_total,
-                             Counters* ctr) {
-    const uint64_t avail = dead_count ? (uint64_t)*dead_count : dead_total;
+// fill's slot-exhaustion check (engine.cpp:512-513): single-shard form (dead_count), or the
+// all-shard dead-slot total (host value, or device value of light li when sharded in-engine)
+__global__ void k_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint64_t* dead_total_dev,
+                             uint32_t li, const uint32_t* need_total, Counters* ctr) {
+    const uint64_t avail = dead_count ? (uint64_t)*dead_count : (dead_total_dev ? dead_total_dev[li] : dead_total);
     if ((uint64_t)*need_total > avail) atomicAdd(&ctr->fill_overflow, 1ull);
+}
+
+// Sharded exchange: per-rank counts gathered as g[r * n + i]; prefix = the
+// counts of the lower ranks (their paths have the lower ids), total = all ranks.
+__global__ void k_rank_prefix_u32(const uint32_t* g, uint32_t n, uint32_t world, uint32_t rank, uint32_t* prefix,
+                                  uint32_t* total) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t p = 0, t = 0;
+        for (uint32_t r = 0; r < world; ++r) {
+            const uint32_t v = g[(size_t)r * n + i];
+            if (r < rank) p += v;
+            t += v;
+        }
+        prefix[i] = p;
+        total[i] = t;
+    }
+}
+__global__ void k_rank_prefix_u64(const uint32_t* g, uint32_t n, uint32_t world, uint32_t rank, uint64_t* prefix,
+                                  uint64_t* total) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint64_t p = 0, t = 0;
+        for (uint32_t r = 0; r < world; ++r) {
+            const uint64_t v = g[(size_t)r * n + i];
+            if (r < rank) p += v;
+            t += v;
+        }
+        prefix[i] = p;
+        total[i] = t;
+    }
 }
 
 __global__ void k_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells) {
@@ -794,9 +825,9 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_trace(SceneDev S, PathDe
                     m = P.meta[i];
                     epoch = P.epoch[i];
                     b = P.rstart[i];
-                    pos = b == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[2 * (vix(P, b - 1, i))]);
-                    dir = b == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[2 * (vix(P, b - 1, i))]);
-                    energy = b == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[2 * (vix(P, b - 1, i))]);
+                    pos = b == 0 ? ld3(P.origin[i]) : ld3(P.pos_obj[kVS * (vix(P, b - 1, i))]);
+                    dir = b == 0 ? ld3(P.emis[i]) : ld3(P.out_dir[kVS * (vix(P, b - 1, i))]);
+                    energy = b == 0 ? fp->lights[light_of(fp, p)].flux_pp : ld3(P.energy[kVS * (vix(P, b - 1, i))]);
                     if (b >= P.B) {
                         truncate_path(P, i, b, false, m);
                         P.meta[i] = m;
@@ -817,11 +848,11 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_trace(SceneDev S, PathDe
             const float4 am = __ldg(&S.mat[h.obj]);
             energy = mulv(energy, V3{am.x, am.y, am.z});
             const size_t v = vix(P, b, i);
-            __stcs(&P.in_dir[2 * (v)], make_float4(dir.x, dir.y, dir.z, 0.f));
-            __stcs(&P.pos_obj[2 * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
-            __stcs(&P.energy[2 * (v)], make_float4(energy.x, energy.y, energy.z, S.gather_radius));
+            __stcs(&P.in_dir[kVS * (v)], make_float4(dir.x, dir.y, dir.z, 0.f));
+            __stcs(&P.pos_obj[kVS * (v)], make_float4(h.pos.x, h.pos.y, h.pos.z, __uint_as_float(h.obj)));
+            __stcs(&P.energy[kVS * (v)], make_float4(energy.x, energy.y, energy.z, S.gather_radius));
             const V3 out = sample_bounce(S, h.obj, h.normal, dir, p, epoch, b + 1);
-            __stcs(&P.out_dir[2 * (v)], make_float4(out.x, out.y, out.z, 0.f));
+            __stcs(&P.out_dir[kVS * (v)], make_float4(out.x, out.y, out.z, 0.f));
             pos = h.pos;
             dir = out;
             ++b;
@@ -893,7 +924,7 @@ struct AuxRec {  // photon_store.hpp:75-78
 __global__ void k_pack(PathDev P, PhotonRec* ph, AuxRec* aux) {
     const size_t total = (size_t)P.n * P.B;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const float4 po = P.pos_obj[2 * (v)], en = P.energy[2 * (v)], in = P.in_dir[2 * (v)], od = P.out_dir[2 * (v)];
+        const float4 po = P.pos_obj[kVS * (v)], en = P.energy[kVS * (v)], in = P.in_dir[kVS * (v)], od = P.out_dir[kVS * (v)];
         if (ph) ph[v] = PhotonRec{in.x, in.y, in.z, __float_as_uint(po.w), en.x, en.y, en.z, en.w};
         if (aux) aux[v] = AuxRec{po.x, po.y, po.z, od.x, od.y, od.z};
     }
@@ -904,16 +935,16 @@ __global__ void k_unpack(PathDev P, const PhotonRec* ph, const AuxRec* aux) {
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
         if (ph) {
             const PhotonRec r = ph[v];
-            __stcs(&P.in_dir[2 * (v)], make_float4(r.dx, r.dy, r.dz, 0.f));
-            __stcs(&P.energy[2 * (v)], make_float4(r.ex, r.ey, r.ez, r.radius));
-            P.pos_obj[2 * (v)].w = __uint_as_float(r.obj);
+            __stcs(&P.in_dir[kVS * (v)], make_float4(r.dx, r.dy, r.dz, 0.f));
+            __stcs(&P.energy[kVS * (v)], make_float4(r.ex, r.ey, r.ez, r.radius));
+            P.pos_obj[kVS * (v)].w = __uint_as_float(r.obj);
         }
         if (aux) {
             const AuxRec a = aux[v];
-            P.pos_obj[2 * (v)].x = a.px;
-            P.pos_obj[2 * (v)].y = a.py;
-            P.pos_obj[2 * (v)].z = a.pz;
-            __stcs(&P.out_dir[2 * (v)], make_float4(a.ox, a.oy, a.oz, 0.f));
+            P.pos_obj[kVS * (v)].x = a.px;
+            P.pos_obj[kVS * (v)].y = a.py;
+            P.pos_obj[kVS * (v)].z = a.pz;
+            __stcs(&P.out_dir[kVS * (v)], make_float4(a.ox, a.oy, a.oz, 0.f));
         }
     }
 }
@@ -1021,14 +1052,24 @@ void launch_dead_flags(PathDev P, uint32_t lb, uint32_t le, uint8_t* flags, cuda
     if (le > lb) LAUNCH(k_dead_flags, le - lb, P, lb, le, flags);
 }
 void launch_fill_assign(SceneDev S, PathDev P, uint32_t li, const uint32_t* dead, const uint32_t* dead_count,
-                        uint32_t n_max, uint64_t dead_prefix, const uint32_t* need_off,
-                        const uint32_t* need_total, uint32_t cells, Counters* ctr, cudaStream_t st) {
-    LAUNCH(k_fill_assign, n_max, S, P, li, dead, dead_count, dead_prefix, need_off, need_total, cells, ctr);
+                        uint32_t n_max, uint64_t dead_prefix, const uint64_t* dead_prefix_dev,
+                        const uint32_t* need_off, const uint32_t* need_total, uint32_t cells, Counters* ctr,
+                        cudaStream_t st) {
+    LAUNCH(k_fill_assign, n_max, S, P, li, dead, dead_count, dead_prefix, dead_prefix_dev, need_off, need_total,
+           cells, ctr);
 }
-void launch_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint32_t* need_total, Counters* ctr,
-                       cudaStream_t st) {
-    k_fill_check<<<1, 1, 0, st>>>(dead_count, dead_total, need_total, ctr);
+void launch_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint64_t* dead_total_dev, uint32_t li,
+                       const uint32_t* need_total, Counters* ctr, cudaStream_t st) {
+    k_fill_check<<<1, 1, 0, st>>>(dead_count, dead_total, dead_total_dev, li, need_total, ctr);
     ++g_launches;
+}
+void launch_rank_prefix_u32(const uint32_t* g, uint32_t n, uint32_t world, uint32_t rank, uint32_t* prefix,
+                            uint32_t* total, cudaStream_t st) {
+    LAUNCH(k_rank_prefix_u32, n, g, n, world, rank, prefix, total);
+}
+void launch_rank_prefix_u64(const uint32_t* g, uint32_t n, uint32_t world, uint32_t rank, uint64_t* prefix,
+                            uint64_t* total, cudaStream_t st) {
+    LAUNCH(k_rank_prefix_u64, n, g, n, world, rank, prefix, total);
 }
 void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st) {
     LAUNCH(k_dm_after_fill, cells, dm_c, dm_t, cells);

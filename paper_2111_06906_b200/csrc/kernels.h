@@ -50,12 +50,18 @@ void launch_dm_after_prune(uint32_t* dm_c, const uint32_t* dm_t, const uint32_t*
 void launch_fill_need(const uint32_t* dm_t, const uint32_t* dm_c, uint32_t* need, uint32_t cells,
                       cudaStream_t st);
 void launch_dead_flags(PathDev P, uint32_t lb, uint32_t le, uint8_t* flags, cudaStream_t st);
+// the dead-slot rank offset of this shard: dead_prefix_dev[light] when non-null, else dead_prefix
 void launch_fill_assign(SceneDev S, PathDev P, uint32_t light, const uint32_t* dead,
                         const uint32_t* dead_count, uint32_t n_max, uint64_t dead_prefix,
-                        const uint32_t* need_off, const uint32_t* need_total, uint32_t cells,
-                        Counters* ctr, cudaStream_t st);
-void launch_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint32_t* need_total,
-                       Counters* ctr, cudaStream_t st);
+                        const uint64_t* dead_prefix_dev, const uint32_t* need_off,
+                        const uint32_t* need_total, uint32_t cells, Counters* ctr, cudaStream_t st);
+void launch_fill_check(const uint32_t* dead_count, uint64_t dead_total, const uint64_t* dead_total_dev,
+                       uint32_t light, const uint32_t* need_total, Counters* ctr, cudaStream_t st);
+// sharded exchange: prefix over lower ranks / total over all ranks of gathered counts
+void launch_rank_prefix_u32(const uint32_t* gathered, uint32_t n, uint32_t world, uint32_t rank,
+                            uint32_t* prefix, uint32_t* total, cudaStream_t st);
+void launch_rank_prefix_u64(const uint32_t* gathered, uint32_t n, uint32_t world, uint32_t rank,
+                            uint64_t* prefix, uint64_t* total, cudaStream_t st);
 void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st);
 // stage_trace (engine.cpp:548-598)
 void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st);

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kT) k_splat_filter(PathDev P, float radius,
     const uint32_t mask = (1u << bits) - 1u;
     const size_t total = (size_t)P.n * P.B;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const float4 po = __ldcs(&P.pos_obj[2 * (v)]);
+        const float4 po = __ldcs(&P.pos_obj[kVS * (v)]);
         if (__float_as_uint(po.w) == kInvalidObj) continue;
         const unsigned long long key =
             grid_key(cell_coord(po.x, radius), cell_coord(po.y, radius), cell_coord(po.z, radius));
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float rad
     const uint32_t nc = *n_cand;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
         const uint2 vs = cand[c];
-        const float4 po = __ldg(&P.pos_obj[2 * (vs.x)]);
+        const float4 po = __ldg(&P.pos_obj[kVS * (vs.x)]);
         const uint32_t obj = __float_as_uint(po.w);
         const uint32_t n = __ldg(&cnt[vs.y]), o = __ldg(&off[vs.y]);
         float4 en;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float rad
             const V3 d = sub(V3{po.x, po.y, po.z}, V3{g.x, g.y, g.z});  // gather.hpp:54
             if (dot(d, d) > r2) continue;
             if (!have_en) {
-                en = __ldg(&P.energy[2 * (vs.x)]);
+                en = __ldg(&P.energy[kVS * (vs.x)]);
                 have_en = true;
             }
             atomicAdd(&acc[3 * pix], en.x);
@@ -173,7 +173,7 @@ __global__ void k_gather_flag(PathDev P, float radius, const unsigned long long*
     const uint32_t mask = (1u << bits) - 1u;
     const size_t total = (size_t)P.n * P.B;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const float4 po = __ldcs(&P.pos_obj[2 * (v)]);
+        const float4 po = __ldcs(&P.pos_obj[kVS * (v)]);
         uint8_t f = 0;
         if (__float_as_uint(po.w) != kInvalidObj) {
             const unsigned long long key =
@@ -206,8 +206,8 @@ __global__ void k_gather_copy(PathDev P, const uint32_t* __restrict__ vals, cons
     const uint32_t n = *count;
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const uint32_t v = vals[j];
-        spo[j] = P.pos_obj[2 * (v)];
-        sen[j] = P.energy[2 * (v)];
+        spo[j] = P.pos_obj[kVS * (v)];
+        sen[j] = P.energy[kVS * (v)];
     }
 }
 
