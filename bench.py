@@ -56,6 +56,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e replay (profiling passes)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-splat-sweep", action="store_true", help="skip the per-mode splat timings")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: N x the workload's paths over N GPUs; strong: the workload's paths split over N")
     return ap.parse_args()
 
 
@@ -181,14 +183,17 @@ def main():
     rank, world, local = dist_env()
     name = args.workload
     w = WORKLOADS[name]
-    # weak scaling: every GPU holds the workload's full path count (a contiguous shard of the
-    # N-times-larger problem), so per-GPU work is fixed as N grows
-    paths_per_gpu = args.paths or w["paths"]
-    n_paths = paths_per_gpu * (world if args.impl == "ours" else 1)
+    # weak scaling (default): every GPU holds the workload's full path count (a contiguous shard
+    # of the N-times-larger problem), so per-GPU work is fixed as N grows; strong scaling: the
+    # workload's path count is split over the N GPUs (north_star: a 5M-path frame on 8 B200)
+    per_job = args.paths or w["paths"]
+    strong = args.scaling == "strong" and args.impl == "ours"
+    n_paths = per_job if strong else per_job * (world if args.impl == "ours" else 1)
+    paths_per_gpu = n_paths // world if strong else per_job
     unit = "paths/s"
     metric = "verified+retraced photon paths/s (frame = verify+retrace+splat)"
     config = {"workload": f"{name}: {w['desc']}", "n_paths": n_paths, "paths_per_gpu": paths_per_gpu,
-              "parallelism": f"contiguous path shards x{world} (NCCL DM/prune/fill exchanges)",
+              "parallelism": f"contiguous path shards x{world} (in-engine NCCL DM/prune/fill/counter/image exchanges)",
               "max_bounces": w["bounces"],
               "mode": w["mode"], "threshold": w["threshold"], "dm_dims": [8, 8, 64, 64],
               "image": "120x90", "gather_radius": 0.25,
@@ -243,8 +248,14 @@ def main():
                          threshold=w["threshold"], seed=1, device=local, shard=shard)
     import ctypes as C
 
-    stream = torch.cuda.current_stream()
-    if world > 1:  # path-sharded frames over NCCL (paper_2111_06906_b200/distributed.py)
+    # one non-default stream shared by torch and the engine, so the CUDA events below time the
+    # engine's device work (torch's default stream handle is 0, which the engine would replace
+    # by a private stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    legacy = world > 1 and backend != "nccl"
+    comm = None
+    if legacy:  # functional multi-rank check on one device (gloo): the host-phased protocol
         from paper_2111_06906_b200.distributed import GpuExecutor, TorchCollectives, run_frame_distributed
 
         ex = GpuExecutor(scene, cfg, stream)
@@ -253,29 +264,33 @@ def main():
     else:
         eng = pr.Engine(scene, cfg)
         eng.set_stream(stream.cuda_stream)
+    if world > 1 and not legacy:
+        # path-sharded frames: the exchanges run inside the engine over NCCL (comm.cpp); the
+        # unique id travels once through torch.distributed
+        from paper_2111_06906_b200.distributed import Communicator, attach
+
+        obj = [Communicator.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        comm = Communicator.nccl(obj[0], rank, world, local)
+        attach(eng, comm)
     cam = scene.describe().camera
     img_dev = torch.zeros(cam.height * cam.width * 3, dtype=torch.float32, device="cuda")
     frame_no = [0]
 
     def step(collect=None):
-        if world > 1:
+        if legacy:
             d = run_frame_distributed(ex, coll, frame_no[0])
             st = L.FrameStats()
             for k in L.FrameStats.COUNTS + ("live_segments_before", "paths_retraced"):
                 setattr(st, k, int(d[k]))
-            lm = d.get("local_ms", {})  # this rank's device stage times
-            st.ms_frame_update = lm.get("frame_update", 0.0)
-            st.ms_verify = lm.get("verify", 0.0)
-            st.t_trace = lm.get("trace", 0.0) * 1e-3  # compaction + trace + finalize
-            st.ms_retrace = lm.get("trace", 0.0)      # prune/fill exchanges not included
-        else:
+        else:  # one prx_run_frame (+ its exchanges when sharded), one read-back
             st = L.FrameStats()
             L.check(L.lib().prx_run_frame(eng.handle, C.byref(st)))
         frame_no[0] += 1
         sst = L.FrameStats()
         L.check(L.lib().prx_splat(eng.handle, C.byref(cam), 0.25, args.splat_mode, None,
                                   C.c_void_p(img_dev.data_ptr()), C.byref(sst)))
-        if world > 1:  # per-rank photon splats summed into one image (NCCL all-reduce)
+        if legacy:
             torch.distributed.all_reduce(img_dev)
         if collect is not None:
             collect.append((st, sst))
@@ -347,17 +362,19 @@ def main():
     # animation, so later frames would not be comparable)
     if args.no_e2e:
         eng2 = eng
-    elif world > 1:
+    elif legacy:
         ex2 = GpuExecutor(scene, cfg, stream)
         eng2 = ex2.engine
     else:
         eng2 = pr.Engine(scene, cfg)
         eng2.set_stream(stream.cuda_stream)
+        if comm is not None:  # the same communicator: its collectives are stream-ordered
+            attach(eng2, comm)
     frame2 = [0]
     e2e_dev = []  # device stage times of the e2e frames (diagnostic: host overhead = wall - this)
 
     def step_e2e(collect):
-        if world > 1:  # sharded frame + reduced image read back to the host
+        if legacy:  # sharded frame + reduced image read back to the host
             run_frame_distributed(ex2, coll, frame2[0])
             L.check(L.lib().prx_splat(eng2.handle, C.byref(cam), 0.25, args.splat_mode, None,
                                       C.c_void_p(img_dev.data_ptr()), None))
@@ -391,7 +408,7 @@ def main():
     # bytes the engine itself copied per step (counted inside the library), plus the reduced
     # image read back by torch on the sharded path
     h2d = (xfer1[0] - xfer0[0]) // max(e2e_steps, 1)
-    d2h = (xfer1[1] - xfer0[1]) // max(e2e_steps, 1) + (12 * cam.width * cam.height if world > 1 else 0)
+    d2h = (xfer1[1] - xfer0[1]) // max(e2e_steps, 1) + (12 * cam.width * cam.height if legacy else 0)
 
     # roofline of the dominant kernel stage (trace): algorithmic bytes per traced segment =
     # 64 B written (4 x float4 vertex streams) + 64 B per retraced path start (meta, rstart,
@@ -409,7 +426,7 @@ def main():
 
     line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (procedural scene, seed 1)", "config": config,
             "stages_ms": {"frame_update": update_ms, "verify": verify_ms, "occlusions": occl_ms,
                           "retrace": retrace_ms, "trace": trace_ms, "splat": splat_ms},

@@ -304,6 +304,39 @@ prx_status prx_fill_count(prx_engine* engine, uint32_t* dead_out);
 prx_status prx_fill_apply(prx_engine* engine, const uint64_t* dead_prefix,
                           const uint64_t* dead_total, prx_frame_stats* stats);
 /* Stream the engine orders its work on (cudaStream_t as void*); NULL = engine-owned. */
+/* ---- in-engine multi-GPU ------------------------------------------
+ * A path-sharded engine (prx_config.shard_begin/end = rank r's contiguous path range, ranks
+ * in ascending path order) with a collectives table attached runs the whole sharded frame
+ * itself: prx_run_frame enqueues the DM_C all-reduce, the per-cell unmarked-count and
+ * dead-slot all-gathers (prefix over lower ranks + totals, computed on the device), and the
+ * counter all-reduce on its stream between its kernels, with one host read-back per frame,
+ * and prx_splat all-reduces the image.  Every rank calls the same entry points in the same
+ * order (collective semantics).  Tables come from prx_comm_* (NCCL, or the in-process local
+ * backend for several engines driven by several host threads) or from the caller. */
+typedef struct prx_collectives {
+    void* ctx;
+    int32_t rank, world;
+    /* each returns 0 on success; enqueued on `stream` (a cudaStream_t); sums in place */
+    int (*all_reduce_sum_u32)(void* ctx, uint32_t* buf, size_t count, void* stream);
+    int (*all_reduce_sum_u64)(void* ctx, uint64_t* buf, size_t count, void* stream);
+    int (*all_reduce_sum_f32)(void* ctx, float* buf, size_t count, void* stream);
+    /* recv[r * count + i] = rank r's send[i] */
+    int (*all_gather_u32)(void* ctx, const uint32_t* send, uint32_t* recv, size_t count, void* stream);
+} prx_collectives;
+/* attach (copied) / detach (NULL); world 1 behaves as an unsharded engine */
+prx_status prx_engine_set_collectives(prx_engine* engine, const prx_collectives* coll);
+
+typedef struct prx_comm prx_comm;
+/* NCCL (loaded at run time, PRX_NCCL_LIB overrides "libnccl.so.2"): rank 0 makes the id,
+ * the caller ships it to the other ranks, every rank creates its communicator */
+prx_status prx_comm_nccl_unique_id(uint8_t id_out[128]);
+prx_status prx_comm_nccl_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device,
+                                prx_comm** out);
+/* in-process: `world` communicators (comms_out[world]), each used by one host thread */
+prx_status prx_comm_local_create(int32_t world, prx_comm** comms_out);
+prx_status prx_comm_collectives(prx_comm* comm, prx_collectives* out);
+void prx_comm_destroy(prx_comm* comm);
+
 prx_status prx_engine_set_stream(prx_engine* engine, void* cuda_stream);
 prx_status prx_engine_synchronize(prx_engine* engine);
 

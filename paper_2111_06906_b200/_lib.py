@@ -124,6 +124,13 @@ class EngineInfo(C.Structure):
                 ("device_bytes", C.c_uint64)]
 
 
+class Collectives(C.Structure):
+    """prx_collectives (include/prx.h): the function pointers stay opaque to Python."""
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
+                ("all_reduce_sum_u32", C.c_void_p), ("all_reduce_sum_u64", C.c_void_p),
+                ("all_reduce_sum_f32", C.c_void_p), ("all_gather_u32", C.c_void_p)]
+
+
 # Every symbol include/prx.h declares: (name, restype, argtypes)
 P = C.c_void_p
 SIGNATURES = [
@@ -165,6 +172,12 @@ SIGNATURES = [
                                   C.POINTER(FrameStats)]),
     ("prx_fill_count", C.c_int, [P, C.POINTER(C.c_uint32)]),
     ("prx_fill_apply", C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(FrameStats)]),
+    ("prx_engine_set_collectives", C.c_int, [P, C.POINTER(Collectives)]),
+    ("prx_comm_nccl_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("prx_comm_nccl_create", C.c_int, [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
+    ("prx_comm_local_create", C.c_int, [C.c_int32, C.POINTER(P)]),
+    ("prx_comm_collectives", C.c_int, [P, C.POINTER(Collectives)]),
+    ("prx_comm_destroy", None, [P]),
     ("prx_engine_set_stream", C.c_int, [P, P]),
     ("prx_engine_synchronize", C.c_int, [P]),
     ("prx_splat", C.c_int, [P, C.POINTER(Camera), C.c_float, C.c_int, P, P,

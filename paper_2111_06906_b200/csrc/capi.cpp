@@ -8,6 +8,7 @@
 #include <memory>
 #include <string>
 
+#include "comm.h"
 #include "engine.h"
 #include "host_scene.h"
 #include "prx.h"
@@ -346,6 +347,48 @@ prx_status prx_fill_apply(prx_engine* engine, const uint64_t* dead_prefix, const
         eng(engine).fill_apply(dead_prefix, dead_total, stats);
     });
 }
+prx_status prx_engine_set_collectives(prx_engine* engine, const prx_collectives* coll) {
+    return guarded([&] { eng(engine).set_collectives(coll); });
+}
+
+struct prx_comm {
+    std::unique_ptr<prx::Comm> comm;
+};
+
+prx_status prx_comm_nccl_unique_id(uint8_t id_out[128]) {
+    return guarded([&] {
+        need(id_out, "id_out");
+        prx::nccl_unique_id(id_out);
+    });
+}
+prx_status prx_comm_nccl_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device, prx_comm** out) {
+    return guarded([&] {
+        need(id, "id");
+        need(out, "out");
+        auto c = std::make_unique<prx_comm>();
+        c->comm = prx::nccl_comm(id, rank, world, device);
+        *out = c.release();
+    });
+}
+prx_status prx_comm_local_create(int32_t world, prx_comm** comms_out) {
+    return guarded([&] {
+        need(comms_out, "comms_out");
+        auto v = prx::local_comms(world);
+        for (int r = 0; r < world; ++r) {
+            comms_out[r] = new prx_comm;
+            comms_out[r]->comm = std::move(v[r]);
+        }
+    });
+}
+prx_status prx_comm_collectives(prx_comm* comm, prx_collectives* out) {
+    return guarded([&] {
+        need(comm, "comm");
+        need(out, "out");
+        comm->comm->table(out);
+    });
+}
+void prx_comm_destroy(prx_comm* comm) { delete comm; }
+
 prx_status prx_engine_set_stream(prx_engine* engine, void* cuda_stream) {
     return guarded([&] { eng(engine).set_stream(static_cast<cudaStream_t>(cuda_stream)); });
 }

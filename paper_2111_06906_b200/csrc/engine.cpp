@@ -4,6 +4,8 @@
 // box arithmetic done here matches the reference's host arithmetic bit for bit.
 #include "engine.h"
 
+#include "comm.h"
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -527,8 +529,9 @@ void Engine::alloc_state() {
     d_pruned_list_.alloc(4ull * n_);
     d_need_.alloc(4ull * max_cells_ + 16);
     d_scratch_.alloc(prim_scratch_bytes(std::max<uint64_t>(n_, max_cells_)));
-    // per-light pointer tables: [0] unm, [1] seg_start, [2] prefix, [3] total (sharded prune)
-    std::vector<uint32_t*> ptrs(4 * PRX_MAX_LIGHTS, nullptr);
+    // per-light pointer tables: [0] unm, [1] seg_start, [2] prefix, [3] total (prx_prune_apply),
+    // [4] prefix, [5] total (in-engine sharded prune, set by set_collectives)
+    std::vector<uint32_t*> ptrs(6 * PRX_MAX_LIGHTS, nullptr);
     for (size_t li = 0; li < lights_.size(); ++li) {
         ptrs[li] = lights_[li].unm.as<uint32_t>();
         ptrs[PRX_MAX_LIGHTS + li] = lights_[li].seg_start.as<uint32_t>();
@@ -720,6 +723,7 @@ void Engine::copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind
 // pinned host memory) + its device part (uploads and kernels), split so that run_frame can
 // replay the device parts of a whole frame as one CUDA graph.
 void Engine::frame_update(prx_frame_stats* st) {
+    PRX_CUDA(cudaSetDevice(device_));
     frame_update_host();
     frame_update_enqueue();
     if (st) {
@@ -795,6 +799,7 @@ void Engine::verify_paths(prx_frame_stats* st) {
     }
     record(kEvDm0);
     stage_compute_dm();
+    if (sharded()) exchange_dm();
     record(kEvPrune0);
 }
 
@@ -860,7 +865,8 @@ void Engine::fill_collect_dead() {
 // Deficit cells ascending <-> dead slots ascending over the whole path range: this shard
 // owns global dead-slot ranks [prefix, prefix + local count).  Without prefix/total the
 // shard is the whole range.
-void Engine::fill_assign_all(const uint64_t* prefix, const uint64_t* total) {
+void Engine::fill_assign_all(const uint64_t* prefix, const uint64_t* total, const uint64_t* prefix_dev,
+                             const uint64_t* total_dev) {
     const PathDev P = path_dev();
     uint32_t* cnt = d_cnt32_.as<uint32_t>();
     for (uint32_t li = 0; li < lights_.size(); ++li) {
@@ -870,10 +876,11 @@ void Engine::fill_assign_all(const uint64_t* prefix, const uint64_t* total) {
         launch_fill_need(b.dm_t.as<uint32_t>(), b.dm_c.as<uint32_t>(), d_need_.as<uint32_t>(), b.cells, stream_);
         scan_exclusive_u32(d_need_.as<uint32_t>(), d_need_.as<uint32_t>(), b.cells, nullptr, need_total,
                            d_scratch_.get(), stream_);
-        launch_fill_check(total ? nullptr : cnt + kCntDead0 + li, total ? total[li] : 0, need_total,
-                          d_ctr_.as<Counters>(), stream_);
+        const bool all_ranks = total || total_dev;
+        launch_fill_check(all_ranks ? nullptr : cnt + kCntDead0 + li, total ? total[li] : 0, total_dev, li,
+                          need_total, d_ctr_.as<Counters>(), stream_);
         launch_fill_assign(scene_dev(), P, li, d_list_.as<uint32_t>() + lb, cnt + kCntDead0 + li,
-                           std::max(1u, le - lb), prefix ? prefix[li] : 0, d_need_.as<uint32_t>(), need_total,
+                           std::max(1u, le - lb), prefix ? prefix[li] : 0, prefix_dev, d_need_.as<uint32_t>(), need_total,
                            b.cells, d_ctr_.as<Counters>(), stream_);
         launch_dm_after_fill(b.dm_c.as<uint32_t>(), b.dm_t.as<uint32_t>(), b.cells, stream_);
     }
@@ -882,6 +889,95 @@ void Engine::fill_assign_all(const uint64_t* prefix, const uint64_t* total) {
 void Engine::stage_fill_local() {
     fill_collect_dead();
     fill_assign_all(nullptr, nullptr);
+}
+
+// ---- in-engine sharded frame: the exchanges enqueued between the kernels
+void Engine::coll_ok(int rc, const char* what) const {
+    if (rc != 0) throw CudaError(std::string("collective failed: ") + what);
+}
+
+// DM_C per light, summed over the ranks (stage_compute_dm counts this shard's live paths)
+void Engine::exchange_dm() {
+    for (LightBlock& b : lights_)
+        coll_ok(coll_.all_reduce_sum_u32(coll_.ctx, b.dm_c.as<uint32_t>(), b.cells, stream_), "DM_C all-reduce");
+}
+
+// stage_prune over shards: Bernoulli marks are per path (key (path, frame)); the trim keeps the
+// lowest path ids, so a rank offsets its survivors' ranks by the unmarked counts of the lower
+// ranks (gathered, prefix on the device) and every rank sets DM_C from the all-rank totals
+void Engine::stage_prune_sharded() {
+    prune_mark_all();
+    const uint32_t W = static_cast<uint32_t>(coll_.world), R = static_cast<uint32_t>(coll_.rank);
+    std::vector<const uint32_t*> totals(lights_.size());
+    for (size_t li = 0; li < lights_.size(); ++li) {
+        LightBlock& b = lights_[li];
+        coll_ok(coll_.all_gather_u32(coll_.ctx, b.unm.as<uint32_t>(), d_gath_.as<uint32_t>(), b.cells, stream_),
+                "unmarked-count all-gather");
+        launch_rank_prefix_u32(d_gath_.as<uint32_t>(), b.cells, W, R, b.pref.as<uint32_t>(), b.tot.as<uint32_t>(),
+                               stream_);
+        totals[li] = b.tot.as<uint32_t>();
+    }
+    uint32_t** tab = d_light_ptrs_.as<uint32_t*>() + 4 * PRX_MAX_LIGHTS;
+    prune_trim_all(tab, tab + PRX_MAX_LIGHTS, totals.data());
+}
+
+// stage_fill over shards: deficit cells ascending <-> dead slots ascending over all ranks;
+// this rank owns dead-slot ranks [prefix, prefix + local count) of each light
+void Engine::stage_fill_sharded() {
+    fill_collect_dead();
+    const uint32_t nl = static_cast<uint32_t>(lights_.size());
+    coll_ok(coll_.all_gather_u32(coll_.ctx, d_cnt32_.as<uint32_t>() + kCntDead0, d_dead_g_.as<uint32_t>(), nl,
+                                 stream_),
+            "dead-slot all-gather");
+    uint64_t* pt = d_dead_pt_.as<uint64_t>();
+    launch_rank_prefix_u64(d_dead_g_.as<uint32_t>(), nl, static_cast<uint32_t>(coll_.world),
+                           static_cast<uint32_t>(coll_.rank), pt, pt + PRX_MAX_LIGHTS, stream_);
+    fill_assign_all(nullptr, nullptr, pt, pt + PRX_MAX_LIGHTS);
+}
+
+// the frame's counters summed over the ranks (read back instead of the local ones)
+void Engine::exchange_counters() {
+    PRX_CUDA(cudaMemcpyAsync(d_ctr_sum_.get(), d_ctr_.get(), sizeof(Counters), cudaMemcpyDeviceToDevice, stream_));
+    coll_ok(coll_.all_reduce_sum_u64(coll_.ctx, d_ctr_sum_.as<uint64_t>(), sizeof(Counters) / 8, stream_),
+            "counter all-reduce");
+    PRX_CUDA(cudaMemcpyAsync(d_cnt32_sum_.get(), d_cnt32_.get(), 4 * kCntN, cudaMemcpyDeviceToDevice, stream_));
+    coll_ok(coll_.all_reduce_sum_u32(coll_.ctx, d_cnt32_sum_.as<uint32_t>(), kCntN, stream_), "count all-reduce");
+}
+
+void Engine::set_collectives(const prx_collectives* c) {
+    PRX_CUDA(cudaSetDevice(device_));
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+    if (!c) {
+        coll_ = prx_collectives{};
+        return;
+    }
+    if (c->world < 1 || c->rank < 0 || c->rank >= c->world)
+        throw std::invalid_argument("collectives: rank must be in [0, world)");
+    if (c->world > 1 &&
+        (!c->all_reduce_sum_u32 || !c->all_reduce_sum_u64 || !c->all_reduce_sum_f32 || !c->all_gather_u32))
+        throw std::invalid_argument("collectives: missing entry point");
+    if (c->world > 1 && sb_ == 0 && se_ == n_total_ && c->rank > 0)
+        throw std::invalid_argument("collectives: a sharded engine needs its rank's path range (shard_begin/end)");
+    coll_ = *c;
+    if (!sharded()) return;
+    const uint32_t W = static_cast<uint32_t>(coll_.world);
+    d_gath_.alloc(4ull * W * max_cells_);
+    std::vector<uint32_t*> tab(2 * PRX_MAX_LIGHTS, nullptr);
+    for (size_t li = 0; li < lights_.size(); ++li) {
+        LightBlock& b = lights_[li];
+        b.pref.alloc(4ull * b.cells);
+        b.tot.alloc(4ull * b.cells);
+        tab[li] = b.pref.as<uint32_t>();
+        tab[PRX_MAX_LIGHTS + li] = b.tot.as<uint32_t>();
+    }
+    PRX_CUDA(cudaMemcpy(d_light_ptrs_.as<uint32_t*>() + 4 * PRX_MAX_LIGHTS, tab.data(), sizeof(uint32_t*) * tab.size(),
+                        cudaMemcpyHostToDevice));
+    d_dead_g_.alloc(4ull * W * PRX_MAX_LIGHTS);
+    d_dead_pt_.alloc(8ull * 2 * PRX_MAX_LIGHTS);
+    d_ctr_sum_.alloc(sizeof(Counters));
+    d_cnt32_sum_.alloc(4 * kCntN);
+    if (!h_ctr_sum_) PRX_CUDA(cudaMallocHost(&h_ctr_sum_, sizeof(Counters)));
+    if (!h_cnt32_sum_) PRX_CUDA(cudaMallocHost(&h_cnt32_sum_, 4 * kCntN));
 }
 
 void Engine::stage_trace() {
@@ -898,22 +994,30 @@ void Engine::stage_trace() {
 void Engine::read_back(prx_frame_stats* st, bool with_times) {
     copy_async(h_ctr_, d_ctr_.get(), sizeof(Counters), cudaMemcpyDeviceToHost);
     copy_async(h_cnt32_, d_cnt32_.get(), 4 * kCntN, cudaMemcpyDeviceToHost);
+    const bool summed = sharded() && in_sharded_frame_;
+    in_sharded_frame_ = false;
+    if (summed) {  // all-rank sums (exchange_counters) for the frame statistics
+        copy_async(h_ctr_sum_, d_ctr_sum_.get(), sizeof(Counters), cudaMemcpyDeviceToHost);
+        copy_async(h_cnt32_sum_, d_cnt32_sum_.get(), 4 * kCntN, cudaMemcpyDeviceToHost);
+    }
     PRX_CUDA(cudaStreamSynchronize(stream_));
     PRX_CUDA(cudaGetLastError());
     n_pruned_ = h_cnt32_[kCntPruned];
     launches_ = g_launches - launch_base_;
-    if (h_ctr_->fill_overflow) throw std::logic_error("fill: ran out of free path slots");
+    const Counters& C = summed ? *h_ctr_sum_ : *h_ctr_;
+    const uint32_t* c32 = summed ? h_cnt32_sum_ : h_cnt32_;
+    if (C.fill_overflow) throw std::logic_error("fill: ran out of free path slots");
     if (!st) return;
     st->frame = cur_frame_;
     st->mode = cfg_.mode;
-    st->rays_traced = h_ctr_->traced;
-    st->rays_reused = h_ctr_->segments - h_ctr_->traced;
-    st->paths_replaced = h_ctr_->replaced;
-    st->paths_pruned = h_cnt32_[kCntPruned];
-    st->paths_filled = h_ctr_->filled;
-    st->visibility_rays = h_ctr_->vis;
-    st->live_segments_before = h_ctr_->live_segments;
-    st->paths_retraced = h_cnt32_[kCntRetrace];
+    st->rays_traced = C.traced;
+    st->rays_reused = C.segments - C.traced;
+    st->paths_replaced = C.replaced;
+    st->paths_pruned = c32[kCntPruned];
+    st->paths_filled = C.filled;
+    st->visibility_rays = C.vis;
+    st->live_segments_before = C.live_segments;
+    st->paths_retraced = c32[kCntRetrace];
     if (with_times) {
         st->t_update = elapsed_ms(kEvVerify0, kEvOccl0) * 1e-3;
         st->t_occlusion = elapsed_ms(kEvOccl0, kEvDm0) * 1e-3;
@@ -936,12 +1040,18 @@ void Engine::retrace_enqueue() {
     PRX_CUDA(cudaSetDevice(device_));
     record(kEvPrune0);
     in_full_frame_ = true;  // prune -> fill -> trace run back to back: skip the prune clears
-    if (cfg_.mode != PRX_MODE_BASELINE) stage_prune_local();
+    in_sharded_frame_ = sharded();
+    if (cfg_.mode != PRX_MODE_BASELINE) {
+        if (sharded()) stage_prune_sharded();
+        else stage_prune_local();
+    }
     in_full_frame_ = false;
     record(kEvFill0);
-    stage_fill_local();
+    if (sharded()) stage_fill_sharded();
+    else stage_fill_local();
     record(kEvTrace0);
     stage_trace();
+    if (sharded()) exchange_counters();
     record(kEvEnd);
 }
 
@@ -951,6 +1061,7 @@ void Engine::retrace_enqueue() {
 // (its uploads read the pinned frame parameters at execution time), removing the per-launch
 // gaps of ~120 small launches. PRX_GRAPHS=0 keeps plain stream launches.
 void Engine::run_frame(prx_frame_stats* st) {
+    PRX_CUDA(cudaSetDevice(device_));
     if (st) std::memset(st, 0, sizeof(*st));
     frame_update_host();
     bool any_moved = false;
@@ -962,10 +1073,12 @@ void Engine::run_frame(prx_frame_stats* st) {
         verify_paths(nullptr);
         retrace_enqueue();
     };
-    auto it = graphs_on_ ? graphs_.find(sig) : graphs_.end();
+    // (sharded frames run plain launches: their exchanges call back into the collectives)
+    const bool graphs = graphs_on_ && !sharded();
+    auto it = graphs ? graphs_.find(sig) : graphs_.end();
     if (it != graphs_.end()) {
         launch_graph(it->second);
-    } else if (graphs_on_ && sig == last_sig_) {
+    } else if (graphs && sig == last_sig_) {
         FrameGraph g;
         if (capture_graph(plain, g)) graphs_[sig] = g;
     } else {
@@ -1034,6 +1147,8 @@ void Engine::launch_graph(const FrameGraph& g) {
 void Engine::run_stage(int stage, prx_frame_stats* st) {
     PRX_CUDA(cudaSetDevice(device_));
     const bool active = cfg_.mode != PRX_MODE_BASELINE && cur_frame_ > 0;
+    if (sharded() && (stage == PRX_STAGE_PRUNE || stage == PRX_STAGE_FILL))
+        throw std::logic_error("run_stage: prune/fill of a sharded engine run inside retrace_invalid / run_frame");
     prx_frame_stats tmp{};
     switch (stage) {
         case PRX_STAGE_UPDATE_ORIGINS:
@@ -1115,7 +1230,7 @@ void Engine::fill_apply(const uint64_t* dead_prefix, const uint64_t* dead_total,
 // ----------------------------------------------------------------------- splat
 void Engine::splat(const prx_camera* cam, float radius, int mode, float* rgb_host, float* rgb_dev,
                    prx_frame_stats* st) {
-    splat_store(path_dev(), cam, radius, mode, rgb_host, rgb_dev, st);
+    splat_store(path_dev(), cam, radius, mode, rgb_host, rgb_dev, st, sharded());
 }
 
 // gather_image(state, photons, aux, ...) over a host photon map (gather.hpp:81-83): the
@@ -1151,13 +1266,12 @@ void Engine::gather_photons(const void* photons, const void* aux, uint32_t n_pat
     P.pos_obj = store.as<float4>();
     P.energy = store.as<float4>() + second;
     d_gather_.reset();  // sized for this store
-    splat_store(P, cam, radius, mode, rgb_host, nullptr, nullptr);
+    splat_store(P, cam, radius, mode, rgb_host, nullptr, nullptr, false);
     d_gather_.reset();
-    if (d_splat_cand_.size() > 16 + 8ull * n_ * B_) d_splat_cand_.reset();
 }
 
 void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, int mode, float* rgb_host,
-                         float* rgb_dev, prx_frame_stats* st) {
+                         float* rgb_dev, prx_frame_stats* st, bool reduce_ranks) {
     PRX_CUDA(cudaSetDevice(device_));
     if (!(radius > 0.0f)) throw std::invalid_argument("gather: radius must be positive");
     if (mode != 0 && mode != 1) throw std::invalid_argument("splat: mode must be 0 (atomic splat) or 1 (ordered gather)");
@@ -1192,16 +1306,17 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
         img_h_ = c.height;
     }
     const uint64_t nv = static_cast<uint64_t>(P.n) * P.B;
-    if (d_splat_cand_.size() < 16 + 8 * nv) d_splat_cand_.alloc(16 + 8 * nv);
     const float inv_area = 1.0f / (static_cast<float>(M_PI) * radius * radius);
     const float inv_pi = 1.0f / static_cast<float>(M_PI);
-    if (mode == 1 && d_gather_.size() == 0) d_gather_.alloc(gather_work_bytes(nv, npx));
+    if (d_gather_.size() == 0) d_gather_.alloc(gather_work_bytes(nv, npx));  // both modes
     float* out = rgb_dev ? rgb_dev : d_img_.as<float>();
     const SceneDev S = scene_dev();
     // (plain launches: a captured graph of these ~25 launches measured slower, 1.93 vs 1.89 ms)
     record(kEvSplat0);
     launch_splat(S, P, C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, d_splat_work_.get(),
                  d_splat_cand_.get(), mode, d_gather_.get(), stream_);
+    if (reduce_ranks)  // every rank splats its own photons; the image is their sum
+        coll_ok(coll_.all_reduce_sum_f32(coll_.ctx, out, 3ull * npx, stream_), "image all-reduce");
     record(kEvSplat1);
     if (rgb_host)
         copy_async(rgb_host, out, 12ull * npx, cudaMemcpyDeviceToHost);

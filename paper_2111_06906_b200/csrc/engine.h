@@ -88,6 +88,7 @@ public:
     void set_frame_counter(int frames_run);
     void intersect_batch(const float* rays, size_t n, int any_hit, float* hits);
     void set_stream(cudaStream_t s);
+    void set_collectives(const prx_collectives* c);  // in-engine sharded frames (comm.cpp)
     void synchronize();
     void info(prx_engine_info* out) const;
     uint64_t launches() const { return launches_; }
@@ -102,6 +103,7 @@ private:
     void copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
     uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
     bool in_full_frame_ = false;  // retrace_invalid: prune/fill/trace back to back
+    bool in_sharded_frame_ = false;  // the counters of this read-back were summed over ranks
 
     struct LightBlock {
         const Light* light = nullptr;
@@ -112,6 +114,7 @@ private:
         LightPose pose_prev, pose_now;
         bool moved = false;
         DevBuf dm_t, dm_c, unm, seg_start;
+        DevBuf pref, tot;  // sharded prune: unmarked counts of the lower ranks / of all ranks
     };
     struct DynInfo {
         uint32_t obj = 0, tri_begin = 0, tri_count = 0, node_begin = kLbvhBrute, sah_root = kLbvhBrute;
@@ -143,11 +146,21 @@ private:
     void prune_mark_all();
     void prune_trim_all(uint32_t* const* prefix_tab, uint32_t* const* total_tab, const uint32_t* const* total_host);
     void fill_collect_dead();
-    void fill_assign_all(const uint64_t* prefix, const uint64_t* total);
+    void fill_assign_all(const uint64_t* prefix, const uint64_t* total, const uint64_t* prefix_dev = nullptr,
+                         const uint64_t* total_dev = nullptr);
+    // in-engine sharded frame (prx_collectives attached, world > 1)
+    // a collectives table is attached: the exchanges run (world 1 included: identity exchanges,
+    // which is how a one-GPU box exercises the NCCL backend end to end)
+    bool sharded() const { return coll_.world >= 1; }
+    void coll_ok(int rc, const char* what) const;
+    void exchange_dm();
+    void stage_prune_sharded();
+    void stage_fill_sharded();
+    void exchange_counters();
     void stage_trace();
     void read_back(prx_frame_stats* st, bool with_times);
     void splat_store(const PathDev& P, const prx_camera* cam, float radius, int mode, float* rgb_host,
-                     float* rgb_dev, prx_frame_stats* st);
+                     float* rgb_dev, prx_frame_stats* st, bool reduce_ranks);
     void record(int idx);
     double elapsed_ms(int a, int b);
     SceneDev scene_dev() const;
@@ -202,6 +215,10 @@ private:
     Counters* h_ctr_ = nullptr;
     uint32_t* h_cnt32_ = nullptr;
     uint32_t n_pruned_ = 0;
+    prx_collectives coll_{};                        // world 0: no table attached
+    DevBuf d_gath_, d_dead_g_, d_dead_pt_, d_ctr_sum_, d_cnt32_sum_;
+    Counters* h_ctr_sum_ = nullptr;                 // pinned: the all-rank sums read back
+    uint32_t* h_cnt32_sum_ = nullptr;
     uint32_t max_cells_ = 1;
 
     // splat buffers

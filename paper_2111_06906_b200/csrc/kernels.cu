@@ -9,7 +9,7 @@
 
 namespace prx {
 
-uint64_t g_launches = 0;
+std::atomic<uint64_t> g_launches{0};
 
 int launch_grid(uint64_t n, int threads) {
     const uint64_t blocks = (n + threads - 1) / threads;

@@ -5,12 +5,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "dev_types.h"
 
 namespace prx {
 
 int launch_grid(uint64_t n, int threads);
-extern uint64_t g_launches;  // kernels launched by this library (bench evidence)
+extern std::atomic<uint64_t> g_launches;  // kernels launched by this library (bench evidence, all engines of the process)
 
 // dm_t histogram of init_dm_target (light.cpp:230-252)
 void launch_init_dm_target(const LightDev* light_host, uint32_t n_samples, uint64_t seed_mix,

@@ -5,11 +5,13 @@
 // round is one coalesced 1 KiB access and element order within a tile is preserved.
 #include "prims.h"
 
+#include <atomic>
+
 #include <cstdio>
 
 namespace prx {
 
-extern uint64_t g_launches;  // kernels.cu: launches by this library (bench evidence)
+extern std::atomic<uint64_t> g_launches;  // kernels.cu: launches by this library (bench evidence)
 
 namespace {
 

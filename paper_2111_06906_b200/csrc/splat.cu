@@ -12,10 +12,15 @@
 //               summed per pixel in the reference's order -- one warp per pixel with staged
 //               in-order accumulation (k_gather_staged), or, for large images, one warp per 32
 //               pixels that share a home cell walking the shared candidates (k_gather_groups);
-//   mode 0 (fast, fp32 atomics): every photon probes the table with its own cell and adds its
-//               energy to the listed pixels with shared-memory atomics (k_splat_filter,
-//               k_splat); same contributing set, different summation order;
-//   resolve     L = sum(E) * albedo / pi / (pi r^2) (gather.cpp:71).
+//   mode 0 (atomic splat, fp32 atomics): the same candidate photons binned per cell without
+//               order (block-aggregated append + per-cell atomic counts, k_bin_filter; atomic
+//               cursors, k_bin_scatter), then splatted: for large images each 32-pixel group
+//               sharing a home cell keeps its accumulators in shared memory and every lane
+//               adds one photon's energy to the group pixels it reaches with shared-memory
+//               atomics (k_splat_tiles); small images / small groups use one warp per pixel with
+//               lane partial sums and a warp reduction (k_splat_pixels).  Same contributing
+//               set as gather_image, different fp32 summation order;
+//   both        L = sum(E) * albedo / pi / (pi r^2) (gather.cpp:71).
 #include <cstdlib>
 
 #include "device_scene.cuh"
@@ -89,75 +94,207 @@ __global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float 
     }
 }
 
-// K12b pass 1: stream every photon record once at full occupancy and keep only the photons
-// whose grid cell is registered by some pixel (most are not near any visible point).
-__global__ void __launch_bounds__(kT) k_splat_filter(PathDev P, float radius,
-                                                     const unsigned long long* __restrict__ keys, int bits,
-                                                     uint2* __restrict__ cand, uint32_t* __restrict__ n_cand) {
+// ---------------------------------------------------------------- mode 0: atomic splat
+// Binning without order: every live photon whose grid cell some pixel registered is appended
+// to a candidate list (block-aggregated: one global atomic per 256 photons) and counted per
+// cell (global atomics spread over the cells); the candidates are then scattered into per-cell
+// runs by atomic cursors (counting sort, any order inside a cell).
+__global__ void __launch_bounds__(kT) k_bin_filter(PathDev P, float radius, const unsigned long long* __restrict__ keys,
+                                                   int bits, uint2* __restrict__ cand, uint32_t* __restrict__ n_cand,
+                                                   uint32_t* __restrict__ pcnt) {
+    __shared__ uint32_t warp_n[kT / 32];
+    __shared__ uint32_t block_base;
     const uint32_t mask = (1u << bits) - 1u;
     const size_t total = (size_t)P.n * P.B;
-    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const float4 po = __ldcs(&P.pos_obj[kVS * (v)]);
-        if (__float_as_uint(po.w) == kInvalidObj) continue;
-        const unsigned long long key =
-            grid_key(cell_coord(po.x, radius), cell_coord(po.y, radius), cell_coord(po.z, radius));
-        uint32_t s = slot_of(key, bits);
-        unsigned long long k;
-        while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
-        if (k != key) continue;
-        const unsigned m = __activemask();
-        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(n_cand, (unsigned)__popc(m));
-        base = __shfl_sync(m, base, leader);
-        cand[base + __popc(m & ((1u << lane) - 1u))] = make_uint2((uint32_t)v, s);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (size_t t0 = (size_t)blockIdx.x * kT; t0 < total; t0 += (size_t)gridDim.x * kT) {  // block-uniform
+        const size_t v = t0 + threadIdx.x;
+        uint32_t s = 0;
+        bool hit = false;
+        if (v < total) {
+            const float4 po = __ldcs(&P.pos_obj[kVS * (v)]);
+            if (__float_as_uint(po.w) != kInvalidObj) {
+                const unsigned long long key =
+                    grid_key(cell_coord(po.x, radius), cell_coord(po.y, radius), cell_coord(po.z, radius));
+                s = slot_of(key, bits);
+                unsigned long long k;
+                while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
+                hit = k == key;
+            }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) warp_n[warp] = __popc(b);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t sum = 0;
+            for (int w = 0; w < kT / 32; ++w) {
+                const uint32_t c = warp_n[w];
+                warp_n[w] = sum;
+                sum += c;
+            }
+            block_base = sum ? atomicAdd(n_cand, sum) : 0u;
+        }
+        __syncthreads();
+        if (hit) {
+            cand[block_base + warp_n[warp] + __popc(b & ((1u << lane) - 1u))] = make_uint2((uint32_t)v, s);
+            atomicAdd(&pcnt[s], 1u);
+        }
+        __syncthreads();
     }
 }
 
-// K12b pass 2: every candidate photon against its cell's pixel list; reference filters
-// (same object, |x_ph - x_px|^2 <= r^2); energies added with shared-memory atomics into a
-// CTA-private image (global atomics when the image does not fit).
-template <bool kShared>
-__global__ void __launch_bounds__(kT) k_splat(PathDev P, uint32_t npx, float radius,
-                                              const float4* __restrict__ gbuf, const uint2* __restrict__ cand,
-                                              const uint32_t* __restrict__ n_cand, const uint32_t* __restrict__ cnt,
-                                              const uint32_t* __restrict__ off, const uint32_t* __restrict__ list,
-                                              float* __restrict__ img) {
-    extern __shared__ float simg[];
-    if (kShared) {
-        for (uint32_t k = threadIdx.x; k < 3 * npx; k += blockDim.x) simg[k] = 0.0f;
-        __syncthreads();
+__global__ void k_bin_scatter(PathDev P, const uint2* __restrict__ cand, const uint32_t* __restrict__ n_cand,
+                              const uint32_t* __restrict__ pstart, uint32_t* __restrict__ cursor, float4* __restrict__ spo,
+                              float4* __restrict__ sen) {
+    const uint32_t n = *n_cand;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint2 vs = cand[j];
+        const uint32_t at = __ldg(&pstart[vs.y]) + atomicAdd(&cursor[vs.y], 1u);
+        spo[at] = __ldg(&P.pos_obj[kVS * (vs.x)]);
+        sen[at] = __ldg(&P.energy[kVS * (vs.x)]);
     }
-    float* acc = kShared ? simg : img;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Per-pixel accumulation, any order: one warp per pixel (work counter), lanes test 32
+// candidates at a time and keep per-lane partial sums, one warp reduction per pixel.
+__global__ void __launch_bounds__(kT) k_splat_pixels(const float4* __restrict__ gbuf, uint32_t npx, float radius,
+                                                     const unsigned long long* __restrict__ keys, int bits,
+                                                     const uint32_t* __restrict__ pstart,
+                                                     const uint32_t* __restrict__ pcnt, const float4* __restrict__ spo,
+                                                     const float4* __restrict__ sen, const float4* __restrict__ mat,
+                                                     float inv_pi, float inv_area, uint32_t* work,
+                                                     float* __restrict__ img, const uint32_t* __restrict__ pix_list,
+                                                     const uint32_t* pix_count) {
+    const uint32_t n_items = pix_list ? *pix_count : npx;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t mask = (1u << bits) - 1u;
     const float r2 = radius * radius;
-    const uint32_t nc = *n_cand;
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
-        const uint2 vs = cand[c];
-        const float4 po = __ldg(&P.pos_obj[kVS * (vs.x)]);
-        const uint32_t obj = __float_as_uint(po.w);
-        const uint32_t n = __ldg(&cnt[vs.y]), o = __ldg(&off[vs.y]);
-        float4 en;
-        bool have_en = false;
-        for (uint32_t j = 0; j < n; ++j) {
-            const uint32_t pix = __ldg(&list[o + j]);
-            const float4 g = __ldg(&gbuf[pix]);
-            if (__float_as_uint(g.w) != obj) continue;
-            const V3 d = sub(V3{po.x, po.y, po.z}, V3{g.x, g.y, g.z});  // gather.hpp:54
-            if (dot(d, d) > r2) continue;
-            if (!have_en) {
-                en = __ldg(&P.energy[kVS * (vs.x)]);
-                have_en = true;
+    while (true) {
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(work, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items) break;
+        const uint32_t pix = pix_list ? pix_list[item] : item;
+        const float4 g = gbuf[pix];
+        const uint32_t obj = __float_as_uint(g.w);
+        if (obj == kInvalidObj) {
+            if (lane < 3) img[3 * pix + lane] = 0.0f;
+            continue;
+        }
+        const V3 x{g.x, g.y, g.z};
+        const long long cx = cell_coord(g.x, radius), cy = cell_coord(g.y, radius), cz = cell_coord(g.z, radius);
+        float ax = 0.0f, ay = 0.0f, az = 0.0f;
+        for (int o = 0; o < 27; ++o) {
+            const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+            const unsigned long long key = grid_key(cx + dx, cy + dy, cz + dz);
+            uint32_t s = slot_of(key, bits);
+            unsigned long long k;
+            while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
+            if (k != key) continue;
+            const uint32_t b0 = __ldg(&pstart[s]), n = __ldg(&pcnt[s]);
+            for (uint32_t j = lane; j < n; j += 32) {
+                const float4 po = __ldg(&spo[b0 + j]);
+                const V3 d = sub(V3{po.x, po.y, po.z}, x);  // gather.hpp:54
+                if (dot(d, d) <= r2 && __float_as_uint(po.w) == obj) {
+                    const float4 e = __ldg(&sen[b0 + j]);
+                    ax += e.x;
+                    ay += e.y;
+                    az += e.z;
+                }
             }
-            atomicAdd(&acc[3 * pix], en.x);
-            atomicAdd(&acc[3 * pix + 1], en.y);
-            atomicAdd(&acc[3 * pix + 2], en.z);
+        }
+        ax = warp_sum(ax);
+        ay = warp_sum(ay);
+        az = warp_sum(az);
+        if (lane == 0) {
+            const float4 a = mat[obj];
+            img[3 * pix] = ((ax * a.x) * inv_pi) * inv_area;  // gather.cpp:71
+            img[3 * pix + 1] = ((ay * a.y) * inv_pi) * inv_area;
+            img[3 * pix + 2] = ((az * a.z) * inv_pi) * inv_area;
         }
     }
-    if (kShared) {
-        __syncthreads();
-        for (uint32_t k2 = threadIdx.x; k2 < 3 * npx; k2 += blockDim.x) {
-            const float s2 = simg[k2];
-            if (s2 != 0.0f) atomicAdd(&img[k2], s2);
+}
+
+// Tiled splat for pixel groups (large images): one warp per chunk of <= 32 pixels sharing a
+// home cell (so the same 27 cells).  The chunk's hit points and fp32 accumulators live in
+// shared memory; each lane takes one candidate photon of a 32-photon slab and splats it onto
+// the chunk's pixels it reaches (same object, |x_ph - x_px|^2 <= r^2) with shared-memory
+// atomics, walking the pixels from a lane-rotated start so concurrent adds hit different
+// addresses.
+__global__ void __launch_bounds__(kT) k_splat_tiles(const float4* __restrict__ gbuf, float radius,
+                                                    const unsigned long long* __restrict__ keys, int bits,
+                                                    const uint32_t* __restrict__ pstart,
+                                                    const uint32_t* __restrict__ pcnt, const float4* __restrict__ spo,
+                                                    const float4* __restrict__ sen, const float4* __restrict__ mat,
+                                                    float inv_pi, float inv_area, const uint2* __restrict__ chunks,
+                                                    const uint32_t* n_chunks, const uint32_t* __restrict__ pv,
+                                                    uint32_t* work, float* __restrict__ img) {
+    __shared__ float4 s_px[kT];       // per warp: its pixels' hit points {x, obj}
+    __shared__ float s_acc[kT * 3];   // per warp: 32 pixels x 3 channels
+    const uint32_t lane = threadIdx.x & 31;
+    float4* const wpx = s_px + (threadIdx.x & ~31u);
+    float* const wacc = s_acc + 3 * (threadIdx.x & ~31u);
+    const uint32_t mask = (1u << bits) - 1u;
+    const float r2 = radius * radius;
+    const uint32_t nch = *n_chunks;
+    while (true) {
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(work, 1u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= nch) break;
+        const uint2 ch = chunks[c];
+        const uint32_t m = ch.y;
+        __syncwarp();
+        if (lane < m) wpx[lane] = gbuf[pv[ch.x + lane]];
+        wacc[lane] = 0.0f;
+        wacc[32 + lane] = 0.0f;
+        wacc[64 + lane] = 0.0f;
+        __syncwarp();
+        const float4 g0 = wpx[0];
+        const uint32_t lane0 = lane % m;
+        const long long cx = cell_coord(g0.x, radius), cy = cell_coord(g0.y, radius), cz = cell_coord(g0.z, radius);
+        for (int o = 0; o < 27; ++o) {
+            const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+            const unsigned long long key = grid_key(cx + dx, cy + dy, cz + dz);
+            uint32_t s = slot_of(key, bits);
+            unsigned long long k;
+            while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
+            if (k != key) continue;
+            const uint32_t b0 = __ldg(&pstart[s]), n = __ldg(&pcnt[s]);
+            for (uint32_t j = lane; j < n; j += 32) {
+                const float4 po = __ldg(&spo[b0 + j]);
+                const uint32_t obj = __float_as_uint(po.w);
+                float4 e;
+                bool have = false;
+                uint32_t t = lane0;  // lane-rotated pixel walk (no per-step modulo)
+                for (uint32_t q = 0; q < m; ++q, t = t + 1 == m ? 0u : t + 1) {
+                    const float4 px = wpx[t];
+                    const V3 d = sub(V3{po.x, po.y, po.z}, V3{px.x, px.y, px.z});  // gather.hpp:54
+                    if (__float_as_uint(px.w) != obj || dot(d, d) > r2) continue;
+                    if (!have) {
+                        e = __ldg(&sen[b0 + j]);
+                        have = true;
+                    }
+                    atomicAdd(&wacc[3 * t], e.x);
+                    atomicAdd(&wacc[3 * t + 1], e.y);
+                    atomicAdd(&wacc[3 * t + 2], e.z);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane < m) {
+            const float4 px = wpx[lane];
+            const uint32_t pix = pv[ch.x + lane];
+            const float4 a = mat[__float_as_uint(px.w)];
+            img[3 * pix] = ((wacc[3 * lane] * a.x) * inv_pi) * inv_area;  // gather.cpp:71
+            img[3 * pix + 1] = ((wacc[3 * lane + 1] * a.y) * inv_pi) * inv_area;
+            img[3 * pix + 2] = ((wacc[3 * lane + 2] * a.z) * inv_pi) * inv_area;
         }
     }
 }
@@ -430,23 +567,6 @@ __global__ void __launch_bounds__(kT) k_gather_groups(const float4* __restrict__
     }
 }
 
-__global__ void k_resolve(const float4* __restrict__ gbuf, const float4* __restrict__ mat, float* img, uint32_t n,
-                          float inv_pi, float inv_area) {
-    for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < n; pix += gridDim.x * blockDim.x) {
-        const uint32_t obj = __float_as_uint(gbuf[pix].w);
-        if (obj == kInvalidObj) {
-            img[3 * pix] = img[3 * pix + 1] = img[3 * pix + 2] = 0.0f;
-            continue;
-        }
-        const float4 a = mat[obj];
-        const V3 rad{img[3 * pix], img[3 * pix + 1], img[3 * pix + 2]};
-        const V3 out = mul(mul(mulv(rad, V3{a.x, a.y, a.z}), inv_pi), inv_area);  // gather.cpp:71
-        img[3 * pix] = out.x;
-        img[3 * pix + 1] = out.y;
-        img[3 * pix + 2] = out.z;
-    }
-}
-
 }  // namespace
 
 int splat_table_bits(uint32_t npx) {
@@ -466,7 +586,7 @@ size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
     const uint64_t nv = n_vertices;
     uint64_t scan_n = nv > slots ? nv : slots;
     if (npx > scan_n) scan_n = npx;
-    return 64 + nv * (1 + 4 + 4 + 16 + 32) + slots * 8 + 41ull * npx + 2 * prim_scratch_bytes(scan_n) + 32 * 256;
+    return 64 + nv * (1 + 4 + 4 + 16 + 32) + slots * 12 + 41ull * npx + 2 * prim_scratch_bytes(scan_n) + 64 * 256;
 }
 
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
@@ -475,29 +595,89 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
     const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
     auto* keys = static_cast<unsigned long long*>(work);
-    auto* cnt = reinterpret_cast<uint32_t*>(keys + slots);
-    uint32_t* off = cnt + slots;
-    uint32_t* cursor = off + slots;
-    uint32_t* list = cursor + slots;
-    void* scratch = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(list + 27ull * npx) + 255) & ~uintptr_t(255));
+    auto* cnt = reinterpret_cast<uint32_t*>(keys + slots);  // pixels per registered cell
+    (void)cand_buf;
 
     k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
     cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
     cudaMemsetAsync(cnt, 0, 4 * slots, st);
-    cudaMemsetAsync(cursor, 0, 4 * slots, st);
     k_pixcells<false><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, nullptr, nullptr,
                                                                   nullptr, bits);
     g_launches += 2;  // gbuffer, pixcells
-    if (mode == 1) {  // ordered, bit-exact gather
-        const uint64_t nv = (uint64_t)P.n * P.B;
-        // carve the work buffer in 256-byte aligned pieces (float4 / u32 views of any n)
-        char* w = static_cast<char*>(gather_buf);
-        auto take = [&](size_t bytes) {
-            char* p = w;
-            w += (bytes + 255) & ~size_t(255);
-            return p;
-        };
-        uint32_t* m_count = reinterpret_cast<uint32_t*>(take(64));
+    const uint64_t nv = (uint64_t)P.n * P.B;
+    // carve the work buffer in 256-byte aligned pieces (float4 / u32 views of any n)
+    char* w = static_cast<char*>(gather_buf);
+    auto take = [&](size_t bytes) {
+        char* p = w;
+        w += (bytes + 255) & ~size_t(255);
+        return p;
+    };
+    uint32_t* m_count = reinterpret_cast<uint32_t*>(take(64));
+    // Large images: pixels grouped by home cell (sorted), groups of >= kGroupMin pixels cut in
+    // 32-pixel chunks, the rest walked per pixel.  Small images go straight to the per-pixel walk.
+    const char* genv = std::getenv("PRX_GATHER_GROUPS");
+    const bool groups = genv ? genv[0] == '1' : npx >= (1u << 18);
+    struct Groups {
+        uint32_t *pv, *small, *ctl;
+        uint2* chunks;
+    };
+    auto group_pixels = [&](void* gscratch_unused) {
+        (void)gscratch_unused;
+        Groups G{};
+        uint32_t* hk = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        G.pv = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        uint32_t* hk2 = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        uint32_t* pv2 = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        uint8_t* head = reinterpret_cast<uint8_t*>(take(npx));
+        uint32_t* starts = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        G.chunks = reinterpret_cast<uint2*>(take(8ull * npx));
+        G.small = reinterpret_cast<uint32_t*>(take(4ull * npx));
+        void* gscratch2 = take(0);
+        G.ctl = m_count + 4;  // [0] group count, [1] chunks, [2] small, [3] / [4] work counters
+        cudaMemsetAsync(G.ctl, 0, 5 * 4, st);
+        k_pixel_home<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, hk, G.pv);
+        radix_sort_pairs(hk, G.pv, hk2, pv2, npx, nullptr, bits + 1, gscratch2, st);
+        k_group_heads<<<launch_grid(npx, kT), kT, 0, st>>>(hk, npx, head);
+        compact_u8(head, npx, nullptr, 0, starts, G.ctl + 0, gscratch2, st);
+        k_group_split<<<launch_grid(npx, kT), kT, 0, st>>>(starts, G.ctl + 0, npx, hk, G.pv, bits, G.chunks, G.ctl + 1,
+                                                         G.small, G.ctl + 2);
+        g_launches += 3;  // home, heads, split (the prims count their own)
+        return G;
+    };
+    if (mode == 0) {  // atomic splat: unordered binning + tiled shared-memory atomics
+        uint2* cand = reinterpret_cast<uint2*>(take(8 * nv));
+        float4* spo = reinterpret_cast<float4*>(take(16 * nv));
+        float4* sen = reinterpret_cast<float4*>(take(16 * nv));
+        uint32_t* pcnt = reinterpret_cast<uint32_t*>(take(4 * slots));
+        uint32_t* pstart = reinterpret_cast<uint32_t*>(take(4 * slots));
+        uint32_t* pcur = reinterpret_cast<uint32_t*>(take(4 * slots));
+        void* gscratch = take(0);
+        cudaMemsetAsync(m_count, 0, 64, st);
+        cudaMemsetAsync(pcnt, 0, 4 * slots, st);
+        cudaMemsetAsync(pcur, 0, 4 * slots, st);
+        k_bin_filter<<<launch_grid(nv, kT), kT, 0, st>>>(P, radius, keys, bits, cand, m_count, pcnt);
+        scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
+        k_bin_scatter<<<launch_grid(nv, kT), kT, 0, st>>>(P, cand, m_count, pstart, pcur, spo, sen);
+        g_launches += 2;  // filter, scatter
+        if (!groups) {
+            uint32_t* wq = m_count + 4;  // zeroed above
+            k_splat_pixels<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt,
+                                                                        spo, sen, S.mat, inv_pi, inv_area, wq, img,
+                                                                        nullptr, nullptr);
+            ++g_launches;
+            return;
+        }
+        const Groups G = group_pixels(gscratch);
+        k_splat_tiles<<<launch_grid(32ull * npx / 8 + 32, kT), kT, 0, st>>>(gbuf, radius, keys, bits, pstart, pcnt, spo,
+                                                                           sen, S.mat, inv_pi, inv_area, G.chunks,
+                                                                           G.ctl + 1, G.pv, G.ctl + 3, img);
+        k_splat_pixels<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt, spo,
+                                                                    sen, S.mat, inv_pi, inv_area, G.ctl + 4, img,
+                                                                    G.small, G.ctl + 2);
+        g_launches += 2;
+        return;
+    }
+    {  // mode 1: ordered, bit-exact gather
         uint32_t* pslot = reinterpret_cast<uint32_t*>(take(4 * nv));
         uint32_t* cand = reinterpret_cast<uint32_t*>(take(4 * nv));
         uint32_t* sk = reinterpret_cast<uint32_t*>(take(4 * nv));
@@ -518,10 +698,6 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
         k_gather_copy<<<launch_grid(nv, kT), kT, 0, st>>>(P, sv, m_count, spo, sen);
         g_launches += 3;  // flag, keys, copy (the prims count their own)
-        // Large images: pixel groups by home cell (sorted), big groups in 32-pixel chunks, the
-        // rest per pixel.  Small images (few pixels per cell) go straight to the per-pixel walk.
-        const char* genv = std::getenv("PRX_GATHER_GROUPS");
-        const bool groups = genv ? genv[0] == '1' : npx >= (1u << 18);
         if (!groups) {
             uint32_t* wq = m_count + 4;
             cudaMemsetAsync(wq, 0, 4, st);
@@ -531,53 +707,15 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
             ++g_launches;
             return;
         }
-        uint32_t* hk = reinterpret_cast<uint32_t*>(take(4ull * npx));
-        uint32_t* pv = reinterpret_cast<uint32_t*>(take(4ull * npx));
-        uint32_t* hk2 = reinterpret_cast<uint32_t*>(take(4ull * npx));
-        uint32_t* pv2 = reinterpret_cast<uint32_t*>(take(4ull * npx));
-        uint8_t* head = reinterpret_cast<uint8_t*>(take(npx));
-        uint32_t* starts = reinterpret_cast<uint32_t*>(take(4ull * npx));
-        uint2* chunks = reinterpret_cast<uint2*>(take(8ull * npx));
-        uint32_t* small = reinterpret_cast<uint32_t*>(take(4ull * npx));
-        void* gscratch2 = take(0);
-        uint32_t* ctl = m_count + 4;  // [0] group count, [1] chunks, [2] small, [3] / [4] work counters
-        cudaMemsetAsync(ctl, 0, 5 * 4, st);
-        k_pixel_home<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, hk, pv);
-        radix_sort_pairs(hk, pv, hk2, pv2, npx, nullptr, bits + 1, gscratch2, st);
-        k_group_heads<<<launch_grid(npx, kT), kT, 0, st>>>(hk, npx, head);
-        compact_u8(head, npx, nullptr, 0, starts, ctl + 0, gscratch2, st);
-        k_group_split<<<launch_grid(npx, kT), kT, 0, st>>>(starts, ctl + 0, npx, hk, pv, bits, chunks, ctl + 1, small,
-                                                         ctl + 2);
+        const Groups G = group_pixels(gscratch);
         k_gather_groups<<<launch_grid(32ull * npx / 8 + 32, kT), kT, 0, st>>>(
-            gbuf, radius, keys, bits, pstart, pcnt, spo, sen, S.mat, inv_pi, inv_area, chunks, ctl + 1, pv, ctl + 3,
-            img);
+            gbuf, radius, keys, bits, pstart, pcnt, spo, sen, S.mat, inv_pi, inv_area, G.chunks, G.ctl + 1, G.pv,
+            G.ctl + 3, img);
         k_gather_staged<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt, spo,
-                                                                     sen, S.mat, inv_pi, inv_area, ctl + 4, img, small,
-                                                                     ctl + 2);
-        g_launches += 5;  // home, heads, split, groups, staged
-        return;
+                                                                     sen, S.mat, inv_pi, inv_area, G.ctl + 4, img,
+                                                                     G.small, G.ctl + 2);
+        g_launches += 2;  // groups, staged
     }
-    scan_exclusive_u32(cnt, off, (uint32_t)slots, nullptr, nullptr, scratch, st);
-    k_pixcells<true><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, off, cursor, list,
-                                                                 bits);
-    uint32_t* n_cand = static_cast<uint32_t*>(cand_buf);
-    uint2* cand = reinterpret_cast<uint2*>(static_cast<char*>(cand_buf) + 16);
-    cudaMemsetAsync(n_cand, 0, 4, st);
-    k_splat_filter<<<launch_grid((uint64_t)P.n * P.B, kT), kT, 0, st>>>(P, radius, keys, bits, cand, n_cand);
-    cudaMemsetAsync(img, 0, 12ull * npx, st);
-    const size_t smem = 12ull * npx;
-    int dev = 0, n_sm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (smem <= 200u * 1024u) {
-        cudaFuncSetAttribute(k_splat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_splat<true><<<n_sm, kT, smem, st>>>(P, npx, radius, gbuf, cand, n_cand, cnt, off, list, img);
-    } else {
-        k_splat<false><<<launch_grid((uint64_t)P.n * P.B, kT), kT, 0, st>>>(P, npx, radius, gbuf, cand, n_cand, cnt,
-                                                                           off, list, img);
-    }
-    k_resolve<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, S.mat, img, npx, inv_pi, inv_area);
-    g_launches += 4;  // pixcells, filter, splat, resolve
 }
 
 }  // namespace prx

@@ -13,9 +13,14 @@ replicated; the only cross-rank data of a frame are
 and, for the image, the per-rank splat buffers (reduce).  With these exchanges every rank
 computes exactly what the single-engine reference computes for its slice.
 
-The frame is written as phases over an *executor* (one shard) so the same protocol runs
-with real collectives (torch.distributed: NCCL on B200, gloo on CPU) or with an
-in-process loopback over several executors (several shards on one device).
+Two drivers of the same protocol:
+  * in-engine (the product path): an engine with a collectives table (Communicator: NCCL,
+    or the in-process local backend of EngineGroup) enqueues every exchange on its own
+    stream inside prx_run_frame / prx_splat -- one host read-back per frame;
+  * host-phased (run_frame_distributed / run_frame_loopback): the frame written as phases
+    over an *executor* (one shard, the C engine's prx_prune_count/apply, prx_fill_count/apply
+    entry points, or the C oracle port in the gloo CPU tests) with torch.distributed
+    collectives between the phases -- the protocol's CPU test harness.
 """
 from __future__ import annotations
 
@@ -244,58 +249,130 @@ def run_frame_loopback(exs: List, frame: int) -> dict:
     return _stats_from(total.tolist(), frame, exs[0].mode)
 
 
-class ShardedEngine:
-    """User-facing sharded engine: one rank's slice of a multi-GPU path store."""
+# ------------------------------------------------------------------ in-engine collectives
+class Communicator:
+    """prx_comm (include/prx.h): a collectives table for in-engine sharded frames.
 
-    def __init__(self, scene: Scene, rank: int, world: int, device: int = 0, group=None, **cfg):
-        import torch
+    nccl():        one rank of an NCCL communicator (libnccl loaded by _prx.so at run time);
+    local_group(): `world` in-process communicators, one per host thread / shard.
+    """
 
-        n = cfg.get("paths", 10000)
-        self.config = make_config(shard=shard_range(n, rank, world), device=device, **cfg)
-        self.exec = GpuExecutor(scene, self.config, torch.cuda.current_stream(device))
-        self.coll = TorchCollectives(group) if world > 1 else None
-        self.frame = 0
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
 
-    def run_frame(self) -> dict:
-        if self.coll is None:
-            st = self.exec.engine.run_frame()
-            self.frame += 1
-            d = {k: getattr(st, k) for k in L.FrameStats.COUNTS}
-            d.update(frame=st.frame, mode=L.MODE_NAMES[st.mode])
-            return d
-        out = run_frame_distributed(self.exec, self.coll, self.frame)
-        self.frame += 1
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            L.lib().prx_comm_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        L.check(L.lib().prx_comm_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, rank: int, world: int, device: int) -> "Communicator":
+        buf = (C.c_uint8 * 128)(*unique_id)
+        h = C.c_void_p()
+        L.check(L.lib().prx_comm_nccl_create(buf, int(rank), int(world), int(device), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def local_group(cls, world: int) -> list:
+        arr = (C.c_void_p * world)()
+        L.check(L.lib().prx_comm_local_create(int(world), arr))
+        return [cls(arr[r]) for r in range(world)]
+
+    def collectives(self) -> L.Collectives:
+        out = L.Collectives()
+        L.check(L.lib().prx_comm_collectives(self._h, C.byref(out)))
         return out
 
 
-class MultiGpuEngine:
-    """One process driving path shards on several GPUs (the reference's single Engine object
-    over N devices): the exchange protocol of run_frame_distributed run in-process
-    (run_frame_loopback), the image summed over the shards.  Frames and images are
-    bit-identical to one engine except the fp32 image sum order across shards."""
+def attach(engine: Engine, comm: Communicator) -> None:
+    """Make `engine` (one rank's path shard) run sharded frames over `comm` in-engine."""
+    L.check(L.lib().prx_engine_set_collectives(engine.handle, C.byref(comm.collectives())))
+    engine._comm = comm  # keep the communicator alive as long as the engine uses it
+
+
+class EngineGroup:
+    """One process, `world` path shards (on `devices`; several may share one device), each
+    driven by its own host thread; the exchanges run inside the engines over the local
+    collectives backend (comm.cpp), so a sharded frame is each engine's own prx_run_frame with
+    one host read-back.  Frames are bit-identical to one engine; the image is the sum of the
+    per-shard splats (fp32 order differs across shards)."""
+
+    def __init__(self, scene: Scene, devices: Sequence[int], **cfg):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.world = len(devices)
+        n = cfg.get("paths", 10000)
+        self.engines = [Engine(scene, make_config(shard=shard_range(n, r, self.world), device=d, **cfg))
+                        for r, d in enumerate(devices)]
+        self.comms = Communicator.local_group(self.world)
+        for e, c in zip(self.engines, self.comms):
+            attach(e, c)
+        self.pool = ThreadPoolExecutor(max_workers=self.world)
+
+    def _all(self, fn):
+        return list(self.pool.map(fn, self.engines))  # collective: every shard in its own thread
+
+    def run_frame(self) -> L.FrameStats:
+        return self._all(lambda e: e.run_frame())[0]  # all-rank sums, identical on every shard
+
+    def splat(self, camera=None, radius: float = 0.25, mode: int = 1) -> np.ndarray:
+        return self._all(lambda e: e.splat(camera=camera, radius=radius, mode=mode))[0]
+
+    def close(self):
+        self.pool.shutdown()
+        for e in self.engines:
+            e.close()
+
+
+class ShardedEngine:
+    """User-facing sharded engine: this rank's slice of a multi-GPU path store, one process per
+    GPU (torch.distributed initialised).  The exchanges run inside the engine over NCCL; the
+    NCCL unique id travels through torch.distributed once."""
+
+    def __init__(self, scene: Scene, rank: int, world: int, device: int = 0, group=None, **cfg):
+        import torch.distributed as dist
+
+        n = cfg.get("paths", 10000)
+        self.config = make_config(shard=shard_range(n, rank, world), device=device, **cfg)
+        self.engine = Engine(scene, self.config)
+        self.comm = None
+        if world > 1:
+            obj = [Communicator.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            self.comm = Communicator.nccl(obj[0], rank, world, device)
+            attach(self.engine, self.comm)
+
+    def run_frame(self) -> dict:
+        st = self.engine.run_frame()
+        d = {k: getattr(st, k) for k in L.FrameStats.COUNTS}
+        d.update(frame=st.frame, mode=L.MODE_NAMES[st.mode])
+        return d
+
+    def splat(self, camera=None, radius: float = 0.25, mode: int = 1) -> np.ndarray:
+        return self.engine.splat(camera=camera, radius=radius, mode=mode)
+
+
+class MultiGpuEngine(EngineGroup):
+    """One process driving path shards on several GPUs (default: every visible device; shards
+    share the device when there is one) -- the reference's single Engine object over N GPUs."""
 
     def __init__(self, scene: Scene, devices: Sequence[int] | None = None, **cfg):
         import torch
 
-        self.torch = torch
         devs = list(devices) if devices is not None else list(range(torch.cuda.device_count()))
-        n = cfg.get("paths", 10000)
-        self.execs = []
-        for r, dev in enumerate(devs):
-            c = make_config(shard=shard_range(n, r, len(devs)), device=dev, **cfg)
-            with torch.cuda.device(dev):
-                self.execs.append(GpuExecutor(scene, c, torch.cuda.current_stream(dev)))
-        self.frame = 0
+        super().__init__(scene, devs, **cfg)
 
     def run_frame(self) -> dict:
-        out = run_frame_loopback(self.execs, self.frame)
-        self.frame += 1
-        return out
-
-    def splat(self, camera=None, radius: float = 0.25, mode: int = 1):
-        """Per-shard photons splatted on each device, summed on the host (float64 then fp32)."""
-        imgs = [ex.engine.splat(camera=camera, radius=radius, mode=mode) for ex in self.execs]
-        total = imgs[0].astype(np.float64)
-        for im in imgs[1:]:
-            total += im
-        return total.astype(np.float32)
+        st = super().run_frame()
+        d = {k: getattr(st, k) for k in L.FrameStats.COUNTS}
+        d.update(frame=st.frame, mode=L.MODE_NAMES[st.mode])
+        return d

@@ -62,3 +62,64 @@ def test_multi_gpu_engine_matches_single_engine():
     img_multi = multi.splat(radius=0.25)
     assert np.allclose(img_multi, img_single, rtol=1e-4, atol=0)  # shard sums reorder the fp32 adds
     assert np.array_equal(img_multi == 0, img_single == 0)
+
+
+# ---- in-engine sharded frames (collectives enqueued by the engine itself, comm.cpp)
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("scene,mode,synthetic", [("moving-cube", "error", False), ("parallel-spot", "naive", False),
+                                                  ("villa-analog", "naive", False), ("moving-cube", "baseline", False),
+                                                  ("C4", "error", True)])
+def test_engine_group_matches_single_engine(world, scene, mode, synthetic):
+    from paper_2111_06906_b200.distributed import EngineGroup
+
+    cfg = dict(mode=mode, paths=6001, bounces=6, dm=[2, 2, 8, 8], seed=7)
+    sc = pr.Scene.synthetic(scene) if synthetic else pr.Scene.builtin(scene)
+    single = pr.Engine(sc, pr.make_config(**cfg))
+    group = EngineGroup(sc, [0] * world, **cfg)
+    B, N = cfg["bounces"], cfg["paths"]
+    for f in range(4):
+        st = single.run_frame()
+        got = group.run_frame()
+        for k in ("rays_traced", "rays_reused", "paths_replaced", "paths_pruned", "paths_filled", "visibility_rays",
+                  "live_segments_before", "paths_retraced"):
+            assert getattr(got, k) == getattr(st, k), (f, k)
+        for fld in FIELDS:
+            ref = single.download(fld)
+            parts = [e.download(fld) for e in group.engines]
+            if fld == "photons":
+                cat = np.concatenate([p.reshape(B, -1) for p in parts], axis=1)
+                ref = ref.reshape(B, N)
+            else:
+                cat = np.concatenate(parts, axis=0)
+            assert cat.tobytes() == ref.tobytes(), (f, fld)
+        for li in range(single.info().n_lights):
+            for e in group.engines:
+                assert np.array_equal(e.download("dm_current", li), single.download("dm_current", li))
+    img_g, img_s = group.splat(radius=0.25), single.splat(radius=0.25)
+    assert np.array_equal(img_g == 0, img_s == 0)
+    assert np.allclose(img_g, img_s, rtol=1e-5, atol=0)  # per-shard sums, then the rank sum
+    group.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("backend", ["nccl", "local"])
+def test_world1_collectives_bit_exact(backend):
+    """One rank with a collectives table runs every exchange (identity sums): through NCCL
+    (libnccl loaded at run time) and the local backend the frames and the image are the
+    unsharded engine's, bit for bit."""
+    from paper_2111_06906_b200.distributed import Communicator, attach
+
+    cfg = dict(mode="error", paths=8000, bounces=5, dm=[2, 2, 8, 8], seed=5)
+    sc = pr.Scene.builtin("villa-analog")
+    single = pr.Engine(sc, pr.make_config(**cfg))
+    eng = pr.Engine(sc, pr.make_config(**cfg))
+    comm = (Communicator.nccl(Communicator.nccl_unique_id(), 0, 1, 0) if backend == "nccl"
+            else Communicator.local_group(1)[0])
+    attach(eng, comm)
+    for f in range(4):
+        a, b = eng.run_frame(), single.run_frame()
+        for k in ("rays_traced", "rays_reused", "paths_pruned", "paths_filled", "visibility_rays"):
+            assert getattr(a, k) == getattr(b, k), (f, k)
+    assert eng.download("photons").tobytes() == single.download("photons").tobytes()
+    assert eng.splat(radius=0.25).tobytes() == single.splat(radius=0.25).tobytes()
