@@ -13,13 +13,14 @@
 //               in-order accumulation (k_gather_staged), or, for large images, one warp per 32
 //               pixels that share a home cell walking the shared candidates (k_gather_groups);
 //   mode 0 (atomic splat, fp32 atomics): the same candidate photons binned per cell without
-//               order (block-aggregated append + per-cell atomic counts, k_bin_filter; atomic
-//               cursors, k_bin_scatter), then splatted: for large images each 32-pixel group
-//               sharing a home cell keeps its accumulators in shared memory and every lane
-//               adds one photon's energy to the group pixels it reaches with shared-memory
-//               atomics (k_splat_tiles); small images / small groups use one warp per pixel with
-//               lane partial sums and a warp reduction (k_splat_pixels).  Same contributing
-//               set as gather_image, different fp32 summation order;
+//               order -- block-aggregated append + per-cell atomic counts (k_bin_filter), atomic
+//               cursors (k_bin_scatter): no stable sort, no candidate compaction pass -- then
+//               accumulated in any order: one warp per pixel with lane partial sums and a warp
+//               reduction (k_splat_pixels); for large images 32-pixel groups sharing a home cell
+//               with register accumulators over shared photon slabs (k_gather_groups), or
+//               (PRX_SPLAT_TILES=1) photon-parallel tiles adding into shared-memory pixel
+//               accumulators with shared-memory atomics (k_splat_tiles, measured slower).  Same
+//               contributing set as gather_image, different fp32 summation order;
 //   both        L = sum(E) * albedo / pi / (pi r^2) (gather.cpp:71).
 #include <cstdlib>
 
@@ -668,9 +669,18 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
             return;
         }
         const Groups G = group_pixels(gscratch);
-        k_splat_tiles<<<launch_grid(32ull * npx / 8 + 32, kT), kT, 0, st>>>(gbuf, radius, keys, bits, pstart, pcnt, spo,
-                                                                           sen, S.mat, inv_pi, inv_area, G.chunks,
-                                                                           G.ctl + 1, G.pv, G.ctl + 3, img);
+        // 32-pixel groups: lanes own pixels and accumulate in registers over the shared photon
+        // slabs (k_gather_groups) -- measured 3x faster at 1920x1080 than the photon-parallel
+        // shared-memory-atomic tiles (k_splat_tiles, PRX_SPLAT_TILES=1; profiles/r02_sweeps.md)
+        const char* tenv = std::getenv("PRX_SPLAT_TILES");
+        if (tenv && tenv[0] == '1')
+            k_splat_tiles<<<launch_grid(32ull * npx / 8 + 32, kT), kT, 0, st>>>(gbuf, radius, keys, bits, pstart, pcnt,
+                                                                               spo, sen, S.mat, inv_pi, inv_area,
+                                                                               G.chunks, G.ctl + 1, G.pv, G.ctl + 3, img);
+        else
+            k_gather_groups<<<launch_grid(32ull * npx / 8 + 32, kT), kT, 0, st>>>(
+                gbuf, radius, keys, bits, pstart, pcnt, spo, sen, S.mat, inv_pi, inv_area, G.chunks, G.ctl + 1, G.pv,
+                G.ctl + 3, img);
         k_splat_pixels<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt, spo,
                                                                     sen, S.mat, inv_pi, inv_area, G.ctl + 4, img,
                                                                     G.small, G.ctl + 2);

@@ -132,3 +132,21 @@ def test_ordered_gather_pixel_groups(monkeypatch, groups, w, h):
     cam = gpu.scene.describe().camera
     c = L.Camera(cam.position, cam.look_at, cam.fov_deg, w, h)
     assert gpu.splat(camera=c, radius=0.25, mode=1).tobytes() == cpu.gather(camera=c, radius=0.25)[0].tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tiles", ["0", "1"])
+@pytest.mark.parametrize("w,h", [(120, 90), (640, 480)])
+def test_atomic_splat_pixel_groups(monkeypatch, tiles, w, h):
+    """mode 0 with pixel groups forced on: register-accumulating groups (default) and the
+    photon-parallel shared-memory-atomic tiles (PRX_SPLAT_TILES=1), both within tolerance."""
+    from paper_2111_06906_b200 import _lib as L
+
+    monkeypatch.setenv("PRX_GATHER_GROUPS", "1")
+    monkeypatch.setenv("PRX_SPLAT_TILES", tiles)
+    gpu, cpu = pair("C2", synthetic=True, mode="naive", paths=40000, bounces=4, dm=[2, 2, 8, 8], seed=19)
+    gpu.run_frame()
+    cpu.run_frame()
+    cam = gpu.scene.describe().camera
+    c = L.Camera(cam.position, cam.look_at, cam.fov_deg, w, h)
+    check_within_tolerance(gpu.splat(camera=c, radius=0.25, mode=0), cpu.gather(camera=c, radius=0.25)[0])
