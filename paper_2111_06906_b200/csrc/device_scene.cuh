@@ -740,11 +740,12 @@ constexpr uint32_t kTreeBit = 0x40000000u;
 template <bool kAny>
 __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r, float t_min, float t_max,
                                               float& best_t, uint32_t& best_tree, uint32_t& best_pos,
-                                              float& t_cert) {
+                                              float& t_cert, uint32_t& best_slot) {
     constexpr uint32_t kNone = 0xFFFFFFFFu;
     best_t = t_max;
     best_pos = kNone;
     best_tree = 0;
+    best_slot = 0;
     float second = t_max;
     bool found = false;
     uint2* const ss = trav_short_stack();
@@ -827,6 +828,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
                         best_t = t;
                         best_tree = tree;
                         best_pos = pos;
+                        best_slot = k;
                         t_cert = t_max;
                         return true;
                     }
@@ -836,6 +838,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
                         best_t = t;
                         best_tree = tree;
                         best_pos = pos;
+                        best_slot = k;
                         found = true;
                     } else if (t > best_t && t < second) {
                         second = t;
@@ -869,6 +872,17 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
 // ancestor box contains the leaf box, and the double slab test is monotone under box
 // inclusion (fl(lo' - o) <= fl(lo - o) for lo' <= lo, division by d keeps the order, so the
 // entry bound can only drop and the exit bound only rise).
+// (the joint walk's form: the winner's fast-tree slot carries its reference leaf in ftris[3k+2].w,
+// one dependent load less than leaf_of[position])
+__device__ __forceinline__ bool static_cert_slot(const SceneDev& S, const RayPre& r, float t_min, float t_lim,
+                                                 uint32_t slot) {
+    if (S.cert_off) return false;
+    const uint32_t leaf = __float_as_uint(__ldg(&S.ftris[3 * slot + 2]).w);
+    const float4 A = __ldg(&S.nodes[2 * leaf]);
+    const float4 B = __ldg(&S.nodes[2 * leaf + 1]);
+    return ray_box(r, t_min, t_lim, Box{{A.x, A.y, A.z}, {B.x, B.y, B.z}});
+}
+
 __device__ __forceinline__ bool static_cert(const SceneDev& S, const RayPre& r, float t_min, float t_lim,
                                             uint32_t pos) {
     if (S.cert_off) return false;
@@ -981,6 +995,21 @@ __device__ __forceinline__ void make_hit(const SceneDev& S, V3 o, V3 d, int kind
     h.normal = n;
 }
 
+// make_hit for a winner of the joint walk, from the fast tree's own triangle copy (the same
+// e1/e2 floats as S.stris / S.dtris, already touched by the walk) -- no random access into
+// the reference-order arrays on the hot path
+__device__ __forceinline__ void make_hit_slot(const float4* __restrict__ tris, uint32_t slot, uint32_t obj, V3 o,
+                                              V3 d, float t, Hit& h) {
+    const V3 e1 = ld3(__ldg(&tris[3 * slot + 1]));
+    const V3 e2 = ld3(__ldg(&tris[3 * slot + 2]));
+    h.obj = obj;
+    h.t = t;
+    h.pos = add(o, mul(d, t));
+    V3 n = normalized(cross(e1, e2));  // Triangle::geometric_normal (geometry.hpp:64)
+    if (dot(n, d) > 0.0f) n = neg(n);
+    h.normal = n;
+}
+
 // intersect_scene (scene.cpp:136-168), one-shot form: static phase, then the dynamic phase.
 // `t_max` is the ray's (Ray::t_max, FLT_MAX in every engine query); `tri` (optional) receives
 // Hit::triangle: the static triangle's index in scene order, or the index inside its mesh.
@@ -993,21 +1022,23 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
         // dynamic winner is strictly nearer than every static hit, and its gate is certified
         // at the bound (which the reference's running t_max at that object exceeds)
         float bt, tc;
-        uint32_t tree, pos;
+        uint32_t tree, pos, slot;
         PRX_CERT_COUNT(0);
-        if (!joint_closest<false>(S, r, t_min, t_max, bt, tree, pos, tc)) return false;
+        if (!joint_closest<false>(S, r, t_min, t_max, bt, tree, pos, tc, slot)) return false;
         bool ok;
-        uint32_t dj = 0, dtri = 0;
+        uint32_t dj = 0;
         if (tree == 0) {
-            ok = static_cert(S, r, t_min, tc, pos);
+            ok = static_cert_slot(S, r, t_min, tc, slot);
         } else {
-            dj = __ldg(&S.dtri_obj[pos]);
-            dtri = pos - S.fp->dyn[dj].tri_begin;
+            dj = __float_as_uint(__ldg(&S.datris[3 * slot + 1]).w);  // dynamic object of the winner
             ok = !S.cert_off && ray_box(r, t_min, tc, S.fp->dyn[dj].cur);
         }
         if (ok) {
-            if (tri) *tri = tree == 0 ? __float_as_uint(__ldg(&S.stris[3 * pos]).w) : dtri;
-            make_hit(S, o, d, tree == 0 ? 0 : 1, pos, dj, dtri, bt, h);
+            if (tri) *tri = tree == 0 ? __float_as_uint(__ldg(&S.stris[3 * pos]).w) : pos - S.fp->dyn[dj].tri_begin;
+            if (tree == 0)
+                make_hit_slot(S.ftris, slot, __float_as_uint(__ldg(&S.ftris[3 * slot + 1]).w), o, d, bt, h);
+            else
+                make_hit_slot(S.datris, slot, S.fp->dyn[dj].obj, o, d, bt, h);
             return true;
         }
         PRX_CERT_COUNT(1);
@@ -1032,11 +1063,12 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
         // one walk over both trees to the first accepted triangle; it decides when its own
         // reference path (static leaf, or its object's gate) passes at the fixed t_max
         float bt, tc;
-        uint32_t tree, pos;
+        uint32_t tree, pos, slot;
         PRX_CERT_COUNT(2);
-        if (!joint_closest<true>(S, r, t_min, t_max, bt, tree, pos, tc)) return false;
-        if (tree == 0 ? static_cert(S, r, t_min, t_max, pos)
-                      : !S.cert_off && ray_box(r, t_min, t_max, S.fp->dyn[__ldg(&S.dtri_obj[pos])].cur))
+        if (!joint_closest<true>(S, r, t_min, t_max, bt, tree, pos, tc, slot)) return false;
+        if (tree == 0 ? static_cert_slot(S, r, t_min, t_max, slot)
+                      : !S.cert_off &&
+                            ray_box(r, t_min, t_max, S.fp->dyn[__float_as_uint(__ldg(&S.datris[3 * slot + 1]).w)].cur))
             return true;
         PRX_CERT_COUNT(3);
     }

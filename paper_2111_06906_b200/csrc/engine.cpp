@@ -339,6 +339,7 @@ void Engine::upload_scene() {
             ft[3 * k] = float4{tris[3 * pos].x, tris[3 * pos].y, tris[3 * pos].z, f_of_u(pos)};
             ft[3 * k + 1] = tris[3 * pos + 1];
             ft[3 * k + 2] = tris[3 * pos + 2];
+            ft[3 * k + 2].w = f_of_u(leaf_of[pos]);  // the certificate's reference leaf (static_cert_slot)
         }
         // hot arena, hottest first: a window over its prefix keeps what fits persisting in L2
         const auto up = [](size_t b) { return (b + 255) & ~size_t(255); };

@@ -20,10 +20,11 @@ for k in k_trace k_verify_error_walk k_occlusion_flags k_compute_dm k_gather_fla
     skip=3
     [ "$k" = k_rs_scatter ] && skip=18   # 6 radix passes per frame (prune + gather sorts)
     [ "$k" = k_fill_assign ] && skip=6   # one per light
+    case "$k" in k_verify_error_walk|k_occlusion_flags|k_update_origins) skip=2 ;; esac  # from frame 1 on
     ncu $common -k "regex:${k}(<|$)" --launch-skip $skip -c 1 -o "$out/${tag}_full_${k}" $bench \
         > "$out/${tag}_ncu_${k}.log" 2>&1 || echo "ncu $k rc=$?"
 done
-for k in k_splat_filter k_splat; do
+for k in k_bin_filter k_bin_scatter k_splat_pixels; do
     ncu $common -k "regex:${k}(<|$)" --launch-skip 3 -c 1 -o "$out/${tag}_full_${k}" $bench --splat-mode 0 \
         > "$out/${tag}_ncu_${k}.log" 2>&1 || echo "ncu $k rc=$?"
 done
