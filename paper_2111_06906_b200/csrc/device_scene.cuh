@@ -737,6 +737,24 @@ constexpr uint32_t kTreeBit = 0x40000000u;
 #ifndef PRX_JOINT_STATIC_FIRST
 #define PRX_JOINT_STATIC_FIRST 0
 #endif
+#ifndef PRX_LEAF_PREFETCH
+#define PRX_LEAF_PREFETCH 1
+#endif
+#ifndef PRX_FAR_PREFETCH
+#define PRX_FAR_PREFETCH 0
+#endif
+// L1 prefetch of a parked leaf's triangles (48 B each, <= 8): the leaf round that tests them
+// runs only once enough lanes hold a leaf, so the lines arrive while the node walk continues
+__device__ __forceinline__ void prefetch_leaf(const SceneDev& S, uint32_t leaf) {
+    const float4* tris = (leaf & kTreeBit) ? S.datris : S.ftris;
+    const uint32_t first = (leaf & ~(kLeafBit | kTreeBit)) >> 3, count = (leaf & 7u) + 1u;
+    const char* a = reinterpret_cast<const char*>(tris + 3ull * first);
+    const char* e = a + 48u * count;
+    for (const char* p = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(127)); p < e;
+         p += 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 template <bool kAny>
 __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r, float t_min, float t_max,
                                               float& best_t, uint32_t& best_tree, uint32_t& best_pos,
@@ -797,10 +815,21 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
             const bool hl = tl != INFINITY, hr = tr != INFINITY, left_first = tl <= tr;
             uint32_t next = kNone;
             if (hl || hr) next = (hl && (left_first || !hr)) ? c0 : c1;
-            if (hl && hr) push(left_first ? c1 : c0, left_first ? tr : tl);
+            if (hl && hr) {
+                const uint32_t far = left_first ? c1 : c0;
+                push(far, left_first ? tr : tl);
+#if PRX_FAR_PREFETCH
+                if (!(far & kLeafBit))  // the deferred child's node, for when it is popped
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(
+                        ((far & kTreeBit) ? S.danodes : S.fnodes) + 4ull * (far & ~kTreeBit)));
+#endif
+            }
             if (next != kNone && (next & kLeafBit) && leaf == kNone) {  // park the leaf
                 leaf = next;
                 next = kNone;
+#if PRX_LEAF_PREFETCH
+                prefetch_leaf(S, leaf);  // its triangles stream into L1 while the walk goes on
+#endif
             }
             node = next != kNone ? next : pop();
             if (leaf_round_due(leaf != kNone)) break;
