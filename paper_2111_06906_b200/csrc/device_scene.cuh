@@ -738,7 +738,7 @@ constexpr uint32_t kTreeBit = 0x40000000u;
 #define PRX_JOINT_STATIC_FIRST 0
 #endif
 #ifndef PRX_LEAF_PREFETCH
-#define PRX_LEAF_PREFETCH 1
+#define PRX_LEAF_PREFETCH 0  // measured slower (profiles/r02_sweeps.md)
 #endif
 #ifndef PRX_FAR_PREFETCH
 #define PRX_FAR_PREFETCH 0

@@ -830,9 +830,12 @@ void Engine::prune_trim_all(uint32_t* const* prefix_tab, uint32_t* const* total_
                       d_vals_.as<uint32_t>(), n_, stream_);
     int light_bits = 0;
     while ((1u << light_bits) < lights_.size()) ++light_bits;
-    radix_sort_pairs(d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), d_keys_tmp_.as<uint32_t>(),
-                     d_vals_tmp_.as<uint32_t>(), n_, cnt + kCntTrim, 22 + light_bits, d_scratch_.get(), stream_);
-    launch_prune_trim(P, d_fp_.as<FrameParams>(), d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), cnt + kCntTrim,
+    const bool in_tmp = radix_sort_pairs_nocopy(d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(),
+                                                d_keys_tmp_.as<uint32_t>(), d_vals_tmp_.as<uint32_t>(), n_,
+                                                cnt + kCntTrim, 22 + light_bits, d_scratch_.get(), stream_);
+    const uint32_t* sk = in_tmp ? d_keys_tmp_.as<uint32_t>() : d_keys_.as<uint32_t>();
+    const uint32_t* sv = in_tmp ? d_vals_tmp_.as<uint32_t>() : d_vals_.as<uint32_t>();
+    launch_prune_trim(P, d_fp_.as<FrameParams>(), sk, sv, cnt + kCntTrim,
                       n_, d_light_ptrs_.as<uint32_t*>() + PRX_MAX_LIGHTS, prefix_tab, d_flags8_.as<uint8_t>(),
                       stream_);
     launch_prune_apply(P, d_flags8_.as<uint8_t>(), in_full_frame_ ? 0 : 1, stream_);

@@ -5,6 +5,7 @@
 // round is one coalesced 1 KiB access and element order within a tile is preserved.
 #include "prims.h"
 
+#include <algorithm>
 #include <atomic>
 
 #include <cstdio>
@@ -300,10 +301,9 @@ void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, u
     g_launches += 2;
 }
 
-void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
-                      uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch,
-                      cudaStream_t st) {
-    if (n_max == 0 || bits <= 0) return;
+bool radix_sort_pairs_nocopy(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
+                             uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch, cudaStream_t st) {
+    if (n_max == 0 || bits <= 0) return false;
     Scratch s = carve(scratch, n_max);
     const uint32_t tiles = prim_tiles(n_max);
     uint32_t *ki = keys, *vi = vals, *ko = keys_tmp, *vo = vals_tmp;
@@ -323,10 +323,28 @@ void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32
         vi = vo;
         vo = t;
     }
-    if (passes & 1) {  // result is in the tmp buffers: copy back
-        const uint64_t bytes = 4ull * n_max;
-        cudaMemcpyAsync(keys, ki, bytes, cudaMemcpyDeviceToDevice, st);
-        cudaMemcpyAsync(vals, vi, bytes, cudaMemcpyDeviceToDevice, st);
+    return (passes & 1) != 0;
+}
+
+namespace {
+__global__ void k_copy_pairs(const uint32_t* __restrict__ ks, const uint32_t* __restrict__ vs, uint32_t* kd,
+                             uint32_t* vd, uint32_t n_max, const uint32_t* n_dev) {
+    const uint32_t n = n_of(n_max, n_dev);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        kd[i] = ks[i];
+        vd[i] = vs[i];
+    }
+}
+}  // namespace
+
+void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
+                      uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch,
+                      cudaStream_t st) {
+    if (radix_sort_pairs_nocopy(keys, vals, keys_tmp, vals_tmp, n_max, n_dev, bits, scratch, st)) {
+        // result in the tmp buffers: copy back the live elements only (n_dev, not n_max)
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((n_max + 255) / 256, 148u * 16u);
+        k_copy_pairs<<<grid, 256, 0, st>>>(keys_tmp, vals_tmp, keys, vals, n_max, n_dev);
+        ++g_launches;
     }
 }
 

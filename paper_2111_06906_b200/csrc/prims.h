@@ -32,6 +32,10 @@ void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, u
 
 // Stable LSD radix sort of `bits` low key bits; results land back in keys/vals
 // (keys_tmp/vals_tmp are ping-pong buffers of the same size).
+// as radix_sort_pairs without the final copy: returns true when the sorted pairs are in
+// keys_tmp / vals_tmp (odd number of passes), false when in keys / vals
+bool radix_sort_pairs_nocopy(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
+                             uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch, cudaStream_t st);
 void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
                       uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch,
                       cudaStream_t st);

@@ -704,9 +704,9 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         k_gather_flag<<<launch_grid(nv, kT), kT, 0, st>>>(P, radius, keys, bits, flag, pslot, pcnt);
         compact_u8(flag, (uint32_t)nv, nullptr, 0, cand, m_count, gscratch, st);
         k_gather_keys<<<launch_grid(nv, kT), kT, 0, st>>>(cand, m_count, pslot, sk, sv);
-        radix_sort_pairs(sk, sv, sk2, sv2, (uint32_t)nv, m_count, bits, gscratch, st);
+        const bool in_tmp = radix_sort_pairs_nocopy(sk, sv, sk2, sv2, (uint32_t)nv, m_count, bits, gscratch, st);
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
-        k_gather_copy<<<launch_grid(nv, kT), kT, 0, st>>>(P, sv, m_count, spo, sen);
+        k_gather_copy<<<launch_grid(nv, kT), kT, 0, st>>>(P, in_tmp ? sv2 : sv, m_count, spo, sen);
         g_launches += 3;  // flag, keys, copy (the prims count their own)
         if (!groups) {
             uint32_t* wq = m_count + 4;
