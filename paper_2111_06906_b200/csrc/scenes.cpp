@@ -2,7 +2,8 @@
 //
 // 1. The reference builtins (scene.cpp:404-611): same names, geometry, keyframes, lights
 //    and cameras, so `run_builtin`/`render_builtin` are drop-ins.  Parity is checked by
-//    tests/test_scenes.py against the reference's own make_builtin_scene.
+//    tests/test_abi.py::test_builtin_scene_bvh_matches_reference and tests/test_io.py::
+//    test_builtin_sources against the reference's own make_builtin_scene.
 // 2. Procedural BASELINE configurations C1..C5: Cornell box (~1K tris),
 //    Sponza-scale (~300K static + 4 x 20K dynamic), Villa-scale (~1M static + 8 x 20K
 //    dynamic + 2 moving lights) and the dynamic-object stress sweep.  Both the GPU engine
