@@ -56,6 +56,10 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e replay (profiling passes)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-splat-sweep", action="store_true", help="skip the per-mode splat timings")
+    ap.add_argument("--extra", default="C1,C2,C3,C5w,C5b",
+                    help="secondary workloads measured after the headline (N=1 only; 'none' skips): "
+                         "C1-C3, C5w = C5 worst case (32M paths, 64 movers, baseline: full retrace), "
+                         "C5b = C5 best case (32M paths, 1 mover, error mode)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: N x the workload's paths over N GPUs; strong: the workload's paths split over N")
     return ap.parse_args()
@@ -176,6 +180,57 @@ def run_reference(args, name, n_paths, steps, warmup):
         times.append(time.perf_counter() - t0)
     mean = sum(times) / len(times)
     return n_paths / mean, {"frame_s_mean": mean, "frames": steps, "warmup": warmup}
+
+
+EXTRA = {  # the other BASELINE.json configurations, one B200
+    "C1": dict(scene=("C1", 0), **{k: WORKLOADS["C1"][k] for k in ("mode", "paths", "bounces", "threshold")}),
+    "C2": dict(scene=("C2", 0), **{k: WORKLOADS["C2"][k] for k in ("mode", "paths", "bounces", "threshold")}),
+    "C3": dict(scene=("C3", 0), **{k: WORKLOADS["C3"][k] for k in ("mode", "paths", "bounces", "threshold")}),
+    "C5w": dict(scene=("C5", 64), mode="baseline", paths=32 << 20, bounces=7, threshold=0.001),
+    "C5b": dict(scene=("C5", 1), mode="error", paths=32 << 20, bounces=7, threshold=0.001),
+}
+
+
+def measure_extra(pr, L, torch, stream, key, steps=5, warmup=3):
+    """Device ms/frame (frame + 120x90 ordered splat) of one secondary workload."""
+    import ctypes as C
+
+    w = EXTRA[key]
+    scene = pr.Scene.synthetic(*w["scene"])
+    eng = pr.Engine(scene, pr.make_config(mode=w["mode"], paths=w["paths"], bounces=w["bounces"],
+                                          dm=[8, 8, 64, 64], threshold=w["threshold"], seed=1))
+    eng.set_stream(stream.cuda_stream)
+    cam = scene.describe().camera
+    img = torch.zeros(cam.height * cam.width * 3, dtype=torch.float32, device="cuda")
+    sts = []
+
+    def one(collect):
+        st, sst = L.FrameStats(), L.FrameStats()
+        L.check(L.lib().prx_run_frame(eng.handle, C.byref(st)))
+        L.check(L.lib().prx_splat(eng.handle, C.byref(cam), 0.25, 1, None, C.c_void_p(img.data_ptr()), C.byref(sst)))
+        if collect:
+            sts.append((st, sst))
+
+    for _ in range(warmup):
+        one(False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one(True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    counts = scene.counts()
+    out = {"scene": f"{w['scene'][0]} ({counts['static_triangles']} static + {counts['dynamic_triangles']} dynamic tris)",
+           "mode": w["mode"], "paths": w["paths"], "bounces": w["bounces"], "ms_per_step": ms,
+           "paths_per_s": w["paths"] / (ms * 1e-3),
+           "stages_ms": {k: statistics.median(getattr(a, f) for a, _ in sts)
+                         for k, f in (("verify", "ms_verify"), ("retrace", "ms_retrace"))},
+           "rays_traced_per_frame": statistics.median(a.rays_traced for a, _ in sts)}
+    out["stages_ms"]["splat"] = statistics.median(b.ms_splat for _, b in sts)
+    eng.close()
+    return out
 
 
 def main():
@@ -440,6 +495,15 @@ def main():
             "gpu_launches": launches, "clocks": clk, "roofline": roofline,
             "scene_counts": {"static_tris": scene_counts["static_triangles"],
                              "dynamic_tris": scene_counts["dynamic_triangles"]}}
+
+    if world == 1 and args.extra != "none":  # the other BASELINE configurations, device time
+        if not args.no_e2e:
+            eng2.close()
+        eng.close()
+        torch.cuda.synchronize()
+        line["workloads"] = {}
+        for key in [k for k in args.extra.split(",") if k]:
+            line["workloads"][key] = measure_extra(pr, L, torch, stream, key)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sample = args.cpu_sample or CPU_SAMPLE_PATHS[name]
