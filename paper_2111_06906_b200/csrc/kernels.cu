@@ -195,6 +195,9 @@ __global__ void __launch_bounds__(kT) k_update_origins(SceneDev S, PathDev P, Co
 #ifndef PRX_OCC_MINB
 #define PRX_OCC_MINB 4
 #endif
+#ifndef PRX_OCC_PREFETCH2
+#define PRX_OCC_PREFETCH2 1
+#endif
 __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S, PathDev P, int mode, int record,
                                                         uint32_t* list, uint32_t* masks, Counters* ctr) {
     __shared__ Box boxes[kMaxDyn];
@@ -250,8 +253,12 @@ __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S
         uint32_t mask = 0;
         V3 prev = live ? ld3(P.origin[i]) : V3{0.f, 0.f, 0.f};
         uint32_t prev_obj = kInvalidObj;
-        // vertex s+1 is loaded while segment s is tested (the loop is load-latency bound)
+        // vertices s+1 (and s+2, PRX_OCC_PREFETCH2) are loaded while segment s is tested (the
+        // loop is load-latency bound)
         float4 nextv = k > 0 ? __ldcs(&P.pos_obj[kVS * (vix(P, 0, i))]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#if PRX_OCC_PREFETCH2
+        float4 next2 = k > 1 ? __ldcs(&P.pos_obj[kVS * (vix(P, 1, i))]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
         const uint32_t s_end = __reduce_max_sync(0xffffffffu, segs);
         for (uint32_t s = 0; s < s_end; ++s) {
             const bool act = s < segs;
@@ -259,7 +266,12 @@ __global__ void __launch_bounds__(kT, PRX_OCC_MINB) k_occlusion_flags(SceneDev S
             uint32_t cur_obj = kInvalidObj;
             if (act && s < k) {
                 const float4 v = nextv;
+#if PRX_OCC_PREFETCH2
+                nextv = next2;
+                if (s + 2 < k) next2 = __ldcs(&P.pos_obj[kVS * (vix(P, s + 2, i))]);
+#else
                 if (s + 1 < k) nextv = __ldcs(&P.pos_obj[kVS * (vix(P, s + 1, i))]);
+#endif
                 cur = ld3(v);
                 cur_obj = __float_as_uint(v.w);
             }
