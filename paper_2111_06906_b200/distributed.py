@@ -98,7 +98,10 @@ class GpuExecutor:
         return out
 
     def dm_commit(self, bufs):  # buffers alias the engine's DM_C
-        self.engine.synchronize()
+        # the all-reduce ran on torch's stream, which need not be the engine's (a 0 handle
+        # gives the engine a private stream): a device-wide sync orders it before the next
+        # engine kernel in every mode (baseline frames have no prune sync)
+        self.torch.cuda.synchronize(self.device)
 
     def prune_count(self) -> list:
         self.torch.cuda.synchronize(self.device)
