@@ -309,6 +309,8 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     legacy = world > 1 and backend != "nccl"
+    if legacy:
+        config["parallelism"] = f"contiguous path shards x{world} (host-phased {backend} exchanges: functional check)"
     comm = None
     if legacy:  # functional multi-rank check on one device (gloo): the host-phased protocol
         from paper_2111_06906_b200.distributed import GpuExecutor, TorchCollectives, run_frame_distributed
