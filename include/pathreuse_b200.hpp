@@ -640,6 +640,53 @@ inline Image gather_image(const SceneState& state, const PhotonMap& photons, std
     return img;
 }
 
+// ---------------------------------------------------------------- multi-GPU (B200 extension)
+// One Engine over several GPUs (devices may repeat): contiguous path shards, the exchanges
+// inside the engines (prx_group_*).  Frames are bit-identical to one Engine; the image is
+// the sum of the shards' splats (fp32 order differs).
+class MultiGpuEngine {
+public:
+    MultiGpuEngine(Scene scene, EngineConfig cfg, const std::vector<int>& devices)
+        : scene_(std::move(scene)), cfg_(std::move(cfg)) {
+        if (!scene_.handle) finalize_scene(scene_);
+        prx_config c{};
+        c.mode = static_cast<int32_t>(cfg_.mode);
+        c.n_paths = cfg_.n_paths;
+        c.max_bounces = cfg_.max_bounces;
+        for (int i = 0; i < 4; ++i) c.dm_dims[i] = cfg_.dm_dims.at(i);
+        c.threshold = cfg_.threshold;
+        c.seed = cfg_.seed;
+        c.gather_radius = cfg_.gather_radius;
+        c.workers = cfg_.workers;
+        c.record_flags = cfg_.record_flags;
+        std::vector<int32_t> devs(devices.begin(), devices.end());
+        prx_group* g = nullptr;
+        detail::check(prx_group_create(scene_.handle.get(), &c, devs.data(), static_cast<int32_t>(devs.size()), &g));
+        group_.reset(g, prx_group_destroy);
+    }
+    FrameStats run_frame() {
+        prx_frame_stats s{};
+        detail::check(prx_group_run_frame(group_.get(), &s));
+        return Engine::convert(s);
+    }
+    Image splat(const Camera& cam, float radius, int mode = 1) {
+        Image img;
+        img.width = cam.width;
+        img.height = cam.height;
+        img.pixels.assign(3ull * cam.width * cam.height, 0.0f);
+        const prx_camera c{detail::v(cam.position), detail::v(cam.look_at), cam.fov_deg, cam.width, cam.height};
+        detail::check(prx_group_splat(group_.get(), &c, radius, mode, img.pixels.data()));
+        return img;
+    }
+    int size() const { return prx_group_size(group_.get()); }
+    const Scene& scene() const { return scene_; }
+
+private:
+    Scene scene_;
+    EngineConfig cfg_;
+    std::shared_ptr<prx_group> group_;
+};
+
 // ---------------------------------------------------------------- scene documents (scene.hpp)
 namespace detail {
 inline Scene adopt(prx_scene* h) {

@@ -326,6 +326,21 @@ typedef struct prx_collectives {
 /* attach (copied) / detach (NULL); world 1 behaves as an unsharded engine */
 prx_status prx_engine_set_collectives(prx_engine* engine, const prx_collectives* coll);
 
+/* One process over several GPUs (several shards may share a device): `n_devices` engines on
+ * contiguous path shards of cfg->n_paths, attached to in-process local collectives, driven
+ * by one persistent host thread each.  prx_group_run_frame runs every shard's frame
+ * concurrently (stats: the all-shard counters); prx_group_splat returns the summed image;
+ * prx_group_engine gives a shard's engine (owned by the group) for downloads. */
+typedef struct prx_group prx_group;
+prx_status prx_group_create(const prx_scene* scene, const prx_config* cfg, const int32_t* devices,
+                            int32_t n_devices, prx_group** out);
+prx_status prx_group_run_frame(prx_group* group, prx_frame_stats* stats);
+prx_status prx_group_splat(prx_group* group, const prx_camera* camera, float radius, int mode,
+                           float* rgb_out);
+prx_engine* prx_group_engine(prx_group* group, int32_t rank);
+int32_t prx_group_size(const prx_group* group);
+void prx_group_destroy(prx_group* group);
+
 typedef struct prx_comm prx_comm;
 /* NCCL (loaded at run time, PRX_NCCL_LIB overrides "libnccl.so.2"): rank 0 makes the id,
  * the caller ships it to the other ranks, every rank creates its communicator */

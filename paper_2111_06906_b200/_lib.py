@@ -173,6 +173,12 @@ SIGNATURES = [
     ("prx_fill_count", C.c_int, [P, C.POINTER(C.c_uint32)]),
     ("prx_fill_apply", C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(FrameStats)]),
     ("prx_engine_set_collectives", C.c_int, [P, C.POINTER(Collectives)]),
+    ("prx_group_create", C.c_int, [P, C.POINTER(Config), C.POINTER(C.c_int32), C.c_int32, C.POINTER(P)]),
+    ("prx_group_run_frame", C.c_int, [P, C.POINTER(FrameStats)]),
+    ("prx_group_splat", C.c_int, [P, C.POINTER(Camera), C.c_float, C.c_int, P]),
+    ("prx_group_engine", P, [P, C.c_int32]),
+    ("prx_group_size", C.c_int32, [P]),
+    ("prx_group_destroy", None, [P]),
     ("prx_comm_nccl_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
     ("prx_comm_nccl_create", C.c_int, [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
     ("prx_comm_local_create", C.c_int, [C.c_int32, C.POINTER(P)]),

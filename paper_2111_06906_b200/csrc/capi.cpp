@@ -10,6 +10,7 @@
 
 #include "comm.h"
 #include "engine.h"
+#include "group.h"
 #include "host_scene.h"
 #include "prx.h"
 #include "wire.h"
@@ -354,6 +355,71 @@ prx_status prx_engine_set_collectives(prx_engine* engine, const prx_collectives*
 struct prx_comm {
     std::unique_ptr<prx::Comm> comm;
 };
+
+struct prx_group {
+    std::vector<std::unique_ptr<prx_engine>> engines;
+    std::unique_ptr<prx::EngineGroup> group;
+};
+
+prx_status prx_group_create(const prx_scene* scene, const prx_config* cfg, const int32_t* devices,
+                            int32_t n_devices, prx_group** out) {
+    return guarded([&] {
+        need(scene, "scene");
+        need(cfg, "cfg");
+        need(devices, "devices");
+        need(out, "out");
+        if (n_devices < 1 || n_devices > prx::kMaxLocalRanks)
+            throw std::invalid_argument("group: n_devices must be 1..16");
+        auto g = std::make_unique<prx_group>();
+        std::vector<prx::Engine*> raw;
+        const uint64_t n = cfg->n_paths;
+        for (int32_t r = 0; r < n_devices; ++r) {
+            prx_config c = *cfg;
+            c.device = devices[r];
+            c.shard_begin = static_cast<uint32_t>(n * r / n_devices);
+            c.shard_end = static_cast<uint32_t>(n * (r + 1) / n_devices);
+            auto e = std::make_unique<prx_engine>();
+            e->engine = std::make_unique<prx::Engine>(scene->scene, c);
+            raw.push_back(e->engine.get());
+            g->engines.push_back(std::move(e));
+        }
+        g->group = std::make_unique<prx::EngineGroup>(raw, prx::local_comms(n_devices));
+        *out = g.release();
+    });
+}
+
+prx_status prx_group_run_frame(prx_group* group, prx_frame_stats* stats) {
+    return guarded([&] {
+        need(group, "group");
+        std::vector<prx_frame_stats> st(group->engines.size());
+        group->group->run_all([&](int r, prx::Engine& e) { e.run_frame(&st[r]); });
+        if (stats) *stats = st[0];  // the counters are all-shard sums on every shard
+    });
+}
+
+prx_status prx_group_splat(prx_group* group, const prx_camera* camera, float radius, int mode, float* rgb_out) {
+    return guarded([&] {
+        need(group, "group");
+        group->group->run_all([&](int r, prx::Engine& e) {
+            e.splat(camera, radius, mode, r == 0 ? rgb_out : nullptr, nullptr, nullptr);
+        });
+    });
+}
+
+prx_engine* prx_group_engine(prx_group* group, int32_t rank) {
+    if (!group || rank < 0 || rank >= static_cast<int32_t>(group->engines.size())) return nullptr;
+    return group->engines[rank].get();
+}
+
+int32_t prx_group_size(const prx_group* group) {
+    return group ? static_cast<int32_t>(group->engines.size()) : 0;
+}
+
+void prx_group_destroy(prx_group* group) {
+    if (!group) return;
+    group->group.reset();  // joins the shard threads before the engines go
+    delete group;
+}
 
 prx_status prx_comm_nccl_unique_id(uint8_t id_out[128]) {
     return guarded([&] {

@@ -303,37 +303,46 @@ def attach(engine: Engine, comm: Communicator) -> None:
 
 
 class EngineGroup:
-    """One process, `world` path shards (on `devices`; several may share one device), each
-    driven by its own host thread; the exchanges run inside the engines over the local
-    collectives backend (comm.cpp), so a sharded frame is each engine's own prx_run_frame with
-    one host read-back.  Frames are bit-identical to one engine; the image is the sum of the
-    per-shard splats (fp32 order differs across shards)."""
+    """One process, `world` path shards (on `devices`; several may share one device), driven by
+    the C++ group (prx_group_*, csrc/group.cpp): one persistent host thread per shard, the
+    exchanges inside the engines over the local collectives backend (comm.cpp), so a sharded
+    frame is each engine's own prx_run_frame with one host read-back.  Frames are
+    bit-identical to one engine; the image is the sum of the per-shard splats (fp32 order
+    differs across shards)."""
 
     def __init__(self, scene: Scene, devices: Sequence[int], **cfg):
-        from concurrent.futures import ThreadPoolExecutor
-
         self.world = len(devices)
-        n = cfg.get("paths", 10000)
-        self.engines = [Engine(scene, make_config(shard=shard_range(n, r, self.world), device=d, **cfg))
-                        for r, d in enumerate(devices)]
-        self.comms = Communicator.local_group(self.world)
-        for e, c in zip(self.engines, self.comms):
-            attach(e, c)
-        self.pool = ThreadPoolExecutor(max_workers=self.world)
-
-    def _all(self, fn):
-        return list(self.pool.map(fn, self.engines))  # collective: every shard in its own thread
+        self.scene = scene
+        self.config = make_config(**cfg)
+        devs = (C.c_int32 * self.world)(*devices)
+        h = C.c_void_p()
+        L.check(L.lib().prx_group_create(scene.handle, C.byref(self.config), devs, self.world, C.byref(h)))
+        self._h = h
+        self.engines = []
+        for r in range(self.world):
+            c = make_config(shard=shard_range(self.config.n_paths, r, self.world), device=devices[r], **cfg)
+            self.engines.append(Engine._borrowed(L.lib().prx_group_engine(h, r), scene, c, self))
 
     def run_frame(self) -> L.FrameStats:
-        return self._all(lambda e: e.run_frame())[0]  # all-rank sums, identical on every shard
+        st = L.FrameStats()
+        L.check(L.lib().prx_group_run_frame(self._h, C.byref(st)))  # all-shard counters
+        return st
 
     def splat(self, camera=None, radius: float = 0.25, mode: int = 1) -> np.ndarray:
-        return self._all(lambda e: e.splat(camera=camera, radius=radius, mode=mode))[0]
+        cam = camera if camera is not None else self.scene.describe().camera
+        out = np.zeros((int(cam.height), int(cam.width), 3), dtype=np.float32)
+        L.check(L.lib().prx_group_splat(self._h, C.byref(cam), float(radius), int(mode),
+                                        out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def close(self):
-        self.pool.shutdown()
-        for e in self.engines:
-            e.close()
+        if getattr(self, "_h", None) is not None and self._h.value:
+            L.lib().prx_group_destroy(self._h)
+        self._h = None
+        self.engines = []
+
+    def __del__(self):
+        self.close()
 
 
 class ShardedEngine:

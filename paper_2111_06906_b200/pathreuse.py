@@ -205,10 +205,17 @@ class Engine:
         L.check(L.lib().prx_engine_create(scene.handle, C.byref(self.config), C.byref(h)))
         self._h = h
 
+    @classmethod
+    def _borrowed(cls, handle: int, scene: Scene, config: L.Config, owner) -> "Engine":
+        """A view of an engine owned by someone else (a prx_group shard): never destroyed here."""
+        e = cls.__new__(cls)
+        e.scene, e.config, e._h, e._owner = scene, config, C.c_void_p(handle), owner
+        return e
+
     def close(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and L is not None:  # (module globals may be gone at exit)
-            L.lib().prx_engine_destroy(h)
+        if getattr(self, "_owner", None) is None and h is not None and h.value and L is not None:
+            L.lib().prx_engine_destroy(h)  # (module globals may be gone at exit)
         self._h = None
 
     def __del__(self):

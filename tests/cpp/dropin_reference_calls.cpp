@@ -99,5 +99,14 @@ int main(int argc, char** argv) {
     std::vector<uint32_t> exact(600);
     std::iota(exact.begin(), exact.end(), 0u);
     std::printf("prune_exact %zu\n", select_paths_to_prune(exact, 600, 600, 5, 3).size());
+
+    // the same frames on a 2-shard MultiGpuEngine (both shards on device 0)
+    MultiGpuEngine multi(make_builtin_scene(scene_name), cfg, {0, 0});
+    for (int f = 0; f < frames; ++f) {
+        const FrameStats s = multi.run_frame();
+        std::printf("group %d %llu %llu %llu %llu %llu\n", s.frame, (unsigned long long)s.rays_traced,
+                    (unsigned long long)s.rays_reused, (unsigned long long)s.paths_pruned,
+                    (unsigned long long)s.paths_filled, (unsigned long long)s.visibility_rays);
+    }
     return 0;
 }

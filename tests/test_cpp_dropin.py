@@ -73,8 +73,12 @@ def test_reference_call_patterns_match_reference(tmp_path, scene, mode, frames):
     cfg = pr.make_config(mode=mode, paths=6000, bounces=5, dm=[1, 1, 8, 8], seed=7)
     rs = ref.RefScene.builtin(scene)
     eng = ref.RefEngine(rs, cfg)
+    ref_rows = []
     for _ in range(frames):
-        eng.run_frame()
+        st = eng.run_frame()
+        ref_rows.append([st.frame, st.rays_traced, st.rays_reused, st.paths_pruned, st.paths_filled,
+                         st.visibility_rays])
+    assert rows["group"] == ref_rows  # the 2-shard MultiGpuEngine: the reference's counters
 
     def fnv(b):
         h = 1469598103934665603
