@@ -352,7 +352,9 @@ def main():
         if collect is not None:
             collect.append((st, sst))
 
-    for _ in range(max(3, args.warmup)):
+    first = []
+    step(first)  # frame 0: the cold fill (reported separately)
+    for _ in range(max(3, args.warmup) - 1):
         step()
     stats = []
     clocks = ClockSampler(local)
@@ -489,6 +491,11 @@ def main():
                           "retrace": retrace_ms, "trace": trace_ms, "splat": splat_ms},
             "splat_ms": splat_modes,
             "verified_segments_per_s": seg_before / (verify_ms * 1e-3) if verify_ms else None,
+            "retraced_paths_per_s": retraced / (retrace_ms * 1e-3) if retrace_ms else None,
+            "rays_traced_per_s": traced / (trace_ms * 1e-3) if trace_ms else None,
+            "frame0_ms": {"frame_update": first[0][0].ms_frame_update, "verify": first[0][0].ms_verify,
+                          "retrace": first[0][0].ms_retrace, "splat": first[0][1].ms_splat,
+                          "rays_traced": first[0][0].rays_traced},
             "retraced_paths_per_frame": retraced, "rays_traced_per_frame": traced,
             "visibility_rays_per_frame": vis,
             "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,

@@ -65,12 +65,17 @@ def test_multi_gpu_engine_matches_single_engine():
 
 
 # ---- in-engine sharded frames (collectives enqueued by the engine itself, comm.cpp)
-@pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("scene,mode,synthetic", [("moving-cube", "error", False), ("parallel-spot", "naive", False),
+GROUP_CASES = [(w, sc) for w in (2, 3) for sc in (("moving-cube", "error", False), ("parallel-spot", "naive", False),
                                                   ("villa-analog", "naive", False), ("moving-cube", "baseline", False),
-                                                  ("C4", "error", True)])
-def test_engine_group_matches_single_engine(world, scene, mode, synthetic):
+                                                  ("C4", "error", True))]
+# Class A/B outputs bitwise identical for G in {1, 2, 4, 8}
+GROUP_CASES += [(w, sc) for w in (4, 8) for sc in (("villa-analog", "error", False), ("C4", "error", True))]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,case", GROUP_CASES, ids=[f"{w}-{c[0]}-{c[1]}" for w, c in GROUP_CASES])
+def test_engine_group_matches_single_engine(world, case):
+    scene, mode, synthetic = case
     from paper_2111_06906_b200.distributed import EngineGroup
 
     cfg = dict(mode=mode, paths=6001, bounces=6, dm=[2, 2, 8, 8], seed=7)
