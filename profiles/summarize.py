@@ -91,6 +91,15 @@ def full_metrics(rep):
     return out
 
 
+def hbm_peak():
+    """MEASURED_PEAKS.json hbm_gbs (driver-written), else B200_PROFILING.md's fallback."""
+    try:
+        with open(os.path.join(HERE, "..", "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0
+
+
 def main(tag, src="gpurun_out"):
     lc = os.path.join(src, f"{tag}_launches.csv")
     shutil.copy(lc, os.path.join(HERE, f"{tag}_launches.csv"))
@@ -111,13 +120,14 @@ def main(tag, src="gpurun_out"):
     if reps:
         fm = [row for rep in reps for row in full_metrics(rep)]
         md += ["### `ncu --set full` (one steady-state launch each)", "",
-               "| kernel | ms | DRAM read GB | DRAM write GB | DRAM % peak | L2 hit % | L1 hit % | warps active % | issue active % | thr/inst | inst (M) | regs | global atom/red | shared atom |",
+               "| kernel | ms | DRAM read GB | DRAM write GB | DRAM GB/s (% of HBM peak) | L2 hit % | L1 hit % | warps active % | issue active % | thr/inst | inst (M) | regs | global atom/red | shared atom |",
                "|---|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|"]
         for r in fm:
-            md.append("| `{}` | {:.3f} | {:.3f} | {:.3f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.0f} | {:.0f} |".format(
-                r["kernel"], r.get("gpu__time_duration.sum", 0), r.get("dram__bytes_read.sum", 0) / 1e9,
-                r.get("dram__bytes_write.sum", 0) / 1e9,
-                r.get("dram__throughput.avg.pct_of_peak_sustained_elapsed", 0),
+            ms = r.get("gpu__time_duration.sum", 0)
+            gbs = (r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0)) / (ms * 1e-3) / 1e9 if ms else 0.0
+            md.append("| `{}` | {:.3f} | {:.3f} | {:.3f} | {:.0f} ({:.0f}%) | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.0f} | {:.0f} |".format(
+                r["kernel"], ms, r.get("dram__bytes_read.sum", 0) / 1e9,
+                r.get("dram__bytes_write.sum", 0) / 1e9, gbs, 100.0 * gbs / hbm_peak(),
                 r.get("lts__t_sector_hit_rate.pct", 0),
                 r.get("l1tex__t_sector_hit_rate.pct", 0),
                 r.get("sm__warps_active.avg.pct_of_peak_sustained_active", 0),
