@@ -73,3 +73,29 @@ def test_c4_5m_bench_frames(k):
                                                       vis_rays=sg.visibility_rays,
                                                       retraced=sg.paths_retraced))
     assert not any(bad.values()), bad
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,cfg,k", [
+    ("C2", dict(mode="naive", paths=1_048_576, bounces=5, dm=[8, 8, 64, 64], threshold=0.001, seed=1), 4),
+    ("C3", dict(mode="error", paths=2_097_152, bounces=7, dm=[8, 8, 64, 64], threshold=0.01, seed=1), 4),
+])
+def test_full_size_injected_frame(name, cfg, k):
+    """C2 and C3 at their BASELINE path counts: GPU frames 0..k-1, state injected into the
+    reference, frame k on both -- every field, the DMs and the image bit-exact."""
+    gpu, cpu = pair(name, synthetic=True, **cfg)
+    n_lights = gpu.info().n_lights
+    for _ in range(k):
+        gpu.run_frame()
+    ref.copy_state(gpu, cpu, n_lights)
+    cpu.set_frame_counter(k)
+    t0 = time.perf_counter()
+    sc = cpu.run_frame()
+    t_ref = time.perf_counter() - t0
+    sg = gpu.run_frame()
+    bad = compare_state(gpu, cpu, n_lights)
+    bad["image_px"], _ = _image_mismatch(gpu, cpu)
+    bad["counters"] = int(counts(sg) != counts(sc))
+    report_parity(f"{name} {cfg['paths']} frame {k} (injected)",
+                  dict(bad, ref_s=round(t_ref, 1), rays_traced=sg.rays_traced, retraced=sg.paths_retraced))
+    assert not any(bad.values()), bad
