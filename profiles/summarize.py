@@ -61,8 +61,9 @@ def full_metrics(rep):
             "smsp__thread_inst_executed_per_inst_executed.ratio",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
             "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
-            "l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum",
-            "l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum",
+            "lts__t_requests_srcunit_tex_op_atom_dot_alu.sum", "lts__t_requests_srcunit_tex_op_red.sum",
+            "lts__t_sectors_srcunit_tex_op_atom_dot_alu.avg.per_cycle_elapsed",
+            "lts__t_sectors_srcunit_tex_op_atom_dot_alu.avg.peak_sustained",
             "smsp__inst_executed_op_shared_atom.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
             "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -120,12 +121,12 @@ def main(tag, src="gpurun_out"):
     if reps:
         fm = [row for rep in reps for row in full_metrics(rep)]
         md += ["### `ncu --set full` (one steady-state launch each)", "",
-               "| kernel | ms | DRAM read GB | DRAM write GB | DRAM GB/s (% of HBM peak) | L2 hit % | L1 hit % | warps active % | issue active % | thr/inst | inst (M) | regs | global atom/red | shared atom |",
+               "| kernel | ms | DRAM read GB | DRAM write GB | DRAM GB/s (% of HBM peak) | L2 hit % | L1 hit % | warps active % | issue active % | thr/inst | inst (M) | regs | global atom/red (L2 atomic unit busy %) | shared atom wavefronts |",
                "|---|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|"]
         for r in fm:
             ms = r.get("gpu__time_duration.sum", 0)
             gbs = (r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0)) / (ms * 1e-3) / 1e9 if ms else 0.0
-            md.append("| `{}` | {:.3f} | {:.3f} | {:.3f} | {:.0f} ({:.0f}%) | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.0f} | {:.0f} |".format(
+            md.append("| `{}` | {:.3f} | {:.3f} | {:.3f} | {:.0f} ({:.0f}%) | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.0f} ({:.1f}%) | {:.0f} |".format(
                 r["kernel"], ms, r.get("dram__bytes_read.sum", 0) / 1e9,
                 r.get("dram__bytes_write.sum", 0) / 1e9, gbs, 100.0 * gbs / hbm_peak(),
                 r.get("lts__t_sector_hit_rate.pct", 0),
@@ -135,8 +136,10 @@ def main(tag, src="gpurun_out"):
                 r.get("smsp__thread_inst_executed_per_inst_executed.ratio", 0),
                 r.get("smsp__inst_executed.sum", 0) / 1e6,
                 r.get("launch__registers_per_thread", 0),
-                r.get("l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum", 0)
-                + r.get("l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum", 0),
+                r.get("lts__t_requests_srcunit_tex_op_atom_dot_alu.sum", 0)
+                + r.get("lts__t_requests_srcunit_tex_op_red.sum", 0),
+                100.0 * r.get("lts__t_sectors_srcunit_tex_op_atom_dot_alu.avg.per_cycle_elapsed", 0)
+                / max(r.get("lts__t_sectors_srcunit_tex_op_atom_dot_alu.avg.peak_sustained", 1.0), 1e-9),
                 r.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", 0)))
             traffic[r["kernel"]] = {"dram_bytes": r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0),
                                     "ms": r.get("gpu__time_duration.sum", 0),
