@@ -66,10 +66,9 @@ __global__ void k_gbuffer(SceneDev S, CamDev C, float4* gbuf) {
     }
 }
 
-// pass 0: count (fill == false) / pass 1: fill per-key pixel lists
-template <bool kFill>
+// every hit pixel registers its 27 neighbour-cell keys in an open-addressing table (the
+// cells any pixel can read: the photons of other cells never contribute)
 __global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float r, unsigned long long* keys,
-                           uint32_t* cnt, const uint32_t* __restrict__ off, uint32_t* cursor, uint32_t* list,
                            int bits) {
     const uint32_t mask = (1u << bits) - 1u;
     for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < 27u * npx; w += gridDim.x * blockDim.x) {
@@ -81,16 +80,10 @@ __global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float 
         const long long cz = cell_coord(g.z, r) + (long long)(o / 9) - 1;
         const unsigned long long key = grid_key(cx, cy, cz);
         uint32_t s = slot_of(key, bits);
-        if (!kFill) {
-            while (true) {
-                const unsigned long long prev = atomicCAS(&keys[s], kEmptyKey, key);
-                if (prev == kEmptyKey || prev == key) break;
-                s = (s + 1) & mask;
-            }
-            atomicAdd(&cnt[s], 1u);
-        } else {
-            while (keys[s] != key) s = (s + 1) & mask;
-            list[off[s] + atomicAdd(&cursor[s], 1u)] = pix;
+        while (true) {
+            const unsigned long long prev = atomicCAS(&keys[s], kEmptyKey, key);
+            if (prev == kEmptyKey || prev == key) break;
+            s = (s + 1) & mask;
         }
     }
 }
@@ -589,7 +582,7 @@ int splat_table_bits(uint32_t npx) {
 
 size_t splat_work_bytes(uint32_t npx) {
     const uint64_t slots = 1ull << splat_table_bits(npx);
-    return slots * (8 + 4 + 4 + 4) + 4ull * 27 * npx + prim_scratch_bytes(slots) + 64 + 256;
+    return slots * 8 + 256;  // the cell-key table
 }
 
 size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
@@ -606,14 +599,11 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
     const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
     auto* keys = static_cast<unsigned long long*>(work);
-    auto* cnt = reinterpret_cast<uint32_t*>(keys + slots);  // pixels per registered cell
     (void)cand_buf;
 
     k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
     cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
-    cudaMemsetAsync(cnt, 0, 4 * slots, st);
-    k_pixcells<false><<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, cnt, nullptr, nullptr,
-                                                                  nullptr, bits);
+    k_pixcells<<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
     g_launches += 2;  // gbuffer, pixcells
     const uint64_t nv = (uint64_t)P.n * P.B;
     // carve the work buffer in 256-byte aligned pieces (float4 / u32 views of any n)
