@@ -172,6 +172,10 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     PRX_CUDA(cudaSetDevice(device_));
     PRX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     for (auto& e : ev_) PRX_CUDA(cudaEventCreate(&e));
+    PRX_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
+    PRX_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    PRX_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    if (const char* e = std::getenv("PRX_SPLAT_PREFIX")) pre_on_ = e[0] != '0';
     launch_base_ = g_launches;
 
     // light blocks (engine.cpp:76-101)
@@ -247,6 +251,15 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     PRX_CUDA(cudaStreamSynchronize(stream_));
 }
 
+// Forget the captured frame graphs (they are re-captured on the next repeated frame signature).
+void Engine::drop_graphs() {
+    if (stream_) PRX_CUDA(cudaStreamSynchronize(stream_));
+    for (auto& kv : graphs_)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs_.clear();
+    last_sig_ = ~0u;
+}
+
 Engine::~Engine() {
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto& e : ev_)
@@ -259,6 +272,12 @@ Engine::~Engine() {
     for (auto& kv : graphs_)
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (capture_stream_) cudaStreamDestroy(capture_stream_);
+    if (side_stream_) {
+        cudaStreamSynchronize(side_stream_);
+        cudaStreamDestroy(side_stream_);
+    }
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
     if (stream_ && own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -703,6 +722,7 @@ bool Engine::place_dynamics_host(bool force) {
 }
 
 void Engine::place_dynamics_enqueue() {
+    pre_ok_ = false;  // the splat prefix saw the previous placement
     copy_async(d_dyn_xf_.get(), h_xf_, sizeof(float4) * 2 * dyn_.size(), cudaMemcpyHostToDevice);
     launch_transform_dynamic(d_dyn_local_.as<float4>(), d_dyn_tri_xf_.as<uint32_t>(),
                              d_dyn_xf_.as<float4>(), n_dyn_tris_, d_dyn_world_.as<float4>(), stream_);
@@ -1074,8 +1094,10 @@ void Engine::run_frame(prx_frame_stats* st) {
                          (dyn_changed_ ? 8u : 0u) | (static_cast<uint32_t>(cfg_.mode) << 4);
     auto plain = [&] {
         frame_update_enqueue();
+        const bool pre = splat_prefix_fork();
         verify_paths(nullptr);
         retrace_enqueue();
+        if (pre) splat_prefix_join();
     };
     // (sharded frames run plain launches: their exchanges call back into the collectives)
     const bool graphs = graphs_on_ && !sharded();
@@ -1089,6 +1111,7 @@ void Engine::run_frame(prx_frame_stats* st) {
         plain();
     }
     last_sig_ = sig;
+    pre_ok_ = pre_on_ && pre_radius_ > 0.0f;  // (graphs are dropped when the prefix radius changes)
     if (st) {
         st->frame = cur_frame_;
         st->mode = cfg_.mode;
@@ -1274,21 +1297,8 @@ void Engine::gather_photons(const void* photons, const void* aux, uint32_t n_pat
     d_gather_.reset();
 }
 
-void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, int mode, float* rgb_host,
-                         float* rgb_dev, prx_frame_stats* st, bool reduce_ranks) {
-    PRX_CUDA(cudaSetDevice(device_));
-    if (!(radius > 0.0f)) throw std::invalid_argument("gather: radius must be positive");
-    if (mode != 0 && mode != 1) throw std::invalid_argument("splat: mode must be 0 (atomic splat) or 1 (ordered gather)");
-    Camera c = scene_->camera;
-    if (cam) {
-        c.position = V3{cam->position.x, cam->position.y, cam->position.z};
-        c.look_at = V3{cam->look_at.x, cam->look_at.y, cam->look_at.z};
-        c.fov_deg = cam->fov_deg;
-        c.width = cam->width;
-        c.height = cam->height;
-    }
-    if (c.width == 0 || c.height == 0) throw std::invalid_argument("splat: empty image");
-    // camera_ray (gather.cpp:22-33): per-image constants on the host libm
+// camera_ray (gather.cpp:22-33): per-image constants on the host libm
+CamDev Engine::camera_dev(const Camera& c) const {
     CamDev C{};
     C.pos = c.position;
     C.fwd = normalized(sub(c.look_at, c.position));
@@ -1300,7 +1310,65 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
     C.aspect = static_cast<float>(c.width) / static_cast<float>(c.height);
     C.w = c.width;
     C.h = c.height;
+    return C;
+}
+
+// Fork the splat prefix of the scene camera onto the side stream once the frame has placed the
+// dynamics; it overlaps verify/retrace (it reads only the scene). false: no prefix this frame.
+bool Engine::splat_prefix_fork() {
+    if (!pre_on_ || !(pre_radius_ > 0.0f)) return false;
+    const Camera& c = scene_->camera;
+    if (c.width == 0 || c.height == 0) return false;
     const uint32_t npx = c.width * c.height;
+    if (d_pre_gbuf_.size() == 0) {
+        d_pre_gbuf_.alloc(16ull * npx);
+        d_pre_work_.alloc(splat_work_bytes(npx));
+    }
+    PRX_CUDA(cudaEventRecord(ev_fork_, stream_));
+    PRX_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
+    launch_splat_prefix(scene_dev(), camera_dev(c), pre_radius_, d_pre_gbuf_.as<float4>(), d_pre_work_.get(),
+                        side_stream_);
+    return true;
+}
+
+void Engine::splat_prefix_join() {
+    PRX_CUDA(cudaEventRecord(ev_join_, side_stream_));
+    PRX_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+}
+
+void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, int mode, float* rgb_host,
+                         float* rgb_dev, prx_frame_stats* st, bool reduce_ranks) {
+    PRX_CUDA(cudaSetDevice(device_));
+    if (!(radius > 0.0f)) throw std::invalid_argument("gather: radius must be positive");
+    if (mode != 0 && mode != 1) throw std::invalid_argument("splat: mode must be 0 (atomic splat) or 1 (ordered gather)");
+    Camera c = scene_->camera;
+    bool scene_cam = true;
+    if (cam) {
+        c.position = V3{cam->position.x, cam->position.y, cam->position.z};
+        c.look_at = V3{cam->look_at.x, cam->look_at.y, cam->look_at.z};
+        c.fov_deg = cam->fov_deg;
+        c.width = cam->width;
+        c.height = cam->height;
+        const Camera& s = scene_->camera;
+        auto eq = [](const V3& a, const V3& b) { return a.x == b.x && a.y == b.y && a.z == b.z; };
+        scene_cam = eq(c.position, s.position) && eq(c.look_at, s.look_at) && c.fov_deg == s.fov_deg &&
+                    c.width == s.width && c.height == s.height;
+    }
+    if (c.width == 0 || c.height == 0) throw std::invalid_argument("splat: empty image");
+    const CamDev C = camera_dev(c);
+    const uint32_t npx = c.width * c.height;
+    // a scene-camera splat at the radius the frame's side stream used skips the G-buffer and
+    // the cell keys; a new radius becomes the prefix radius of the following frames
+    bool use_pre = false;
+    if (scene_cam && pre_on_) {
+        if (radius == pre_radius_) {
+            use_pre = pre_ok_;
+        } else {
+            pre_radius_ = radius;
+            pre_ok_ = false;
+            drop_graphs();  // their side branch bakes the old radius in
+        }
+    }
     if (c.width != img_w_ || c.height != img_h_) {
         d_gbuf_.alloc(16ull * npx);
         d_img_.alloc(12ull * npx);
@@ -1317,8 +1385,12 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
     const SceneDev S = scene_dev();
     // (plain launches: a captured graph of these ~25 launches measured slower, 1.93 vs 1.89 ms)
     record(kEvSplat0);
-    launch_splat(S, P, C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, d_splat_work_.get(),
-                 d_splat_cand_.get(), mode, d_gather_.get(), stream_);
+    if (use_pre)
+        launch_splat(S, P, C, radius, d_pre_gbuf_.as<float4>(), out, inv_pi, inv_area, d_pre_work_.get(),
+                     d_splat_cand_.get(), mode, d_gather_.get(), true, stream_);
+    else
+        launch_splat(S, P, C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, d_splat_work_.get(),
+                     d_splat_cand_.get(), mode, d_gather_.get(), false, stream_);
     if (reduce_ranks)  // every rank splats its own photons; the image is their sum
         coll_ok(coll_.all_reduce_sum_f32(coll_.ctx, out, 3ull * npx, stream_), "image all-reduce");
     record(kEvSplat1);

@@ -224,6 +224,18 @@ private:
     // splat buffers
     DevBuf d_gbuf_, d_img_, d_splat_work_, d_splat_cand_, d_gather_;
     uint32_t img_w_ = 0, img_h_ = 0;
+    // the splat's photon-independent prefix (G-buffer + cell keys) for the scene camera at the
+    // radius of the last scene-camera splat, run on a side stream during verify/retrace
+    cudaStream_t side_stream_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    DevBuf d_pre_gbuf_, d_pre_work_;
+    float pre_radius_ = 0.0f;  // 0: no scene-camera splat yet, no prefix
+    bool pre_ok_ = false;      // d_pre_* match the current placement of the scene
+    bool pre_on_ = true;       // PRX_SPLAT_PREFIX=0: always compute the prefix in the splat
+    bool splat_prefix_fork();
+    void splat_prefix_join();
+    void drop_graphs();
+    CamDev camera_dev(const Camera& c) const;
 
     cudaEvent_t ev_[12] = {};
     bool ev_recorded_[12] = {};

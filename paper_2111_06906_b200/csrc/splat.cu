@@ -593,18 +593,30 @@ size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
     return 64 + nv * (1 + 4 + 4 + 16 + 32) + slots * 12 + 41ull * npx + 2 * prim_scratch_bytes(scan_n) + 64 * 256;
 }
 
+// The photon-independent part of a splat: the G-buffer and the key table of the cells the
+// pixels' gather spheres touch. It depends only on the placed scene, the camera and the radius,
+// so the engine can run it on a side stream during verify/retrace (Engine::splat_prefix_fork).
+void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf, void* work, cudaStream_t st) {
+    const uint32_t npx = C.w * C.h;
+    const int bits = splat_table_bits(npx);
+    const uint64_t slots = 1ull << bits;
+    auto* keys = static_cast<unsigned long long*>(work);
+    k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
+    cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
+    k_pixcells<<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
+    g_launches += 2;  // gbuffer, pixcells
+}
+
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
-                  float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, cudaStream_t st) {
+                  float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, bool prefix_done,
+                  cudaStream_t st) {
     const uint32_t npx = C.w * C.h;
     const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
     auto* keys = static_cast<unsigned long long*>(work);
     (void)cand_buf;
 
-    k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
-    cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
-    k_pixcells<<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
-    g_launches += 2;  // gbuffer, pixcells
+    if (!prefix_done) launch_splat_prefix(S, C, radius, gbuf, work, st);
     const uint64_t nv = (uint64_t)P.n * P.B;
     // carve the work buffer in 256-byte aligned pieces (float4 / u32 views of any n)
     char* w = static_cast<char*>(gather_buf);
