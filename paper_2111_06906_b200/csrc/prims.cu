@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include <cstdio>
 
@@ -140,20 +141,35 @@ __global__ void k_flag_count(const T* __restrict__ flags, uint32_t n_max, const 
     }
 }
 
+// out[k] = base_id + i for the k-th flagged i; with key_of, also keys[k] = key_of[i]
 template <typename T>
 __global__ void k_flag_scatter(const T* __restrict__ flags, uint32_t n_max, const uint32_t* n_dev,
                                uint32_t base_id, const uint32_t* __restrict__ offs,
-                               uint32_t* __restrict__ out) {
+                               uint32_t* __restrict__ out, const uint32_t* __restrict__ key_of = nullptr,
+                               uint32_t* __restrict__ keys = nullptr) {
     __shared__ uint32_t sh[kPrimThreads / 32];
     const uint32_t n = n_of(n_max, n_dev);
     const uint64_t base = (uint64_t)blockIdx.x * kPrimTile;
     if (base >= n) return;
     uint32_t run = offs[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // every load of the tile in flight before the ordered rounds
+    bool fl[kPrimItems];
+    uint32_t kv[kPrimItems];
 #pragma unroll
     for (int k = 0; k < kPrimItems; ++k) {
         const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
-        const bool f = i < n && flags[i] != 0;
+        fl[k] = i < n && flags[i] != 0;
+    }
+    if (key_of) {
+#pragma unroll
+        for (int k = 0; k < kPrimItems; ++k)
+            kv[k] = fl[k] ? __ldg(&key_of[base + (uint64_t)k * kPrimThreads + threadIdx.x]) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kPrimItems; ++k) {
+        const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
+        const bool f = fl[k];
         const uint32_t ball = __ballot_sync(0xffffffffu, f);
         if (lane == 0) sh[warp] = __popc(ball);
         __syncthreads();
@@ -164,7 +180,11 @@ __global__ void k_flag_scatter(const T* __restrict__ flags, uint32_t n_max, cons
             before += w < warp ? c : 0u;
             total += c;
         }
-        if (f) out[run + before + __popc(ball & ((1u << lane) - 1u))] = base_id + (uint32_t)i;
+        if (f) {
+            const uint32_t o = run + before + __popc(ball & ((1u << lane) - 1u));
+            out[o] = base_id + (uint32_t)i;
+            if (key_of) keys[o] = kv[k];
+        }
         run += total;
         __syncthreads();
     }
@@ -177,23 +197,28 @@ __global__ void k_flag_scatter(const T* __restrict__ flags, uint32_t n_max, cons
 // large n_max costs what its live elements cost.  The scatter ranks a tile in shared memory
 // (warp w owns tile elements [512 w, 512 w + 512), warp-private digit counters with
 // match_any leaders), stages it digit-sorted, and writes each digit's run contiguously.
-constexpr int kRadixBits = 8;
-constexpr int kRadix = 1 << kRadixBits;
+// Digits are 8 bits (10-bit digits as an opt-in knob, see digit_bits); the final pass can write two gathered float4 payload streams instead of the pairs.
 constexpr int kRsItems = 16;
 constexpr uint32_t kRsTile = kPrimThreads * kRsItems;  // 4096
 constexpr int kRsWarps = kPrimThreads / 32;
-static_assert(kRadix == kPrimThreads, "one digit per thread in the per-digit loops");
+constexpr int kRadixMax = 1024;                        // widest digit: 10 bits
 
 inline uint32_t rs_tiles(uint64_t n) { return static_cast<uint32_t>((n + kRsTile - 1) / kRsTile); }
+template <int B>
+constexpr size_t rs_scatter_smem() {
+    return sizeof(uint32_t) * ((size_t)(2 + kRsWarps) * (1u << B) + 2 * kRsTile);
+}
 
+template <int B>
 __global__ void __launch_bounds__(kPrimThreads) k_rs_hist(const uint32_t* __restrict__ keys, uint32_t n_max,
                                                           const uint32_t* n_dev, int shift, uint32_t mask,
                                                           uint32_t tiles, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[kRadix];
+    constexpr int D = 1 << B;
+    __shared__ uint32_t h[D];
     const uint32_t n = n_of(n_max, n_dev);
     const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
     if (base >= n) return;  // beyond the live tiles: never read
-    h[threadIdx.x] = 0;
+    for (int d = threadIdx.x; d < D; d += kPrimThreads) h[d] = 0;
     __syncthreads();
 #pragma unroll 4
     for (int k = 0; k < kRsItems; ++k) {
@@ -201,7 +226,7 @@ __global__ void __launch_bounds__(kPrimThreads) k_rs_hist(const uint32_t* __rest
         if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
     }
     __syncthreads();
-    hist[(uint64_t)threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];
+    for (int d = threadIdx.x; d < D; d += kPrimThreads) hist[(uint64_t)d * tiles + blockIdx.x] = h[d];
 }
 
 // one CTA per digit: exclusive scan of the digit's row over the live tiles, row total out
@@ -233,30 +258,45 @@ __global__ void __launch_bounds__(kPrimThreads) k_rs_rowscan(uint32_t* __restric
     if (threadIdx.x == 0) rowtot[blockIdx.x] = carry;
 }
 
+template <int B, bool GATHER>
 __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* __restrict__ kin,
-                                                             const uint32_t* __restrict__ vin,
-                                                             uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                             uint32_t n_max, const uint32_t* n_dev, int shift,
-                                                             uint32_t mask, uint32_t tiles,
-                                                             const uint32_t* __restrict__ hist,
-                                                             const uint32_t* __restrict__ rowtot) {
-    __shared__ uint32_t gbase[kRadix];           // global start of the tile's run of digit d
-    __shared__ uint32_t tstart[kRadix];          // tile-local start of digit d
-    __shared__ uint32_t wc[kRsWarps][kRadix];    // warp digit counters -> warp digit starts
-    __shared__ uint32_t sk[kRsTile], sv[kRsTile];  // staged keys, their tile indices
+                                                                const uint32_t* __restrict__ vin,
+                                                                uint32_t* __restrict__ kout,
+                                                                uint32_t* __restrict__ vout, uint32_t n_max,
+                                                                const uint32_t* n_dev, int shift, uint32_t mask,
+                                                                uint32_t tiles, const uint32_t* __restrict__ hist,
+                                                                const uint32_t* __restrict__ rowtot, SortGather pg) {
+    constexpr int D = 1 << B, DPT = D / kPrimThreads;  // digits per thread in the per-digit loops
+    static_assert(DPT >= 1 && D % kPrimThreads == 0, "digit count");
+    extern __shared__ uint32_t smem[];
+    uint32_t* gbase = smem;                  // [D] global start of the tile's run of digit d
+    uint32_t* tstart = gbase + D;            // [D] tile-local start of digit d
+    uint32_t* wc = tstart + D;               // [kRsWarps][D] warp digit counters -> starts
+    uint32_t* sk = wc + kRsWarps * D;        // [kRsTile] staged keys
+    uint32_t* sv = sk + kRsTile;             // [kRsTile] their tile indices
     __shared__ uint32_t sh[kPrimThreads / 32];
     const uint32_t n = n_of(n_max, n_dev);
     const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
     if (base >= n) return;
     const uint32_t cnt = n - base < kRsTile ? (uint32_t)(n - base) : kRsTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t d0 = threadIdx.x * DPT;  // this thread's digits in the per-digit loops
     {
-        uint32_t total;
-        const uint32_t d0 = block_exclusive(rowtot[threadIdx.x], total, sh);  // digits below d
-        gbase[threadIdx.x] = d0 + hist[(uint64_t)threadIdx.x * tiles + blockIdx.x];
-    }
+        uint32_t r[DPT], sum = 0;
 #pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) wc[w][threadIdx.x] = 0;
+        for (int q = 0; q < DPT; ++q) {
+            r[q] = rowtot[d0 + q];
+            sum += r[q];
+        }
+        uint32_t total;
+        uint32_t below = block_exclusive(sum, total, sh);  // all digits < d0
+#pragma unroll
+        for (int q = 0; q < DPT; ++q) {
+            gbase[d0 + q] = below + hist[(uint64_t)(d0 + q) * tiles + blockIdx.x];
+            below += r[q];
+        }
+    }
+    for (int e = threadIdx.x; e < kRsWarps * D; e += kPrimThreads) wc[e] = 0;
     __syncthreads();
     // rank: warp `warp` walks its 512 elements in order, 32 per round
     uint32_t key[kRsItems], rk[kRsItems];  // (values follow through their tile index)
@@ -266,33 +306,43 @@ __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* 
         const uint32_t j = wbase + k * 32 + lane;
         key[k] = j < cnt ? kin[base + j] : 0u;
     }
+    uint32_t* mine = wc + warp * D;
 #pragma unroll
     for (int k = 0; k < kRsItems; ++k) {
         const uint32_t j = wbase + k * 32 + lane;
-        const uint32_t d = j < cnt ? ((key[k] >> shift) & mask) : (uint32_t)kRadix;  // sentinel
+        const uint32_t d = j < cnt ? ((key[k] >> shift) & mask) : (uint32_t)D;  // sentinel
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const uint32_t below = __popc(peers & ((1u << lane) - 1u));
-        const uint32_t prior = d < kRadix ? wc[warp][d] : 0u;
+        const uint32_t prior = d < D ? mine[d] : 0u;
         __syncwarp();
-        if (d < kRadix && below == 0) wc[warp][d] = prior + __popc(peers);
+        if (d < D && below == 0) mine[d] = prior + __popc(peers);
         __syncwarp();
         rk[k] = prior + below;
     }
     __syncthreads();
     {  // digit-major offsets: (digit, warp) order == (digit, element) order
-        const uint32_t d = threadIdx.x;
-        uint32_t s = 0;
+        uint32_t cnt_d[DPT], sum = 0;
 #pragma unroll
-        for (int w = 0; w < kRsWarps; ++w) {
-            const uint32_t c = wc[w][d];
-            wc[w][d] = s;
-            s += c;
+        for (int q = 0; q < DPT; ++q) {
+            uint32_t s = 0;
+#pragma unroll
+            for (int w = 0; w < kRsWarps; ++w) {
+                const uint32_t c = wc[w * D + d0 + q];
+                wc[w * D + d0 + q] = s;
+                s += c;
+            }
+            cnt_d[q] = s;
+            sum += s;
         }
         uint32_t total;
-        const uint32_t t0 = block_exclusive(s, total, sh);
-        tstart[d] = t0;
+        uint32_t t0 = block_exclusive(sum, total, sh);
 #pragma unroll
-        for (int w = 0; w < kRsWarps; ++w) wc[w][d] += t0;
+        for (int q = 0; q < DPT; ++q) {
+            tstart[d0 + q] = t0;
+#pragma unroll
+            for (int w = 0; w < kRsWarps; ++w) wc[w * D + d0 + q] += t0;
+            t0 += cnt_d[q];
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -300,7 +350,7 @@ __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* 
         const uint32_t j = wbase + k * 32 + lane;
         if (j < cnt) {
             const uint32_t d = (key[k] >> shift) & mask;
-            const uint32_t pos = wc[warp][d] + rk[k];
+            const uint32_t pos = mine[d] + rk[k];
             sk[pos] = key[k];
             sv[pos] = j;
         }
@@ -310,8 +360,14 @@ __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* 
         const uint32_t k = sk[j];
         const uint32_t d = (k >> shift) & mask;
         const uint32_t g = gbase[d] + (j - tstart[d]);
-        kout[g] = k;
-        vout[g] = __ldg(&vin[base + sv[j]]);
+        const uint32_t v = __ldg(&vin[base + sv[j]]);
+        if (GATHER) {
+            pg.out_a[g] = __ldg(&pg.a[(size_t)pg.stride * v]);
+            pg.out_b[g] = __ldg(&pg.b[(size_t)pg.stride * v]);
+        } else {
+            kout[g] = k;
+            vout[g] = v;
+        }
     }
 }
 
@@ -328,7 +384,7 @@ Scratch carve(void* p, uint64_t n_max) {
     s.tile = static_cast<uint32_t*>(p);
     s.tile2 = s.tile + tiles + 64;
     s.rowtot = s.tile2 + prim_tiles(tiles) + 64;
-    s.hist = s.rowtot + kRadix + 64;
+    s.hist = s.rowtot + kRadixMax + 64;
     return s;
 }
 
@@ -350,7 +406,7 @@ void scan_inplace(uint32_t* v, uint32_t m, uint32_t* total_dev, uint32_t* tmp, c
 
 size_t prim_scratch_bytes(uint64_t n_max) {
     const uint64_t tiles = prim_tiles(n_max ? n_max : 1);
-    return 4ull * (tiles + 64 + prim_tiles(tiles) + 64 + kRadix + 64 + (uint64_t)rs_tiles(n_max ? n_max : 1) * kRadix + 64);
+    return 4ull * (tiles + 64 + prim_tiles(tiles) + 64 + kRadixMax + 64 + (uint64_t)rs_tiles(n_max ? n_max : 1) * kRadixMax + 64);
 }
 
 void scan_exclusive_u32(const uint32_t* in, uint32_t* out, uint32_t n_max, const uint32_t* n_dev,
@@ -378,6 +434,20 @@ void compact_u8(const uint8_t* flags, uint32_t n_max, const uint32_t* n_dev, uin
     g_launches += 2;
 }
 
+void compact_u8_pairs(const uint8_t* flags, const uint32_t* key_of, uint32_t n_max, uint32_t* keys,
+                      uint32_t* vals, uint32_t* count_dev, void* scratch, cudaStream_t st) {
+    if (n_max == 0) {
+        cudaMemsetAsync(count_dev, 0, 4, st);
+        return;
+    }
+    Scratch s = carve(scratch, n_max);
+    const uint32_t tiles = prim_tiles(n_max);
+    k_flag_count<uint8_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, nullptr, s.tile);
+    scan_inplace(s.tile, tiles, count_dev, s.tile2, st);
+    k_flag_scatter<uint8_t><<<tiles, kPrimThreads, 0, st>>>(flags, n_max, nullptr, 0, s.tile, vals, key_of, keys);
+    g_launches += 2;
+}
+
 void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, uint32_t base,
                  uint32_t* out, uint32_t* count_dev, void* scratch, cudaStream_t st) {
     if (n_max == 0) {
@@ -392,29 +462,78 @@ void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, u
     g_launches += 2;
 }
 
+namespace {
+// digit width per sort: 8 bits; PRX_RADIX10=1: 10-bit digits where they save a pass (measured
+// slower on the splat's 20-bit slots: 0.62 vs 0.50 ms, the wider scatter holds 72 KB of shared memory)
+int digit_bits(int bits) {
+    static const bool wide = [] {
+        const char* e = std::getenv("PRX_RADIX10");
+        return e && e[0] == '1';
+    }();
+    const int p8 = (bits + 7) / 8, p10 = (bits + 9) / 10;
+    return wide && p10 < p8 ? 10 : 8;
+}
+
+template <int B, bool GATHER>
+void rs_pass(const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo, uint32_t n_max,
+             const uint32_t* n_dev, int shift, int w, uint32_t tiles, const Scratch& s, const SortGather& pg,
+             cudaStream_t st) {
+    constexpr size_t smem = rs_scatter_smem<B>();
+    static bool attr = [] {
+        cudaFuncSetAttribute(k_rs_scatter<B, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+    }();
+    (void)attr;
+    const uint32_t mask = (1u << w) - 1u;
+    k_rs_hist<B><<<tiles, kPrimThreads, 0, st>>>(ki, n_max, n_dev, shift, mask, tiles, s.hist);
+    k_rs_rowscan<<<1u << B, kPrimThreads, 0, st>>>(s.hist, tiles, n_max, n_dev, s.rowtot);
+    k_rs_scatter<B, GATHER><<<tiles, kPrimThreads, smem, st>>>(ki, vi, ko, vo, n_max, n_dev, shift, mask, tiles,
+                                                                s.hist, s.rowtot, pg);
+    g_launches += 3;
+}
+
+// the passes; with pg set the last pass writes the gathered payloads.  Returns the number of
+// passes that wrote pairs (their parity says where the pairs are).
+int rs_run(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t n_max,
+           const uint32_t* n_dev, int bits, void* scratch, const SortGather* pg, cudaStream_t st) {
+    Scratch s = carve(scratch, n_max);
+    const uint32_t tiles = rs_tiles(n_max);
+    const int db = digit_bits(bits);
+    const int passes = (bits + db - 1) / db;
+    uint32_t *ki = keys, *vi = vals, *ko = keys_tmp, *vo = vals_tmp;
+    int shift = 0, written = 0;
+    const SortGather none{};
+    for (int p = 0; p < passes; ++p) {
+        const int w = (bits - shift + (passes - p) - 1) / (passes - p);  // even split of the rest
+        const bool gather = pg && p == passes - 1;
+        if (db == 10) {
+            if (gather) rs_pass<10, true>(ki, vi, ko, vo, n_max, n_dev, shift, w, tiles, s, *pg, st);
+            else rs_pass<10, false>(ki, vi, ko, vo, n_max, n_dev, shift, w, tiles, s, none, st);
+        } else {
+            if (gather) rs_pass<8, true>(ki, vi, ko, vo, n_max, n_dev, shift, w, tiles, s, *pg, st);
+            else rs_pass<8, false>(ki, vi, ko, vo, n_max, n_dev, shift, w, tiles, s, none, st);
+        }
+        shift += w;
+        if (!gather) {
+            ++written;
+            std::swap(ki, ko);
+            std::swap(vi, vo);
+        }
+    }
+    return written;
+}
+}  // namespace
+
 bool radix_sort_pairs_nocopy(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
                              uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch, cudaStream_t st) {
     if (n_max == 0 || bits <= 0) return false;
-    Scratch s = carve(scratch, n_max);
-    const uint32_t tiles = rs_tiles(n_max);
-    uint32_t *ki = keys, *vi = vals, *ko = keys_tmp, *vo = vals_tmp;
-    int passes = 0;
-    for (int shift = 0; shift < bits; shift += kRadixBits, ++passes) {
-        const int w = bits - shift < kRadixBits ? bits - shift : kRadixBits;
-        const uint32_t mask = (1u << w) - 1u;
-        k_rs_hist<<<tiles, kPrimThreads, 0, st>>>(ki, n_max, n_dev, shift, mask, tiles, s.hist);
-        k_rs_rowscan<<<kRadix, kPrimThreads, 0, st>>>(s.hist, tiles, n_max, n_dev, s.rowtot);
-        k_rs_scatter<<<tiles, kPrimThreads, 0, st>>>(ki, vi, ko, vo, n_max, n_dev, shift, mask, tiles, s.hist,
-                                                     s.rowtot);
-        g_launches += 3;
-        uint32_t* t = ki;
-        ki = ko;
-        ko = t;
-        t = vi;
-        vi = vo;
-        vo = t;
-    }
-    return (passes & 1) != 0;
+    return (rs_run(keys, vals, keys_tmp, vals_tmp, n_max, n_dev, bits, scratch, nullptr, st) & 1) != 0;
+}
+
+void radix_sort_gather(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t n_max,
+                       const uint32_t* n_dev, int bits, const SortGather& pg, void* scratch, cudaStream_t st) {
+    if (n_max == 0 || bits <= 0) return;
+    rs_run(keys, vals, keys_tmp, vals_tmp, n_max, n_dev, bits, scratch, &pg, st);
 }
 
 namespace {

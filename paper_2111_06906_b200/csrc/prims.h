@@ -26,6 +26,9 @@ void scan_exclusive_u32(const uint32_t* in, uint32_t* out, uint32_t n_max, const
 // Stable compaction: out[k] = base + i for the k-th i (ascending) with flags[i] != 0.
 void compact_u8(const uint8_t* flags, uint32_t n_max, const uint32_t* n_dev, uint32_t base,
                 uint32_t* out, uint32_t* count_dev, void* scratch, cudaStream_t st);
+// Stable compaction into pairs: for the k-th flagged i, vals[k] = i and keys[k] = key_of[i].
+void compact_u8_pairs(const uint8_t* flags, const uint32_t* key_of, uint32_t n_max, uint32_t* keys,
+                      uint32_t* vals, uint32_t* count_dev, void* scratch, cudaStream_t st);
 // Same with a u32 flag array (nonzero = keep).
 void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, uint32_t base,
                  uint32_t* out, uint32_t* count_dev, void* scratch, cudaStream_t st);
@@ -36,6 +39,19 @@ void compact_u32(const uint32_t* flags, uint32_t n_max, const uint32_t* n_dev, u
 // keys_tmp / vals_tmp (odd number of passes), false when in keys / vals
 bool radix_sort_pairs_nocopy(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
                              uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch, cudaStream_t st);
+// Payload gathered by the last pass of radix_sort_gather: out_a[k] = a[stride * v_k],
+// out_b[k] = b[stride * v_k] for the k-th sorted value v_k.
+struct SortGather {
+    const float4* a = nullptr;
+    const float4* b = nullptr;
+    uint32_t stride = 1;
+    float4* out_a = nullptr;
+    float4* out_b = nullptr;
+};
+// Stable sort by `bits` low key bits whose result is the payload records of the sorted
+// values (keys/vals and the tmp buffers are clobbered).
+void radix_sort_gather(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t n_max,
+                       const uint32_t* n_dev, int bits, const SortGather& pg, void* scratch, cudaStream_t st);
 void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
                       uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch,
                       cudaStream_t st);

@@ -332,26 +332,6 @@ __global__ void k_gather_flag(PathDev P, float radius, const unsigned long long*
     }
 }
 
-__global__ void k_gather_keys(const uint32_t* __restrict__ cand, const uint32_t* count,
-                              const uint32_t* __restrict__ pslot, uint32_t* keys, uint32_t* vals) {
-    const uint32_t n = *count;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const uint32_t v = cand[j];
-        keys[j] = pslot[v];
-        vals[j] = v;
-    }
-}
-
-__global__ void k_gather_copy(PathDev P, const uint32_t* __restrict__ vals, const uint32_t* count, float4* spo,
-                              float4* sen) {
-    const uint32_t n = *count;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const uint32_t v = vals[j];
-        spo[j] = P.pos_obj[kVS * (v)];
-        sen[j] = P.energy[kVS * (v)];
-    }
-}
-
 // Fused ordered gather, staged: one warp per pixel taken from a work counter (heavy pixels
 // cluster in the image, so static striding would pile them onto a few SMs); per 32-photon
 // chunk the warp tests the candidates in parallel, compacts the contributors' energies into
@@ -701,7 +681,6 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
     }
     {  // mode 1: ordered, bit-exact gather
         uint32_t* pslot = reinterpret_cast<uint32_t*>(take(4 * nv));
-        uint32_t* cand = reinterpret_cast<uint32_t*>(take(4 * nv));
         uint32_t* sk = reinterpret_cast<uint32_t*>(take(4 * nv));
         uint32_t* sv = reinterpret_cast<uint32_t*>(take(4 * nv));
         uint32_t* sk2 = reinterpret_cast<uint32_t*>(take(4 * nv));
@@ -714,12 +693,18 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         void* gscratch = take(0);
         cudaMemsetAsync(pcnt, 0, 4 * slots, st);
         k_gather_flag<<<launch_grid(nv, kT), kT, 0, st>>>(P, radius, keys, bits, flag, pslot, pcnt);
-        compact_u8(flag, (uint32_t)nv, nullptr, 0, cand, m_count, gscratch, st);
-        k_gather_keys<<<launch_grid(nv, kT), kT, 0, st>>>(cand, m_count, pslot, sk, sv);
-        const bool in_tmp = radix_sort_pairs_nocopy(sk, sv, sk2, sv2, (uint32_t)nv, m_count, bits, gscratch, st);
+        // candidates as (cell slot, record) pairs in record order, stably sorted by slot; the
+        // sort's last pass writes the candidates' {position, object} and energy contiguous
+        compact_u8_pairs(flag, pslot, (uint32_t)nv, sk, sv, m_count, gscratch, st);
+        SortGather pg;
+        pg.a = P.pos_obj;
+        pg.b = P.energy;
+        pg.stride = kVS;
+        pg.out_a = spo;
+        pg.out_b = sen;
+        radix_sort_gather(sk, sv, sk2, sv2, (uint32_t)nv, m_count, bits, pg, gscratch, st);
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
-        k_gather_copy<<<launch_grid(nv, kT), kT, 0, st>>>(P, in_tmp ? sv2 : sv, m_count, spo, sen);
-        g_launches += 3;  // flag, keys, copy (the prims count their own)
+        g_launches += 1;  // flag (the prims count their own)
         if (!groups) {
             uint32_t* wq = m_count + 4;
             cudaMemsetAsync(wq, 0, 4, st);

@@ -70,6 +70,30 @@ static int check_sort(std::mt19937_64& rng, uint32_t n_max, uint32_t n, int bits
     std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return k[a] < k[b]; });
     for (uint32_t j = 0; j < n; ++j)
         if (gk[j] != k[idx[j]] || gv[j] != idx[j]) return fail("radix_sort_pairs", n_max, n, bits, j);
+    // the same sort gathering two float4 payload streams (stride 2) in its last pass
+    {
+        std::vector<float4> pay(2 * (size_t)n_max);
+        for (size_t q = 0; q < pay.size(); ++q)
+            pay[q] = make_float4((float)q, (float)(q * 3), (float)(q & 1023), (float)(q % 7));
+        float4 *dp = dev(pay), *oa = dev(std::vector<float4>(n_max)), *ob = dev(std::vector<float4>(n_max));
+        uint32_t *k2 = dev(k), *v2 = dev(v);
+        prx::SortGather g;
+        g.a = dp;
+        g.b = dp + 1;
+        g.stride = 2;
+        g.out_a = oa;
+        g.out_b = ob;
+        prx::radix_sort_gather(k2, v2, dk2, dv2, n_max, dn, bits, g, scratch, 0);
+        CK(cudaDeviceSynchronize());
+        const auto ga = host(oa, n), gb = host(ob, n);
+        for (uint32_t j = 0; j < n; ++j) {
+            const float4 a = pay[2 * (size_t)idx[j]], b = pay[2 * (size_t)idx[j] + 1];
+            if (ga[j].x != a.x || ga[j].y != a.y || ga[j].z != a.z || ga[j].w != a.w || gb[j].x != b.x ||
+                gb[j].w != b.w)
+                return fail("radix_sort_gather", n_max, n, bits, j);
+        }
+        cudaFree(dp), cudaFree(oa), cudaFree(ob), cudaFree(k2), cudaFree(v2);
+    }
     // elements beyond n stay untouched in keys/vals
     const auto tail = host(dk + n, n_max - n);
     for (uint32_t j = 0; j < n_max - n; ++j)
@@ -100,6 +124,22 @@ static int check_compact_scan(std::mt19937_64& rng, uint32_t n_max, uint32_t n, 
     const auto got = host(dout, cnt);
     for (uint32_t j = 0; j < cnt; ++j)
         if (got[j] != want[j]) return fail("compact_u8", n_max, n, 0, j);
+    {  // pairs form: keys from a per-element table, all n_max elements
+        std::vector<uint32_t> key_of(n_max);
+        for (uint32_t i = 0; i < n_max; ++i) key_of[i] = static_cast<uint32_t>(rng());
+        uint32_t *dko = dev(key_of), *pk = dev(std::vector<uint32_t>(n_max)), *pv = dev(std::vector<uint32_t>(n_max));
+        prx::compact_u8_pairs(df, dko, n_max, pk, pv, dcnt, scratch, 0);
+        CK(cudaDeviceSynchronize());
+        std::vector<uint32_t> wi;
+        for (uint32_t i = 0; i < n_max; ++i)
+            if (f[i]) wi.push_back(i);
+        const uint32_t c2 = host(dcnt, 1)[0];
+        if (c2 != wi.size()) return fail("compact_u8_pairs count", n_max, n_max, 0, c2);
+        const auto gk = host(pk, c2), gv = host(pv, c2);
+        for (uint32_t j = 0; j < c2; ++j)
+            if (gv[j] != wi[j] || gk[j] != key_of[wi[j]]) return fail("compact_u8_pairs", n_max, n_max, 0, j);
+        cudaFree(dko), cudaFree(pk), cudaFree(pv);
+    }
     prx::scan_exclusive_u32(dx, dx, n_max, dn, dtot, scratch, 0);
     CK(cudaDeviceSynchronize());
     const auto sc = host(dx, n);

@@ -21,7 +21,10 @@ def exe(tmp_path_factory):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("radix10", ["1", "0"])
 @pytest.mark.parametrize("seed", [1, 2])
-def test_prims_random(exe, seed):
-    r = subprocess.run([exe, str(seed)], capture_output=True, text=True, timeout=600)
+def test_prims_random(exe, seed, radix10):
+    """radix10: 8-bit digits throughout (default) or 10-bit digits where they save a pass"""
+    env = dict(os.environ, PRX_RADIX10=radix10)
+    r = subprocess.run([exe, str(seed)], capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
