@@ -176,6 +176,8 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     PRX_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PRX_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     if (const char* e = std::getenv("PRX_SPLAT_PREFIX")) pre_on_ = e[0] != '0';
+    PRX_CUDA(cudaHostAlloc(&h_ncell_, 4, cudaHostAllocDefault));
+    *h_ncell_ = 0;
     launch_base_ = g_launches;
 
     // light blocks (engine.cpp:76-101)
@@ -269,6 +271,7 @@ Engine::~Engine() {
     if (h_cnt32_) cudaFreeHost(h_cnt32_);
     if (h_xf_) cudaFreeHost(h_xf_);
     if (h_prune_frame_) cudaFreeHost(h_prune_frame_);
+    if (h_ncell_) cudaFreeHost(h_ncell_);
     for (auto& kv : graphs_)
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (capture_stream_) cudaStreamDestroy(capture_stream_);
@@ -1328,6 +1331,10 @@ bool Engine::splat_prefix_fork() {
     PRX_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
     launch_splat_prefix(scene_dev(), camera_dev(c), pre_radius_, d_pre_gbuf_.as<float4>(), d_pre_work_.get(),
                         side_stream_);
+    // the registered-cell count sizes the splat's sort keys (read after the frame's sync)
+    PRX_CUDA(cudaMemcpyAsync(h_ncell_, d_pre_work_.as<char>() + splat_ncell_offset(npx), 4, cudaMemcpyDeviceToHost,
+                             side_stream_));
+    d2h_bytes_ += 4;
     return true;
 }
 
@@ -1387,10 +1394,10 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
     record(kEvSplat0);
     if (use_pre)
         launch_splat(S, P, C, radius, d_pre_gbuf_.as<float4>(), out, inv_pi, inv_area, d_pre_work_.get(),
-                     d_splat_cand_.get(), mode, d_gather_.get(), true, stream_);
+                     d_splat_cand_.get(), mode, d_gather_.get(), true, splat_cell_bits(*h_ncell_), stream_);
     else
         launch_splat(S, P, C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, d_splat_work_.get(),
-                     d_splat_cand_.get(), mode, d_gather_.get(), false, stream_);
+                     d_splat_cand_.get(), mode, d_gather_.get(), false, 0, stream_);
     if (reduce_ranks)  // every rank splats its own photons; the image is their sum
         coll_ok(coll_.all_reduce_sum_f32(coll_.ctx, out, 3ull * npx, stream_), "image all-reduce");
     record(kEvSplat1);

@@ -81,10 +81,13 @@ int splat_table_bits(uint32_t npx);
 size_t splat_work_bytes(uint32_t npx);
 size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx);
 // mode 0: tiled shared-memory atomic splat; mode 1: ordered gather (bit-exact vs gather_image)
-// prefix_done: the G-buffer and the cell-key table (launch_splat_prefix) are already in gbuf/work
+size_t splat_ncell_offset(uint32_t npx);  // byte offset of the registered-cell count in `work`
+int splat_cell_bits(uint32_t n_cells);     // key bits of n_cells dense cell ids
+// prefix_done: the G-buffer, the cell-key table and the dense cell ids (launch_splat_prefix)
+// are already in gbuf/work; cell_bits > 0: the dense ids fit that many bits (else the table's)
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img,
                   float inv_pi, float inv_area, void* work, void* cand_buf, int mode, void* gather_buf,
-                  bool prefix_done, cudaStream_t st);
+                  bool prefix_done, int cell_bits, cudaStream_t st);
 void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf, void* work, cudaStream_t st);
 
 // Dynamic LBVH (lbvh.cu)

@@ -88,6 +88,11 @@ __global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float 
     }
 }
 
+__global__ void k_slot_used(const unsigned long long* __restrict__ keys, uint32_t slots, uint32_t* used) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x)
+        used[s] = keys[s] != kEmptyKey ? 1u : 0u;
+}
+
 // ---------------------------------------------------------------- mode 0: atomic splat
 // Binning without order: every live photon whose grid cell some pixel registered is appended
 // to a candidate list (block-aggregated: one global atomic per 256 photons) and counted per
@@ -310,7 +315,8 @@ __global__ void __launch_bounds__(kT) k_splat_tiles(const float4* __restrict__ g
 // contributors strictly in that order -- the same fp32 additions as gather_image's
 // per-pixel loop.
 __global__ void k_gather_flag(PathDev P, float radius, const unsigned long long* __restrict__ keys, int bits,
-                              uint8_t* __restrict__ flag, uint32_t* __restrict__ pslot, uint32_t* __restrict__ pcnt) {
+                              const uint32_t* __restrict__ dense, uint8_t* __restrict__ flag,
+                              uint32_t* __restrict__ pcell, uint32_t* __restrict__ pcnt) {
     const uint32_t mask = (1u << bits) - 1u;
     const size_t total = (size_t)P.n * P.B;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
@@ -324,7 +330,7 @@ __global__ void k_gather_flag(PathDev P, float radius, const unsigned long long*
             while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
             if (k == key) {
                 f = 1;
-                pslot[v] = s;
+                pcell[v] = __ldg(&dense[s]);  // sort key: dense cell id (slot order)
                 atomicAdd(&pcnt[s], 1u);
             }
         }
@@ -560,9 +566,12 @@ int splat_table_bits(uint32_t npx) {
     return bits;
 }
 
+// the prefix's work buffer: cell-key table (8 B/slot) | dense cell ids (4 B/slot) | the
+// registered-cell count | scan scratch
+size_t splat_ncell_offset(uint32_t npx) { return (1ull << splat_table_bits(npx)) * 12; }
 size_t splat_work_bytes(uint32_t npx) {
     const uint64_t slots = 1ull << splat_table_bits(npx);
-    return slots * 8 + 256;  // the cell-key table
+    return slots * 12 + 256 + prim_scratch_bytes(slots) + 256;
 }
 
 size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
@@ -581,15 +590,26 @@ void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf
     const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
     auto* keys = static_cast<unsigned long long*>(work);
+    auto* dense = reinterpret_cast<uint32_t*>(keys + slots);
+    auto* ncell = reinterpret_cast<uint32_t*>(static_cast<char*>(work) + splat_ncell_offset(npx));
     k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
     cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
     k_pixcells<<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
-    g_launches += 2;  // gbuffer, pixcells
+    // dense cell ids in slot order (the ordered gather sorts by these: fewer key bits)
+    k_slot_used<<<launch_grid(slots, kT), kT, 0, st>>>(keys, (uint32_t)slots, dense);
+    scan_exclusive_u32(dense, dense, (uint32_t)slots, nullptr, ncell, ncell + 64, st);
+    g_launches += 3;  // gbuffer, pixcells, slot flags (the scan counts its own)
+}
+
+int splat_cell_bits(uint32_t n_cells) {
+    int b = 1;
+    while ((1ull << b) < n_cells) ++b;
+    return b;
 }
 
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
                   float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, bool prefix_done,
-                  cudaStream_t st) {
+                  int cell_bits, cudaStream_t st) {
     const uint32_t npx = C.w * C.h;
     const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
@@ -692,8 +712,9 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         uint8_t* flag = reinterpret_cast<uint8_t*>(take(nv));
         void* gscratch = take(0);
         cudaMemsetAsync(pcnt, 0, 4 * slots, st);
-        k_gather_flag<<<launch_grid(nv, kT), kT, 0, st>>>(P, radius, keys, bits, flag, pslot, pcnt);
-        // candidates as (cell slot, record) pairs in record order, stably sorted by slot; the
+        const uint32_t* dense = reinterpret_cast<const uint32_t*>(keys + slots);
+        k_gather_flag<<<launch_grid(nv, kT), kT, 0, st>>>(P, radius, keys, bits, dense, flag, pslot, pcnt);
+        // candidates as (cell, record) pairs in record order, stably sorted by cell; the
         // sort's last pass writes the candidates' {position, object} and energy contiguous
         compact_u8_pairs(flag, pslot, (uint32_t)nv, sk, sv, m_count, gscratch, st);
         SortGather pg;
@@ -702,7 +723,8 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         pg.stride = kVS;
         pg.out_a = spo;
         pg.out_b = sen;
-        radix_sort_gather(sk, sv, sk2, sv2, (uint32_t)nv, m_count, bits, pg, gscratch, st);
+        radix_sort_gather(sk, sv, sk2, sv2, (uint32_t)nv, m_count, cell_bits > 0 ? cell_bits : bits, pg, gscratch,
+                          st);
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
         g_launches += 1;  // flag (the prims count their own)
         if (!groups) {

@@ -41,11 +41,12 @@ def test_prefix_images_bit_exact(scene, synthetic, mode):
         img0 = gpu.splat(radius=radius, mode=0)
         img1 = gpu.splat(radius=radius, mode=1)
         assert np.array_equal(img0 == 0, img1 == 0)
-    # frames 1-3, 6 reuse the prefix (scene camera, same radius): two launches fewer than
-    # the other camera; frame 0 (no radius yet) and frame 5 (radius changed back) do not
+    # frames 1-3, 6 reuse the prefix (scene camera, same radius): fewer launches than the
+    # other camera (no G-buffer / cell table, and a sort over the dense cell ids' bits);
+    # frame 0 (no radius yet) and frame 5 (radius changed back) do not
     sc, ot = launches["scene"], launches["other"]
     for f in (1, 2, 3, 6):
-        assert sc[f] == ot[f] - 2, (f, sc, ot)
+        assert sc[f] < ot[f], (f, sc, ot)
         assert launches["explicit"][f] == sc[f]
     assert sc[0] == ot[0] and sc[5] == ot[5], (sc, ot)
 
