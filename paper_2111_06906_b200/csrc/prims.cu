@@ -195,11 +195,12 @@ __global__ void k_flag_scatter(const T* __restrict__ flags, uint32_t n_max, cons
 // (256 threads x 16).  Histograms are digit-major (hist[d * tiles_max + t]); the row scan
 // and the scatter only touch the tiles the device count reaches, so a sort sized for a
 // large n_max costs what its live elements cost.  The scatter ranks a tile in shared memory
-// (warp w owns tile elements [512 w, 512 w + 512), warp-private digit counters with
-// match_any leaders), stages it digit-sorted, and writes each digit's run contiguously.
+// (warp w owns the w-th contiguous eighth of the tile's elements, warp-private digit counters
+// with match_any leaders), stages it digit-sorted, and writes each digit's run contiguously.
 // Digits are 8 bits (10-bit digits as an opt-in knob, see digit_bits); the final pass can write two gathered float4 payload streams instead of the pairs.
 constexpr int kRsItems = 16;
 constexpr uint32_t kRsTile = kPrimThreads * kRsItems;  // 4096
+static_assert(kRsTile == kSortTile, "ragged tiles are sort tiles");
 constexpr int kRsWarps = kPrimThreads / 32;
 constexpr int kRadixMax = 1024;                        // widest digit: 10 bits
 
@@ -209,21 +210,30 @@ constexpr size_t rs_scatter_smem() {
     return sizeof(uint32_t) * ((size_t)(2 + kRsWarps) * (1u << B) + 2 * kRsTile);
 }
 
-template <int B>
-__global__ void __launch_bounds__(kPrimThreads) k_rs_hist(const uint32_t* __restrict__ keys, uint32_t n_max,
-                                                          const uint32_t* n_dev, int shift, uint32_t mask,
-                                                          uint32_t tiles, uint32_t* __restrict__ hist) {
-    constexpr int D = 1 << B;
-    __shared__ uint32_t h[D];
+// the pairs of tile t: [t * kRsTile, t * kRsTile + count); count from the device total, or
+// per tile (`ragged`: tile t holds ragged[t] pairs at its start, every tile live)
+__device__ __forceinline__ uint32_t rs_tile_count(uint32_t n_max, const uint32_t* n_dev, const uint32_t* ragged) {
+    if (ragged) return ragged[blockIdx.x];
     const uint32_t n = n_of(n_max, n_dev);
     const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
-    if (base >= n) return;  // beyond the live tiles: never read
+    return base >= n ? 0u : (n - base < kRsTile ? (uint32_t)(n - base) : kRsTile);
+}
+
+template <int B>
+__global__ void __launch_bounds__(kPrimThreads) k_rs_hist(const uint32_t* __restrict__ keys, uint32_t n_max,
+                                                          const uint32_t* n_dev, const uint32_t* ragged, int shift,
+                                                          uint32_t mask, uint32_t tiles, uint32_t* __restrict__ hist) {
+    constexpr int D = 1 << B;
+    __shared__ uint32_t h[D];
+    const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
+    if (!ragged && base >= n_of(n_max, n_dev)) return;  // beyond the live tiles: never read
+    const uint32_t cnt = rs_tile_count(n_max, n_dev, ragged);
     for (int d = threadIdx.x; d < D; d += kPrimThreads) h[d] = 0;
     __syncthreads();
 #pragma unroll 4
     for (int k = 0; k < kRsItems; ++k) {
-        const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
-        if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+        const uint32_t j = (uint32_t)k * kPrimThreads + threadIdx.x;
+        if (j < cnt) atomicAdd(&h[(keys[base + j] >> shift) & mask], 1u);
     }
     __syncthreads();
     for (int d = threadIdx.x; d < D; d += kPrimThreads) hist[(uint64_t)d * tiles + blockIdx.x] = h[d];
@@ -231,10 +241,10 @@ __global__ void __launch_bounds__(kPrimThreads) k_rs_hist(const uint32_t* __rest
 
 // one CTA per digit: exclusive scan of the digit's row over the live tiles, row total out
 __global__ void __launch_bounds__(kPrimThreads) k_rs_rowscan(uint32_t* __restrict__ hist, uint32_t tiles,
-                                                             uint32_t n_max, const uint32_t* n_dev,
+                                                             uint32_t n_max, const uint32_t* n_dev, bool ragged,
                                                              uint32_t* __restrict__ rowtot) {
     __shared__ uint32_t sh[kPrimThreads / 32];
-    const uint32_t live = rs_tiles_dev(n_of(n_max, n_dev));
+    const uint32_t live = ragged ? tiles : rs_tiles_dev(n_of(n_max, n_dev));
     uint32_t* row = hist + (uint64_t)blockIdx.x * tiles;
     uint32_t carry = 0;
     for (uint32_t b = 0; b < live; b += kPrimThreads * 4) {
@@ -263,7 +273,8 @@ __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* 
                                                                 const uint32_t* __restrict__ vin,
                                                                 uint32_t* __restrict__ kout,
                                                                 uint32_t* __restrict__ vout, uint32_t n_max,
-                                                                const uint32_t* n_dev, int shift, uint32_t mask,
+                                                                const uint32_t* n_dev, const uint32_t* ragged,
+                                                                int shift, uint32_t mask,
                                                                 uint32_t tiles, const uint32_t* __restrict__ hist,
                                                                 const uint32_t* __restrict__ rowtot, SortGather pg) {
     constexpr int D = 1 << B, DPT = D / kPrimThreads;  // digits per thread in the per-digit loops
@@ -275,10 +286,9 @@ __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* 
     uint32_t* sk = wc + kRsWarps * D;        // [kRsTile] staged keys
     uint32_t* sv = sk + kRsTile;             // [kRsTile] their tile indices
     __shared__ uint32_t sh[kPrimThreads / 32];
-    const uint32_t n = n_of(n_max, n_dev);
     const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
-    if (base >= n) return;
-    const uint32_t cnt = n - base < kRsTile ? (uint32_t)(n - base) : kRsTile;
+    if (!ragged && base >= n_of(n_max, n_dev)) return;
+    const uint32_t cnt = rs_tile_count(n_max, n_dev, ragged);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t d0 = threadIdx.x * DPT;  // this thread's digits in the per-digit loops
     {
@@ -296,19 +306,28 @@ __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* 
             below += r[q];
         }
     }
-    for (int e = threadIdx.x; e < kRsWarps * D; e += kPrimThreads) wc[e] = 0;
+    {
+        uint4* wz = reinterpret_cast<uint4*>(wc);
+        for (int e = threadIdx.x; e < kRsWarps * D / 4; e += kPrimThreads) wz[e] = make_uint4(0, 0, 0, 0);
+    }
     __syncthreads();
-    // rank: warp `warp` walks its 512 elements in order, 32 per round
+    // rank: the tile's cnt elements split into kRsWarps contiguous blocks of `per` (a multiple
+    // of 32); warp `warp` walks its block in order, 32 per round (sparse ragged tiles run few
+    // rounds instead of 16 mostly idle ones)
+    const uint32_t per = ((cnt + kPrimThreads - 1) / kPrimThreads) * 32;
+    const uint32_t wbase = warp * per;
+    const uint32_t rounds = (per + 31) / 32;  // same for every warp; elements past cnt idle
     uint32_t key[kRsItems], rk[kRsItems];  // (values follow through their tile index)
-    const uint32_t wbase = warp * (kRsTile / kRsWarps);
 #pragma unroll
     for (int k = 0; k < kRsItems; ++k) {
         const uint32_t j = wbase + k * 32 + lane;
-        key[k] = j < cnt ? kin[base + j] : 0u;
+        key[k] = (k < (int)rounds && j < cnt) ? kin[base + j] : 0u;
     }
+    __syncwarp();
     uint32_t* mine = wc + warp * D;
 #pragma unroll
     for (int k = 0; k < kRsItems; ++k) {
+        if (k >= (int)rounds) break;
         const uint32_t j = wbase + k * 32 + lane;
         const uint32_t d = j < cnt ? ((key[k] >> shift) & mask) : (uint32_t)D;  // sentinel
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
@@ -347,6 +366,7 @@ __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* 
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kRsItems; ++k) {
+        if (k >= (int)rounds) break;
         const uint32_t j = wbase + k * 32 + lane;
         if (j < cnt) {
             const uint32_t d = (key[k] >> shift) & mask;
@@ -476,8 +496,8 @@ int digit_bits(int bits) {
 
 template <int B, bool GATHER>
 void rs_pass(const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo, uint32_t n_max,
-             const uint32_t* n_dev, int shift, int w, uint32_t tiles, const Scratch& s, const SortGather& pg,
-             cudaStream_t st) {
+             const uint32_t* n_dev, const uint32_t* ragged, int shift, int w, uint32_t tiles, const Scratch& s,
+             const SortGather& pg, cudaStream_t st) {
     constexpr size_t smem = rs_scatter_smem<B>();
     static bool attr = [] {
         cudaFuncSetAttribute(k_rs_scatter<B, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -485,17 +505,18 @@ void rs_pass(const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo,
     }();
     (void)attr;
     const uint32_t mask = (1u << w) - 1u;
-    k_rs_hist<B><<<tiles, kPrimThreads, 0, st>>>(ki, n_max, n_dev, shift, mask, tiles, s.hist);
-    k_rs_rowscan<<<1u << B, kPrimThreads, 0, st>>>(s.hist, tiles, n_max, n_dev, s.rowtot);
-    k_rs_scatter<B, GATHER><<<tiles, kPrimThreads, smem, st>>>(ki, vi, ko, vo, n_max, n_dev, shift, mask, tiles,
-                                                                s.hist, s.rowtot, pg);
+    k_rs_hist<B><<<tiles, kPrimThreads, 0, st>>>(ki, n_max, n_dev, ragged, shift, mask, tiles, s.hist);
+    k_rs_rowscan<<<1u << B, kPrimThreads, 0, st>>>(s.hist, tiles, n_max, n_dev, ragged != nullptr, s.rowtot);
+    k_rs_scatter<B, GATHER><<<tiles, kPrimThreads, smem, st>>>(ki, vi, ko, vo, n_max, n_dev, ragged, shift, mask,
+                                                                tiles, s.hist, s.rowtot, pg);
     g_launches += 3;
 }
 
 // the passes; with pg set the last pass writes the gathered payloads.  Returns the number of
 // passes that wrote pairs (their parity says where the pairs are).
 int rs_run(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t n_max,
-           const uint32_t* n_dev, int bits, void* scratch, const SortGather* pg, cudaStream_t st) {
+           const uint32_t* n_dev, int bits, void* scratch, const SortGather* pg, const uint32_t* ragged,
+           cudaStream_t st) {
     Scratch s = carve(scratch, n_max);
     const uint32_t tiles = rs_tiles(n_max);
     const int db = digit_bits(bits);
@@ -506,12 +527,13 @@ int rs_run(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tm
     for (int p = 0; p < passes; ++p) {
         const int w = (bits - shift + (passes - p) - 1) / (passes - p);  // even split of the rest
         const bool gather = pg && p == passes - 1;
+        const uint32_t* rg = p == 0 ? ragged : nullptr;  // the first pass reads the ragged tiles
         if (db == 10) {
-            if (gather) rs_pass<10, true>(ki, vi, ko, vo, n_max, n_dev, shift, w, tiles, s, *pg, st);
-            else rs_pass<10, false>(ki, vi, ko, vo, n_max, n_dev, shift, w, tiles, s, none, st);
+            if (gather) rs_pass<10, true>(ki, vi, ko, vo, n_max, n_dev, rg, shift, w, tiles, s, *pg, st);
+            else rs_pass<10, false>(ki, vi, ko, vo, n_max, n_dev, rg, shift, w, tiles, s, none, st);
         } else {
-            if (gather) rs_pass<8, true>(ki, vi, ko, vo, n_max, n_dev, shift, w, tiles, s, *pg, st);
-            else rs_pass<8, false>(ki, vi, ko, vo, n_max, n_dev, shift, w, tiles, s, none, st);
+            if (gather) rs_pass<8, true>(ki, vi, ko, vo, n_max, n_dev, rg, shift, w, tiles, s, *pg, st);
+            else rs_pass<8, false>(ki, vi, ko, vo, n_max, n_dev, rg, shift, w, tiles, s, none, st);
         }
         shift += w;
         if (!gather) {
@@ -527,13 +549,14 @@ int rs_run(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tm
 bool radix_sort_pairs_nocopy(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
                              uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch, cudaStream_t st) {
     if (n_max == 0 || bits <= 0) return false;
-    return (rs_run(keys, vals, keys_tmp, vals_tmp, n_max, n_dev, bits, scratch, nullptr, st) & 1) != 0;
+    return (rs_run(keys, vals, keys_tmp, vals_tmp, n_max, n_dev, bits, scratch, nullptr, nullptr, st) & 1) != 0;
 }
 
 void radix_sort_gather(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t n_max,
-                       const uint32_t* n_dev, int bits, const SortGather& pg, void* scratch, cudaStream_t st) {
+                       const uint32_t* n_dev, int bits, const SortGather& pg, void* scratch, cudaStream_t st,
+                       const uint32_t* ragged) {
     if (n_max == 0 || bits <= 0) return;
-    rs_run(keys, vals, keys_tmp, vals_tmp, n_max, n_dev, bits, scratch, &pg, st);
+    rs_run(keys, vals, keys_tmp, vals_tmp, n_max, n_dev, bits, scratch, &pg, ragged, st);
 }
 
 namespace {

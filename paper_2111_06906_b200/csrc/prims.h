@@ -49,9 +49,13 @@ struct SortGather {
     float4* out_b = nullptr;
 };
 // Stable sort by `bits` low key bits whose result is the payload records of the sorted
-// values (keys/vals and the tmp buffers are clobbered).
+// values (keys/vals and the tmp buffers are clobbered).  With `ragged`, the input is tiled:
+// tile t (of rs tiles over n_max) holds ragged[t] pairs at keys/vals[t * kSortTile...], in
+// order, and *n_dev is their total.
+constexpr uint32_t kSortTile = 4096;
 void radix_sort_gather(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp, uint32_t n_max,
-                       const uint32_t* n_dev, int bits, const SortGather& pg, void* scratch, cudaStream_t st);
+                       const uint32_t* n_dev, int bits, const SortGather& pg, void* scratch, cudaStream_t st,
+                       const uint32_t* ragged = nullptr);
 void radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
                       uint32_t n_max, const uint32_t* n_dev, int bits, void* scratch,
                       cudaStream_t st);

@@ -314,27 +314,73 @@ __global__ void __launch_bounds__(kT) k_splat_tiles(const float4* __restrict__ g
 // pixel (k_gather_staged) visits its 27 cells in the reference's (dz, dy, dx) order, summing
 // contributors strictly in that order -- the same fp32 additions as gather_image's
 // per-pixel loop.
-__global__ void k_gather_flag(PathDev P, float radius, const unsigned long long* __restrict__ keys, int bits,
-                              const uint32_t* __restrict__ dense, uint8_t* __restrict__ flag,
-                              uint32_t* __restrict__ pcell, uint32_t* __restrict__ pcnt) {
+// One CTA per sort tile of kSortTile records (record order): finds the candidates (live
+// photons whose grid cell some pixel registered, gather.cpp:42-52), counts them per cell, and
+// compacts the tile's candidates in record order as (dense cell id, record) pairs at the
+// tile's start -- the ragged input of the sort's first pass (no flag array, no separate
+// compaction pass).
+constexpr int kBinItems = kSortTile / kT;  // 16
+__global__ void __launch_bounds__(kT) k_gather_bin(PathDev P, float radius, const unsigned long long* __restrict__ keys,
+                                                   int bits, const uint32_t* __restrict__ dense,
+                                                   uint32_t* __restrict__ ck, uint32_t* __restrict__ cv,
+                                                   uint32_t* __restrict__ tile_cnt, uint32_t* __restrict__ total,
+                                                   uint32_t* __restrict__ pcnt) {
+    __shared__ uint32_t wsum[kT / 32];
     const uint32_t mask = (1u << bits) - 1u;
-    const size_t total = (size_t)P.n * P.B;
-    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const float4 po = __ldcs(&P.pos_obj[kVS * (v)]);
-        uint8_t f = 0;
-        if (__float_as_uint(po.w) != kInvalidObj) {
-            const unsigned long long key =
-                grid_key(cell_coord(po.x, radius), cell_coord(po.y, radius), cell_coord(po.z, radius));
-            uint32_t s = slot_of(key, bits);
-            unsigned long long k;
-            while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
-            if (k == key) {
-                f = 1;
-                pcell[v] = __ldg(&dense[s]);  // sort key: dense cell id (slot order)
-                atomicAdd(&pcnt[s], 1u);
+    const uint64_t nvv = (uint64_t)P.n * P.B;
+    const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t run = 0;
+    constexpr int kHalf = kBinItems / 2;  // two halves: loads of a half in flight together
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t cell[kHalf];
+        uint32_t fm = 0;
+#pragma unroll
+        for (int q = 0; q < kHalf; ++q) {
+            const uint64_t v = base + (uint64_t)(h * kHalf + q) * kT + threadIdx.x;
+            cell[q] = 0;
+            if (v < nvv) {
+                const float4 po = __ldcs(&P.pos_obj[kVS * (v)]);
+                if (__float_as_uint(po.w) != kInvalidObj) {
+                    const unsigned long long key =
+                        grid_key(cell_coord(po.x, radius), cell_coord(po.y, radius), cell_coord(po.z, radius));
+                    uint32_t s = slot_of(key, bits);
+                    unsigned long long k;
+                    while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
+                    if (k == key) {
+                        fm |= 1u << q;
+                        cell[q] = __ldg(&dense[s]);  // sort key: dense cell id (slot order)
+                        atomicAdd(&pcnt[s], 1u);
+                    }
+                }
             }
         }
-        flag[v] = f;
+#pragma unroll
+        for (int q = 0; q < kHalf; ++q) {
+            const bool f = (fm >> q) & 1u;
+            const uint32_t ball = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) wsum[warp] = __popc(ball);
+            __syncthreads();
+            uint32_t before = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kT / 32; ++w) {
+                const uint32_t c = wsum[w];
+                before += w < (int)warp ? c : 0u;
+                tot += c;
+            }
+            if (f) {
+                const uint32_t o = run + before + __popc(ball & ((1u << lane) - 1u));
+                ck[base + o] = cell[q];
+                cv[base + o] = (uint32_t)(base + (uint64_t)(h * kHalf + q) * kT + threadIdx.x);
+            }
+            run += tot;
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        tile_cnt[blockIdx.x] = run;
+        if (run) atomicAdd(total, run);
     }
 }
 
@@ -700,7 +746,6 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         return;
     }
     {  // mode 1: ordered, bit-exact gather
-        uint32_t* pslot = reinterpret_cast<uint32_t*>(take(4 * nv));
         uint32_t* sk = reinterpret_cast<uint32_t*>(take(4 * nv));
         uint32_t* sv = reinterpret_cast<uint32_t*>(take(4 * nv));
         uint32_t* sk2 = reinterpret_cast<uint32_t*>(take(4 * nv));
@@ -709,14 +754,15 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         float4* sen = reinterpret_cast<float4*>(take(16 * nv));
         uint32_t* pcnt = reinterpret_cast<uint32_t*>(take(4 * slots));
         uint32_t* pstart = reinterpret_cast<uint32_t*>(take(4 * slots));
-        uint8_t* flag = reinterpret_cast<uint8_t*>(take(nv));
+        const uint32_t tiles = (uint32_t)((nv + kSortTile - 1) / kSortTile);
+        uint32_t* tile_cnt = reinterpret_cast<uint32_t*>(take(4ull * tiles + 4));
         void* gscratch = take(0);
         cudaMemsetAsync(pcnt, 0, 4 * slots, st);
+        cudaMemsetAsync(m_count, 0, 4, st);
         const uint32_t* dense = reinterpret_cast<const uint32_t*>(keys + slots);
-        k_gather_flag<<<launch_grid(nv, kT), kT, 0, st>>>(P, radius, keys, bits, dense, flag, pslot, pcnt);
-        // candidates as (cell, record) pairs in record order, stably sorted by cell; the
-        // sort's last pass writes the candidates' {position, object} and energy contiguous
-        compact_u8_pairs(flag, pslot, (uint32_t)nv, sk, sv, m_count, gscratch, st);
+        // candidates as (cell, record) pairs in record order per tile, stably sorted by cell;
+        // the sort's last pass writes the candidates' {position, object} and energy contiguous
+        k_gather_bin<<<tiles, kT, 0, st>>>(P, radius, keys, bits, dense, sk, sv, tile_cnt, m_count, pcnt);
         SortGather pg;
         pg.a = P.pos_obj;
         pg.b = P.energy;
@@ -724,9 +770,9 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         pg.out_a = spo;
         pg.out_b = sen;
         radix_sort_gather(sk, sv, sk2, sv2, (uint32_t)nv, m_count, cell_bits > 0 ? cell_bits : bits, pg, gscratch,
-                          st);
+                          st, tile_cnt);
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
-        g_launches += 1;  // flag (the prims count their own)
+        g_launches += 1;  // bin (the prims count their own)
         if (!groups) {
             uint32_t* wq = m_count + 4;
             cudaMemsetAsync(wq, 0, 4, st);

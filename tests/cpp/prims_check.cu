@@ -94,6 +94,41 @@ static int check_sort(std::mt19937_64& rng, uint32_t n_max, uint32_t n, int bits
         }
         cudaFree(dp), cudaFree(oa), cudaFree(ob), cudaFree(k2), cudaFree(v2);
     }
+    // ragged tiles: tile t of kSortTile slots holds a random in-order subset of its pairs
+    {
+        const uint32_t T = prx::kSortTile, tiles = (n_max + T - 1) / T;
+        std::vector<uint32_t> rk(n_max, 0xDEADBEEFu), rv(n_max, 0xDEADBEEFu), cnt(tiles, 0), sub_k, sub_v;
+        for (uint32_t t = 0; t < tiles; ++t)
+            for (uint32_t i = t * T; i < std::min<uint64_t>((uint64_t)(t + 1) * T, n_max); ++i)
+                if (rng() % 3 != 0) {
+                    rk[t * T + cnt[t]] = k[i];
+                    rv[t * T + cnt[t]] = i;
+                    ++cnt[t];
+                    sub_k.push_back(k[i]);
+                    sub_v.push_back(i);
+                }
+        const uint32_t tot = static_cast<uint32_t>(sub_k.size());
+        std::vector<float4> pay(n_max);
+        for (uint32_t q = 0; q < n_max; ++q) pay[q] = make_float4((float)q, 0.f, 0.f, (float)(q & 4095));
+        uint32_t *k2 = dev(rk), *v2 = dev(rv), *dc = dev(cnt), *dt = dev(std::vector<uint32_t>{tot});
+        float4 *dp = dev(pay), *oa = dev(std::vector<float4>(n_max)), *ob = dev(std::vector<float4>(n_max));
+        prx::SortGather g;
+        g.a = dp;
+        g.b = dp;
+        g.stride = 1;
+        g.out_a = oa;
+        g.out_b = ob;
+        prx::radix_sort_gather(k2, v2, dk2, dv2, n_max, dt, bits, g, scratch, 0, dc);
+        CK(cudaDeviceSynchronize());
+        std::vector<uint32_t> o(tot);
+        std::iota(o.begin(), o.end(), 0u);
+        std::stable_sort(o.begin(), o.end(), [&](uint32_t a, uint32_t b) { return sub_k[a] < sub_k[b]; });
+        const auto ga = host(oa, tot);
+        for (uint32_t j = 0; j < tot; ++j)
+            if (ga[j].x != pay[sub_v[o[j]]].x || ga[j].w != pay[sub_v[o[j]]].w)
+                return fail("radix_sort_gather ragged", n_max, tot, bits, j);
+        cudaFree(k2), cudaFree(v2), cudaFree(dc), cudaFree(dt), cudaFree(dp), cudaFree(oa), cudaFree(ob);
+    }
     // elements beyond n stay untouched in keys/vals
     const auto tail = host(dk + n, n_max - n);
     for (uint32_t j = 0; j < n_max - n; ++j)
