@@ -325,13 +325,13 @@ __global__ void __launch_bounds__(kT) k_gather_bin(PathDev P, float radius, cons
                                                    uint32_t* __restrict__ ck, uint32_t* __restrict__ cv,
                                                    uint32_t* __restrict__ tile_cnt, uint32_t* __restrict__ total,
                                                    uint32_t* __restrict__ pcnt) {
-    __shared__ uint32_t wsum[kT / 32];
+    constexpr int kHalf = kBinItems / 2;  // two halves: loads of a half in flight together
+    __shared__ uint32_t wsum[kHalf][kT / 32];
     const uint32_t mask = (1u << bits) - 1u;
     const uint64_t nvv = (uint64_t)P.n * P.B;
     const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t run = 0;
-    constexpr int kHalf = kBinItems / 2;  // two halves: loads of a half in flight together
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         uint32_t cell[kHalf];
@@ -356,27 +356,32 @@ __global__ void __launch_bounds__(kT) k_gather_bin(PathDev P, float radius, cons
                 }
             }
         }
+        // one exchange per half: every warp publishes its per-round counts, then each
+        // candidate's offset = run + earlier rounds (all warps) + earlier warps + lane rank
+        uint32_t ball[kHalf];
 #pragma unroll
         for (int q = 0; q < kHalf; ++q) {
-            const bool f = (fm >> q) & 1u;
-            const uint32_t ball = __ballot_sync(0xffffffffu, f);
-            if (lane == 0) wsum[warp] = __popc(ball);
-            __syncthreads();
+            ball[q] = __ballot_sync(0xffffffffu, (fm >> q) & 1u);
+            if (lane == 0) wsum[q][warp] = __popc(ball[q]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kHalf; ++q) {
             uint32_t before = 0, tot = 0;
 #pragma unroll
             for (int w = 0; w < kT / 32; ++w) {
-                const uint32_t c = wsum[w];
+                const uint32_t c = wsum[q][w];
                 before += w < (int)warp ? c : 0u;
                 tot += c;
             }
-            if (f) {
-                const uint32_t o = run + before + __popc(ball & ((1u << lane) - 1u));
+            if ((fm >> q) & 1u) {
+                const uint32_t o = run + before + __popc(ball[q] & ((1u << lane) - 1u));
                 ck[base + o] = cell[q];
                 cv[base + o] = (uint32_t)(base + (uint64_t)(h * kHalf + q) * kT + threadIdx.x);
             }
             run += tot;
-            __syncthreads();
         }
+        __syncthreads();
     }
     if (threadIdx.x == 0) {
         tile_cnt[blockIdx.x] = run;
