@@ -197,8 +197,9 @@ __global__ void __launch_bounds__(kT) k_splat_pixels(const float4* __restrict__ 
             while ((k = __ldg(&keys[s])) != key && k != kEmptyKey) s = (s + 1) & mask;
             if (k != key) continue;
             const uint32_t b0 = __ldg(&pstart[s]), n = __ldg(&pcnt[s]);
-            // kU candidate loads in flight per lane before the tests (latency overlap)
-            constexpr int kU = 4;
+            // kU candidate loads in flight per lane before the tests, then the contributors'
+            // energy loads of the whole step in flight before the adds (latency overlap)
+            constexpr int kU = PRX_GATHER_UNROLL;
             for (uint32_t base = 0; base < n; base += 32 * kU) {
                 float4 po[kU];
 #pragma unroll
@@ -206,15 +207,18 @@ __global__ void __launch_bounds__(kT) k_splat_pixels(const float4* __restrict__ 
                     const uint32_t j = base + 32 * u + lane;
                     po[u] = j < n ? __ldg(&spo[b0 + j]) : make_float4(0.f, 0.f, 0.f, __uint_as_float(kInvalidObj));
                 }
+                float4 en[kU];
 #pragma unroll
                 for (int u = 0; u < kU; ++u) {
                     const V3 d = sub(V3{po[u].x, po[u].y, po[u].z}, x);  // gather.hpp:54
-                    if (dot(d, d) <= r2 && __float_as_uint(po[u].w) == obj) {
-                        const float4 e = __ldg(&sen[b0 + base + 32 * u + lane]);
-                        ax += e.x;
-                        ay += e.y;
-                        az += e.z;
-                    }
+                    const bool hit = dot(d, d) <= r2 && __float_as_uint(po[u].w) == obj;
+                    en[u] = hit ? __ldg(&sen[b0 + base + 32 * u + lane]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    ax += en[u].x;
+                    ay += en[u].y;
+                    az += en[u].z;
                 }
             }
         }

@@ -15,10 +15,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-splat-sweep --extra none > "$out/${tag}_ncu_launches.log" 2>&1
 common="--set full --import-source on --clock-control none"
 bench="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-splat-sweep --extra none"
-for k in k_trace k_verify_error_walk k_occlusion_flags k_compute_dm k_gather_flag k_gather_copy k_gather_staged \
+for k in k_trace k_verify_error_walk k_occlusion_flags k_compute_dm k_gather_bin k_gather_staged \
          k_rs_scatter k_fill_assign k_update_origins; do
     skip=3
-    [ "$k" = k_rs_scatter ] && skip=18   # 6 radix passes per frame (prune + gather sorts)
+    [ "$k" = k_rs_scatter ] && skip=18   # 5 radix passes per frame (3 prune + 2 gather: 18 = frame 3's first gather pass)
     [ "$k" = k_fill_assign ] && skip=6   # one per light
     case "$k" in k_verify_error_walk|k_occlusion_flags|k_update_origins) skip=2 ;; esac  # from frame 1 on
     ncu $common -k "regex:${k}(<|$)" --launch-skip $skip -c 1 -o "$out/${tag}_full_${k}" $bench \
