@@ -410,6 +410,32 @@ __device__ __forceinline__ bool cell_reaches(long long ix, long long iy, long lo
     return gx * gx + gy * gy + gz * gz <= (double)r2 * (1.0 + 1e-4) + 1e-30;
 }
 
+// Conservative reach tests against a box of hit points (pixel groups): false only when every
+// point of the box is farther than r from the cell / point even after rounding.
+__device__ __forceinline__ bool cell_reaches_box(long long ix, long long iy, long long iz, const float4& bmin,
+                                                 const float4& bmax, float radius) {
+    const double rd = radius;
+    auto gap = [&](long long i, float l, float h) {  // cell widened for the rounding of floor(p / r)
+        const double m = 1e-5 * rd * (double)(llabs(i) + 2);
+        const double lo = (double)i * rd - m, hi = (double)(i + 1) * rd + m;
+        return h < lo ? lo - h : (l > hi ? l - hi : 0.0);
+    };
+    const double gx = gap(ix, bmin.x, bmax.x), gy = gap(iy, bmin.y, bmax.y), gz = gap(iz, bmin.z, bmax.z);
+    return gx * gx + gy * gy + gz * gz <= rd * rd * (1.0 + 1e-4) + 1e-30;
+}
+
+__device__ __forceinline__ bool point_reaches_box(const float4& p, const float4& bmin, const float4& bmax,
+                                                  float radius) {
+    // per-axis gap to the box with an absolute slack for the rounding of p - x in the pixel test
+    auto gap = [](float v, float l, float h) {
+        const float slack = 1e-5f * (fabsf(v) + fabsf(l) + fabsf(h)) + 1e-30f;
+        const float g = v < l ? l - v : (v > h ? v - h : 0.0f);
+        return fmaxf(g - slack, 0.0f);
+    };
+    const float gx = gap(p.x, bmin.x, bmax.x), gy = gap(p.y, bmin.y, bmax.y), gz = gap(p.z, bmin.z, bmax.z);
+    return gx * gx + gy * gy + gz * gz <= radius * radius * 1.0001f;
+}
+
 __global__ void __launch_bounds__(kT) k_gather_staged(const float4* __restrict__ gbuf, uint32_t npx, float radius,
                                                       const unsigned long long* __restrict__ keys, int bits,
                                                       const uint32_t* __restrict__ pstart,
@@ -570,10 +596,24 @@ __global__ void __launch_bounds__(kT) k_gather_groups(const float4* __restrict__
         // every pixel of the chunk has this home cell (grouped by it)
         const float4 g0 = gbuf[pv[ch.x]];
         const long long cx = cell_coord(g0.x, radius), cy = cell_coord(g0.y, radius), cz = cell_coord(g0.z, radius);
+        // the chunk's hit points' box: candidate photons (and whole cells) farther than r from
+        // it reach none of its pixels and are dropped before the per-pixel loop (in order, so
+        // each pixel's additions are unchanged); the reach test is conservative (float slack)
+        float lo[3] = {x.x, x.y, x.z}, hi[3] = {x.x, x.y, x.z};
+        if (!mine) lo[0] = lo[1] = lo[2] = INFINITY, hi[0] = hi[1] = hi[2] = -INFINITY;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+                hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+            }
+        const float4 gmin = make_float4(lo[0], lo[1], lo[2], 0.f), gmax = make_float4(hi[0], hi[1], hi[2], 0.f);
         float ax = 0.0f, ay = 0.0f, az = 0.0f;  // radiance += E (gather.cpp:68), per lane
         for (int dz = -1; dz <= 1; ++dz)
             for (int dy = -1; dy <= 1; ++dy)
                 for (int dx = -1; dx <= 1; ++dx) {  // gather.hpp:48-50 visiting order
+                    if (!cell_reaches_box(cx + dx, cy + dy, cz + dz, gmin, gmax, radius)) continue;
                     const unsigned long long key = grid_key(cx + dx, cy + dy, cz + dz);
                     uint32_t s = slot_of(key, bits);
                     unsigned long long k;
@@ -582,13 +622,22 @@ __global__ void __launch_bounds__(kT) k_gather_groups(const float4* __restrict__
                     const uint32_t b0 = __ldg(&pstart[s]), n = __ldg(&pcnt[s]);
                     for (uint32_t base = 0; base < n; base += 32) {
                         const uint32_t j = base + lane;
-                        __syncwarp();
+                        float4 cp = make_float4(0.f, 0.f, 0.f, 0.f), ce = cp;
+                        bool keep = false;
                         if (j < n) {
-                            wpos[lane] = __ldg(&spo[b0 + j]);
-                            wen[lane] = __ldg(&sen[b0 + j]);
+                            cp = __ldg(&spo[b0 + j]);
+                            keep = point_reaches_box(cp, gmin, gmax, radius);
+                            if (keep) ce = __ldg(&sen[b0 + j]);
+                        }
+                        const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+                        __syncwarp();
+                        if (keep) {
+                            const uint32_t at = __popc(kb & ((1u << lane) - 1u));
+                            wpos[at] = cp;
+                            wen[at] = ce;
                         }
                         __syncwarp();
-                        const uint32_t m = n - base < 32 ? n - base : 32;
+                        const uint32_t m = __popc(kb);
                         if (mine) {
                             for (uint32_t q = 0; q < m; ++q) {
                                 const float4 po = wpos[q];
