@@ -176,8 +176,8 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     PRX_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PRX_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     if (const char* e = std::getenv("PRX_SPLAT_PREFIX")) pre_on_ = e[0] != '0';
-    PRX_CUDA(cudaHostAlloc(&h_ncell_, 4, cudaHostAllocDefault));
-    *h_ncell_ = 0;
+    PRX_CUDA(cudaHostAlloc(&h_ncell_, 8, cudaHostAllocDefault));
+    h_ncell_[0] = h_ncell_[1] = 0;
     launch_base_ = g_launches;
 
     // light blocks (engine.cpp:76-101)
@@ -1324,16 +1324,18 @@ bool Engine::splat_prefix_fork() {
     if (c.width == 0 || c.height == 0) return false;
     const uint32_t npx = c.width * c.height;
     if (d_pre_gbuf_.size() == 0) {
+        pre_bits_ = splat_table_bits_capped(npx);
         d_pre_gbuf_.alloc(16ull * npx);
-        d_pre_work_.alloc(splat_work_bytes(npx));
+        d_pre_work_.alloc(splat_work_bytes(pre_bits_));
     }
     PRX_CUDA(cudaEventRecord(ev_fork_, stream_));
     PRX_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
     launch_splat_prefix(scene_dev(), camera_dev(c), pre_radius_, d_pre_gbuf_.as<float4>(), d_pre_work_.get(),
-                        side_stream_);
-    // the registered-cell count sizes the splat's sort keys (read after the frame's sync)
-    PRX_CUDA(cudaMemcpyAsync(h_ncell_, d_pre_work_.as<char>() + splat_ncell_offset(npx), 4, cudaMemcpyDeviceToHost,
-                             side_stream_));
+                        pre_bits_, side_stream_);
+    // the registered-cell count sizes the splat's sort keys and shows a table overflow (read
+    // after the frame's sync)
+    PRX_CUDA(cudaMemcpyAsync(h_ncell_, d_pre_work_.as<char>() + splat_ncell_offset(pre_bits_), 4,
+                             cudaMemcpyDeviceToHost, side_stream_));
     d2h_bytes_ += 4;
     return true;
 }
@@ -1376,10 +1378,12 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
             drop_graphs();  // their side branch bakes the old radius in
         }
     }
+    if (use_pre && splat_table_overflow(h_ncell_[0], pre_bits_)) use_pre = false;  // (rebuilt below)
     if (c.width != img_w_ || c.height != img_h_) {
         d_gbuf_.alloc(16ull * npx);
         d_img_.alloc(12ull * npx);
-        d_splat_work_.alloc(splat_work_bytes(npx));
+        d_splat_work_.reset();
+        splat_work_bits_ = 0;
         d_gather_.reset();
         img_w_ = c.width;
         img_h_ = c.height;
@@ -1387,17 +1391,46 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
     const uint64_t nv = static_cast<uint64_t>(P.n) * P.B;
     const float inv_area = 1.0f / (static_cast<float>(M_PI) * radius * radius);
     const float inv_pi = 1.0f / static_cast<float>(M_PI);
-    if (d_gather_.size() == 0) d_gather_.alloc(gather_work_bytes(nv, npx));  // both modes
     float* out = rgb_dev ? rgb_dev : d_img_.as<float>();
     const SceneDev S = scene_dev();
     // (plain launches: a captured graph of these ~25 launches measured slower, 1.93 vs 1.89 ms)
     record(kEvSplat0);
-    if (use_pre)
-        launch_splat(S, P, C, radius, d_pre_gbuf_.as<float4>(), out, inv_pi, inv_area, d_pre_work_.get(),
-                     d_splat_cand_.get(), mode, d_gather_.get(), true, splat_cell_bits(*h_ncell_), stream_);
-    else
-        launch_splat(S, P, C, radius, d_gbuf_.as<float4>(), out, inv_pi, inv_area, d_splat_work_.get(),
-                     d_splat_cand_.get(), mode, d_gather_.get(), false, 0, stream_);
+    int bits = pre_bits_, cell_bits = 0;
+    float4* gbuf = d_pre_gbuf_.as<float4>();
+    void* work = d_pre_work_.get();
+    if (use_pre) {
+        cell_bits = splat_cell_bits(h_ncell_[0]);
+    } else {
+        // the prefix inline: a capped table first; when capped, one read-back of its load (a
+        // rebuild at the worst-case size on overflow) that also sizes the sort keys
+        bits = splat_table_bits_capped(npx);
+        auto run_prefix = [&](int b) {
+            if (splat_work_bits_ < b) {
+                d_splat_work_.alloc(splat_work_bytes(b));
+                splat_work_bits_ = b;
+            }
+            launch_splat_prefix(S, C, radius, d_gbuf_.as<float4>(), d_splat_work_.get(), b, stream_);
+        };
+        run_prefix(bits);
+        if (bits < splat_table_bits(npx)) {
+            copy_async(h_ncell_ + 1, d_splat_work_.as<char>() + splat_ncell_offset(bits), 4, cudaMemcpyDeviceToHost);
+            PRX_CUDA(cudaStreamSynchronize(stream_));
+            if (splat_table_overflow(h_ncell_[1], bits)) {
+                bits = splat_table_bits(npx);
+                run_prefix(bits);
+            } else {
+                cell_bits = splat_cell_bits(h_ncell_[1]);
+            }
+        }
+        gbuf = d_gbuf_.as<float4>();
+        work = d_splat_work_.get();
+    }
+    if (d_gather_.size() == 0 || gather_bits_ < bits) {  // both modes
+        d_gather_.alloc(gather_work_bytes(nv, npx, bits));
+        gather_bits_ = bits;
+    }
+    launch_splat(S, P, C, radius, gbuf, out, inv_pi, inv_area, work, d_splat_cand_.get(), mode, d_gather_.get(), bits,
+                 true, cell_bits, stream_);
     if (reduce_ranks)  // every rank splats its own photons; the image is their sum
         coll_ok(coll_.all_reduce_sum_f32(coll_.ctx, out, 3ull * npx, stream_), "image all-reduce");
     record(kEvSplat1);

@@ -232,7 +232,10 @@ private:
     float pre_radius_ = 0.0f;  // 0: no scene-camera splat yet, no prefix
     bool pre_ok_ = false;      // d_pre_* match the current placement of the scene
     bool pre_on_ = true;       // PRX_SPLAT_PREFIX=0: always compute the prefix in the splat
-    uint32_t* h_ncell_ = nullptr;  // pinned: registered cells of the prefix (sort key bits)
+    uint32_t* h_ncell_ = nullptr;  // pinned: registered cells of the prefix [side stream, inline]
+    int pre_bits_ = 0;             // the side-stream prefix's cell-table bits
+    int splat_work_bits_ = 0;      // d_splat_work_ is sized for a table of this many bits
+    int gather_bits_ = 0;          // d_gather_ is sized for a table of this many bits
     bool splat_prefix_fork();
     void splat_prefix_join();
     void drop_graphs();

@@ -77,18 +77,22 @@ void launch_pack_photons(PathDev P, void* photons, void* aux, cudaStream_t st);
 void launch_unpack_photons(PathDev P, const void* photons, const void* aux, cudaStream_t st);
 
 // G-buffer + splat + resolve (splat.cu), replacing gather_image (gather.cpp:35-75)
-int splat_table_bits(uint32_t npx);
-size_t splat_work_bytes(uint32_t npx);
-size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx);
-// mode 0: tiled shared-memory atomic splat; mode 1: ordered gather (bit-exact vs gather_image)
-size_t splat_ncell_offset(uint32_t npx);  // byte offset of the registered-cell count in `work`
+int splat_table_bits(uint32_t npx);         // worst-case cell-table bits (27 cells per pixel)
+int splat_table_bits_capped(uint32_t npx);  // the first try: at most 2^22 slots
+bool splat_table_overflow(uint32_t n_cells, int bits);  // load above 3/4: rebuild at full size
+size_t splat_work_bytes(int bits);
+size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx, int bits);
+size_t splat_ncell_offset(int bits);       // byte offset of the registered-cell count in `work`
 int splat_cell_bits(uint32_t n_cells);     // key bits of n_cells dense cell ids
-// prefix_done: the G-buffer, the cell-key table and the dense cell ids (launch_splat_prefix)
-// are already in gbuf/work; cell_bits > 0: the dense ids fit that many bits (else the table's)
+// mode 0: tiled shared-memory atomic splat; mode 1: ordered gather (bit-exact vs gather_image)
+// `bits`: the cell table's size; prefix_done: the G-buffer, the cell-key table and the dense
+// cell ids (launch_splat_prefix) are already in gbuf/work; cell_bits > 0: the dense ids fit
+// that many bits (else the table's)
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img,
-                  float inv_pi, float inv_area, void* work, void* cand_buf, int mode, void* gather_buf,
+                  float inv_pi, float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, int bits,
                   bool prefix_done, int cell_bits, cudaStream_t st);
-void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf, void* work, cudaStream_t st);
+void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf, void* work, int bits,
+                         cudaStream_t st);
 
 // Dynamic LBVH (lbvh.cu)
 struct LbvhBuffers {

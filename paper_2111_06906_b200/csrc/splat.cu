@@ -80,7 +80,9 @@ __global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float 
         const long long cz = cell_coord(g.z, r) + (long long)(o / 9) - 1;
         const unsigned long long key = grid_key(cx, cy, cz);
         uint32_t s = slot_of(key, bits);
-        while (true) {
+        // (bounded: a full table drops the key; the occupied-slot count then equals the table
+        // size, which the host reads as an overflow and rebuilds at full size)
+        for (uint32_t probe = 0; probe <= mask; ++probe) {
             const unsigned long long prev = atomicCAS(&keys[s], kEmptyKey, key);
             if (prev == kEmptyKey || prev == key) break;
             s = (s + 1) & mask;
@@ -663,23 +665,34 @@ __global__ void __launch_bounds__(kT) k_gather_groups(const float4* __restrict__
 
 }  // namespace
 
+// Cell-key table sizes: the worst case is 27 distinct cells per pixel (load <= 1/2); large
+// images register far fewer (neighbouring pixels share cells), so they start from a table of
+// at most 2^kTableCapBits slots and fall back to the worst-case size when its load passes 3/4.
+constexpr int kTableCapBits = 22;
 int splat_table_bits(uint32_t npx) {
     uint64_t want = 2ull * 27ull * npx;
     int bits = 10;
     while ((1ull << bits) < want && bits < 30) ++bits;
     return bits;
 }
+int splat_table_bits_capped(uint32_t npx) {
+    int cap = kTableCapBits;
+    if (const char* e = std::getenv("PRX_SPLAT_TABLE_CAP")) cap = std::atoi(e) >= 10 ? std::atoi(e) : 10;  // (tests)
+    const int b = splat_table_bits(npx);
+    return b < cap ? b : cap;
+}
+bool splat_table_overflow(uint32_t n_cells, int bits) { return 4ull * n_cells > (3ull << bits); }
 
 // the prefix's work buffer: cell-key table (8 B/slot) | dense cell ids (4 B/slot) | the
 // registered-cell count | scan scratch
-size_t splat_ncell_offset(uint32_t npx) { return (1ull << splat_table_bits(npx)) * 12; }
-size_t splat_work_bytes(uint32_t npx) {
-    const uint64_t slots = 1ull << splat_table_bits(npx);
+size_t splat_ncell_offset(int bits) { return (1ull << bits) * 12; }
+size_t splat_work_bytes(int bits) {
+    const uint64_t slots = 1ull << bits;
     return slots * 12 + 256 + prim_scratch_bytes(slots) + 256;
 }
 
-size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
-    const uint64_t slots = 1ull << splat_table_bits(npx);
+size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx, int bits) {
+    const uint64_t slots = 1ull << bits;
     const uint64_t nv = n_vertices;
     uint64_t scan_n = nv > slots ? nv : slots;
     if (npx > scan_n) scan_n = npx;
@@ -689,13 +702,13 @@ size_t gather_work_bytes(uint64_t n_vertices, uint32_t npx) {
 // The photon-independent part of a splat: the G-buffer and the key table of the cells the
 // pixels' gather spheres touch. It depends only on the placed scene, the camera and the radius,
 // so the engine can run it on a side stream during verify/retrace (Engine::splat_prefix_fork).
-void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf, void* work, cudaStream_t st) {
+void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf, void* work, int bits,
+                         cudaStream_t st) {
     const uint32_t npx = C.w * C.h;
-    const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
     auto* keys = static_cast<unsigned long long*>(work);
     auto* dense = reinterpret_cast<uint32_t*>(keys + slots);
-    auto* ncell = reinterpret_cast<uint32_t*>(static_cast<char*>(work) + splat_ncell_offset(npx));
+    auto* ncell = reinterpret_cast<uint32_t*>(static_cast<char*>(work) + splat_ncell_offset(bits));
     k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
     cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
     k_pixcells<<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
@@ -712,15 +725,14 @@ int splat_cell_bits(uint32_t n_cells) {
 }
 
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
-                  float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, bool prefix_done,
-                  int cell_bits, cudaStream_t st) {
+                  float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, int bits,
+                  bool prefix_done, int cell_bits, cudaStream_t st) {
     const uint32_t npx = C.w * C.h;
-    const int bits = splat_table_bits(npx);
     const uint64_t slots = 1ull << bits;
     auto* keys = static_cast<unsigned long long*>(work);
     (void)cand_buf;
 
-    if (!prefix_done) launch_splat_prefix(S, C, radius, gbuf, work, st);
+    if (!prefix_done) launch_splat_prefix(S, C, radius, gbuf, work, bits, st);
     const uint64_t nv = (uint64_t)P.n * P.B;
     // carve the work buffer in 256-byte aligned pieces (float4 / u32 views of any n)
     char* w = static_cast<char*>(gather_buf);

@@ -150,3 +150,24 @@ def test_atomic_splat_pixel_groups(monkeypatch, tiles, w, h):
     cam = gpu.scene.describe().camera
     c = L.Camera(cam.position, cam.look_at, cam.fov_deg, w, h)
     check_within_tolerance(gpu.splat(camera=c, radius=0.25, mode=0), cpu.gather(camera=c, radius=0.25)[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cap", ["10", "14"])
+def test_cell_table_overflow_rebuild(monkeypatch, cap):
+    """Large images start from a capped cell-key table and rebuild it at the worst-case size
+    when its load passes 3/4 (PRX_SPLAT_TABLE_CAP lowers the cap to 2^10 / 2^14 slots, far
+    below the ~30K cells a 320x240 view of C4 registers, so the rebuild runs); both modes stay
+    exact / within tolerance."""
+    from paper_2111_06906_b200 import _lib as L
+
+    monkeypatch.setenv("PRX_SPLAT_TABLE_CAP", cap)
+    gpu, cpu = pair("C4", synthetic=True, mode="error", paths=40000, bounces=5, dm=[2, 2, 8, 8], seed=3)
+    for _ in range(2):
+        gpu.run_frame()
+        cpu.run_frame()
+    cam = gpu.scene.describe().camera
+    big = L.Camera(cam.position, cam.look_at, cam.fov_deg, 320, 240)
+    ref = cpu.gather(camera=big, radius=0.25)[0]
+    assert np.array_equal(gpu.splat(camera=big, radius=0.25, mode=1), ref)
+    check_within_tolerance(gpu.splat(camera=big, radius=0.25, mode=0), ref)
