@@ -67,26 +67,41 @@ __global__ void k_gbuffer(SceneDev S, CamDev C, float4* gbuf) {
 }
 
 // every hit pixel registers its 27 neighbour-cell keys in an open-addressing table (the
-// cells any pixel can read: the photons of other cells never contribute)
+// cells any pixel can read: the photons of other cells never contribute).  Pixels of a warp
+// that share a home cell register its neighbours once, split over those pixels.
+__device__ __forceinline__ void insert_key(unsigned long long* keys, unsigned long long key, int bits) {
+    const uint32_t mask = (1u << bits) - 1u;
+    uint32_t s = slot_of(key, bits);
+    // (bounded: a full table drops the key; the occupied-slot count then equals the table
+    // size, which the host reads as an overflow and rebuilds at full size)
+    for (uint32_t probe = 0; probe <= mask; ++probe) {
+        const unsigned long long prev = atomicCAS(&keys[s], kEmptyKey, key);
+        if (prev == kEmptyKey || prev == key) break;
+        s = (s + 1) & mask;
+    }
+}
+
 __global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float r, unsigned long long* keys,
                            int bits) {
-    const uint32_t mask = (1u << bits) - 1u;
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < 27u * npx; w += gridDim.x * blockDim.x) {
-        const uint32_t pix = w / 27u, o = w % 27u;
-        const float4 g = gbuf[pix];
-        if (__float_as_uint(g.w) == kInvalidObj) continue;
-        const long long cx = cell_coord(g.x, r) + (long long)(o % 3) - 1;
-        const long long cy = cell_coord(g.y, r) + (long long)((o / 3) % 3) - 1;
-        const long long cz = cell_coord(g.z, r) + (long long)(o / 9) - 1;
-        const unsigned long long key = grid_key(cx, cy, cz);
-        uint32_t s = slot_of(key, bits);
-        // (bounded: a full table drops the key; the occupied-slot count then equals the table
-        // size, which the host reads as an overflow and rebuilds at full size)
-        for (uint32_t probe = 0; probe <= mask; ++probe) {
-            const unsigned long long prev = atomicCAS(&keys[s], kEmptyKey, key);
-            if (prev == kEmptyKey || prev == key) break;
-            s = (s + 1) & mask;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < npx; base += stride) {  // warp-uniform trips
+        const uint32_t pix = base + threadIdx.x;
+        bool hit = false;
+        long long cx = 0, cy = 0, cz = 0;
+        if (pix < npx) {
+            const float4 g = gbuf[pix];
+            hit = __float_as_uint(g.w) != kInvalidObj;
+            cx = cell_coord(g.x, r), cy = cell_coord(g.y, r), cz = cell_coord(g.z, r);
         }
+        const unsigned long long home = hit ? grid_key(cx, cy, cz) : kEmptyKey;
+        const uint32_t peers = __match_any_sync(0xffffffffu, home);
+        if (!hit) continue;
+        const uint32_t n = __popc(peers), rank = __popc(peers & ((1u << lane) - 1u));
+        for (uint32_t o = rank; o < 27u; o += n)
+            insert_key(keys, grid_key(cx + (long long)(o % 3) - 1, cy + (long long)((o / 3) % 3) - 1,
+                                      cz + (long long)(o / 9) - 1),
+                       bits);
     }
 }
 
@@ -711,7 +726,7 @@ void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf
     auto* ncell = reinterpret_cast<uint32_t*>(static_cast<char*>(work) + splat_ncell_offset(bits));
     k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
     cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
-    k_pixcells<<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
+    k_pixcells<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
     // dense cell ids in slot order (the ordered gather sorts by these: fewer key bits)
     k_slot_used<<<launch_grid(slots, kT), kT, 0, st>>>(keys, (uint32_t)slots, dense);
     scan_exclusive_u32(dense, dense, (uint32_t)slots, nullptr, ncell, ncell + 64, st);
