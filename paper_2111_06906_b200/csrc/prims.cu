@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(kPrimThreads, 3) k_rs_scatter(const uint32_t* 
     const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
     if (!ragged && base >= n_of(n_max, n_dev)) return;
     const uint32_t cnt = rs_tile_count(n_max, n_dev, ragged);
+    if (cnt == 0) return;  // (an empty ragged tile)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t d0 = threadIdx.x * DPT;  // this thread's digits in the per-digit loops
     {
