@@ -81,6 +81,20 @@ __device__ __forceinline__ void insert_key(unsigned long long* keys, unsigned lo
     }
 }
 
+// small images: one thread per (pixel, neighbour) -- enough threads to hide the CAS latency
+__global__ void k_pixcells_each(const float4* __restrict__ gbuf, uint32_t npx, float r, unsigned long long* keys,
+                                int bits) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < 27u * npx; w += gridDim.x * blockDim.x) {
+        const uint32_t pix = w / 27u, o = w % 27u;
+        const float4 g = gbuf[pix];
+        if (__float_as_uint(g.w) == kInvalidObj) continue;
+        insert_key(keys,
+                   grid_key(cell_coord(g.x, r) + (long long)(o % 3) - 1, cell_coord(g.y, r) + (long long)((o / 3) % 3) - 1,
+                            cell_coord(g.z, r) + (long long)(o / 9) - 1),
+                   bits);
+    }
+}
+
 __global__ void k_pixcells(const float4* __restrict__ gbuf, uint32_t npx, float r, unsigned long long* keys,
                            int bits) {
     const uint32_t lane = threadIdx.x & 31;
@@ -726,7 +740,10 @@ void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf
     auto* ncell = reinterpret_cast<uint32_t*>(static_cast<char*>(work) + splat_ncell_offset(bits));
     k_gbuffer<<<launch_grid(npx, kT), kT, 0, st>>>(S, C, gbuf);
     cudaMemsetAsync(keys, 0xFF, 8 * slots, st);
-    k_pixcells<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
+    if (npx < (1u << 16))
+        k_pixcells_each<<<launch_grid(27ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
+    else
+        k_pixcells<<<launch_grid(npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits);
     // dense cell ids in slot order (the ordered gather sorts by these: fewer key bits)
     k_slot_used<<<launch_grid(slots, kT), kT, 0, st>>>(keys, (uint32_t)slots, dense);
     scan_exclusive_u32(dense, dense, (uint32_t)slots, nullptr, ncell, ncell + 64, st);
