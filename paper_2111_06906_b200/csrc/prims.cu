@@ -147,7 +147,7 @@ __global__ void k_flag_scatter(const T* __restrict__ flags, uint32_t n_max, cons
                                uint32_t base_id, const uint32_t* __restrict__ offs,
                                uint32_t* __restrict__ out, const uint32_t* __restrict__ key_of = nullptr,
                                uint32_t* __restrict__ keys = nullptr) {
-    __shared__ uint32_t sh[kPrimThreads / 32];
+    __shared__ uint32_t sh[kPrimItems][kPrimThreads / 32];
     const uint32_t n = n_of(n_max, n_dev);
     const uint64_t base = (uint64_t)blockIdx.x * kPrimTile;
     if (base >= n) return;
@@ -166,27 +166,31 @@ __global__ void k_flag_scatter(const T* __restrict__ flags, uint32_t n_max, cons
         for (int k = 0; k < kPrimItems; ++k)
             kv[k] = fl[k] ? __ldg(&key_of[base + (uint64_t)k * kPrimThreads + threadIdx.x]) : 0u;
     }
+    // one exchange for the whole tile: every warp publishes its per-round counts; a flagged
+    // element's slot = run + earlier rounds (all warps) + earlier warps + lane rank
+    uint32_t ball[kPrimItems];
+#pragma unroll
+    for (int k = 0; k < kPrimItems; ++k) {
+        ball[k] = __ballot_sync(0xffffffffu, fl[k]);
+        if (lane == 0) sh[k][warp] = __popc(ball[k]);
+    }
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < kPrimItems; ++k) {
         const uint64_t i = base + (uint64_t)k * kPrimThreads + threadIdx.x;
-        const bool f = fl[k];
-        const uint32_t ball = __ballot_sync(0xffffffffu, f);
-        if (lane == 0) sh[warp] = __popc(ball);
-        __syncthreads();
         uint32_t before = 0, total = 0;
 #pragma unroll
         for (int w = 0; w < kPrimThreads / 32; ++w) {
-            const uint32_t c = sh[w];
+            const uint32_t c = sh[k][w];
             before += w < warp ? c : 0u;
             total += c;
         }
-        if (f) {
-            const uint32_t o = run + before + __popc(ball & ((1u << lane) - 1u));
+        if (fl[k]) {
+            const uint32_t o = run + before + __popc(ball[k] & ((1u << lane) - 1u));
             out[o] = base_id + (uint32_t)i;
             if (key_of) keys[o] = kv[k];
         }
         run += total;
-        __syncthreads();
     }
 }
 
@@ -197,7 +201,8 @@ __global__ void k_flag_scatter(const T* __restrict__ flags, uint32_t n_max, cons
 // large n_max costs what its live elements cost.  The scatter ranks a tile in shared memory
 // (warp w owns the w-th contiguous eighth of the tile's elements, warp-private digit counters
 // with match_any leaders), stages it digit-sorted, and writes each digit's run contiguously.
-// Digits are 8 bits (10-bit digits as an opt-in knob, see digit_bits); the final pass can write two gathered float4 payload streams instead of the pairs.
+// Digits are 8 bits (10-bit digits as an opt-in knob, see digit_bits); the final pass can
+// write two gathered float4 payload streams instead of the pairs.
 constexpr int kRsItems = 16;
 constexpr uint32_t kRsTile = kPrimThreads * kRsItems;  // 4096
 static_assert(kRsTile == kSortTile, "ragged tiles are sort tiles");
