@@ -505,11 +505,16 @@ void rs_pass(const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo,
              const uint32_t* n_dev, const uint32_t* ragged, int shift, int w, uint32_t tiles, const Scratch& s,
              const SortGather& pg, cudaStream_t st) {
     constexpr size_t smem = rs_scatter_smem<B>();
-    static bool attr = [] {
-        cudaFuncSetAttribute(k_rs_scatter<B, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return true;
-    }();
-    (void)attr;
+    if (smem > 48 * 1024) {  // opt-in shared memory, once per device (an uncaptured first use)
+        static std::atomic<uint64_t> set_on{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t bit = 1ull << (dev & 63);
+        if (!(set_on.load() & bit)) {
+            cudaFuncSetAttribute(k_rs_scatter<B, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            set_on.fetch_or(bit);
+        }
+    }
     const uint32_t mask = (1u << w) - 1u;
     k_rs_hist<B><<<tiles, kPrimThreads, 0, st>>>(ki, n_max, n_dev, ragged, shift, mask, tiles, s.hist);
     k_rs_rowscan<<<1u << B, kPrimThreads, 0, st>>>(s.hist, tiles, n_max, n_dev, ragged != nullptr, s.rowtot);
