@@ -581,10 +581,40 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
 // box_entry for the fast (culling-only) walks.  Regular rays (no zero or tiny direction
 // component) take a branch-free slab with single-instruction min/max; the others fall back
 // to box_entry.  Same values and the same relative slack as box_entry.
+#ifndef PRX_F32X2
+#define PRX_F32X2 1
+#endif
+// packed fp32 pairs (sm_100 FADD2 / FMUL2): two IEEE single operations per instruction, the
+// same per-lane rounding as the scalar forms
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long f2_slab(unsigned long long a, unsigned long long o,
+                                                      unsigned long long inv) {  // (a - o) * inv
+    unsigned long long d, t;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(o));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(d), "l"(inv));
+    return t;
+}
+
 __device__ __forceinline__ float box_entry_fast(const RayPre& r, float t_min, float t_lim, float4 A, float4 B) {
     if (!r.regular) return box_entry(r, t_min, t_lim, A, B, 0.0f);
+#if PRX_F32X2
+    float tnx, tny, tfx, tfy;
+    {
+        const unsigned long long oxy = f2_pack(r.o.x, r.o.y), ixy = f2_pack(r.inv[0], r.inv[1]);
+        f2_unpack(f2_slab(f2_pack(A.x, A.y), oxy, ixy), tnx, tny);
+        f2_unpack(f2_slab(f2_pack(B.x, B.y), oxy, ixy), tfx, tfy);
+    }
+#else
     const float tnx = (A.x - r.o.x) * r.inv[0], tfx = (B.x - r.o.x) * r.inv[0];
     const float tny = (A.y - r.o.y) * r.inv[1], tfy = (B.y - r.o.y) * r.inv[1];
+#endif
     const float tnz = (A.z - r.o.z) * r.inv[2], tfz = (B.z - r.o.z) * r.inv[2];
     const float t0 = fmaxf(fmaxf(t_min, fminf(tnx, tfx)), fmaxf(fminf(tny, tfy), fminf(tnz, tfz)));
     const float t1 = fminf(fminf(t_lim, fmaxf(tnx, tfx)), fminf(fmaxf(tny, tfy), fmaxf(tnz, tfz)));
