@@ -584,6 +584,9 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
 #ifndef PRX_F32X2
 #define PRX_F32X2 1
 #endif
+#ifndef PRX_CACHE_CL
+#define PRX_CACHE_CL 1  // the joint walk keeps cull_limit(best_t) instead of recomputing it
+#endif
 // packed fp32 pairs (sm_100 FADD2 / FMUL2): two IEEE single operations per instruction, the
 // same per-lane rounding as the scalar forms
 __device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
@@ -803,6 +806,12 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
     best_slot = 0;
     float second = t_max;
     bool found = false;
+#if PRX_CACHE_CL
+    float cl = cull_limit(best_t);  // cull_limit(best_t), updated with best_t
+#define PRX_CL cl
+#else
+#define PRX_CL cull_limit(best_t)
+#endif
     uint2* const ss = trav_short_stack();
     const uint32_t stride = blockDim.x;
     uint2 overflow[64 - kShortStack];
@@ -814,7 +823,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
         ++sp;
     };
     auto pop = [&]() -> uint32_t {
-        const float lim = cull_limit(best_t);
+        const float lim = PRX_CL;
         while (sp > 0) {
             --sp;
             uint2 e;
@@ -845,7 +854,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
             const float4 n0 = __ldg(&N[0]), n1 = __ldg(&N[1]), n2 = __ldg(&N[2]), n3 = __ldg(&N[3]);
             const uint32_t c0 = __float_as_uint(n0.w) | tree, c1r = __float_as_uint(n1.w);
             const uint32_t c1 = c1r | tree;
-            const float lim = cull_limit(best_t);
+            const float lim = PRX_CL;
             const float tl = box_entry_fast(r, t_min, lim, n0, n1);  // boxes are pre-inflated
             const float tr = c1r != kNone ? box_entry_fast(r, t_min, lim, n2, n3) : INFINITY;
             // near child next, far child pushed; one pop site for "both missed" and "parked"
@@ -888,7 +897,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
                 const float4 t2 = __ldg(&tris[3 * k + 2]);
                 const uint32_t pos = __float_as_uint(ta.w);
                 float t;
-                const float lim = found ? fminf(cull_limit(best_t), t_max) : t_max;
+                const float lim = found ? fminf(PRX_CL, t_max) : t_max;
                 if (intersect_tri(r.o, r.d, t_min, lim, ld3(ta), ld3(t1), ld3(t2), t)) {
                     if (kAny) {
                         best_t = t;
@@ -906,6 +915,9 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
                         best_pos = pos;
                         best_slot = k;
                         found = true;
+#if PRX_CACHE_CL
+                        cl = cull_limit(t);
+#endif
                     } else if (t > best_t && t < second) {
                         second = t;
                     }
@@ -919,6 +931,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
         }
     }
     t_cert = fminf(fminf(second, cull_limit(best_t)), t_max);
+#undef PRX_CL
 #ifdef PRX_CERT_STATS
     PRX_CERT_ADD(4, st_n[0]);
     PRX_CERT_ADD(5, st_n[1]);
