@@ -395,6 +395,7 @@ struct Trav {
 __device__ __forceinline__ void trav_init(const SceneDev& S, Trav& T, V3 o, V3 d, float t_min, float t_max,
                                           bool any) {
     T.r = make_ray(o, d);
+    if (!(t_min >= 0.0f)) T.r.regular = false;  // box_entry_fast's slack form assumes t_min >= 0
     T.t_min = t_min;
     T.t_max = t_max;
     T.kind = -1;
@@ -584,6 +585,9 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
 #ifndef PRX_F32X2
 #define PRX_F32X2 1
 #endif
+#ifndef PRX_SLACK_MUL
+#define PRX_SLACK_MUL 1
+#endif
 #ifndef PRX_CACHE_CL
 #define PRX_CACHE_CL 1  // the joint walk keeps cull_limit(best_t) instead of recomputing it
 #endif
@@ -628,7 +632,14 @@ __device__ __forceinline__ float box_entry_fast(const RayPre& r, float t_min, fl
     const float tnz = (A.z - r.o.z) * r.inv[2], tfz = (B.z - r.o.z) * r.inv[2];
     const float t0 = fmaxf(fmaxf(t_min, fminf(tnx, tfx)), fmaxf(fminf(tny, tfy), fminf(tnz, tfz)));
     const float t1 = fminf(fminf(t_lim, fmaxf(tnx, tfx)), fminf(fmaxf(tny, tfy), fmaxf(tnz, tfz)));
+#if PRX_SLACK_MUL
+    // t0 >= t_min >= 0, so the relative slack t0 - t1 <= 2e-6 (|t0| + |t1|) is
+    // t0 <= t1 (1 + 2e-6) / (1 - 2e-6) for t1 >= 0 (and a miss for t1 < 0): one product with a
+    // slightly larger factor accepts a superset (the culling only has to be conservative)
+    return t0 <= t1 * 1.000005f ? t0 : INFINITY;
+#else
     return t0 - t1 <= 2.0e-6f * (fabsf(t0) + fabsf(t1)) ? t0 : INFINITY;
+#endif
 }
 
 __device__ __forceinline__ float cull_limit(float best_t) { return best_t + 1e-4f * fabsf(best_t) + 1e-6f; }
@@ -1094,7 +1105,8 @@ __device__ __forceinline__ void make_hit_slot(const float4* __restrict__ tris, u
 // Hit::triangle: the static triangle's index in scene order, or the index inside its mesh.
 __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, float t_min, Hit& h,
                                                 float t_max = FLT_MAX, uint32_t* tri = nullptr) {
-    const RayPre r = make_ray(o, d);
+    RayPre r = make_ray(o, d);
+    if (!(t_min >= 0.0f)) r.regular = false;  // box_entry_fast's slack form assumes t_min >= 0
     if (S.fast && S.dfast && S.n_nodes > 0 && S.fp->n_dyn > 0) {
         // one walk over both trees; the winner's certificate makes it the two-phase answer:
         // a static winner beats every dynamic hit, so the dynamic phase adds nothing; a
@@ -1137,7 +1149,8 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
 // t_max holds an accepted triangle; the first accepted triangle of the combined walk
 // certifies when its own object's gate passes, else the sequential loop decides.
 __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_min, float t_max) {
-    const RayPre r = make_ray(o, d);
+    RayPre r = make_ray(o, d);
+    if (!(t_min >= 0.0f)) r.regular = false;  // box_entry_fast's slack form assumes t_min >= 0
     if (S.fast && S.dfast && S.n_nodes > 0 && S.fp->n_dyn > 0) {
         // one walk over both trees to the first accepted triangle; it decides when its own
         // reference path (static leaf, or its object's gate) passes at the fixed t_max
