@@ -650,7 +650,7 @@ __device__ __forceinline__ float cull_limit(float best_t) { return best_t + 1e-4
 constexpr int kShortStack = PRX_SHORT_STACK;
 constexpr int kMaxBlock = 256;  // every kernel that traverses launches <= 256 threads per block
 
-// this thread's column of the block's shared short stack (entry k at [k * blockDim.x])
+// this thread's column of the block's shared short stack (entry k at [k * kMaxBlock])
 __device__ __forceinline__ uint2* trav_short_stack() {
     __shared__ uint2 s_stack[kShortStack * kMaxBlock];
     return s_stack + threadIdx.x;
@@ -693,7 +693,7 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
     // usual traversal never touches -- a 64-deep local stack per thread would exceed L1 and
     // L2 at full occupancy and stream to DRAM.
     uint2* const ss = trav_short_stack();
-    const uint32_t stride = blockDim.x;
+    constexpr uint32_t stride = kMaxBlock;  // (compile-time: cheap shared addresses; blockDim.x <= kMaxBlock)
     uint2 overflow[64 - kShortStack];
     int sp = 0;
     uint32_t node = root;  // always an internal node
@@ -824,7 +824,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
 #define PRX_CL cull_limit(best_t)
 #endif
     uint2* const ss = trav_short_stack();
-    const uint32_t stride = blockDim.x;
+    constexpr uint32_t stride = kMaxBlock;  // (compile-time: cheap shared addresses; blockDim.x <= kMaxBlock)
     uint2 overflow[64 - kShortStack];
     int sp = 0;
     auto push = [&](uint32_t c, float ent) {
