@@ -588,6 +588,9 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
 #ifndef PRX_SLACK_MUL
 #define PRX_SLACK_MUL 1
 #endif
+#ifndef PRX_SS_ADDR
+#define PRX_SS_ADDR 1
+#endif
 #ifndef PRX_CACHE_CL
 #define PRX_CACHE_CL 1  // the joint walk keeps cull_limit(best_t) instead of recomputing it
 #endif
@@ -823,13 +826,26 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
 #else
 #define PRX_CL cull_limit(best_t)
 #endif
+#if PRX_SS_ADDR
+    // the column's 32-bit shared address, kept (recomputing the generic->shared base costs
+    // two S2R and a few ALU ops per push / pop)
+    uint32_t ss_addr;  // (opaque to the compiler, so it is kept rather than rematerialized)
+    asm volatile("mov.u32 %0, %1;" : "=r"(ss_addr) : "r"((uint32_t)__cvta_generic_to_shared(trav_short_stack())));
+#else
     uint2* const ss = trav_short_stack();
+#endif
     constexpr uint32_t stride = kMaxBlock;  // (compile-time: cheap shared addresses; blockDim.x <= kMaxBlock)
     uint2 overflow[64 - kShortStack];
     int sp = 0;
     auto push = [&](uint32_t c, float ent) {
         const uint2 e = make_uint2(c, __float_as_uint(ent));
+#if PRX_SS_ADDR
+        if (sp < kShortStack)
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(ss_addr + sp * stride * 8), "r"(e.x), "r"(e.y)
+                         : "memory");
+#else
         if (sp < kShortStack) ss[sp * stride] = e;
+#endif
         else overflow[sp - kShortStack] = e;
         ++sp;
     };
@@ -838,7 +854,13 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
         while (sp > 0) {
             --sp;
             uint2 e;
+#if PRX_SS_ADDR
+            if (sp < kShortStack)
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(ss_addr + sp * stride * 8)
+                             : "memory");
+#else
             if (sp < kShortStack) e = ss[sp * stride];
+#endif
             else e = overflow[sp - kShortStack];
             if (__uint_as_float(e.y) <= lim) return e.x;
         }
