@@ -40,6 +40,14 @@ struct RayPre {
     bool regular;  // safe and no zero component: the fast culling slabs need no branches
 };
 
+// hide a per-ray flag from rematerialization (kept in a register instead of being re-derived
+// from its inputs -- kernel parameters -- at every use in the traversal loop)
+__device__ __forceinline__ void opaque_flag(bool& f) {
+    uint32_t v = f ? 1u : 0u;
+    asm volatile("mov.u32 %0, %0;" : "+r"(v));
+    f = v != 0u;
+}
+
 __device__ __forceinline__ RayPre make_ray(V3 o, V3 d) {
     RayPre r;
     r.o = o;
@@ -1129,6 +1137,7 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
                                                 float t_max = FLT_MAX, uint32_t* tri = nullptr) {
     RayPre r = make_ray(o, d);
     if (!(t_min >= 0.0f)) r.regular = false;  // box_entry_fast's slack form assumes t_min >= 0
+    opaque_flag(r.regular);
     if (S.fast && S.dfast && S.n_nodes > 0 && S.fp->n_dyn > 0) {
         // one walk over both trees; the winner's certificate makes it the two-phase answer:
         // a static winner beats every dynamic hit, so the dynamic phase adds nothing; a
@@ -1173,6 +1182,7 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
 __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_min, float t_max) {
     RayPre r = make_ray(o, d);
     if (!(t_min >= 0.0f)) r.regular = false;  // box_entry_fast's slack form assumes t_min >= 0
+    opaque_flag(r.regular);
     if (S.fast && S.dfast && S.n_nodes > 0 && S.fp->n_dyn > 0) {
         // one walk over both trees to the first accepted triangle; it decides when its own
         // reference path (static leaf, or its object's gate) passes at the fixed t_max
