@@ -67,7 +67,9 @@ struct SceneDev {
     const float4* dnodes;      // LBVH nodes: 4 float4 per internal node
     const uint32_t* dleaf;     // LBVH leaf -> object-local triangle index
     int32_t dfast;             // 1: combined LBVH over all dynamic triangles is built
-    const float4* danodes;     // combined LBVH, fast-tree layout (4 float4 per node)
+    const float4* danodes;     // combined LBVH, fast-tree layout (4 float4 per node), at fnodes + 4 dnode_off
+    uint32_t dnode_off;        // index of its first node in the fnodes array: its internal child codes
+                               // (and per-object roots) are fnodes indices, so one base serves both trees
     const float4* datris;      // dynamic tris in combined-leaf order: {a, global idx} {e1, obj j} {e2, -}
     const uint32_t* dtri_obj;  // global dynamic triangle -> dynamic object j
     const float4* mat;         // per object {albedo, glossy exponent}

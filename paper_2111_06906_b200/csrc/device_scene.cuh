@@ -276,7 +276,7 @@ __device__ __forceinline__ bool dyn_closest(const SceneDev& S, const DynObj& D, 
         // combined SAH tree (fast_closest is exact over the triangles it is given)
         float bt, tc;
         uint32_t g;
-        if (!fast_closest<false>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc, D.sah_root)) return false;
+        if (!fast_closest<false>(S.fnodes, S.datris, r, t_min, t_max, bt, g, tc, D.sah_root)) return false;
         best_tri = g - D.tri_begin;
         t_max = bt;
         return true;
@@ -344,7 +344,7 @@ __device__ __forceinline__ bool dyn_any(const SceneDev& S, const DynObj& D, cons
     if (S.fast && S.dfast && D.sah_root != kLbvhBrute) {
         float bt, tc;
         uint32_t g;
-        return fast_closest<true>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc, D.sah_root);
+        return fast_closest<true>(S.fnodes, S.datris, r, t_min, t_max, bt, g, tc, D.sah_root);
     }
     const float4* T = S.dtris + 3ull * D.tri_begin;
     if (D.node_begin == kLbvhBrute) {
@@ -875,11 +875,11 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
         return kNone;
     };
 #if PRX_JOINT_STATIC_FIRST
-    push(kTreeBit, t_min);     // dynamic root, after the static tree
+    push(kTreeBit | S.dnode_off, t_min);  // dynamic root, after the static tree
     uint32_t node = 0u;        // static root
 #else
-    push(0u, t_min);           // static root, after the (small) dynamic tree
-    uint32_t node = kTreeBit;  // dynamic root
+    push(0u, t_min);                         // static root, after the (small) dynamic tree
+    uint32_t node = kTreeBit | S.dnode_off;  // dynamic root
 #endif
     uint32_t leaf = kNone;
 #ifdef PRX_CERT_STATS
@@ -891,7 +891,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
 #ifdef PRX_CERT_STATS
             ++st_n[tree ? 1 : 0];
 #endif
-            const float4* N = (tree ? S.danodes : S.fnodes) + 4ull * (node & ~kTreeBit);
+            const float4* N = S.fnodes + 4ull * (node & ~kTreeBit);  // (both trees: one node array)
             const float4 n0 = __ldg(&N[0]), n1 = __ldg(&N[1]), n2 = __ldg(&N[2]), n3 = __ldg(&N[3]);
             const uint32_t c0 = __float_as_uint(n0.w) | tree, c1r = __float_as_uint(n1.w);
             const uint32_t c1 = c1r | tree;
@@ -908,7 +908,7 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
 #if PRX_FAR_PREFETCH
                 if (!(far & kLeafBit))  // the deferred child's node, for when it is popped
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(
-                        ((far & kTreeBit) ? S.danodes : S.fnodes) + 4ull * (far & ~kTreeBit)));
+                        S.fnodes + 4ull * (far & ~kTreeBit)));
 #endif
             }
             if (next != kNone && (next & kLeafBit) && leaf == kNone) {  // park the leaf
@@ -1078,7 +1078,7 @@ __device__ __forceinline__ int dyn_closest_exact(const SceneDev& S, const RayPre
     if (!S.fast || !S.dfast) return dyn_closest_seq(S, r, t_min, t_max, dj, dtri);
     float bt, tc;
     uint32_t g;
-    if (!fast_closest<false>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc)) return -1;
+    if (!fast_closest<false>(S.fnodes, S.datris, r, t_min, t_max, bt, g, tc, S.dnode_off)) return -1;
     const uint32_t j = __ldg(&S.dtri_obj[g]);
     const DynObj& D = fp->dyn[j];
     if (!S.cert_off && ray_box(r, t_min, tc, D.cur)) {
@@ -1202,7 +1202,7 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
     if (S.fast && S.dfast) {
         float bt, tc;
         uint32_t g;
-        if (!fast_closest<true>(S.danodes, S.datris, r, t_min, t_max, bt, g, tc)) return false;
+        if (!fast_closest<true>(S.fnodes, S.datris, r, t_min, t_max, bt, g, tc, S.dnode_off)) return false;
         if (!S.cert_off && ray_box(r, t_min, t_max, fp->dyn[__ldg(&S.dtri_obj[g])].cur)) return true;
     }
     for (uint32_t j = 0; j < fp->n_dyn; ++j) {

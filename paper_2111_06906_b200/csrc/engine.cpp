@@ -363,17 +363,27 @@ void Engine::upload_scene() {
             ft[3 * k + 2] = tris[3 * pos + 2];
             ft[3 * k + 2].w = f_of_u(leaf_of[pos]);  // the certificate's reference leaf (static_cert_slot)
         }
-        // hot arena, hottest first: a window over its prefix keeps what fits persisting in L2
+        // hot arena, hottest first: a window over its prefix keeps what fits persisting in L2.
+        // The combined dynamic tree's nodes follow the static tree's in the same array (room
+        // for its largest form: <= 2 n + kMaxDyn nodes), so the joint walk reads both trees
+        // from one base: dynamic internal child codes are offset by the static node count.
+        size_t n_dyn_tris = 0;
+        for (const Object& o : s.objects)
+            if (o.dynamic) n_dyn_tris += o.mesh.size();
+        const size_t dyn_node_cap = n_dyn_tris >= 2 ? 2 * n_dyn_tris + kMaxDyn : 0;
         const auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
-        const size_t b_fn = sizeof(float4) * fn.size(), b_ft = sizeof(float4) * ft.size();
+        const size_t b_fn = sizeof(float4) * (fn.size() + 4 * dyn_node_cap), b_ft = sizeof(float4) * ft.size();
         const size_t b_lo = 4 * leaf_of.size(), b_nd = sizeof(float4) * nodes.size();
         d_hot_.alloc(up(b_fn) + up(b_ft) + up(b_lo) + up(b_nd));
         char* base = static_cast<char*>(d_hot_.get());
         p_fnodes_ = reinterpret_cast<float4*>(base);
+        dnode_off_ = static_cast<uint32_t>(fb.nodes.size());
+        p_dnodes_ = dyn_node_cap ? p_fnodes_ + fn.size() : nullptr;
+        dnode_cap_ = dyn_node_cap;
         p_ftris_ = reinterpret_cast<float4*>(base + up(b_fn));
         p_leaf_of_ = reinterpret_cast<uint32_t*>(base + up(b_fn) + up(b_ft));
         p_nodes_ = reinterpret_cast<float4*>(base + up(b_fn) + up(b_ft) + up(b_lo));
-        PRX_CUDA(cudaMemcpy(p_fnodes_, fn.data(), b_fn, cudaMemcpyHostToDevice));
+        PRX_CUDA(cudaMemcpy(p_fnodes_, fn.data(), sizeof(float4) * fn.size(), cudaMemcpyHostToDevice));
         PRX_CUDA(cudaMemcpy(p_ftris_, ft.data(), b_ft, cudaMemcpyHostToDevice));
         PRX_CUDA(cudaMemcpy(p_leaf_of_, leaf_of.data(), b_lo, cudaMemcpyHostToDevice));
         PRX_CUDA(cudaMemcpy(p_nodes_, nodes.data(), b_nd, cudaMemcpyHostToDevice));
@@ -464,8 +474,22 @@ void Engine::upload_scene() {
             lbvh_.scratch = w + 4 * n + 2 * (2 * n + 2);
             d_dall_tris_.alloc(sizeof(float4) * 3 * n);
             lbvh_.all_tris = d_dall_tris_.as<float4>();
+            // the combined tree's nodes: in the hot arena after the static tree's (codes offset
+            // by dnode_off_), or alone when the scene has no static tree (offset 0)
+            float4* dnodes = nullptr;
+            auto place_dnodes = [&](size_t n_nodes) {
+                if (p_dnodes_ && n_nodes <= dnode_cap_) {
+                    dnodes = p_dnodes_;
+                } else {
+                    d_dall_nodes_.alloc(sizeof(float4) * 4 * n_nodes);
+                    dnodes = d_dall_nodes_.as<float4>();
+                    dnode_off_ = 0;
+                    p_dnodes_ = nullptr;
+                }
+            };
             if (karras_all) {
-                d_dall_nodes_.alloc(sizeof(float4) * 4 * (n - 1));
+                place_dnodes(n - 1);
+                lbvh_.code_off = p_dnodes_ ? dnode_off_ : 0;
             } else {  // per-object SAH topologies, built once, refit per frame
                 std::vector<std::vector<Tri>> objs;
                 std::vector<uint32_t> begins;
@@ -476,9 +500,17 @@ void Engine::upload_scene() {
                     begins.push_back(d.tri_begin);
                     boxes.push_back(transform_box(o.local_bounds, transform_at(o.kfs, 0)));
                 }
-                const DynSahTopology topo = build_dyn_sah(objs, begins, boxes);
-                d_dall_nodes_.alloc(sizeof(float4) * topo.nodes.size());
-                PRX_CUDA(cudaMemcpy(d_dall_nodes_.get(), topo.nodes.data(), d_dall_nodes_.size(),
+                DynSahTopology topo = build_dyn_sah(objs, begins, boxes);
+                place_dnodes(topo.nodes.size() / 4);
+                const uint32_t off = p_dnodes_ ? dnode_off_ : 0;
+                for (size_t k = 0; k < topo.nodes.size(); ++k) {  // internal child codes -> arena indices
+                    if ((k & 3) > 1) continue;  // codes live in the .w of a node's first two float4
+                    uint32_t code;
+                    std::memcpy(&code, &topo.nodes[k].w, 4);
+                    if (code != 0xFFFFFFFFu && !(code & kLeafBit)) code += off;
+                    std::memcpy(&topo.nodes[k].w, &code, 4);
+                }
+                PRX_CUDA(cudaMemcpy(dnodes, topo.nodes.data(), sizeof(float4) * topo.nodes.size(),
                                     cudaMemcpyHostToDevice));
                 const size_t b_perm = 4 * topo.perm.size(), b_leaf = 4 * topo.leaves.size();
                 d_dsah_.alloc(b_perm + b_leaf + 4 * topo.parent.size());
@@ -493,9 +525,10 @@ void Engine::upload_scene() {
                 lbvh_.n_sah_leaves = static_cast<uint32_t>(topo.leaves.size() / 4);
                 lbvh_.n_sah_nodes = static_cast<uint32_t>(topo.parent.size());
                 if (!cfg_.dfs_traversal)
-                    for (size_t j = 0; j < dyn_.size(); ++j) dyn_[j].sah_root = topo.obj_root[j];
+                    for (size_t j = 0; j < dyn_.size(); ++j)
+                        dyn_[j].sah_root = topo.obj_root[j] == kLbvhBrute ? kLbvhBrute : topo.obj_root[j] + off;
             }
-            lbvh_.all_nodes = d_dall_nodes_.as<float4>();
+            lbvh_.all_nodes = dnodes;
         }
     }
 }
@@ -572,14 +605,15 @@ SceneDev Engine::scene_dev() const {
     S.cull_pad = 1e-5f * diag_ + 1e-6f;
     S.fast = cfg_.dfs_traversal ? 0 : 1;
     S.cert_off = cert_off_;
-    S.fnodes = p_fnodes_;
+    S.fnodes = p_fnodes_ ? p_fnodes_ : lbvh_.all_nodes;  // (no static tree: the dynamic tree's own array)
     S.ftris = p_ftris_;
     S.stris = d_stris_.as<float4>();
     S.dtris = d_dyn_world_.as<float4>();
     S.dnodes = d_lbvh_nodes_.as<float4>();
     S.dleaf = d_lbvh_leaf_.as<uint32_t>();
     S.dfast = lbvh_.all_nodes ? 1 : 0;
-    S.danodes = d_dall_nodes_.as<float4>();
+    S.danodes = lbvh_.all_nodes;
+    S.dnode_off = p_dnodes_ ? dnode_off_ : 0;
     S.datris = d_dall_tris_.as<float4>();
     S.dtri_obj = d_dyn_tri_xf_.as<uint32_t>();
     S.mat = d_mat_.as<float4>();

@@ -193,6 +193,9 @@ private:
     // leaf_of | reference nodes) so one L2 access-policy window can cover it (apply_l2_policy)
     DevBuf d_hot_;
     float4 *p_fnodes_ = nullptr, *p_ftris_ = nullptr, *p_nodes_ = nullptr;
+    float4* p_dnodes_ = nullptr;  // the combined dynamic tree's nodes inside the arena (after fnodes)
+    uint32_t dnode_off_ = 0;      // their index offset in fnodes (SceneDev::dnode_off)
+    size_t dnode_cap_ = 0;        // room reserved for them (nodes)
     uint32_t* p_leaf_of_ = nullptr;
     size_t l2_window_ = 0;
     int32_t cert_off_ = 0;

@@ -111,6 +111,7 @@ struct LbvhBuffers {
     const uint4* sah_leaf;       // {first slot, count, parent, side}
     const uint32_t* sah_parent;  // per internal node: parent << 1 | side
     uint32_t n_sah_leaves, n_sah_nodes;
+    uint32_t code_off;           // added to the combined tree's internal child codes (SceneDev::dnode_off)
 };
 void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint32_t n_tris,
                         const DynObj* dyn_host, uint32_t n_dyn, const DynObj* dyn_dev,

@@ -222,6 +222,18 @@ __global__ void k_sorted_tris(const float4* __restrict__ tris, const uint32_t* _
     }
 }
 
+// internal child codes of the combined tree -> indices into the static tree's node array
+__global__ void k_offset_codes(uint32_t n_nodes, float4* nodes, uint32_t off) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_nodes; t += gridDim.x * blockDim.x) {
+        float4* N = nodes + 4ull * t;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const uint32_t code = __float_as_uint(N[c].w);
+            if (code != 0xFFFFFFFFu && !(code & kLeafBit)) N[c].w = __uint_as_float(code + off);
+        }
+    }
+}
+
 __global__ void k_refit_all(const float4* __restrict__ stris, uint32_t n, const DynObj* __restrict__ dyn,
                             float4* nodes, const uint32_t* __restrict__ parent, uint32_t* flags) {
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
@@ -360,6 +372,10 @@ void build_dynamic_lbvh(const float4* world_tris, const uint32_t* tri_obj, uint3
         k_refit_all<<<g, kT, 0, st>>>(buf.all_tris, n_tris, dyn_dev, buf.all_nodes, buf.parent, buf.flags);
         k_collapse_all<<<g, kT, 0, st>>>(n_tris, buf.all_nodes, range);
         g_launches += 4;
+        if (buf.code_off) {
+            k_offset_codes<<<g, kT, 0, st>>>(n_tris - 1, buf.all_nodes, buf.code_off);
+            ++g_launches;
+        }
     }
 }
 
