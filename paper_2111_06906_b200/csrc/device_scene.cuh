@@ -596,6 +596,12 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
 #ifndef PRX_SLACK_MUL
 #define PRX_SLACK_MUL 1
 #endif
+#ifndef PRX_NODE_LD256
+#define PRX_NODE_LD256 1
+#endif
+#ifndef PRX_NODE_EVICT_LAST
+#define PRX_NODE_EVICT_LAST 1
+#endif
 #ifndef PRX_SS_ADDR
 #define PRX_SS_ADDR 1
 #endif
@@ -788,6 +794,23 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
     return found;
 }
 
+// a 64-byte node as two 256-bit loads (sm_100 LDG.256), optionally with an L2 evict-last hint
+// that keeps the hot tree ahead of the streaming path records in L2
+__device__ __forceinline__ void ld_node(const float4* N, float4& n0, float4& n1, float4& n2, float4& n3) {
+#if PRX_NODE_EVICT_LAST
+#define PRX_LD256 "ld.global.nc.L2::evict_last.v8.f32"
+#else
+#define PRX_LD256 "ld.global.nc.v8.f32"
+#endif
+    asm(PRX_LD256 " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(n0.x), "=f"(n0.y), "=f"(n0.z), "=f"(n0.w), "=f"(n1.x), "=f"(n1.y), "=f"(n1.z), "=f"(n1.w)
+        : "l"(N));
+    asm(PRX_LD256 " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(n2.x), "=f"(n2.y), "=f"(n2.z), "=f"(n2.w), "=f"(n3.x), "=f"(n3.y), "=f"(n3.z), "=f"(n3.w)
+        : "l"(N + 2));
+#undef PRX_LD256
+}
+
 // One walk over both fast trees (static SAH tree and combined dynamic LBVH): codes carry
 // kTreeBit for the dynamic tree, and candidates compare as (t, tree, position) -- static
 // before dynamic at equal t, which is intersect_scene's tie rule (the static hit shrinks
@@ -892,7 +915,12 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
             ++st_n[tree ? 1 : 0];
 #endif
             const float4* N = S.fnodes + 4ull * (node & ~kTreeBit);  // (both trees: one node array)
+#if PRX_NODE_LD256
+            float4 n0, n1, n2, n3;
+            ld_node(N, n0, n1, n2, n3);
+#else
             const float4 n0 = __ldg(&N[0]), n1 = __ldg(&N[1]), n2 = __ldg(&N[2]), n3 = __ldg(&N[3]);
+#endif
             const uint32_t c0 = __float_as_uint(n0.w) | tree, c1r = __float_as_uint(n1.w);
             const uint32_t c1 = c1r | tree;
             const float lim = PRX_CL;
