@@ -13,6 +13,9 @@ namespace prx {
 constexpr uint32_t kInvalidObj = 0xFFFFFFFFu;
 constexpr uint32_t kLeafBit = 0x80000000u;
 constexpr int kMaxDyn = 128;
+// float4s per triangle record of the fast trees (ftris / datris): {a, .} {e1, .} {e2, .} and a
+// pad, so a record is two aligned 32-byte halves (two 256-bit loads, whole sectors)
+constexpr int kFT = 4;
 constexpr uint8_t kDead = 0, kLive = 1, kReplace = 2;  // engine.cpp:17-19
 constexpr uint8_t kNoRetrace = 0xFF;                    // engine.hpp:56
 constexpr double kTwoPiD = 6.283185307179586476925286766559;  // 2 * std::numbers::pi

@@ -673,6 +673,30 @@ __device__ __forceinline__ uint2* trav_short_stack() {
     return s_stack + threadIdx.x;
 }
 
+// a 64-byte node as two 256-bit loads (sm_100 LDG.256), optionally with an L2 evict-last hint
+// that keeps the hot tree ahead of the streaming path records in L2
+__device__ __forceinline__ void ld_node(const float4* N, float4& n0, float4& n1, float4& n2, float4& n3) {
+#if PRX_NODE_EVICT_LAST
+#define PRX_LD256 "ld.global.nc.L2::evict_last.v8.f32"
+#else
+#define PRX_LD256 "ld.global.nc.v8.f32"
+#endif
+    asm(PRX_LD256 " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(n0.x), "=f"(n0.y), "=f"(n0.z), "=f"(n0.w), "=f"(n1.x), "=f"(n1.y), "=f"(n1.z), "=f"(n1.w)
+        : "l"(N));
+    asm(PRX_LD256 " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(n2.x), "=f"(n2.y), "=f"(n2.z), "=f"(n2.w), "=f"(n3.x), "=f"(n3.y), "=f"(n3.z), "=f"(n3.w)
+        : "l"(N + 2));
+#undef PRX_LD256
+}
+
+// a fast-tree triangle record (kFT = 4 float4: a, e1, e2, pad) as two 256-bit loads
+__device__ __forceinline__ void ld_tri(const float4* T, float4& a, float4& e1, float4& e2) {
+    float4 pad;
+    ld_node(T, a, e1, e2, pad);
+    (void)pad;
+}
+
 // global (t, position)-minimum over the triangles of a fast tree with t in (t_min, t_max).
 // Static: the SAH tree (fast_bvh.cpp), position = reference permutation position; dynamic:
 // the combined LBVH (lbvh.cu), position = global dynamic triangle index.  While-while
@@ -758,9 +782,8 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
         while (leaf != kNone) {
             const uint32_t first = (leaf & ~kLeafBit) >> 3, count = (leaf & 7u) + 1u;
             for (uint32_t k = first; k < first + count; ++k) {
-                const float4 ta = __ldg(&tris[3 * k]);
-                const float4 t1 = __ldg(&tris[3 * k + 1]);
-                const float4 t2 = __ldg(&tris[3 * k + 2]);
+                float4 ta, t1, t2;
+                ld_tri(tris + (size_t)kFT * k, ta, t1, t2);
                 const uint32_t pos = __float_as_uint(ta.w);
                 float t;
                 // window: (t_min, t_max) before the first hit, then up to the cull limit
@@ -794,23 +817,6 @@ __device__ __forceinline__ bool fast_closest(const float4* __restrict__ nodes, c
     return found;
 }
 
-// a 64-byte node as two 256-bit loads (sm_100 LDG.256), optionally with an L2 evict-last hint
-// that keeps the hot tree ahead of the streaming path records in L2
-__device__ __forceinline__ void ld_node(const float4* N, float4& n0, float4& n1, float4& n2, float4& n3) {
-#if PRX_NODE_EVICT_LAST
-#define PRX_LD256 "ld.global.nc.L2::evict_last.v8.f32"
-#else
-#define PRX_LD256 "ld.global.nc.v8.f32"
-#endif
-    asm(PRX_LD256 " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=f"(n0.x), "=f"(n0.y), "=f"(n0.z), "=f"(n0.w), "=f"(n1.x), "=f"(n1.y), "=f"(n1.z), "=f"(n1.w)
-        : "l"(N));
-    asm(PRX_LD256 " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=f"(n2.x), "=f"(n2.y), "=f"(n2.z), "=f"(n2.w), "=f"(n3.x), "=f"(n3.y), "=f"(n3.z), "=f"(n3.w)
-        : "l"(N + 2));
-#undef PRX_LD256
-}
-
 // One walk over both fast trees (static SAH tree and combined dynamic LBVH): codes carry
 // kTreeBit for the dynamic tree, and candidates compare as (t, tree, position) -- static
 // before dynamic at equal t, which is intersect_scene's tie rule (the static hit shrinks
@@ -833,8 +839,8 @@ constexpr uint32_t kTreeBit = 0x40000000u;
 __device__ __forceinline__ void prefetch_leaf(const SceneDev& S, uint32_t leaf) {
     const float4* tris = (leaf & kTreeBit) ? S.datris : S.ftris;
     const uint32_t first = (leaf & ~(kLeafBit | kTreeBit)) >> 3, count = (leaf & 7u) + 1u;
-    const char* a = reinterpret_cast<const char*>(tris + 3ull * first);
-    const char* e = a + 48u * count;
+    const char* a = reinterpret_cast<const char*>(tris + (size_t)kFT * first);
+    const char* e = a + 16u * kFT * count;
     for (const char* p = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(127)); p < e;
          p += 128)
         asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -961,9 +967,8 @@ __device__ __forceinline__ bool joint_closest(const SceneDev& S, const RayPre& r
             st_t[tree] += count;
 #endif
             for (uint32_t k = first; k < first + count; ++k) {
-                const float4 ta = __ldg(&tris[3 * k]);
-                const float4 t1 = __ldg(&tris[3 * k + 1]);
-                const float4 t2 = __ldg(&tris[3 * k + 2]);
+                float4 ta, t1, t2;
+                ld_tri(tris + (size_t)kFT * k, ta, t1, t2);
                 const uint32_t pos = __float_as_uint(ta.w);
                 float t;
                 const float lim = found ? fminf(PRX_CL, t_max) : t_max;
@@ -1025,7 +1030,7 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
 __device__ __forceinline__ bool static_cert_slot(const SceneDev& S, const RayPre& r, float t_min, float t_lim,
                                                  uint32_t slot) {
     if (S.cert_off) return false;
-    const uint32_t leaf = __float_as_uint(__ldg(&S.ftris[3 * slot + 2]).w);
+    const uint32_t leaf = __float_as_uint(__ldg(&S.ftris[kFT * slot + 2]).w);
     const float4 A = __ldg(&S.nodes[2 * leaf]);
     const float4 B = __ldg(&S.nodes[2 * leaf + 1]);
     return ray_box(r, t_min, t_lim, Box{{A.x, A.y, A.z}, {B.x, B.y, B.z}});
@@ -1148,8 +1153,8 @@ __device__ __forceinline__ void make_hit(const SceneDev& S, V3 o, V3 d, int kind
 // the reference-order arrays on the hot path
 __device__ __forceinline__ void make_hit_slot(const float4* __restrict__ tris, uint32_t slot, uint32_t obj, V3 o,
                                               V3 d, float t, Hit& h) {
-    const V3 e1 = ld3(__ldg(&tris[3 * slot + 1]));
-    const V3 e2 = ld3(__ldg(&tris[3 * slot + 2]));
+    const V3 e1 = ld3(__ldg(&tris[kFT * slot + 1]));
+    const V3 e2 = ld3(__ldg(&tris[kFT * slot + 2]));
     h.obj = obj;
     h.t = t;
     h.pos = add(o, mul(d, t));
@@ -1180,13 +1185,13 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
         if (tree == 0) {
             ok = static_cert_slot(S, r, t_min, tc, slot);
         } else {
-            dj = __float_as_uint(__ldg(&S.datris[3 * slot + 1]).w);  // dynamic object of the winner
+            dj = __float_as_uint(__ldg(&S.datris[kFT * slot + 1]).w);  // dynamic object of the winner
             ok = !S.cert_off && ray_box(r, t_min, tc, S.fp->dyn[dj].cur);
         }
         if (ok) {
             if (tri) *tri = tree == 0 ? __float_as_uint(__ldg(&S.stris[3 * pos]).w) : pos - S.fp->dyn[dj].tri_begin;
             if (tree == 0)
-                make_hit_slot(S.ftris, slot, __float_as_uint(__ldg(&S.ftris[3 * slot + 1]).w), o, d, bt, h);
+                make_hit_slot(S.ftris, slot, __float_as_uint(__ldg(&S.ftris[kFT * slot + 1]).w), o, d, bt, h);
             else
                 make_hit_slot(S.datris, slot, S.fp->dyn[dj].obj, o, d, bt, h);
             return true;
@@ -1220,7 +1225,7 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
         if (!joint_closest<true>(S, r, t_min, t_max, bt, tree, pos, tc, slot)) return false;
         if (tree == 0 ? static_cert_slot(S, r, t_min, t_max, slot)
                       : !S.cert_off &&
-                            ray_box(r, t_min, t_max, S.fp->dyn[__float_as_uint(__ldg(&S.datris[3 * slot + 1]).w)].cur))
+                            ray_box(r, t_min, t_max, S.fp->dyn[__float_as_uint(__ldg(&S.datris[kFT * slot + 1]).w)].cur))
             return true;
         PRX_CERT_COUNT(3);
     }

@@ -355,13 +355,13 @@ void Engine::upload_scene() {
             fn[4 * k + 2] = f4(nd.box[1].lo, 0.0f);
             fn[4 * k + 3] = f4(nd.box[1].hi, 0.0f);
         }
-        std::vector<float4> ft(3 * fb.order.size());
+        std::vector<float4> ft(kFT * fb.order.size(), float4{0.f, 0.f, 0.f, 0.f});
         for (size_t k = 0; k < fb.order.size(); ++k) {
             const uint32_t pos = fb.order[k];
-            ft[3 * k] = float4{tris[3 * pos].x, tris[3 * pos].y, tris[3 * pos].z, f_of_u(pos)};
-            ft[3 * k + 1] = tris[3 * pos + 1];
-            ft[3 * k + 2] = tris[3 * pos + 2];
-            ft[3 * k + 2].w = f_of_u(leaf_of[pos]);  // the certificate's reference leaf (static_cert_slot)
+            ft[kFT * k] = float4{tris[3 * pos].x, tris[3 * pos].y, tris[3 * pos].z, f_of_u(pos)};
+            ft[kFT * k + 1] = tris[3 * pos + 1];
+            ft[kFT * k + 2] = tris[3 * pos + 2];
+            ft[kFT * k + 2].w = f_of_u(leaf_of[pos]);  // the certificate's reference leaf (static_cert_slot)
         }
         // hot arena, hottest first: a window over its prefix keeps what fits persisting in L2.
         // The combined dynamic tree's nodes follow the static tree's in the same array (room
@@ -472,7 +472,8 @@ void Engine::upload_scene() {
             lbvh_.parent = w + 4 * n;
             lbvh_.flags = w + 4 * n + (2 * n + 2);
             lbvh_.scratch = w + 4 * n + 2 * (2 * n + 2);
-            d_dall_tris_.alloc(sizeof(float4) * 3 * n);
+            d_dall_tris_.alloc(sizeof(float4) * kFT * n);
+            PRX_CUDA(cudaMemset(d_dall_tris_.get(), 0, d_dall_tris_.size()));  // (pads stay zero)
             lbvh_.all_tris = d_dall_tris_.as<float4>();
             // the combined tree's nodes: in the hot arena after the static tree's (codes offset
             // by dnode_off_), or alone when the scene has no static tree (offset 0)

@@ -216,9 +216,9 @@ __global__ void k_sorted_tris(const float4* __restrict__ tris, const uint32_t* _
         a.w = __uint_as_float(g);
         e1.w = __uint_as_float(j);
         e2.w = 0.0f;
-        out[3 * t] = a;
-        out[3 * t + 1] = e1;
-        out[3 * t + 2] = e2;
+        out[kFT * t] = a;
+        out[kFT * t + 1] = e1;
+        out[kFT * t + 2] = e2;
     }
 }
 
@@ -237,7 +237,7 @@ __global__ void k_offset_codes(uint32_t n_nodes, float4* nodes, uint32_t off) {
 __global__ void k_refit_all(const float4* __restrict__ stris, uint32_t n, const DynObj* __restrict__ dyn,
                             float4* nodes, const uint32_t* __restrict__ parent, uint32_t* flags) {
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const float4 a = stris[3 * t], e1 = stris[3 * t + 1], e2 = stris[3 * t + 2];
+        const float4 a = stris[kFT * t], e1 = stris[kFT * t + 1], e2 = stris[kFT * t + 2];
         const DynObj D = dyn[__float_as_uint(e1.w)];
         const float ext = fmaxf(fmaxf(D.cur.hi.x - D.cur.lo.x, D.cur.hi.y - D.cur.lo.y), D.cur.hi.z - D.cur.lo.z);
         const float bx = a.x + e1.x, by = a.y + e1.y, bz = a.z + e1.z;
@@ -282,9 +282,9 @@ __global__ void k_dsah_tris(const float4* __restrict__ tris, const uint32_t* __r
         a.w = __uint_as_float(g);
         e1.w = __uint_as_float(tri_obj[g]);
         e2.w = 0.0f;
-        out[3 * t] = a;
-        out[3 * t + 1] = e1;
-        out[3 * t + 2] = e2;
+        out[kFT * t] = a;
+        out[kFT * t + 1] = e1;
+        out[kFT * t + 2] = e2;
     }
 }
 
@@ -297,7 +297,7 @@ __global__ void k_dsah_refit(const float4* __restrict__ stris, const uint4* __re
         const uint4 L = leaves[l];
         float lox = INFINITY, loy = INFINITY, loz = INFINITY, hix = -INFINITY, hiy = -INFINITY, hiz = -INFINITY;
         for (uint32_t t = L.x; t < L.x + L.y; ++t) {
-            const float4 a = stris[3 * t], e1 = stris[3 * t + 1], e2 = stris[3 * t + 2];
+            const float4 a = stris[kFT * t], e1 = stris[kFT * t + 1], e2 = stris[kFT * t + 2];
             const DynObj D = dyn[__float_as_uint(e1.w)];
             const float ext = fmaxf(fmaxf(D.cur.hi.x - D.cur.lo.x, D.cur.hi.y - D.cur.lo.y), D.cur.hi.z - D.cur.lo.z);
             const float bx = a.x + e1.x, by = a.y + e1.y, bz = a.z + e1.z;
