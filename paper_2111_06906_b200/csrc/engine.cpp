@@ -479,13 +479,13 @@ void Engine::upload_scene() {
             // by dnode_off_), or alone when the scene has no static tree (offset 0)
             float4* dnodes = nullptr;
             auto place_dnodes = [&](size_t n_nodes) {
-                if (p_dnodes_ && n_nodes <= dnode_cap_) {
+                if (p_dnodes_) {  // (the joint walk addresses both trees from the arena base)
+                    if (n_nodes > dnode_cap_) throw std::logic_error("dynamic tree larger than its arena room");
                     dnodes = p_dnodes_;
                 } else {
                     d_dall_nodes_.alloc(sizeof(float4) * 4 * n_nodes);
                     dnodes = d_dall_nodes_.as<float4>();
                     dnode_off_ = 0;
-                    p_dnodes_ = nullptr;
                 }
             };
             if (karras_all) {
