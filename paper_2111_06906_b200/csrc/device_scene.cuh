@@ -599,6 +599,9 @@ __device__ __forceinline__ float box_entry(const RayPre& r, float t_min, float t
 #ifndef PRX_NODE_LD256
 #define PRX_NODE_LD256 1
 #endif
+#ifndef PRX_NODE_L1_LAST
+#define PRX_NODE_L1_LAST 1
+#endif
 #ifndef PRX_NODE_EVICT_LAST
 #define PRX_NODE_EVICT_LAST 1
 #endif
@@ -676,7 +679,9 @@ __device__ __forceinline__ uint2* trav_short_stack() {
 // a 64-byte node as two 256-bit loads (sm_100 LDG.256), optionally with an L2 evict-last hint
 // that keeps the hot tree ahead of the streaming path records in L2
 __device__ __forceinline__ void ld_node(const float4* N, float4& n0, float4& n1, float4& n2, float4& n3) {
-#if PRX_NODE_EVICT_LAST
+#if PRX_NODE_EVICT_LAST && PRX_NODE_L1_LAST
+#define PRX_LD256 "ld.global.nc.L1::evict_last.L2::evict_last.v8.f32"
+#elif PRX_NODE_EVICT_LAST
 #define PRX_LD256 "ld.global.nc.L2::evict_last.v8.f32"
 #else
 #define PRX_LD256 "ld.global.nc.v8.f32"
