@@ -50,6 +50,21 @@ __device__ __forceinline__ uint32_t slot_of(unsigned long long key, int bits) {
     return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - bits));
 }
 
+// |p - x|^2 of the gather test (gather.hpp:54): dot(d, d) = ((dx dx) + (dy dy)) + dz dz, with
+// the x and y lanes on packed fp32 pairs (same per-lane rounding)
+__device__ __forceinline__ float gather_d2(const float4& p, V3 x) {
+#if PRX_F32X2
+    float qx, qy;
+    const unsigned long long d = f2_sub(f2_pack(p.x, p.y), f2_pack(x.x, x.y));
+    f2_unpack(f2_mul(d, d), qx, qy);
+    const float dz = p.z - x.z;
+    return (qx + qy) + dz * dz;
+#else
+    const V3 d = sub(V3{p.x, p.y, p.z}, x);
+    return dot(d, d);
+#endif
+}
+
 __global__ void k_gbuffer(SceneDev S, CamDev C, float4* gbuf) {
     const uint32_t n = C.w * C.h;
     for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < n; pix += gridDim.x * blockDim.x) {
@@ -672,8 +687,7 @@ __global__ void __launch_bounds__(kT) k_gather_groups(const float4* __restrict__
                         if (mine) {
                             for (uint32_t q = 0; q < m; ++q) {
                                 const float4 po = wpos[q];
-                                const V3 d = sub(V3{po.x, po.y, po.z}, x);  // gather.hpp:54
-                                if (dot(d, d) <= r2 && __float_as_uint(po.w) == obj) {
+                                if (gather_d2(po, x) <= r2 && __float_as_uint(po.w) == obj) {  // gather.hpp:54
                                     const float4 e = wen[q];
                                     ax = ax + e.x;
                                     ay = ay + e.y;
