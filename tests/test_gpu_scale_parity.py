@@ -3,7 +3,7 @@ lights, error mode T=0.001, DM 8x8x64x64, 7 bounces) at bench-scale path counts,
 compiled reference engine (oracle/_ref, `Engine::run_frame` engine.cpp:201-242 and
 `gather_image` gather.cpp:35-75).
 
-* `test_c4_1m_from_scratch`: 1,048,576 paths (the bench's CPU sample), frames 0-2 run on
+* `test_c4_1m_from_scratch`: 1,048,576 paths (the bench's CPU sample), frames 0-5 run on
   both engines from the same seed; every state field, the DMs, live aux and the image are
   compared every frame.
 * `test_c4_5m_bench_frames`: the bench's own workload, 5,000,000 paths.  The GPU runs
@@ -38,7 +38,7 @@ def test_c4_1m_from_scratch():
     gpu, cpu = pair("C4", synthetic=True, paths=1 << 20, **C4)
     n_lights = gpu.info().n_lights
     failures = []
-    for f in range(3):
+    for f in range(6):
         t0 = time.perf_counter()
         sc = cpu.run_frame()
         t_ref = time.perf_counter() - t0
