@@ -1,4 +1,6 @@
-// Timing of the radix sort passes on synthetic keys (profiling aid, not a test):
+// Timing of the radix sort passes on synthetic keys (profiling aid): nvcc -std=c++17 -O2
+// -gencode arch=compute_100a,code=sm_100a -Ipaper_2111_06906_b200/csrc profiles/prims_bench.cu
+// paper_2111_06906_b200/csrc/prims.cu -o /tmp/pb;
 // prims_bench n bits ragged_fill(0 = dense input, else percent of each tile kept)
 #include <cuda_runtime.h>
 
