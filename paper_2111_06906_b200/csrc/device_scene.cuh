@@ -1030,11 +1030,11 @@ __device__ __forceinline__ bool static_fast(const SceneDev& S, const RayPre& r, 
 // ancestor box contains the leaf box, and the double slab test is monotone under box
 // inclusion (fl(lo' - o) <= fl(lo - o) for lo' <= lo, division by d keeps the order, so the
 // entry bound can only drop and the exit bound only rise).
-// (the joint walk's form: the winner's fast-tree slot carries its reference leaf in ftris[3k+2].w,
+// (the joint walk's form: the winner's fast-tree slot carries its reference leaf in ftris[kFT k + 2].w,
 // one dependent load less than leaf_of[position])
 __device__ __forceinline__ bool static_cert_slot(const SceneDev& S, const RayPre& r, float t_min, float t_lim,
                                                  uint32_t slot) {
-    if (S.cert_off) return false;
+    if (S.cert_off || !(t_min >= 0.0f)) return false;  // (t_min < 0: exact paths only)
     const uint32_t leaf = __float_as_uint(__ldg(&S.ftris[kFT * slot + 2]).w);
     const float4 A = __ldg(&S.nodes[2 * leaf]);
     const float4 B = __ldg(&S.nodes[2 * leaf + 1]);
@@ -1043,7 +1043,7 @@ __device__ __forceinline__ bool static_cert_slot(const SceneDev& S, const RayPre
 
 __device__ __forceinline__ bool static_cert(const SceneDev& S, const RayPre& r, float t_min, float t_lim,
                                             uint32_t pos) {
-    if (S.cert_off) return false;
+    if (S.cert_off || !(t_min >= 0.0f)) return false;
     const uint32_t leaf = __ldg(&S.leaf_of[pos]);
     const float4 A = __ldg(&S.nodes[2 * leaf]);
     const float4 B = __ldg(&S.nodes[2 * leaf + 1]);
@@ -1119,7 +1119,7 @@ __device__ __forceinline__ int dyn_closest_exact(const SceneDev& S, const RayPre
     if (!fast_closest<false>(S.fnodes, S.datris, r, t_min, t_max, bt, g, tc, S.dnode_off)) return -1;
     const uint32_t j = __ldg(&S.dtri_obj[g]);
     const DynObj& D = fp->dyn[j];
-    if (!S.cert_off && ray_box(r, t_min, tc, D.cur)) {
+    if (!S.cert_off && t_min >= 0.0f && ray_box(r, t_min, tc, D.cur)) {
         t_max = bt;
         dj = j;
         dtri = g - D.tri_begin;
@@ -1191,7 +1191,7 @@ __device__ __forceinline__ bool intersect_scene(const SceneDev& S, V3 o, V3 d, f
             ok = static_cert_slot(S, r, t_min, tc, slot);
         } else {
             dj = __float_as_uint(__ldg(&S.datris[kFT * slot + 1]).w);  // dynamic object of the winner
-            ok = !S.cert_off && ray_box(r, t_min, tc, S.fp->dyn[dj].cur);
+            ok = !S.cert_off && t_min >= 0.0f && ray_box(r, t_min, tc, S.fp->dyn[dj].cur);
         }
         if (ok) {
             if (tri) *tri = tree == 0 ? __float_as_uint(__ldg(&S.stris[3 * pos]).w) : pos - S.fp->dyn[dj].tri_begin;
@@ -1229,7 +1229,7 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
         PRX_CERT_COUNT(2);
         if (!joint_closest<true>(S, r, t_min, t_max, bt, tree, pos, tc, slot)) return false;
         if (tree == 0 ? static_cert_slot(S, r, t_min, t_max, slot)
-                      : !S.cert_off &&
+                      : !S.cert_off && t_min >= 0.0f &&
                             ray_box(r, t_min, t_max, S.fp->dyn[__float_as_uint(__ldg(&S.datris[kFT * slot + 1]).w)].cur))
             return true;
         PRX_CERT_COUNT(3);
@@ -1241,7 +1241,7 @@ __device__ __forceinline__ bool occluded(const SceneDev& S, V3 o, V3 d, float t_
         float bt, tc;
         uint32_t g;
         if (!fast_closest<true>(S.fnodes, S.datris, r, t_min, t_max, bt, g, tc, S.dnode_off)) return false;
-        if (!S.cert_off && ray_box(r, t_min, t_max, fp->dyn[__ldg(&S.dtri_obj[g])].cur)) return true;
+        if (!S.cert_off && t_min >= 0.0f && ray_box(r, t_min, t_max, fp->dyn[__ldg(&S.dtri_obj[g])].cur)) return true;
     }
     for (uint32_t j = 0; j < fp->n_dyn; ++j) {
         const DynObj& D = fp->dyn[j];

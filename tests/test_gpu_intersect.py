@@ -205,3 +205,26 @@ def test_far_from_origin_bit_exact(tmp_path, offset):
     got, want = eng.intersect(rays), rs.intersect(frame, rays)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     assert np.array_equal(eng.intersect(rays, any_hit=True), rs.occluded(frame, rays))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scene,synthetic", [("villa-analog", False), ("C4", True)])
+def test_negative_t_min_bit_exact(scene, synthetic):
+    """Rays with t_min < 0 (hits behind the origin count) take the careful culling slabs (the
+    fast slabs' one-product acceptance assumes t_min >= 0); results stay bit-exact."""
+    from oracle import ref
+
+    sc = pr.Scene.synthetic(scene) if synthetic else pr.Scene.builtin(scene)
+    rs = ref.RefScene.from_desc(sc.describe()) if synthetic else ref.RefScene.builtin(scene)
+    eng = pr.Engine(sc, pr.make_config("naive", paths=1000, bounces=2, dm=[2, 2, 4, 4]))
+    eng.run_frame()
+    frame = eng.info().frames_run - 1
+    rng = np.random.default_rng(23)
+    rays = make_rays(sc.describe(), 30000, rng, sc.diagonal)
+    neg = rng.random(len(rays)) < 0.5
+    rays[neg, 6] = -(rng.random(int(neg.sum())) * sc.diagonal * 0.5).astype(np.float32)
+    got = eng.intersect(rays)
+    want = rs.intersect(frame, rays)
+    bad = np.any(got.view(np.uint32) != want.view(np.uint32), axis=1)
+    assert not bad.any(), f"{bad.sum()} of {len(rays)} rays differ"
+    assert np.array_equal(eng.intersect(rays, any_hit=True), rs.occluded(frame, rays))
