@@ -228,3 +228,31 @@ def test_negative_t_min_bit_exact(scene, synthetic):
     bad = np.any(got.view(np.uint32) != want.view(np.uint32), axis=1)
     assert not bad.any(), f"{bad.sum()} of {len(rays)} rays differ"
     assert np.array_equal(eng.intersect(rays, any_hit=True), rs.occluded(frame, rays))
+
+
+@pytest.mark.gpu
+def test_degenerate_query_rays_bit_exact():
+    """Scene-query rays the engine itself never casts: zero direction, negative zero
+    components, inverted windows (t_max < t_min), infinite t_max, origins far outside the
+    scene -- all against the reference's intersect_scene / occluded."""
+    from oracle import ref
+
+    sc = pr.Scene.synthetic("C4")
+    rs = ref.RefScene.from_desc(sc.describe())
+    eng = pr.Engine(sc, pr.make_config("naive", paths=1000, bounces=2, dm=[2, 2, 4, 4]))
+    eng.run_frame()
+    frame = eng.info().frames_run - 1
+    rng = np.random.default_rng(29)
+    rays = make_rays(sc.describe(), 6000, rng, sc.diagonal)
+    n = len(rays)
+    q = n // 6
+    rays[:q, 3:6] = 0.0                                   # zero direction
+    rays[q:2 * q, 3] = np.float32(-0.0)                   # a negative-zero component
+    rays[2 * q:3 * q, 6], rays[2 * q:3 * q, 7] = 1.0, 0.5  # inverted window
+    rays[3 * q:4 * q, 7] = np.inf                          # infinite t_max
+    rays[4 * q:5 * q, :3] *= np.float32(1e3)               # far outside the scene
+    got = eng.intersect(rays)
+    want = rs.intersect(frame, rays)
+    bad = np.any(got.view(np.uint32) != want.view(np.uint32), axis=1)
+    assert not bad.any(), f"{bad.sum()} of {n} rays differ, first {np.nonzero(bad)[0][:5]}"
+    assert np.array_equal(eng.intersect(rays, any_hit=True), rs.occluded(frame, rays))
