@@ -104,6 +104,12 @@ def test_engine_group_matches_single_engine(world, case):
     img_g, img_s = group.splat(radius=0.25), single.splat(radius=0.25)
     assert np.array_equal(img_g == 0, img_s == 0)
     assert np.allclose(img_g, img_s, rtol=1e-5, atol=0)  # per-shard sums, then the rank sum
+    for _ in range(2):  # frames whose side streams precompute the splat prefix on every rank
+        single.run_frame()
+        group.run_frame()
+    img_g, img_s = group.splat(radius=0.25), single.splat(radius=0.25)
+    assert np.array_equal(img_g == 0, img_s == 0)
+    assert np.allclose(img_g, img_s, rtol=1e-5, atol=0)
     group.close()
 
 
