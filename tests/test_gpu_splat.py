@@ -171,3 +171,22 @@ def test_cell_table_overflow_rebuild(monkeypatch, cap):
     ref = cpu.gather(camera=big, radius=0.25)[0]
     assert np.array_equal(gpu.splat(camera=big, radius=0.25, mode=1), ref)
     check_within_tolerance(gpu.splat(camera=big, radius=0.25, mode=0), ref)
+
+
+@pytest.mark.gpu
+def test_empty_views():
+    """A camera that sees no geometry (no registered cells, no candidates) and a 1x1 image:
+    both modes give the reference image (zeros where nothing is hit)."""
+    from paper_2111_06906_b200 import _lib as L
+
+    gpu, cpu = pair("C4", synthetic=True, mode="error", paths=20000, bounces=5, dm=[2, 2, 8, 8], seed=9)
+    gpu.run_frame()
+    cpu.run_frame()
+    cam = gpu.scene.describe().camera
+    away = L.Camera(cam.position, L.Vec3(cam.position.x - (cam.look_at.x - cam.position.x) * 1e3,
+                                         cam.position.y + 1e6, cam.position.z), cam.fov_deg, 40, 30)
+    tiny = L.Camera(cam.position, cam.look_at, cam.fov_deg, 1, 1)
+    for c in (away, tiny):
+        ref = cpu.gather(camera=c, radius=0.25)[0]
+        assert gpu.splat(camera=c, radius=0.25, mode=1).tobytes() == ref.tobytes()
+        assert np.array_equal(gpu.splat(camera=c, radius=0.25, mode=0) == 0, ref == 0)
