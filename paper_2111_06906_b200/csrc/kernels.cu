@@ -588,7 +588,10 @@ __global__ void __launch_bounds__(kT, PRX_TRACE_MINB) k_verify_error_walk(SceneD
     warp_add(&ctr->vis, vis);
 }
 
-__global__ void __launch_bounds__(kT, 4) k_compute_dm(SceneDev S, PathDev P, Counters* ctr) {
+#ifndef PRX_DM_MINB
+#define PRX_DM_MINB 4
+#endif
+__global__ void __launch_bounds__(kT, PRX_DM_MINB) k_compute_dm(SceneDev S, PathDev P, Counters* ctr) {
     const FrameParams* fp = S.fp;
     unsigned long long replaced = 0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
