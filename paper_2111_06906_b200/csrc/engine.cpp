@@ -18,6 +18,10 @@
 #include "fast_bvh.h"
 #include "prims.h"
 
+#ifndef PRX_TRACE_LONGEST_FIRST
+#define PRX_TRACE_LONGEST_FIRST 1  // trace queue ordered by retrace start (most bounces left first)
+#endif
+
 namespace prx {
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -1045,11 +1049,26 @@ void Engine::set_collectives(const prx_collectives* c) {
 void Engine::stage_trace() {
     const PathDev P = path_dev();
     uint32_t* cnt = d_cnt32_.as<uint32_t>();
-    launch_retrace_flags(P, d_flags8_.as<uint8_t>(), stream_);
+    const uint32_t* list = d_list_.as<uint32_t>();
+#if PRX_TRACE_LONGEST_FIRST
+    // queue order = retrace start ascending (most bounces left first, stable within a start):
+    // the persistent trace's tail is then made of the shortest paths.  Each path's result
+    // depends on its own data only, so the order changes timing, not bits.
+    int bits = 1;
+    while ((1u << bits) <= B_) ++bits;
+    launch_retrace_flags(P, d_flags8_.as<uint8_t>(), d_masks_.as<uint32_t>(), stream_);
+    compact_u8_pairs(d_flags8_.as<uint8_t>(), d_masks_.as<uint32_t>(), n_, d_keys_.as<uint32_t>(),
+                     d_vals_.as<uint32_t>(), cnt + kCntRetrace, d_scratch_.get(), stream_);
+    list = radix_sort_pairs_nocopy(d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(), d_keys_tmp_.as<uint32_t>(),
+                                   d_vals_tmp_.as<uint32_t>(), n_, cnt + kCntRetrace, bits, d_scratch_.get(), stream_)
+               ? d_vals_tmp_.as<uint32_t>()
+               : d_vals_.as<uint32_t>();
+#else
+    launch_retrace_flags(P, d_flags8_.as<uint8_t>(), nullptr, stream_);
     compact_u8(d_flags8_.as<uint8_t>(), n_, nullptr, 0, d_list_.as<uint32_t>(), cnt + kCntRetrace,
                d_scratch_.get(), stream_);
-    launch_trace(scene_dev(), P, d_list_.as<uint32_t>(), cnt + kCntRetrace, d_work_.as<uint32_t>(),
-                 d_ctr_.as<Counters>(), stream_);
+#endif
+    launch_trace(scene_dev(), P, list, cnt + kCntRetrace, d_work_.as<uint32_t>(), d_ctr_.as<Counters>(), stream_);
     launch_finalize(P, d_ctr_.as<Counters>(), stream_);
 }
 

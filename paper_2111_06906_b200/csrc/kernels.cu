@@ -810,9 +810,13 @@ __global__ void k_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t c
 }
 
 // ---------------------------------------------------------------- trace (engine.cpp:548-598)
-__global__ void k_retrace_flags(PathDev P, uint8_t* flags) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x)
-        flags[i] = (P.meta[i].z == kLive && P.rstart[i] != kNoRetrace) ? 1 : 0;
+__global__ void k_retrace_flags(PathDev P, uint8_t* flags, uint32_t* start_of) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        const uint8_t r = P.rstart[i];
+        const bool f = P.meta[i].z == kLive && r != kNoRetrace;
+        flags[i] = f ? 1 : 0;
+        if (start_of && f) start_of[i] = r;
+    }
 }
 
 // stage_trace's per-path bounce loop (engine.cpp:557-586).  Persistent lanes at ray
@@ -1089,8 +1093,8 @@ void launch_rank_prefix_u64(const uint32_t* g, uint32_t n, uint32_t world, uint3
 void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st) {
     LAUNCH(k_dm_after_fill, cells, dm_c, dm_t, cells);
 }
-void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st) {
-    LAUNCH(k_retrace_flags, P.n, P, flags);
+void launch_retrace_flags(PathDev P, uint8_t* flags, uint32_t* start_of, cudaStream_t st) {
+    LAUNCH(k_retrace_flags, P.n, P, flags, start_of);
 }
 void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count, uint32_t* work,
                   Counters* ctr, cudaStream_t st) {

@@ -66,7 +66,8 @@ void launch_rank_prefix_u64(const uint32_t* gathered, uint32_t n, uint32_t world
                             uint64_t* prefix, uint64_t* total, cudaStream_t st);
 void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st);
 // stage_trace (engine.cpp:548-598)
-void launch_retrace_flags(PathDev P, uint8_t* flags, cudaStream_t st);
+// flags[i] = path i is retraced; with start_of, start_of[i] = its retrace start (flagged i only)
+void launch_retrace_flags(PathDev P, uint8_t* flags, uint32_t* start_of, cudaStream_t st);
 void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count,
                   uint32_t* work, Counters* ctr, cudaStream_t st);
 void launch_finalize(PathDev P, Counters* ctr, cudaStream_t st);
