@@ -21,6 +21,9 @@
 #ifndef PRX_TRACE_LONGEST_FIRST
 #define PRX_TRACE_LONGEST_FIRST 1  // trace queue ordered by retrace start (most bounces left first)
 #endif
+#ifndef PRX_WALK_ORDER
+#define PRX_WALK_ORDER 1  // verify-walk queue: 0 append order, 1 most flagged segments first, 2 earliest flag first
+#endif
 
 namespace prx {
 
@@ -45,7 +48,7 @@ void DevBuf::reset() {
 
 namespace {
 
-enum { kCntTrim = 0, kCntPruned = 1, kCntRetrace = 2, kCntDead0 = 8, kCntNeed0 = 24, kCntN = 40 };
+enum { kCntTrim = 0, kCntPruned = 1, kCntRetrace = 2, kCntWalk = 3, kCntDead0 = 8, kCntNeed0 = 24, kCntN = 40 };
 enum {
     kEvFrame0 = 0,
     kEvVerify0 = 1,
@@ -838,10 +841,30 @@ void Engine::stage_occlusions() {
     if (h_fp_->n_boxes == 0) return;  // engine.cpp:308-312
     launch_occlusion_flags(scene_dev(), path_dev(), cfg_.mode, cfg_.record_flags, d_list_.as<uint32_t>(),
                            d_masks_.as<uint32_t>(), d_ctr_.as<Counters>(), stream_);
-    if (cfg_.mode == PRX_MODE_ERROR)
-        launch_verify_error(scene_dev(), path_dev(), cfg_.threshold, d_list_.as<uint32_t>(),
-                            d_masks_.as<uint32_t>(), d_ctr_.as<Counters>(), d_work_.as<uint32_t>(),
-                            d_ctr_.as<Counters>(), stream_);
+    if (cfg_.mode == PRX_MODE_ERROR) {
+        const uint32_t* list = d_list_.as<uint32_t>();
+        const uint32_t* masks = d_masks_.as<uint32_t>();
+#if PRX_WALK_ORDER
+        // the flagged list (atomic append order) sorted by expected walk length, longest first
+        uint32_t* n32 = d_cnt32_.as<uint32_t>() + kCntWalk;
+        const uint32_t top = B_ + 1;  // segments per path <= B + 1
+        int bits = 1;
+        while ((1u << bits) <= top) ++bits;
+        launch_walk_keys(masks, d_ctr_.as<Counters>(), n32, top, PRX_WALK_ORDER, n_, d_keys_.as<uint32_t>(),
+                         d_vals_.as<uint32_t>(), stream_);
+        const bool in_tmp = radix_sort_pairs_nocopy(d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(),
+                                                    d_keys_tmp_.as<uint32_t>(), d_vals_tmp_.as<uint32_t>(), n_, n32,
+                                                    bits, d_scratch_.get(), stream_);
+        uint32_t* l2 = in_tmp ? d_keys_.as<uint32_t>() : d_keys_tmp_.as<uint32_t>();
+        uint32_t* m2 = in_tmp ? d_vals_.as<uint32_t>() : d_vals_tmp_.as<uint32_t>();
+        launch_walk_permute(list, masks, in_tmp ? d_vals_tmp_.as<uint32_t>() : d_vals_.as<uint32_t>(), n32, n_, l2,
+                            m2, stream_);
+        list = l2;
+        masks = m2;
+#endif
+        launch_verify_error(scene_dev(), path_dev(), cfg_.threshold, list, masks, d_ctr_.as<Counters>(),
+                            d_work_.as<uint32_t>(), d_ctr_.as<Counters>(), stream_);
+    }
 }
 
 void Engine::stage_compute_dm() {

@@ -809,6 +809,31 @@ __global__ void k_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t c
         dm_c[c] = dm_c[c] < dm_t[c] ? dm_t[c] : dm_c[c];
 }
 
+// Verify-walk queue order (PRX_WALK_ORDER): sort keys of the flagged list, most expected rays
+// first -- 1: most flagged segments, 2: earliest flagged segment.  Each walk depends on its own
+// path only, so the order changes the persistent kernel's tail, not its results.
+__global__ void k_walk_keys(const uint32_t* __restrict__ masks, const Counters* cnt, uint32_t* n32, uint32_t top,
+                            int how, uint32_t n_max, uint32_t* keys, uint32_t* vals) {
+    const uint32_t n = (uint32_t)cnt->flagged;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n32 = n;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n && j < n_max; j += gridDim.x * blockDim.x) {
+        const uint32_t f = masks[j];
+        const uint32_t c = how == 1 ? (uint32_t)__popc(f) : 0u;
+        keys[j] = how == 1 ? (c < top ? top - c : 0u) : (f ? (uint32_t)(__ffs(f) - 1) : top);
+        vals[j] = j;
+    }
+}
+__global__ void k_walk_permute(const uint32_t* __restrict__ list, const uint32_t* __restrict__ masks,
+                               const uint32_t* __restrict__ order, const uint32_t* n32, uint32_t* list2,
+                               uint32_t* masks2) {
+    const uint32_t n = *n32;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t o = order[j];
+        list2[j] = list[o];
+        masks2[j] = masks[o];
+    }
+}
+
 // ---------------------------------------------------------------- trace (engine.cpp:548-598)
 __global__ void k_retrace_flags(PathDev P, uint8_t* flags, uint32_t* start_of) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
@@ -1019,6 +1044,14 @@ static void cert_report(const char* stage, cudaStream_t st) {
 #define CERT_REPORT(stage) ((void)0)
 #endif
 
+void launch_walk_keys(const uint32_t* masks, const Counters* cnt, uint32_t* n32, uint32_t top, int how,
+                      uint32_t n_max, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
+    LAUNCH(k_walk_keys, n_max, masks, cnt, n32, top, how, n_max, keys, vals);
+}
+void launch_walk_permute(const uint32_t* list, const uint32_t* masks, const uint32_t* order, const uint32_t* n32,
+                         uint32_t n_max, uint32_t* list2, uint32_t* masks2, cudaStream_t st) {
+    LAUNCH(k_walk_permute, n_max, list, masks, order, n32, list2, masks2);
+}
 void launch_verify_error(SceneDev S, PathDev P, float threshold, const uint32_t* list, const uint32_t* masks,
                          const Counters* cnt, uint32_t* work, Counters* ctr, cudaStream_t st) {
     if (S.fast) {  // one-shot walks on the fast traversal

@@ -66,6 +66,12 @@ void launch_rank_prefix_u64(const uint32_t* gathered, uint32_t n, uint32_t world
                             uint64_t* prefix, uint64_t* total, cudaStream_t st);
 void launch_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t cells, cudaStream_t st);
 // stage_trace (engine.cpp:548-598)
+// verify-walk queue order: keys of the flagged list (cnt->flagged entries, copied to *n32) and
+// the permutation of list / masks by the sorted slots
+void launch_walk_keys(const uint32_t* masks, const Counters* cnt, uint32_t* n32, uint32_t top, int how,
+                      uint32_t n_max, uint32_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_walk_permute(const uint32_t* list, const uint32_t* masks, const uint32_t* order, const uint32_t* n32,
+                         uint32_t n_max, uint32_t* list2, uint32_t* masks2, cudaStream_t st);
 // flags[i] = path i is retraced; with start_of, start_of[i] = its retrace start (flagged i only)
 void launch_retrace_flags(PathDev P, uint8_t* flags, uint32_t* start_of, cudaStream_t st);
 void launch_trace(SceneDev S, PathDev P, const uint32_t* list, const uint32_t* count,
