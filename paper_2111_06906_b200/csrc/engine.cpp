@@ -22,7 +22,7 @@
 #define PRX_TRACE_LONGEST_FIRST 1  // trace queue ordered by retrace start (most bounces left first)
 #endif
 #ifndef PRX_WALK_ORDER
-#define PRX_WALK_ORDER 1  // verify-walk queue: 0 append order, 1 most flagged segments first, 2 earliest flag first
+#define PRX_WALK_ORDER 1  // verify-walk queue: 0 append order, 1 most flagged segments first, 2 earliest flag first, 3 = 1 then 2
 #endif
 
 namespace prx {
@@ -850,6 +850,7 @@ void Engine::stage_occlusions() {
         const uint32_t top = B_ + 1;  // segments per path <= B + 1
         int bits = 1;
         while ((1u << bits) <= top) ++bits;
+        if (PRX_WALK_ORDER == 3) bits += 4;
         launch_walk_keys(masks, d_ctr_.as<Counters>(), n32, top, PRX_WALK_ORDER, n_, d_keys_.as<uint32_t>(),
                          d_vals_.as<uint32_t>(), stream_);
         const bool in_tmp = radix_sort_pairs_nocopy(d_keys_.as<uint32_t>(), d_vals_.as<uint32_t>(),

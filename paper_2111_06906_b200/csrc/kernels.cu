@@ -371,7 +371,7 @@ __device__ __forceinline__ uint32_t fetch_work(uint32_t* counter) {
 // take consecutive queue slots with one atomic, so the state-load latency is paid once per
 // batch instead of once per lane.
 #ifndef PRX_REFILL
-#define PRX_REFILL 8
+#define PRX_REFILL 24
 #endif
 __device__ __forceinline__ bool refill_due(bool idle, bool working) {
     const unsigned iw = __ballot_sync(0xffffffffu, idle);
@@ -810,7 +810,8 @@ __global__ void k_dm_after_fill(uint32_t* dm_c, const uint32_t* dm_t, uint32_t c
 }
 
 // Verify-walk queue order (PRX_WALK_ORDER): sort keys of the flagged list, most expected rays
-// first -- 1: most flagged segments, 2: earliest flagged segment.  Each walk depends on its own
+// first -- 1: most flagged segments, 2: earliest flagged segment, 3: most flagged segments,
+// then earliest flagged segment.  Each walk depends on its own
 // path only, so the order changes the persistent kernel's tail, not its results.
 __global__ void k_walk_keys(const uint32_t* __restrict__ masks, const Counters* cnt, uint32_t* n32, uint32_t top,
                             int how, uint32_t n_max, uint32_t* keys, uint32_t* vals) {
@@ -818,8 +819,9 @@ __global__ void k_walk_keys(const uint32_t* __restrict__ masks, const Counters* 
     if (blockIdx.x == 0 && threadIdx.x == 0) *n32 = n;
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n && j < n_max; j += gridDim.x * blockDim.x) {
         const uint32_t f = masks[j];
-        const uint32_t c = how == 1 ? (uint32_t)__popc(f) : 0u;
-        keys[j] = how == 1 ? (c < top ? top - c : 0u) : (f ? (uint32_t)(__ffs(f) - 1) : top);
+        const uint32_t c = (uint32_t)__popc(f), first = f ? (uint32_t)(__ffs(f) - 1) : top;
+        const uint32_t more = c < top ? top - c : 0u;
+        keys[j] = how == 1 ? more : (how == 2 ? first : (more << 4 | (first < 15u ? first : 15u)));
         vals[j] = j;
     }
 }
