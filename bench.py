@@ -56,6 +56,10 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e replay (profiling passes)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-splat-sweep", action="store_true", help="skip the per-mode splat timings")
+    ap.add_argument("--splat-overlap", type=int, default=1,
+                    help="1: the device-timed loop runs each frame's splat on the engine's side stream, "
+                         "overlapping the next frame's scene update and occlusion flags "
+                         "(prx_engine_set_splat_overlap); 0: splat, then the next frame")
     ap.add_argument("--extra", default="C1,C2,C3,C5w,C5b",
                     help="secondary workloads measured after the headline (N=1 only; 'none' skips): "
                          "C1-C3, C5w = C5 worst case (32M paths, 64 movers, baseline: full retrace), "
@@ -334,7 +338,13 @@ def main():
     img_dev = torch.zeros(cam.height * cam.width * 3, dtype=torch.float32, device="cuda")
     frame_no = [0]
 
-    def step(collect=None):
+    overlap = bool(args.splat_overlap) and not legacy
+    L.check(L.lib().prx_engine_set_splat_overlap(eng.handle, 1 if overlap else 0))
+    config["splat_overlap"] = ("on: each frame's splat runs on the engine's side stream during the next frame's "
+                               "scene update and occlusion flags (the frame's verify stage time includes its wait; "
+                               "the last splat completes inside the timed region)") if overlap else "off"
+
+    def step(collect=None, sync_splat=False):
         if legacy:
             d = run_frame_distributed(ex, coll, frame_no[0])
             st = L.FrameStats()
@@ -345,15 +355,17 @@ def main():
             L.check(L.lib().prx_run_frame(eng.handle, C.byref(st)))
         frame_no[0] += 1
         sst = L.FrameStats()
+        # (stats request a host wait for the splat's timing: the overlapped loop passes none)
         L.check(L.lib().prx_splat(eng.handle, C.byref(cam), 0.25, args.splat_mode, None,
-                                  C.c_void_p(img_dev.data_ptr()), C.byref(sst)))
+                                  C.c_void_p(img_dev.data_ptr()),
+                                  None if overlap and not sync_splat else C.byref(sst)))
         if legacy:
             torch.distributed.all_reduce(img_dev)
         if collect is not None:
             collect.append((st, sst))
 
     first = []
-    step(first)  # frame 0: the cold fill (reported separately)
+    step(first, sync_splat=True)  # frame 0: the cold fill (reported separately)
     for _ in range(max(3, args.warmup) - 1):
         step()
     stats = []
@@ -367,6 +379,8 @@ def main():
     ev0.record(stream)
     for _ in range(args.steps):
         step(stats)
+    if overlap:  # the engine stream waits for the last step's splat (side stream) before ev1
+        L.check(L.lib().prx_engine_synchronize(eng.handle))
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -415,6 +429,9 @@ def main():
         for mode, tag in ((1, "ordered"), (0, "atomic")):
             for w_px, h_px in ((cam.width, cam.height), (1920, 1080)):
                 splat_modes[f"{tag}_{w_px}x{h_px}"] = time_splat(mode, w_px, h_px)
+    if overlap:  # the overlapped splats carry no timing: the splat stage alone on the final map
+        splat_ms = splat_modes.get(f"{'ordered' if args.splat_mode == 1 else 'atomic'}_{cam.width}x{cam.height}") \
+            or time_splat(args.splat_mode, cam.width, cam.height)
 
     # e2e through the public API with host buffers (stats + image read back every step), on a
     # fresh engine replaying the same frames as the timed loop (the workload drifts with the

@@ -354,6 +354,13 @@ void prx_comm_destroy(prx_comm* comm);
 
 prx_status prx_engine_set_stream(prx_engine* engine, void* cuda_stream);
 prx_status prx_engine_synchronize(prx_engine* engine);
+/* Overlapped splat (no reference counterpart; default off).  When on, a prx_splat of the scene
+ * camera at the frame's prefix radius with a device output only (rgb_out NULL, stats NULL,
+ * unsharded) is enqueued on the engine's side stream and returns at once: it runs while the
+ * next prx_run_frame updates the scene and computes the occlusion flags, and that frame waits
+ * for it before its first write to the photon map.  rgb_dev is complete after the next
+ * engine call that touches engine state, or after prx_engine_synchronize. */
+prx_status prx_engine_set_splat_overlap(prx_engine* engine, int32_t on);
 
 /* gather_image (gather.cpp:35-75) as a GPU splat over the engine's live photons.
  * rgb_out: host float[3*w*h] (may be NULL) -- top-left origin, RGB rows;

@@ -186,6 +186,7 @@ SIGNATURES = [
     ("prx_comm_destroy", None, [P]),
     ("prx_engine_set_stream", C.c_int, [P, P]),
     ("prx_engine_synchronize", C.c_int, [P]),
+    ("prx_engine_set_splat_overlap", C.c_int, [P, C.c_int32]),
     ("prx_splat", C.c_int, [P, C.POINTER(Camera), C.c_float, C.c_int, P, P,
                             C.POINTER(FrameStats)]),
     ("prx_gather_photons", C.c_int, [P, P, P, C.c_uint32, C.c_uint32, C.c_int32, C.POINTER(Camera),

@@ -54,9 +54,15 @@ void need(const void* p, const char* what) {
     if (!p) throw std::invalid_argument(std::string(what) + " is NULL");
 }
 
-prx::Engine& eng(prx_engine* e) {
+// (every entry but run_frame / splat first orders the engine stream after an overlapped splat)
+prx::Engine& eng_raw(prx_engine* e) {
     need(e, "engine");
     return *e->engine;
+}
+prx::Engine& eng(prx_engine* e) {
+    prx::Engine& E = eng_raw(e);
+    E.join_splat();
+    return E;
 }
 
 }  // namespace
@@ -302,7 +308,7 @@ prx_status prx_engine_get_info(const prx_engine* engine, prx_engine_info* out) {
 }
 
 prx_status prx_run_frame(prx_engine* engine, prx_frame_stats* stats) {
-    return guarded([&] { eng(engine).run_frame(stats); });
+    return guarded([&] { eng_raw(engine).run_frame(stats); });
 }
 prx_status prx_frame_update(prx_engine* engine, prx_frame_stats* stats) {
     return guarded([&] { eng(engine).frame_update(stats); });
@@ -462,9 +468,13 @@ prx_status prx_engine_synchronize(prx_engine* engine) {
     return guarded([&] { eng(engine).synchronize(); });
 }
 
+prx_status prx_engine_set_splat_overlap(prx_engine* engine, int32_t on) {
+    return guarded([&] { eng(engine).set_splat_overlap(on != 0); });
+}
+
 prx_status prx_splat(prx_engine* engine, const prx_camera* camera, float radius, int mode, float* rgb_out,
                      float* rgb_dev, prx_frame_stats* stats) {
-    return guarded([&] { eng(engine).splat(camera, radius, mode, rgb_out, rgb_dev, stats); });
+    return guarded([&] { eng_raw(engine).splat(camera, radius, mode, rgb_out, rgb_dev, stats); });
 }
 
 prx_status prx_gather_photons(prx_engine* engine, const void* photons, const void* aux, uint32_t n_paths,

@@ -182,6 +182,8 @@ Engine::Engine(std::shared_ptr<const Scene> scene, const prx_config& cfg)
     PRX_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
     PRX_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     PRX_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    PRX_CUDA(cudaEventCreateWithFlags(&ev_splat_, cudaEventDisableTiming));
+    PRX_CUDA(cudaEventCreateWithFlags(&ev_splat_read_, cudaEventDisableTiming));
     if (const char* e = std::getenv("PRX_SPLAT_PREFIX")) pre_on_ = e[0] != '0';
     PRX_CUDA(cudaHostAlloc(&h_ncell_, 8, cudaHostAllocDefault));
     h_ncell_[0] = h_ncell_[1] = 0;
@@ -288,6 +290,8 @@ Engine::~Engine() {
     }
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (ev_splat_) cudaEventDestroy(ev_splat_);
+    if (ev_splat_read_) cudaEventDestroy(ev_splat_read_);
     if (stream_ && own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -825,6 +829,7 @@ void Engine::frame_update_enqueue() {
     if (dyn_changed_) place_dynamics_enqueue();
     launch_frame_reset(path_dev(), cfg_.record_flags, d_ctr_.as<Counters>(), stream_);
     if (cfg_.mode == PRX_MODE_BASELINE) {  // engine.cpp:228-232
+        wait_splat(stream_, false);  // (truncates every path: a photon-map write)
         launch_release_all(path_dev(), stream_);
         for (LightBlock& b : lights_) PRX_CUDA(cudaMemsetAsync(b.dm_c.get(), 0, 4ull * b.cells, stream_));
     }
@@ -842,6 +847,7 @@ void Engine::stage_occlusions() {
     launch_occlusion_flags(scene_dev(), path_dev(), cfg_.mode, cfg_.record_flags, d_list_.as<uint32_t>(),
                            d_masks_.as<uint32_t>(), d_ctr_.as<Counters>(), stream_);
     if (cfg_.mode == PRX_MODE_ERROR) {
+        wait_splat(stream_, false);  // the walk rewrites vertices an overlapped splat may still read
         const uint32_t* list = d_list_.as<uint32_t>();
         const uint32_t* masks = d_masks_.as<uint32_t>();
 #if PRX_WALK_ORDER
@@ -884,6 +890,7 @@ void Engine::verify_paths(prx_frame_stats* st) {
     } else {
         record(kEvOccl0);
     }
+    wait_splat(stream_, false);  // (compute_dm truncates paths: the first photon-map write otherwise)
     record(kEvDm0);
     stage_compute_dm();
     if (sharded()) exchange_dm();
@@ -1192,6 +1199,7 @@ void Engine::run_frame(prx_frame_stats* st) {
         plain();
     }
     last_sig_ = sig;
+    splat_pending_ = false;  // (the frame waited for it)
     pre_ok_ = pre_on_ && pre_radius_ > 0.0f;  // (graphs are dropped when the prefix radius changes)
     if (st) {
         st->frame = cur_frame_;
@@ -1408,6 +1416,7 @@ bool Engine::splat_prefix_fork() {
     }
     PRX_CUDA(cudaEventRecord(ev_fork_, stream_));
     PRX_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
+    wait_splat(side_stream_, true);  // (the prefix rewrites the tables an overlapped splat reads)
     launch_splat_prefix(scene_dev(), camera_dev(c), pre_radius_, d_pre_gbuf_.as<float4>(), d_pre_work_.get(),
                         pre_bits_, side_stream_);
     // the registered-cell count sizes the splat's sort keys and shows a table overflow (read
@@ -1457,6 +1466,8 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
         }
     }
     if (use_pre && splat_table_overflow(h_ncell_[0], pre_bits_)) use_pre = false;  // (rebuilt below)
+    const bool overlap = splat_overlap_ && use_pre && !rgb_host && rgb_dev && !st && !reduce_ranks && !capturing_;
+    if (!overlap) join_splat();
     if (c.width != img_w_ || c.height != img_h_) {
         d_gbuf_.alloc(16ull * npx);
         d_img_.alloc(12ull * npx);
@@ -1506,6 +1517,17 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
     if (d_gather_.size() == 0 || gather_bits_ < bits) {  // both modes
         d_gather_.alloc(gather_work_bytes(nv, npx, bits));
         gather_bits_ = bits;
+    }
+    if (overlap) {  // on the side stream after the frame; no host wait (see prx_engine_set_splat_overlap)
+        PRX_CUDA(cudaEventRecord(ev_fork_, stream_));
+        PRX_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
+        launch_splat(S, P, C, radius, gbuf, out, inv_pi, inv_area, work, d_splat_cand_.get(), mode, d_gather_.get(),
+                     bits, true, cell_bits, side_stream_, ev_splat_read_);
+        PRX_CUDA(cudaEventRecord(ev_splat_, side_stream_));
+        PRX_CUDA(cudaGetLastError());
+        splat_pending_ = true;
+        launches_ = g_launches - launch_base_;
+        return;
     }
     launch_splat(S, P, C, radius, gbuf, out, inv_pi, inv_area, work, d_splat_cand_.get(), mode, d_gather_.get(), bits,
                  true, cell_bits, stream_);
@@ -1698,7 +1720,36 @@ void Engine::set_stream(cudaStream_t s) {
     }
 }
 
-void Engine::synchronize() { PRX_CUDA(cudaStreamSynchronize(stream_)); }
+void Engine::synchronize() {
+    join_splat();
+    PRX_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::set_splat_overlap(bool on) {
+    if (on == splat_overlap_) return;
+    join_splat();
+    splat_overlap_ = on;
+    drop_graphs();  // (captured frames carry the overlap waits or not)
+}
+
+void Engine::join_splat() {
+    if (!splat_pending_) return;
+    PRX_CUDA(cudaStreamWaitEvent(stream_, ev_splat_, 0));
+    splat_pending_ = false;
+}
+
+// a frame's wait for an overlapped splat: a plain stream wait, or inside a frame-graph capture an
+// external event-wait node (it waits for the splat enqueued before each replay; when none is,
+// the event's last record has long completed)
+// (whole: the splat's end; else its last read of the photon map -- the sort's gather pass)
+void Engine::wait_splat(cudaStream_t s, bool whole) {
+    if (!splat_overlap_) return;
+    cudaEvent_t e = whole ? ev_splat_ : ev_splat_read_;
+    if (capturing_)
+        PRX_CUDA(cudaStreamWaitEvent(s, e, cudaEventWaitExternal));
+    else if (splat_pending_)
+        PRX_CUDA(cudaStreamWaitEvent(s, e, 0));
+}
 
 void Engine::info(prx_engine_info* out) const {
     std::memset(out, 0, sizeof(*out));

@@ -90,6 +90,10 @@ public:
     void set_stream(cudaStream_t s);
     void set_collectives(const prx_collectives* c);  // in-engine sharded frames (comm.cpp)
     void synchronize();
+    // overlapped splat (prx_engine_set_splat_overlap): join_splat orders the engine stream
+    // after a pending one (every C-ABI entry but run_frame / splat calls it)
+    void set_splat_overlap(bool on);
+    void join_splat();
     void info(prx_engine_info* out) const;
     uint64_t launches() const { return launches_; }
     // bytes moved host->device / device->host by this engine since creation
@@ -231,6 +235,11 @@ private:
     // radius of the last scene-camera splat, run on a side stream during verify/retrace
     cudaStream_t side_stream_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    // overlapped splat: enqueued on the side stream, ev_splat_ marks its end; the next frame
+    // waits for it before its first photon-map write and before its own prefix
+    cudaEvent_t ev_splat_ = nullptr, ev_splat_read_ = nullptr;  // its end / its last photon-map read
+    bool splat_overlap_ = false, splat_pending_ = false;
+    void wait_splat(cudaStream_t s, bool whole);
     DevBuf d_pre_gbuf_, d_pre_work_;
     float pre_radius_ = 0.0f;  // 0: no scene-camera splat yet, no prefix
     bool pre_ok_ = false;      // d_pre_* match the current placement of the scene

@@ -97,7 +97,7 @@ int splat_cell_bits(uint32_t n_cells);     // key bits of n_cells dense cell ids
 // that many bits (else the table's)
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img,
                   float inv_pi, float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, int bits,
-                  bool prefix_done, int cell_bits, cudaStream_t st);
+                  bool prefix_done, int cell_bits, cudaStream_t st, cudaEvent_t photons_read = nullptr);
 void launch_splat_prefix(SceneDev S, const CamDev& C, float radius, float4* gbuf, void* work, int bits,
                          cudaStream_t st);
 

@@ -772,7 +772,7 @@ int splat_cell_bits(uint32_t n_cells) {
 
 void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* gbuf, float* img, float inv_pi,
                   float inv_area, void* work, void* cand_buf, int mode, void* gather_buf, int bits,
-                  bool prefix_done, int cell_bits, cudaStream_t st) {
+                  bool prefix_done, int cell_bits, cudaStream_t st, cudaEvent_t photons_read) {
     const uint32_t npx = C.w * C.h;
     const uint64_t slots = 1ull << bits;
     auto* keys = static_cast<unsigned long long*>(work);
@@ -834,6 +834,7 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
         k_bin_scatter<<<launch_grid(nv, kT), kT, 0, st>>>(P, cand, m_count, pstart, pcur, spo, sen);
         g_launches += 2;  // filter, scatter
+        if (photons_read) cudaEventRecord(photons_read, st);  // (the photon map is not read past here)
         if (!groups) {
             uint32_t* wq = m_count + 4;  // zeroed above
             k_splat_pixels<<<launch_grid(32ull * npx, kT), kT, 0, st>>>(gbuf, npx, radius, keys, bits, pstart, pcnt,
@@ -887,6 +888,7 @@ void launch_splat(SceneDev S, PathDev P, const CamDev& C, float radius, float4* 
         pg.out_b = sen;
         radix_sort_gather(sk, sv, sk2, sv2, (uint32_t)nv, m_count, cell_bits > 0 ? cell_bits : bits, pg, gscratch,
                           st, tile_cnt);
+        if (photons_read) cudaEventRecord(photons_read, st);  // (the photon map is not read past here)
         scan_exclusive_u32(pcnt, pstart, (uint32_t)slots, nullptr, nullptr, gscratch, st);
         g_launches += 1;  // bin (the prims count their own)
         if (!groups) {

@@ -305,6 +305,19 @@ class Engine:
     def synchronize(self) -> None:
         L.check(L.lib().prx_engine_synchronize(self._h))
 
+    def set_splat_overlap(self, on: bool) -> None:
+        """Device-output splats of the scene camera run on a side stream, overlapping the next
+        frame's scene update and occlusion flags (prx_engine_set_splat_overlap)."""
+        L.check(L.lib().prx_engine_set_splat_overlap(self._h, 1 if on else 0))
+
+    def splat_device(self, rgb_dev_ptr: int, camera: L.Camera | None = None, radius: float | None = None,
+                     mode: int = 1) -> None:
+        """splat into a device float[3*w*h] buffer (asynchronous when the overlap is on)."""
+        cam = camera if camera is not None else self.scene.describe().camera
+        r = self.config.gather_radius if radius is None else radius
+        L.check(L.lib().prx_splat(self._h, C.byref(cam), float(r), int(mode), None, C.c_void_p(int(rgb_dev_ptr)),
+                                  None))
+
     def photon_map(self) -> np.ndarray:
         return self.download("photons")
 
