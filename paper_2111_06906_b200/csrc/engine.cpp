@@ -281,6 +281,7 @@ Engine::~Engine() {
     if (h_xf_) cudaFreeHost(h_xf_);
     if (h_prune_frame_) cudaFreeHost(h_prune_frame_);
     if (h_ncell_) cudaFreeHost(h_ncell_);
+    if (h_img_stage_) cudaFreeHost(h_img_stage_);
     for (auto& kv : graphs_)
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (capture_stream_) cudaStreamDestroy(capture_stream_);
@@ -1199,7 +1200,10 @@ void Engine::run_frame(prx_frame_stats* st) {
         plain();
     }
     last_sig_ = sig;
-    splat_pending_ = false;  // (the frame waited for it)
+    if (splat_pending_) {  // (the frame waited for it: its prefix branch joined after the splat's end)
+        splat_pending_ = false;
+        finish_splat();
+    }
     pre_ok_ = pre_on_ && pre_radius_ > 0.0f;  // (graphs are dropped when the prefix radius changes)
     if (st) {
         st->frame = cur_frame_;
@@ -1466,7 +1470,7 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
         }
     }
     if (use_pre && splat_table_overflow(h_ncell_[0], pre_bits_)) use_pre = false;  // (rebuilt below)
-    const bool overlap = splat_overlap_ && use_pre && !rgb_host && rgb_dev && !st && !reduce_ranks && !capturing_;
+    const bool overlap = splat_overlap_ && use_pre && !st && !reduce_ranks && !capturing_;
     if (!overlap) join_splat();
     if (c.width != img_w_ || c.height != img_h_) {
         d_gbuf_.alloc(16ull * npx);
@@ -1523,6 +1527,18 @@ void Engine::splat_store(const PathDev& P, const prx_camera* cam, float radius, 
         PRX_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
         launch_splat(S, P, C, radius, gbuf, out, inv_pi, inv_area, work, d_splat_cand_.get(), mode, d_gather_.get(),
                      bits, true, cell_bits, side_stream_, ev_splat_read_);
+        if (rgb_host) {  // -> pinned staging now, -> rgb_host in finish_splat
+            const size_t bytes = 12ull * npx;
+            if (h_img_stage_bytes_ < bytes) {
+                if (h_img_stage_) PRX_CUDA(cudaFreeHost(h_img_stage_));
+                PRX_CUDA(cudaHostAlloc(&h_img_stage_, bytes, cudaHostAllocDefault));
+                h_img_stage_bytes_ = bytes;
+            }
+            PRX_CUDA(cudaMemcpyAsync(h_img_stage_, out, bytes, cudaMemcpyDeviceToHost, side_stream_));
+            d2h_bytes_ += bytes;
+            pending_host_out_ = rgb_host;
+            pending_host_bytes_ = bytes;
+        }
         PRX_CUDA(cudaEventRecord(ev_splat_, side_stream_));
         PRX_CUDA(cudaGetLastError());
         splat_pending_ = true;
@@ -1736,6 +1752,15 @@ void Engine::join_splat() {
     if (!splat_pending_) return;
     PRX_CUDA(cudaStreamWaitEvent(stream_, ev_splat_, 0));
     splat_pending_ = false;
+    finish_splat();
+}
+
+// the host part of an overlapped splat with a host output: wait for it, copy out of staging
+void Engine::finish_splat() {
+    if (!pending_host_out_) return;
+    PRX_CUDA(cudaEventSynchronize(ev_splat_));
+    std::memcpy(pending_host_out_, h_img_stage_, pending_host_bytes_);
+    pending_host_out_ = nullptr;
 }
 
 // a frame's wait for an overlapped splat: a plain stream wait, or inside a frame-graph capture an

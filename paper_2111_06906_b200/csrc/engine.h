@@ -239,7 +239,14 @@ private:
     // waits for it before its first photon-map write and before its own prefix
     cudaEvent_t ev_splat_ = nullptr, ev_splat_read_ = nullptr;  // its end / its last photon-map read
     bool splat_overlap_ = false, splat_pending_ = false;
+    // a host output of the overlapped splat: copied to pinned staging on the side stream, then
+    // to the caller's buffer once the splat is known complete (finish_splat)
+    float* h_img_stage_ = nullptr;
+    size_t h_img_stage_bytes_ = 0;
+    float* pending_host_out_ = nullptr;
+    size_t pending_host_bytes_ = 0;
     void wait_splat(cudaStream_t s, bool whole);
+    void finish_splat();
     DevBuf d_pre_gbuf_, d_pre_work_;
     float pre_radius_ = 0.0f;  // 0: no scene-camera splat yet, no prefix
     bool pre_ok_ = false;      // d_pre_* match the current placement of the scene

@@ -198,6 +198,8 @@ _VEC4 = {"pos_obj", "energy", "in_dir", "out_dir", "origin", "emission_dir", "ca
 class Engine:
     """pathreuse::Engine (engine.hpp:69-179) on one B200 (optionally one path shard)."""
 
+    _overlap = False  # set_splat_overlap
+
     def __init__(self, scene: Scene, config: L.Config | None = None, **kwargs):
         self.scene = scene  # keeps the scene alive
         self.config = config if config is not None else make_config(**kwargs)
@@ -260,6 +262,8 @@ class Engine:
         L.check(L.lib().prx_splat(self._h, C.byref(cam), float(r), int(mode),
                                   out.ctypes.data_as(C.c_void_p), None,
                                   C.byref(st) if st is not None else None))
+        if self._overlap:  # (an overlapped splat fills `out` at the next engine call)
+            self.synchronize()
         del info
         return out
 
@@ -309,6 +313,20 @@ class Engine:
         """Device-output splats of the scene camera run on a side stream, overlapping the next
         frame's scene update and occlusion flags (prx_engine_set_splat_overlap)."""
         L.check(L.lib().prx_engine_set_splat_overlap(self._h, 1 if on else 0))
+        self._overlap = bool(on)
+
+    def splat_into(self, out: np.ndarray, camera: L.Camera | None = None, radius: float | None = None,
+                   mode: int = 1) -> np.ndarray:
+        """splat into a host float32 [h, w, 3] array.  With the overlap on (scene camera at the
+        prefix radius), the call returns at once and `out` is filled when the next engine call
+        (run_frame, synchronize, ...) returns."""
+        cam = camera if camera is not None else self.scene.describe().camera
+        if out.dtype != np.float32 or not out.flags.c_contiguous or out.size != 3 * cam.width * cam.height:
+            raise ValueError("splat_into: out must be a C-contiguous float32 [h, w, 3] array of the camera's size")
+        r = self.config.gather_radius if radius is None else radius
+        L.check(L.lib().prx_splat(self._h, C.byref(cam), float(r), int(mode), out.ctypes.data_as(C.c_void_p), None,
+                                  None))
+        return out
 
     def splat_device(self, rgb_dev_ptr: int, camera: L.Camera | None = None, radius: float | None = None,
                      mode: int = 1) -> None:

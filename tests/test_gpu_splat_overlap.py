@@ -65,3 +65,24 @@ def test_overlap_toggle_and_other_camera():
         assert np.array_equal(obuf.cpu().numpy().reshape(48, 64, 3), cpu.gather(camera=other, radius=0.25)[0]), f
         gpu.synchronize()
         assert np.array_equal(_img(buf, cam), cpu.gather(radius=0.25)[0]), f
+
+
+@pytest.mark.gpu
+def test_overlapped_host_splat():
+    """splat_into a host array with the overlap on: filled by the next engine call, equal to
+    gather_image of its frame (the bench's pipelined e2e loop)."""
+    gpu, cpu = pair("C4", synthetic=True, mode="error", paths=30000, bounces=5, dm=[2, 2, 8, 8], seed=8)
+    gpu.set_splat_overlap(True)
+    cam = gpu.scene.describe().camera
+    out = np.zeros((cam.height, cam.width, 3), dtype=np.float32)
+    pending = None
+    for f in range(7):
+        gpu.run_frame()
+        if pending is not None:
+            assert np.array_equal(out, pending), f
+        cpu.run_frame()
+        pending = cpu.gather(radius=0.25)[0]
+        out[...] = -1.0
+        gpu.splat_into(out, radius=0.25)
+    gpu.synchronize()
+    assert np.array_equal(out, pending)
