@@ -12,9 +12,11 @@ out=gpurun_out
 mkdir -p "$out"
 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > "$out/${tag}_bench.json" 2> "$out/${tag}_bench.err" || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/${tag}_launches.csv" \
-    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-splat-sweep --extra none > "$out/${tag}_ncu_launches.log" 2>&1
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-splat-sweep --extra none --splat-overlap 0 > "$out/${tag}_ncu_launches.log" 2>&1
 common="--set full --import-source on --clock-control none"
-bench="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-splat-sweep --extra none"
+# (ncu serialises kernels, so the overlapped splat has nothing to overlap under it: the launch
+# list and the captures use the serial loop, whose frames list each splat after its frame)
+bench="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-splat-sweep --extra none --splat-overlap 0"
 for k in k_trace k_verify_error_walk k_occlusion_flags k_compute_dm k_gather_bin k_gather_staged \
          k_rs_scatter k_fill_assign k_update_origins; do
     skip=3
