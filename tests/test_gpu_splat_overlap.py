@@ -16,11 +16,14 @@ def _img(buf, cam):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("scene,synthetic,mode", [("C4", True, "error"), ("moving-cube", False, "naive"),
-                                                  ("merry-go-round-analog", False, "baseline")])
-def test_overlapped_splat_bit_exact(scene, synthetic, mode):
+@pytest.mark.parametrize("scene,synthetic,mode,graphs", [("C4", True, "error", "1"), ("C4", True, "error", "0"),
+                                                         ("moving-cube", False, "naive", "1"),
+                                                         ("merry-go-round-analog", False, "baseline", "1")])
+def test_overlapped_splat_bit_exact(monkeypatch, scene, synthetic, mode, graphs):
+    """graphs "0": plain stream launches (PRX_GRAPHS=0) instead of replayed frame graphs."""
     import torch
 
+    monkeypatch.setenv("PRX_GRAPHS", graphs)
     gpu, cpu = pair(scene, synthetic=synthetic, mode=mode, paths=30000, bounces=5, dm=[2, 2, 8, 8], seed=11)
     gpu.set_splat_overlap(True)
     cam = gpu.scene.describe().camera
