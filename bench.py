@@ -197,8 +197,9 @@ EXTRA = {  # the other BASELINE.json configurations, one B200
 }
 
 
-def measure_extra(pr, L, torch, stream, key, steps=5, warmup=3):
-    """Device ms/frame (frame + 120x90 ordered splat) of one secondary workload."""
+def measure_extra(pr, L, torch, stream, key, steps=5, warmup=3, overlap=True):
+    """Device ms/frame (frame + 120x90 ordered splat) of one secondary workload (with the
+    overlapped splat like the headline loop, unless overlap=False)."""
     import ctypes as C
 
     w = EXTRA[key]
@@ -209,11 +210,13 @@ def measure_extra(pr, L, torch, stream, key, steps=5, warmup=3):
     cam = scene.describe().camera
     img = torch.zeros(cam.height * cam.width * 3, dtype=torch.float32, device="cuda")
     sts = []
+    eng.set_splat_overlap(overlap)
 
-    def one(collect):
+    def one(collect, timed_splat=False):
         st, sst = L.FrameStats(), L.FrameStats()
         L.check(L.lib().prx_run_frame(eng.handle, C.byref(st)))
-        L.check(L.lib().prx_splat(eng.handle, C.byref(cam), 0.25, 1, None, C.c_void_p(img.data_ptr()), C.byref(sst)))
+        L.check(L.lib().prx_splat(eng.handle, C.byref(cam), 0.25, 1, None, C.c_void_p(img.data_ptr()),
+                                  C.byref(sst) if timed_splat or not overlap else None))
         if collect:
             sts.append((st, sst))
 
@@ -224,9 +227,18 @@ def measure_extra(pr, L, torch, stream, key, steps=5, warmup=3):
     e0.record(stream)
     for _ in range(steps):
         one(True)
+    if overlap:
+        L.check(L.lib().prx_engine_synchronize(eng.handle))  # (joins the last splat before e1)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    splat_alone = []
+    if overlap:  # the splat stage alone (serial splats with their own events) on the last frames
+        for _ in range(3):
+            sst = L.FrameStats()
+            L.check(L.lib().prx_splat(eng.handle, C.byref(cam), 0.25, 1, None, C.c_void_p(img.data_ptr()),
+                                      C.byref(sst)))
+            splat_alone.append(sst.ms_splat)
     counts = scene.counts()
     out = {"scene": f"{w['scene'][0]} ({counts['static_triangles']} static + {counts['dynamic_triangles']} dynamic tris)",
            "mode": w["mode"], "paths": w["paths"], "bounces": w["bounces"], "ms_per_step": ms,
@@ -234,7 +246,8 @@ def measure_extra(pr, L, torch, stream, key, steps=5, warmup=3):
            "stages_ms": {k: statistics.median(getattr(a, f) for a, _ in sts)
                          for k, f in (("verify", "ms_verify"), ("retrace", "ms_retrace"))},
            "rays_traced_per_frame": statistics.median(a.rays_traced for a, _ in sts)}
-    out["stages_ms"]["splat"] = statistics.median(b.ms_splat for _, b in sts)
+    out["stages_ms"]["splat"] = statistics.median(splat_alone) if overlap else statistics.median(b.ms_splat for _, b in sts)
+    out["splat_overlap"] = overlap
     eng.close()
     return out
 
@@ -548,7 +561,7 @@ def main():
         torch.cuda.synchronize()
         line["workloads"] = {}
         for key in [k for k in args.extra.split(",") if k]:
-            line["workloads"][key] = measure_extra(pr, L, torch, stream, key)
+            line["workloads"][key] = measure_extra(pr, L, torch, stream, key, overlap=bool(args.splat_overlap))
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sample = args.cpu_sample or CPU_SAMPLE_PATHS[name]
